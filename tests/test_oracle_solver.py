@@ -1,0 +1,174 @@
+"""Pins for the oracle's assembly, policy evaluation, policy iteration and time march against
+what the paper prints and what the mathematics fixes.  CPU only."""
+import itertools
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+from oracle.howard import control_search, howard_step, march
+from oracle.scheme import Geometry, apply_operator
+from oracle.system import assemble, dense_solve, solve
+from synth import bj_config, problem_A, problem_B
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "paper_table4.json")
+
+
+def _psi_full(p, t):
+    psi = np.zeros(p.N)
+    b = p.boundary_idx()
+    psi[b] = p.psi(t, b)
+    return psi
+
+
+@pytest.mark.parametrize("cfg,n", [(0, 9), (2, 9), (3, 5)])
+def test_assembled_m_matrix_and_inverse(cfg, n):
+    """A^pi is an M-matrix with nonnegative row sums; here: sign pattern, interior row sums
+    >= 1 - dt c_max > 0, and (dense) A^{-1} >= 0 with ||A^{-1}||_inf <= 1/(1 - dt c_max) (D6)."""
+    p = bj_config(cfg, n=n)
+    rng = np.random.default_rng(3)
+    pol = rng.integers(0, p.K, size=p.N)
+    dt = 0.25
+    U0 = p.g(p.all_idx())
+    sysm = assemble(p, pol, dt, dt, U0, _psi_full(p, dt))
+    A = sysm.A.toarray()
+    off = A - np.diag(np.diag(A))
+    assert np.all(np.diag(A) > 0) and np.all(off <= 0)
+    # full row sum (incl. boundary couplings) is exactly 1 - dt c (D3); moving the (negative)
+    # boundary couplings to the rhs can only increase the interior row sum
+    assert A.sum(1).min() >= 1 + 0.1 * dt - 1e-10 * np.abs(A).max()
+    Ainv = np.linalg.inv(A)
+    assert Ainv.min() >= -1e-12
+    assert np.abs(Ainv).sum(1).max() <= 1.0 / (1 + 0.1 * dt) + 1e-10
+
+
+def test_assembled_matches_matrix_free_operator():
+    """The CSR rows (interior) plus boundary couplings reproduce the matrix-free row
+    (A x)_j = x_j - dt (L_hat[x] + c x_j) of P:415-426 on a random full-grid x."""
+    p = bj_config(2, n=33)
+    rng = np.random.default_rng(5)
+    pol = rng.integers(0, p.K, size=p.N)
+    x = rng.uniform(-1, 1, size=p.N)
+    dt = 0.1
+    zero = np.zeros(p.N)
+    sysm = assemble(p, pol, dt, 0.0, zero, x)            # F = dt f + dt sum_boundary l psi, psi = x
+    f_only = assemble(p, pol, dt, 0.0, zero, zero).F
+    y_mf = apply_operator(p, pol, x, dt)
+    y_csr = sysm.A @ x[sysm.interior] - (sysm.F - f_only)
+    assert np.abs(y_mf - y_csr).max() < 1e-12 * np.abs(y_mf).max() * 1e3
+
+
+def test_solve_matches_dense_lu_tiny():
+    p = bj_config(0, n=9)
+    U0 = p.g(p.all_idx())
+    pol = np.random.default_rng(2).integers(0, p.K, size=p.N)
+    sysm = assemble(p, pol, p.dt, p.dt, U0, _psi_full(p, p.dt))
+    X, rres = solve(sysm)
+    Xd = dense_solve(sysm)
+    assert rres < 1e-13 and np.abs(X - Xd).max() < 1e-13 * np.abs(Xd).max()
+    X2, rres2 = solve(sysm, direct_limit=0)               # iterative branch to 1e-13
+    assert rres2 < 1e-13 and np.abs(X2 - Xd).max() < 1e-11 * np.abs(Xd).max()
+
+
+def test_howard_equals_min_over_all_policies():
+    """D7 (Howard, P:154-155 with [bokanowski_Howard]): U* = min over ALL policies of U^pi,
+    componentwise.  Tiny grid: 2x2 interior, 3 controls -> 3^4 = 81 linear solves."""
+    p = bj_config(0, n=4, K=3)
+    dt = 0.5
+    U0 = p.g(p.all_idx())
+    U, pol, st = howard_step(p, U0, dt, dt, tol_pi=0.0)
+    geo = Geometry.of(p)
+    inter = geo.interior_idx()
+    psi = _psi_full(p, dt)
+    best = np.full(inter.size, np.inf)
+    for choice in itertools.product(range(p.K), repeat=inter.size):
+        pf = np.zeros(p.N, dtype=int)
+        pf[inter] = choice
+        best = np.minimum(best, dense_solve(assemble(p, pf, dt, dt, U0, psi)))
+    assert np.abs(U[inter] - best).max() < 1e-13
+
+
+def test_single_control_one_iteration():
+    """N_alpha = 1 -> one policy evaluation; the confirming search sees no change."""
+    p = bj_config(0, n=17, K=1)
+    U, pol, st = howard_step(p, p.g(p.all_idx()), p.dt, p.dt)
+    assert st.pi_iters == 1 and st.changed[-1] == 0
+
+
+def test_control_search_is_argmin_of_row_residual():
+    """D1: argmin_a H^a_j(U) equals argmax_a ((A^a U)_j - F^a_j) computed from assembled systems
+    (P:149, 152)."""
+    p = bj_config(0, n=9, K=5)
+    dt = p.dt
+    rng = np.random.default_rng(9)
+    U = p.g(p.all_idx()) + 0.01 * rng.normal(size=p.N)
+    Uprev = p.g(p.all_idx())
+    sr = control_search(p, U, Uprev, dt, dt)
+    psi = U.copy()                                         # boundary values of U act as psi
+    inter = Geometry.of(p).interior_idx()
+    res = []
+    for a in range(p.K):
+        pf = np.full(p.N, a)
+        s = assemble(p, pf, dt, dt, Uprev, psi)
+        res.append(s.A @ U[inter] - s.F)
+    res = np.array(res)
+    assert np.array_equal(np.argmax(res, axis=0), sr.policy)
+    assert np.abs(res.max(0) - (U[inter] - Uprev[inter] - dt * sr.H)).max() < 1e-12 * np.abs(res).max()
+
+
+def test_residual_certificate_bound():
+    """D6: ||U - U*||_inf <= R(U)/(1 - dt c_max) for any U (here: U* perturbed)."""
+    p = bj_config(0, n=17)
+    dt = p.dt
+    U0 = p.g(p.all_idx())
+    Ustar, pol, _ = howard_step(p, U0, dt, dt, tol_pi=0.0)
+    inter = Geometry.of(p).interior_idx()
+    rng = np.random.default_rng(4)
+    for amp in (1e-3, 1e-6):
+        U = Ustar.copy()
+        U[inter] += amp * rng.uniform(-1, 1, size=inter.size)
+        R = control_search(p, U, U0, dt, dt).R.max()
+        assert np.abs(U - Ustar).max() <= R / (1 + 0.1 * dt) * (1 + 1e-9) + 1e-14
+
+
+@pytest.mark.parametrize("which", ["A", "B"])
+def test_paper_table4_implicit_truncation(which):
+    """PAPER.md Table 4 / Table 4-B: theta = 1, dt = T, N_alpha = 40,
+    L-inf error over the whole grid within +-20 % at N_x = 41, 81."""
+    gold = json.load(open(GOLDEN))["problem_" + which]
+    mk = problem_A if which == "A" else problem_B
+    errs = []
+    for nx in (41, 81):
+        p = mk(nx)
+        U, _, _ = march(p)
+        e = np.abs(U - p.u_exact(p.T, p.all_idx())).max()
+        errs.append(e)
+        assert abs(e / gold[str(nx)] - 1) < 0.2, (nx, e, gold[str(nx)])
+    if which == "A":
+        assert abs(math.log2(errs[0] / errs[1]) - 1.03) < 0.15
+
+
+@pytest.mark.slow
+def test_paper_table4_161():
+    for which, mk in (("A", problem_A), ("B", problem_B)):
+        gold = json.load(open(GOLDEN))["problem_" + which]["161"]
+        p = mk(161)
+        U, _, _ = march(p)
+        e = np.abs(U - p.u_exact(p.T, p.all_idx())).max()
+        assert abs(e / gold - 1) < 0.2
+
+
+def test_manufactured_convergence_rate():
+    """cfg0 family with K = (n-1)/2 so theta*(x_j) lies on the control grid at every node
+    (reading xii: u* is then exact for the discrete control set): errors shrink at a rate in
+    [0.5, 1.3] on average (O(sqrt dx) worst case from the truncated layer, ~O(dx) observed)."""
+    errs = []
+    for n in (17, 33, 65):
+        p = bj_config(0, n=n, K=(n - 1) // 2, n_steps=2)
+        U, _, _ = march(p)
+        errs.append(np.abs(U - p.u_exact(p.T, p.all_idx())).max())
+    rate = 0.5 * math.log2(errs[0] / errs[2])     # averaged over two refinements
+    assert 0.5 <= rate <= 1.3 and errs[1] < errs[0] and errs[2] < errs[1], errs
+    assert errs[-1] < 0.02
