@@ -1,0 +1,220 @@
+/*
+ * hjb.h -- C-ABI of libhjb: the B200-native hot path of the implicit semi-Lagrangian
+ * (LISL, Scheme 2 with boundary truncation) discretisation of the HJB equation
+ *
+ *     u_t - inf_a { L^a u + c^a u + f^a } = 0  in (0,T] x Omega,  u(0,.) = g,  u = psi on dOmega
+ *     L^a u = tr[a^a D^2 u] + b^a . Du,   a^a = 1/2 sigma^a sigma^a^T,  sigma^a in R^{d x P}
+ *                                                          (arXiv:1605.04821)
+ *
+ * one implicit Euler step (theta = 1) solved by policy iteration: a per-node
+ * exhaustive control search, then a GMG-preconditioned BiCGSTAB solve of the policy system.
+ * All arithmetic is fp64 and runs in sm_100a kernels; there is no CPU fallback.
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  Grid:    Omega = [lo,hi]^d, d in {2,3}, n nodes per dimension including the boundary,
+ *           h = (hi-lo)/(n-1), node x_i = lo + i*h.  Flat index lexicographic, x1 fastest.
+ *  Layout:  every per-node array ("grid array") is a DEVICE array of hjb_layout.local_elems
+ *           fp64 (or u8) elements holding the local slab rows [local_row0, local_row0+local_rows)
+ *           of the slowest axis; with nranks == 1 this is simply the full n^d grid.
+ *  Boundary: Dirichlet nodes are identity rows (reading ix in DESIGN.md); their values in U are
+ *           psi(t_n) and the stencil interpolates them (truncated endpoints land on dOmega,
+ *           PAPER.md:216-227, interpolate-at-boundary mode of PAPER.md:387-432).
+ *  Streams: all work is enqueued on desc.stream (a cudaStream_t, 0 = legacy default).  Calls
+ *           that return statistics synchronise that stream.
+ *  Host buffers: hjb_step accepts host (pageable or pinned) pointers for U_prev/U/policy/psi
+ *           and stages them through device memory inside the call (used by the e2e benchmark).
+ *  Errors:  every call returns an hjb_status, never aborts; hjb_last_error() gives a message
+ *           (thread-local, valid until the next call on that thread).
+ *  Ownership: the handle and all workspaces (Krylov vectors, multigrid levels) are owned by the
+ *           library from hjb_grid_create until hjb_grid_destroy.  Caller arrays stay caller-owned;
+ *           hjb_set_coeffs RETAINS the device field pointers (not copied) until the next
+ *           hjb_set_coeffs or hjb_grid_destroy.
+ */
+#ifndef HJB_H
+#define HJB_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HJB_VERSION 1
+#define HJB_MAX_K 255
+#define HJB_MAX_Q 16
+#define HJB_MAX_PI_LOG 64
+
+typedef struct hjb_grid* hjb_grid_t;
+
+typedef enum {
+  HJB_OK = 0,
+  HJB_ERR_INVALID_ARG = 1,   /* null handle/pointer, d not in {2,3}, P > d, K not in [1,255],
+                                Q > 16, n < 3, hi <= lo, dt <= 0, dt*max(c) >= 1 */
+  HJB_ERR_UNSUPPORTED = 2,   /* multigrid on n != 2^l+1, nranks > 1 without NCCL support     */
+  HJB_ERR_STATE = 3,         /* apply/search/step before hjb_set_coeffs; solve before mg_setup */
+  HJB_ERR_OOM = 4,
+  HJB_ERR_CUDA = 5,
+  HJB_ERR_NCCL = 6,
+  HJB_ERR_NOT_CONVERGED = 7, /* Krylov or policy iteration hit max iterations; U holds the best iterate */
+  HJB_ERR_BREAKDOWN = 8,     /* BiCGSTAB rho or (r_hat, v) == 0 */
+  HJB_ERR_NONFINITE = 9      /* NaN/Inf in a residual */
+} hjb_status;
+
+const char* hjb_last_error(void);
+int32_t hjb_version(void);
+
+/* ------------------------------------------------------------------------------ grid */
+typedef struct {
+  int32_t dim;         /* d in {2,3}                                                          */
+  int32_t P;           /* columns of sigma, 1 <= P <= d                                       */
+  int32_t K;           /* number of discrete controls, 1..255 (policy stored as uint8)        */
+  int32_t Q;           /* number of source features f_feat, 0..16                             */
+  int64_t n;           /* nodes per dimension incl. boundary, >= 3                            */
+  double lo, hi;       /* Omega = [lo,hi]^d                                                   */
+  int32_t rank;        /* slab decomposition along the slowest axis: this rank ...           */
+  int32_t nranks;      /* ... of nranks (1 in this release; >1 returns HJB_ERR_UNSUPPORTED)  */
+  const void* nccl_id; /* reserved: ncclUniqueId when nranks > 1                              */
+  void* stream;        /* cudaStream_t                                                        */
+  int32_t device;      /* CUDA device ordinal                                                 */
+} hjb_grid_desc;
+
+typedef struct {
+  int64_t n;            /* nodes per dimension                                                */
+  int64_t row_elems;    /* elements per slab row = n^(d-1)                                    */
+  int64_t row0, row1;   /* owned rows [row0,row1) of the slowest axis (global indices)        */
+  int64_t halo;         /* halo rows held on each side (0 when nranks == 1)                   */
+  int64_t local_row0;   /* global row of local row 0 (= row0 - halo)                          */
+  int64_t local_rows;   /* rows in every grid array                                           */
+  int64_t local_elems;  /* local_rows * row_elems: length of every grid array                 */
+  int64_t n_interior;   /* interior unknowns owned by this rank                               */
+  int64_t n_boundary;   /* boundary nodes of the full grid (length of the packed psi array)   */
+  int32_t n_levels;     /* multigrid levels after hjb_mg_setup (0 before)                     */
+  double h, k;          /* mesh width and SL step k = sqrt(h)                   */
+} hjb_layout;
+
+/* Create a grid handle; allocates the Krylov workspace (about 10 grid arrays). */
+hjb_status hjb_grid_create(const hjb_grid_desc* desc, hjb_grid_t* out);
+hjb_status hjb_grid_query(hjb_grid_t g, hjb_layout* out);
+hjb_status hjb_grid_destroy(hjb_grid_t g);
+
+/* ------------------------------------------------------------------------ coefficients
+ * Affine-separable coefficient model (covers PAPER.md Problems A/B and every BASELINE config):
+ *   sigma^a_p(x) = sigma_scale[p](x) * sigma_dir[a][p][:] + sigma_node[p][:](x)
+ *   b^a(x)       = b_scale(x) * b_dir[a][:] + b_node[:](x)
+ *   c^a(x)       = c_node(x) + c_ctrl[a]            (dt * max c < 1 is required)
+ *   f^a(x)       = f_ctrl[a] + sum_q f_basis[a][q] * f_feat[q](x)
+ * Tables (sigma_dir [K][P][d], b_dir [K][d], c_ctrl [K], f_basis [K][Q], f_ctrl [K] or NULL)
+ * are HOST arrays, copied.  Fields are DEVICE grid arrays (plane stride = local_elems), NULL =
+ * absent (scales default to 1, offsets to 0); they are retained, not copied.  Only the owned
+ * entries of a field are read.                                                              */
+typedef struct {
+  const double* sigma_dir;
+  const double* b_dir;
+  const double* c_ctrl;
+  const double* f_basis;
+  const double* f_ctrl;
+  const double* sigma_scale; /* [P][local_elems] */
+  const double* sigma_node;  /* [P][d][local_elems] */
+  const double* b_scale;     /* [local_elems] */
+  const double* b_node;      /* [d][local_elems] */
+  const double* c_node;      /* [local_elems] */
+  const double* f_feat;      /* [Q][local_elems] */
+} hjb_coeffs;
+
+hjb_status hjb_set_coeffs(hjb_grid_t g, const hjb_coeffs* c);
+/* Replace only the (time-dependent) source tables f_basis [K][Q] and f_ctrl [K] (host). */
+hjb_status hjb_set_source(hjb_grid_t g, const double* f_basis, const double* f_ctrl);
+
+/* --------------------------------------------------------------------- policy improvement
+ * For every owned interior node j and every control a (in index order) evaluate
+ *   H^a_j(U) = L_hat^a[U](x_j) + c^a_j U_j + f^a_j          (eq. Lhat)
+ * and take the lowest-index argmin, which is the row-wise argmax of the positive-type residual
+ * max_a (A^a U - F^a)_j (derivation D1 in DESIGN.md).  Writes
+ *   policy[j] (in: previous policy, out: new), F[j] = U_prev_j + dt f^{policy_j}_j,
+ * and returns R = max_j |U_j - U_prev_j - dt min_a H^a_j| and the number of changed entries.
+ * U must hold psi on boundary nodes.  Non-interior entries of policy/F are not written.     */
+typedef struct {
+  int64_t changed;   /* nodes whose policy changed */
+  double R_max;      /* nonlinear residual max_j |max_a (A^a U - F^a)_j| */
+} hjb_pi_stats;
+
+hjb_status hjb_policy_update(hjb_grid_t g, double dt, const double* U, const double* U_prev,
+                             uint8_t* policy, double* F, hjb_pi_stats* out);
+
+/* ---------------------------------------------------------------- policy operator apply
+ * y = A^pi x matrix-free (theta = 1):
+ *   (A x)_j = x_j - dt [ sum_e w_e (I x(z_e) - x_j) + c^{pi_j}_j x_j ]   at interior nodes,
+ *   y_j = x_j at boundary nodes (identity rows).
+ * w_e = A_p/(2h), B_p/(2h) for the 2P truncated diffusion endpoints and 1/(mu_d h) for the drift
+ * endpoint.  x is read on the full local grid (boundary values as given).   */
+hjb_status hjb_apply(hjb_grid_t g, double dt, const uint8_t* policy, const double* x, double* y);
+
+/* ------------------------------------------------------------------------ multigrid
+ * Geometric multigrid for A^pi (NS: damped Jacobi smoother, full-weighting restriction,
+ * bilinear/trilinear prolongation, coarse operators REDISCRETISED from the injected policy;
+ * PAPER.md:932-937 is the paper's Galerkin variant).  Requires n = 2^l + 1.                   */
+typedef struct {
+  int32_t nu_pre, nu_post;   /* smoothing sweeps (default 2, 2)                               */
+  double omega;              /* Jacobi damping in (0,1] (default 1.0; Gershgorin-safe)        */
+  int32_t coarse_max_n;      /* coarsen while n > coarse_max_n (default 17 in 2D, 9 in 3D)   */
+  int32_t coarse_k_mode;     /* 0: coarse levels keep the fine SL step k (default);
+                                1: k_l = sqrt(h_l) (the scheme's own rule on each level)      */
+  int32_t max_levels;        /* cap on levels (default 32)                                     */
+} hjb_mg_params;
+
+void hjb_mg_params_default(int32_t dim, hjb_mg_params* out);
+hjb_status hjb_mg_setup(hjb_grid_t g, double dt, const uint8_t* policy, const hjb_mg_params* p);
+/* x = M^{-1} b: one V(nu_pre, nu_post) cycle from x = 0 (interior entries; boundary of x = 0). */
+hjb_status hjb_mg_apply(hjb_grid_t g, const double* b, double* x);
+
+/* --------------------------------------------------------------------------- solve
+ * Policy evaluation A^pi X = F: right-preconditioned BiCGSTAB with one
+ * V-cycle per preconditioner application, from x (in: initial guess with boundary = psi,
+ * out: solution), stopping at ||F - A X||_2 <= rtol ||F||_2 over interior rows (BJ cfg1).     */
+typedef struct {
+  double krylov_rtol;        /* 1e-12 */
+  int32_t krylov_maxit;      /* 2000 */
+  int32_t use_mg;            /* 1 = GMG preconditioner, 0 = none */
+  double tol_pi;             /* policy-iteration stop: R <= tol_pi (1e-10) */
+  int32_t max_pi;            /* 50 */
+  hjb_mg_params mg;
+} hjb_solve_params;
+
+typedef struct {
+  int32_t iters;             /* BiCGSTAB iterations */
+  double rres;               /* final true relative residual ||F - A X||_2 / ||F||_2 */
+  double rres_inf;           /* ||F - A X||_inf / ||F||_inf */
+} hjb_solve_stats;
+
+void hjb_solve_params_default(int32_t dim, hjb_solve_params* out);
+hjb_status hjb_solve(hjb_grid_t g, double dt, const uint8_t* policy, const double* F, double* x,
+                     const hjb_solve_params* p, hjb_solve_stats* out);
+
+/* ---------------------------------------------------------------------------- step
+ * One implicit Euler step t_{n-1} -> t_n = t_{n-1} + dt by policy iteration:
+ *   U <- U_prev with boundary entries psi(t_n) (psi_packed: the n_boundary boundary values in
+ *   lexicographic order; NULL keeps U's boundary entries), then repeat
+ *     policy improvement (hjb_policy_update) -> stop if it > 1 and (changed == 0 or R <= tol_pi)
+ *     -> mg setup -> BiCGSTAB solve of A^pi U = F^pi from the current U.
+ * The initial policy is the greedy policy at U_prev (reading iii).  f must already be
+ * at t_n (hjb_set_source).  policy may be NULL (internal buffer).  Pointers may be host.      */
+typedef struct {
+  int32_t pi_iters;                          /* policy evaluations (linear solves) performed */
+  int32_t krylov_iters_total;
+  int32_t krylov_iters[HJB_MAX_PI_LOG];      /* per policy iteration */
+  int64_t changed[HJB_MAX_PI_LOG];           /* policy changes seen by each search */
+  double R[HJB_MAX_PI_LOG];                  /* nonlinear residual seen by each search */
+  double final_R;
+  double final_rres;                         /* true relative residual of the last solve */
+  double ms_search, ms_setup, ms_solve;      /* device time per phase (CUDA events) */
+  int32_t n_levels;
+} hjb_step_stats;
+
+hjb_status hjb_step(hjb_grid_t g, double dt, const double* U_prev, double* U, uint8_t* policy,
+                    const double* psi_packed, const hjb_solve_params* p, hjb_step_stats* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HJB_H */

@@ -1,0 +1,558 @@
+// hjb_kernels.cuh -- __global__ kernels of the hot path (sm_100a, fp64).
+#pragma once
+#include "hjb_device.cuh"
+
+namespace hjb {
+
+// ================================================================== operator-family kernel
+enum OpMode : int {
+  OP_APPLY = 0,    // y = A x                    (+ optional dots with y)
+  OP_RESID = 1,    // y = b - A x                (+ optional dots)
+  OP_JACOBI = 2,   // y = x + omega (b - A x) / D
+  OP_JACOBI0 = 3,  // y = omega b / D            (x = 0; geometry only, no gathers)
+};
+
+// NDOT: 0, 1 -> partial[0] = sum y*u ; 2 -> partial[0] = sum y*u, partial[1] = sum y*y
+template <int D, int MODE, int NDOT>
+__global__ void __launch_bounds__(kThreads) k_operator(LevelDev L, CoefDev C, double dt, double omega,
+                                                      const uint8_t* __restrict__ pol,
+                                                      const double* __restrict__ x,
+                                                      const double* __restrict__ b, double* __restrict__ y,
+                                                      const double* __restrict__ u, double* partial) {
+  constexpr bool GATHER = (MODE != OP_JACOBI0);
+  constexpr bool SELF = (MODE == OP_JACOBI || MODE == OP_JACOBI0);
+  double dots[2] = {0.0, 0.0};
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < L.n_own; t += stride) {
+    NodeCtx<D> nd;
+    node_from_interior<D>(L, t, nd);
+    load_fields<D>(C, nd);
+    const int a = pol[nd.loc];
+    double acc, wsum, self;
+    row_eval<D, GATHER, SELF>(L, C, nd, a, x, acc, wsum, self);
+    const double c = nd.cn + __ldg(C.c_ctrl + a);
+    double out;
+    if (MODE == OP_JACOBI0) {
+      const double diag = 1.0 + dt * (wsum - self - c);
+      out = omega * __ldg(b + nd.loc) / diag;
+    } else {
+      const double xj = __ldg(x + nd.loc);
+      const double Ax = xj - dt * (acc - wsum * xj + c * xj);
+      if (MODE == OP_APPLY) {
+        out = Ax;
+      } else if (MODE == OP_RESID) {
+        out = __ldg(b + nd.loc) - Ax;
+      } else {
+        const double diag = 1.0 + dt * (wsum - self - c);
+        out = xj + omega * (__ldg(b + nd.loc) - Ax) / diag;
+      }
+    }
+    y[nd.loc] = out;
+    if (NDOT >= 1) dots[0] = fma(out, __ldg(u + nd.loc), dots[0]);
+    if (NDOT >= 2) dots[1] = fma(out, out, dots[1]);
+  }
+  if (NDOT > 0) block_reduce_store<2>(dots, partial);
+}
+
+// ================================================================== control search
+// For every owned interior node: H^a = acc_a - wsum_a U_j + c^a U_j + f^a for all a (lowest-index
+// argmin), policy/F outputs, partials: [max R, changed count].
+template <int D>
+__global__ void __launch_bounds__(kThreads) k_search(LevelDev L, CoefDev C, double dt,
+                                                    const double* __restrict__ U,
+                                                    const double* __restrict__ Uprev,
+                                                    uint8_t* __restrict__ pol, double* __restrict__ F,
+                                                    double* partial) {
+  double red[2] = {0.0, 0.0};
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < L.n_own; t += stride) {
+    NodeCtx<D> nd;
+    node_from_interior<D>(L, t, nd);
+    load_fields<D>(C, nd);
+    double feat[kMaxQ];
+#pragma unroll
+    for (int q = 0; q < kMaxQ; ++q) feat[q] = (q < C.Q) ? __ldg(C.f_feat + q * C.ld + nd.loc) : 0.0;
+    const double Uj = __ldg(U + nd.loc);
+    double best = INFINITY, fbest = 0.0;
+    int arg = 0;
+    for (int a = 0; a < C.K; ++a) {
+      double acc, wsum, self;
+      row_eval<D, true, false>(L, C, nd, a, U, acc, wsum, self);
+      double f = __ldg(C.f_ctrl + a);
+      const double* fb = C.f_basis + (int64_t)a * C.Q;
+#pragma unroll
+      for (int q = 0; q < kMaxQ; ++q)
+        if (q < C.Q) f = fma(__ldg(fb + q), feat[q], f);
+      const double c = nd.cn + __ldg(C.c_ctrl + a);
+      const double H = (acc - wsum * Uj) + c * Uj + f;
+      if (H < best) {  // strict: lowest index wins exact ties (reading iv)
+        best = H;
+        arg = a;
+        fbest = f;
+      }
+    }
+    const double Up = __ldg(Uprev + nd.loc);
+    const double R = fabs(Uj - Up - dt * best);
+    const int old = pol[nd.loc];
+    pol[nd.loc] = (uint8_t)arg;
+    F[nd.loc] = fma(dt, fbest, Up);
+    red[0] = fmax(red[0], (R == R) ? R : INFINITY);  // NaN -> inf (reported NONFINITE)
+    red[1] += (old != arg) ? 1.0 : 0.0;
+  }
+  block_reduce_store<2>(red, partial, 0x1u);
+}
+
+// ================================================================== Krylov vector kernels
+// Device-resident BiCGSTAB scalars (right preconditioning).
+struct KScal {
+  double rho, rho_old, alpha, omega;
+  double rhat_v, ts, tt, rr, ss;
+  double bnorm2;
+  int breakdown;
+};
+
+enum ScalOp : int { SC_NONE = 0, SC_INIT = 1, SC_AFTER_V = 2, SC_AFTER_T = 3, SC_AFTER_R = 4 };
+
+__device__ __forceinline__ void scal_update(KScal* S, const double* red, int which) {
+  if (which == SC_INIT) {          // red[0] = (r,r)
+    S->rho = red[0]; S->rho_old = 1.0; S->alpha = 1.0; S->omega = 1.0; S->rr = red[0]; S->breakdown = 0;
+  } else if (which == SC_AFTER_V) {  // red[0] = (rhat, v)
+    S->rhat_v = red[0];
+    if (red[0] == 0.0 || !(red[0] == red[0])) S->breakdown = 1;
+    S->alpha = S->rho / red[0];
+  } else if (which == SC_AFTER_T) {  // red = [(t,s), (t,t)]
+    S->ts = red[0]; S->tt = red[1];
+    S->omega = (red[1] > 0.0) ? red[0] / red[1] : 0.0;
+    if (S->omega == 0.0) S->breakdown = 2;
+  } else if (which == SC_AFTER_R) {  // red = [(rhat,r), (r,r)]
+    S->rho_old = S->rho; S->rho = red[0]; S->rr = red[1];
+    if (red[0] == 0.0 || !(red[1] == red[1])) S->breakdown = 3;
+  }
+}
+
+// fixed-order deterministic reduction of nblk x 2 partials by one block (bit k of maxmask: max),
+// then the BiCGSTAB scalar update `which` (no host round trip).
+__global__ void __launch_bounds__(1024) k_finalize(const double* __restrict__ partial, int nblk, double* out,
+                                                 unsigned maxmask, KScal* S, int which) {
+  __shared__ double sm[2][1024];
+  double v[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const bool mx = (maxmask >> k) & 1u;
+    v[k] = mx ? -INFINITY : 0.0;
+    for (int i = threadIdx.x; i < nblk; i += blockDim.x) {
+      const double q = partial[i * 2 + k];
+      v[k] = mx ? fmax(v[k], q) : v[k] + q;
+    }
+    sm[k][threadIdx.x] = v[k];
+  }
+  __syncthreads();
+  for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+    if (threadIdx.x < st) {
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const bool mx = (maxmask >> k) & 1u;
+        sm[k][threadIdx.x] = mx ? fmax(sm[k][threadIdx.x], sm[k][threadIdx.x + st]) : sm[k][threadIdx.x] + sm[k][threadIdx.x + st];
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double red[2] = {sm[0][0], sm[1][0]};
+    out[0] = red[0];
+    out[1] = red[1];
+    if (which != SC_NONE) scal_update(S, red, which);
+  }
+}
+
+// interior-node iteration helper for vector kernels
+template <int D>
+__device__ __forceinline__ int64_t interior_loc(const LevelDev& L, int64_t t) {
+  const int64_t nI = L.nI;
+  if (D == 2) {
+    const int64_t r = t / nI;
+    return (L.row_first + r - L.local_row0) * L.n + 1 + (t - r * nI);
+  } else {
+    const int64_t r = t / nI;
+    const int64_t r2 = r / nI;
+    return ((L.row_first + r2 - L.local_row0) * L.n + 1 + (r - r2 * nI)) * L.n + 1 + (t - r * nI);
+  }
+}
+
+// r_hat = r, p = r ; partial: (r,r)
+template <int D>
+__global__ void __launch_bounds__(kThreads) k_bicg_init(LevelDev L, const double* __restrict__ r,
+                                                       double* __restrict__ rhat, double* __restrict__ p,
+                                                       double* partial) {
+  double red[2] = {0.0, 0.0};
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < L.n_own; t += stride) {
+    const int64_t j = interior_loc<D>(L, t);
+    const double v = r[j];
+    rhat[j] = v;
+    p[j] = v;
+    red[0] = fma(v, v, red[0]);
+  }
+  block_reduce_store<2>(red, partial);
+}
+
+// p = r + beta (p - omega v),  beta = (rho/rho_old)(alpha/omega)
+template <int D>
+__global__ void __launch_bounds__(kThreads) k_bicg_p(LevelDev L, const KScal* __restrict__ S,
+                                                    const double* __restrict__ r, double* __restrict__ p,
+                                                    const double* __restrict__ v) {
+  const double beta = (S->rho / S->rho_old) * (S->alpha / S->omega);
+  const double om = S->omega;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < L.n_own; t += stride) {
+    const int64_t j = interior_loc<D>(L, t);
+    p[j] = fma(beta, fma(-om, v[j], p[j]), r[j]);
+  }
+}
+
+// s = r - alpha v ; partial (s,s)
+template <int D>
+__global__ void __launch_bounds__(kThreads) k_bicg_s(LevelDev L, const KScal* __restrict__ S,
+                                                    const double* __restrict__ r, const double* __restrict__ v,
+                                                    double* __restrict__ s, double* partial) {
+  const double al = S->alpha;
+  double red[2] = {0.0, 0.0};
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < L.n_own; t += stride) {
+    const int64_t j = interior_loc<D>(L, t);
+    const double sv = fma(-al, v[j], r[j]);
+    s[j] = sv;
+    red[0] = fma(sv, sv, red[0]);
+  }
+  block_reduce_store<2>(red, partial);
+}
+
+// x += alpha phat + omega shat ; r = s - omega t ; partials (rhat, r), (r, r)
+template <int D>
+__global__ void __launch_bounds__(kThreads) k_bicg_x(LevelDev L, const KScal* __restrict__ S,
+                                                    double* __restrict__ x, const double* __restrict__ phat,
+                                                    const double* __restrict__ shat,
+                                                    const double* __restrict__ s, const double* __restrict__ tv,
+                                                    double* __restrict__ r, const double* __restrict__ rhat,
+                                                    double* partial) {
+  const double al = S->alpha, om = S->omega;
+  double red[2] = {0.0, 0.0};
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < L.n_own; t += stride) {
+    const int64_t j = interior_loc<D>(L, t);
+    x[j] = fma(om, shat[j], fma(al, phat[j], x[j]));
+    const double rv = fma(-om, tv[j], s[j]);
+    r[j] = rv;
+    red[0] = fma(rhat[j], rv, red[0]);
+    red[1] = fma(rv, rv, red[1]);
+  }
+  block_reduce_store<2>(red, partial);
+}
+
+// squared 2-norm and max-norm partials of a vector over owned interior nodes
+template <int D>
+__global__ void __launch_bounds__(kThreads) k_norms(LevelDev L, const double* __restrict__ v, double* partial) {
+  double red[2] = {0.0, 0.0};
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < L.n_own; t += stride) {
+    const double a = v[interior_loc<D>(L, t)];
+    red[0] = fma(a, a, red[0]);
+    red[1] = fmax(red[1], (a == a) ? fabs(a) : INFINITY);
+  }
+  block_reduce_store<2>(red, partial, 0x2u);
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads) k_copy_interior(LevelDev L, const double* __restrict__ a,
+                                                           double* __restrict__ b) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < L.n_own; t += stride) {
+    const int64_t j = interior_loc<D>(L, t);
+    b[j] = a[j];
+  }
+}
+
+// ================================================================== boundary data
+// scatter the packed boundary values (lexicographic order of boundary nodes) into U
+template <int D>
+__global__ void k_scatter_psi(LevelDev L, int64_t nb, const double* __restrict__ psi, double* __restrict__ U) {
+  const int64_t n = L.n;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nb; q += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i[3] = {0, 0, 0};
+    if (D == 2) {
+      if (q < n) { i[0] = q; i[1] = 0; }
+      else if (q < n + 2 * (n - 2)) { const int64_t r = q - n; i[1] = 1 + r / 2; i[0] = (r & 1) ? n - 1 : 0; }
+      else { i[1] = n - 1; i[0] = q - n - 2 * (n - 2); }
+    } else {
+      const int64_t plane = n * n, ring = 4 * n - 4;
+      if (q < plane) { i[2] = 0; i[1] = q / n; i[0] = q % n; }
+      else if (q < plane + (n - 2) * ring) {
+        const int64_t r = q - plane;
+        i[2] = 1 + r / ring;
+        const int64_t w = r % ring;
+        if (w < n) { i[1] = 0; i[0] = w; }
+        else if (w < n + 2 * (n - 2)) { const int64_t v = w - n; i[1] = 1 + v / 2; i[0] = (v & 1) ? n - 1 : 0; }
+        else { i[1] = n - 1; i[0] = w - n - 2 * (n - 2); }
+      } else {
+        const int64_t r = q - plane - (n - 2) * ring;
+        i[2] = n - 1; i[1] = r / n; i[0] = r % n;
+      }
+    }
+    const int64_t slow = i[D - 1];
+    if (slow < L.local_row0 || slow >= L.local_row0 + L.local_rows) continue;
+    int64_t loc = (slow - L.local_row0);
+    for (int d = D - 2; d >= 0; --d) loc = loc * n + i[d];
+    U[loc] = psi[q];
+  }
+}
+
+// ================================================================== multigrid transfers
+// full weighting r_f -> b_c at coarse interior nodes (weights 1/4,1/2,1/4 per dim)
+template <int D>
+__global__ void __launch_bounds__(kThreads) k_restrict(LevelDev Lf, LevelDev Lc, const double* __restrict__ rf,
+                                                      double* __restrict__ bc) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < Lc.n_own; t += stride) {
+    NodeCtx<D> nd;
+    node_from_interior<D>(Lc, t, nd);
+    double acc = 0.0;
+    if (D == 2) {
+      const int64_t base = (int64_t)(2 * nd.i[1] - Lf.local_row0) * Lf.n + 2 * nd.i[0];
+#pragma unroll
+      for (int o2 = -1; o2 <= 1; ++o2) {
+        const double w2 = o2 == 0 ? 0.5 : 0.25;
+#pragma unroll
+        for (int o1 = -1; o1 <= 1; ++o1) {
+          const double w1 = o1 == 0 ? 0.5 : 0.25;
+          acc = fma(w1 * w2, __ldg(rf + base + o2 * Lf.n + o1), acc);
+        }
+      }
+    } else {
+      const int64_t nf = Lf.n;
+      const int64_t base = ((int64_t)(2 * nd.i[2] - Lf.local_row0) * nf + 2 * nd.i[1]) * nf + 2 * nd.i[0];
+#pragma unroll
+      for (int o3 = -1; o3 <= 1; ++o3) {
+        const double w3 = o3 == 0 ? 0.5 : 0.25;
+#pragma unroll
+        for (int o2 = -1; o2 <= 1; ++o2) {
+          const double w2 = o2 == 0 ? 0.5 : 0.25;
+#pragma unroll
+          for (int o1 = -1; o1 <= 1; ++o1) {
+            const double w1 = o1 == 0 ? 0.5 : 0.25;
+            acc = fma(w1 * w2 * w3, __ldg(rf + base + (o3 * nf + o2) * nf + o1), acc);
+          }
+        }
+      }
+    }
+    bc[nd.loc] = acc;
+  }
+}
+
+// x_f += P e_c (multilinear prolongation) at fine interior nodes
+template <int D>
+__global__ void __launch_bounds__(kThreads) k_prolong_add(LevelDev Lf, LevelDev Lc, const double* __restrict__ ec,
+                                                         double* __restrict__ xf) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < Lf.n_own; t += stride) {
+    NodeCtx<D> nd;
+    node_from_interior<D>(Lf, t, nd);
+    int c0[D], c1[D];
+    double w1[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      c0[d] = nd.i[d] >> 1;
+      const bool odd = nd.i[d] & 1;
+      c1[d] = odd ? c0[d] + 1 : c0[d];
+      w1[d] = odd ? 0.5 : 0.0;
+    }
+    double acc = 0.0;
+    const int64_t nc = Lc.n;
+#pragma unroll
+    for (int m = 0; m < (1 << D); ++m) {
+      double w = 1.0;
+      int cc[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        const bool hi = (m >> d) & 1;
+        cc[d] = hi ? c1[d] : c0[d];
+        w *= hi ? w1[d] : (1.0 - w1[d]);
+      }
+      if (w == 0.0) continue;
+      int64_t loc = (int64_t)(cc[D - 1] - Lc.local_row0);
+#pragma unroll
+      for (int d = D - 2; d >= 0; --d) loc = loc * nc + cc[d];
+      acc = fma(w, __ldg(ec + loc), acc);
+    }
+    xf[nd.loc] += acc;
+  }
+}
+
+// inject the policy from level f to level c (coarse node J <- fine node 2J), all local coarse nodes
+template <int D>
+__global__ void k_inject_u8(LevelDev Lf, LevelDev Lc, const uint8_t* __restrict__ pf, uint8_t* __restrict__ pc) {
+  const int64_t nloc = Lc.local_rows * Lc.row_elems;
+  const int64_t nc = Lc.n, nf = Lf.n;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nloc; q += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i[3];
+    int64_t r = q;
+#pragma unroll
+    for (int d = 0; d < D - 1; ++d) { i[d] = r % nc; r /= nc; }
+    const int64_t fr = 2 * (r + Lc.local_row0) - Lf.local_row0;
+    if (fr < 0 || fr >= Lf.local_rows) continue;
+    int64_t loc = fr;
+#pragma unroll
+    for (int d = D - 2; d >= 0; --d) loc = loc * nf + 2 * i[d];
+    pc[q] = pf[loc];
+  }
+}
+
+// inject nplanes fp64 field planes (plane strides ldf / ldc)
+template <int D>
+__global__ void k_inject_f64(LevelDev Lf, LevelDev Lc, const double* __restrict__ ff, int64_t ldf,
+                             double* __restrict__ fc, int64_t ldc, int nplanes) {
+  const int64_t nloc = Lc.local_rows * Lc.row_elems;
+  const int64_t nc = Lc.n, nf = Lf.n;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nloc; q += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i[3];
+    int64_t r = q;
+#pragma unroll
+    for (int d = 0; d < D - 1; ++d) { i[d] = r % nc; r /= nc; }
+    const int64_t fr = 2 * (r + Lc.local_row0) - Lf.local_row0;
+    if (fr < 0 || fr >= Lf.local_rows) continue;
+    int64_t loc = fr;
+#pragma unroll
+    for (int d = D - 2; d >= 0; --d) loc = loc * nf + 2 * i[d];
+    for (int k = 0; k < nplanes; ++k) fc[k * ldc + q] = ff[k * ldf + loc];
+  }
+}
+
+// ================================================================== coarsest level (dense)
+// assemble the dense interior matrix of the coarsest level: A[j][i] (row-major, Nc x Nc)
+template <int D>
+__global__ void k_coarse_assemble(LevelDev L, CoefDev C, double dt, const uint8_t* __restrict__ pol,
+                                  double* __restrict__ A) {
+  const int64_t Nc = L.n_own;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < Nc; t += (int64_t)gridDim.x * blockDim.x) {
+    NodeCtx<D> nd;
+    node_from_interior<D>(L, t, nd);
+    load_fields<D>(C, nd);
+    const int a = pol[nd.loc];
+    double* row = A + t * Nc;
+    double wsum = 0.0;
+    const int nI = L.nI;
+    // visit every endpoint tap: emulate row_eval with explicit taps
+    auto add_tap = [&](const double* z, double w) {
+      int c[D];
+      double s[D];
+      cell_of<D>(L, z, c, s);
+#pragma unroll
+      for (int m = 0; m < (1 << D); ++m) {
+        double ww = w;
+        int64_t col = 0;
+        bool interior = true;
+#pragma unroll
+        for (int d = D - 1; d >= 0; --d) {
+          const bool hi = (m >> d) & 1;
+          const int id = c[d] + (hi ? 1 : 0);
+          ww *= hi ? s[d] : (1.0 - s[d]);
+          interior &= (id >= 1 && id <= L.n - 2);
+          col = col * nI + (id - 1);
+        }
+        if (interior && ww != 0.0) row[col] -= dt * ww;
+      }
+    };
+    const double* sd = C.sigma_dir + (int64_t)a * C.P * D;
+    for (int p = 0; p < C.P; ++p) {
+      double y[D], ym[D];
+      bool nz = false;
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        y[d] = L.k * fma(nd.sc[p], sd[p * D + d], nd.sn[p][d]);
+        ym[d] = -y[d];
+        nz |= (y[d] != 0.0);
+      }
+      if (!nz) continue;
+      int bp, bm;
+      const double mup = ray_mu<D>(L, nd.x, y, bp);
+      const double mum = ray_mu<D>(L, nd.x, ym, bm);
+      double Aw = 1.0, Bw = 1.0;
+      if (bp >= 0 || bm >= 0) {
+        const double sum = mup + mum;
+        Aw = 2.0 / (mup * sum);
+        Bw = 2.0 / (mum * sum);
+      }
+      double zp[D], zm[D];
+      endpoint<D>(L, nd.x, y, mup, bp, zp);
+      endpoint<D>(L, nd.x, y, -mum, bm, zm);
+      wsum += (Aw + Bw) * L.inv_2k2;
+      add_tap(zp, Aw * L.inv_2k2);
+      add_tap(zm, Bw * L.inv_2k2);
+    }
+    {
+      double y[D];
+      bool nz = false;
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        y[d] = L.k2 * fma(nd.bs, C.b_dir[a * D + d], nd.bn[d]);
+        nz |= (y[d] != 0.0);
+      }
+      if (nz) {
+        int bdim;
+        const double mu = ray_mu<D>(L, nd.x, y, bdim);
+        double z[D];
+        endpoint<D>(L, nd.x, y, mu, bdim, z);
+        const double w = (bdim >= 0) ? L.inv_k2 / mu : L.inv_k2;
+        wsum += w;
+        add_tap(z, w);
+      }
+    }
+    const double c = nd.cn + C.c_ctrl[a];
+    row[t] += 1.0 + dt * (wsum - c);
+  }
+}
+
+// in-place Gauss-Jordan inverse (no pivoting: the interior matrix is strictly row diagonally
+// dominant, row sums >= 1 - dt c > 0), single block, matrix in shared memory (Nc <= 160).
+__global__ void k_coarse_invert(double* __restrict__ A, int Nc) {
+  extern __shared__ double M[];
+  __shared__ double colk[160];
+  const int NN = Nc * Nc;
+  for (int e = threadIdx.x; e < NN; e += blockDim.x) M[e] = A[e];
+  __syncthreads();
+  for (int k = 0; k < Nc; ++k) {
+    const double piv = M[k * Nc + k];
+    __syncthreads();
+    for (int j = threadIdx.x; j < Nc; j += blockDim.x) {
+      const double v = (j == k) ? 1.0 : M[k * Nc + j];
+      M[k * Nc + j] = v / piv;
+    }
+    for (int i = threadIdx.x; i < Nc; i += blockDim.x) colk[i] = (i == k) ? 0.0 : M[i * Nc + k];
+    __syncthreads();
+    for (int e = threadIdx.x; e < NN; e += blockDim.x) {
+      const int i = e / Nc, j = e - i * Nc;
+      if (i == k) continue;
+      const double base = (j == k) ? 0.0 : M[e];
+      M[e] = fma(-colk[i], M[k * Nc + j], base);
+    }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < NN; e += blockDim.x) A[e] = M[e];
+}
+
+// x_c = Ainv b_c on the coarsest interior
+template <int D>
+__global__ void k_coarse_solve(LevelDev L, const double* __restrict__ Ainv, const double* __restrict__ b,
+                               double* __restrict__ x) {
+  extern __shared__ double bs[];
+  const int Nc = (int)L.n_own;
+  for (int t = threadIdx.x; t < Nc; t += blockDim.x) bs[t] = b[interior_loc<D>(L, t)];
+  __syncthreads();
+  for (int t = threadIdx.x; t < Nc; t += blockDim.x) {
+    double acc = 0.0;
+    const double* row = Ainv + (int64_t)t * Nc;
+    for (int i = 0; i < Nc; ++i) acc = fma(row[i], bs[i], acc);
+    x[interior_loc<D>(L, t)] = acc;
+  }
+}
+
+}  // namespace hjb

@@ -114,10 +114,17 @@ class Problem:
             b = b | (i == 0) | (i == self.n - 1)
         return b
 
-    def boundary_idx(self, xp=np, device=None):
+    def boundary_idx(self):
         """Boundary node flat indices in lexicographic order (the packed psi layout of hjb.h)."""
-        idx = self.all_idx(xp, device)
-        return idx[self.is_boundary(idx)]
+        n = self.n
+        full = np.arange(n, dtype=np.int64)
+        ring = np.concatenate([full, (np.arange(1, n - 1, dtype=np.int64)[:, None] * n
+                                      + np.array([0, n - 1])).ravel(), (n - 1) * n + full])
+        if self.d == 2:
+            return ring
+        plane = np.arange(n * n, dtype=np.int64)
+        mid = (np.arange(1, n - 1, dtype=np.int64)[:, None] * n * n + ring[None, :]).ravel()
+        return np.concatenate([plane, mid, (n - 1) * n * n + plane])
 
     # ---------------------------------------------------------------- data
     def fields(self, idx):

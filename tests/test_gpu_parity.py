@@ -1,0 +1,206 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle on the same seeded inputs.
+
+Tolerances (BASELINE.json north_star):
+  operator apply    |y_gpu - y_orc| <= 1e-12 * (|A||x|)_j   row-wise (reading xvi)
+  policy            identical except at near-ties (H gap <= 1e-12 S_j, reading iv)
+  solution          ||U_gpu - U_orc||_inf <= 1e-8 ||u||_inf, both solved to rel. residual <= 1e-12
+"""
+import numpy as np
+import pytest
+
+from gpu_util import require_gpu, row_scale, setup, to_dev
+from oracle.howard import control_search, howard_step
+from oracle.scheme import Geometry, apply_operator
+from oracle.system import assemble, solve
+from synth import bj_config, problem_A, problem_B, random_vector
+
+pytestmark = pytest.mark.gpu
+
+CASES = [
+    ("cfg0", lambda: bj_config(0)),
+    ("cfg1", lambda: bj_config(1)),
+    ("cfg2_129", lambda: bj_config(2, n=129)),
+    ("cfg2_ragged_100", lambda: bj_config(2, n=100, K=7)),
+    ("cfg3_17", lambda: bj_config(3, n=17)),
+    ("cfg3_ragged_12", lambda: bj_config(3, n=12, )),
+    ("probA_41", lambda: problem_A(41)),
+    ("probB_41", lambda: problem_B(41)),
+]
+
+
+def _random_policy(p, seed=7):
+    return np.random.default_rng(seed).integers(0, p.K, size=p.N).astype(np.uint8)
+
+
+@pytest.mark.parametrize("name,mk", CASES, ids=[c[0] for c in CASES])
+def test_apply_parity(name, mk):
+    torch = require_gpu()
+    p = mk()
+    g, fields = setup(p)
+    pol = _random_policy(p)
+    x = random_vector(p)                                  # seed 43, U[-1,1], boundary included
+    dt = p.dt
+    y = torch.empty(p.N, dtype=torch.float64, device="cuda")
+    g.apply(dt, to_dev(pol, torch), to_dev(x, torch), y)
+    torch.cuda.synchronize()
+    yg = y.cpu().numpy()
+    geo = Geometry.of(p)
+    inter = geo.interior_idx()
+    yo = apply_operator(p, pol.astype(np.int64), x, dt)
+    scale = row_scale(p, pol.astype(np.int64), x, dt, inter)
+    err = np.abs(yg[inter] - yo) / scale
+    assert err.max() <= 1e-12, (name, err.max())
+    bnd = np.ones(p.N, bool)
+    bnd[inter] = False
+    assert np.array_equal(yg[bnd], x[bnd])               # identity Dirichlet rows
+
+
+@pytest.mark.parametrize("name,mk", CASES, ids=[c[0] for c in CASES])
+def test_policy_update_parity(name, mk):
+    torch = require_gpu()
+    p = mk()
+    g, fields = setup(p)
+    rng = np.random.default_rng(11)
+    Uprev = p.g(p.all_idx())
+    U = Uprev + 0.05 * rng.uniform(-1, 1, size=p.N)
+    dt = p.dt
+    pol = torch.zeros(p.N, dtype=torch.uint8, device="cuda")
+    F = torch.zeros(p.N, dtype=torch.float64, device="cuda")
+    st = g.policy_update(dt, to_dev(U, torch), to_dev(Uprev, torch), pol, F)
+    torch.cuda.synchronize()
+    sr = control_search(p, U, Uprev, dt, dt)
+    inter = Geometry.of(p).interior_idx()
+    pg = pol.cpu().numpy()[inter].astype(np.int64)
+    Fg = F.cpu().numpy()[inter]
+    decisive = sr.ties == 1
+    assert np.array_equal(pg[decisive], sr.policy[decisive]), (name, np.sum(pg[decisive] != sr.policy[decisive]))
+    # everywhere: the GPU's control is within the near-tie window of the oracle's minimum
+    from oracle.howard import hamiltonian
+    Hg, _, _ = hamiltonian(p, inter, pg, U, dt, p.fields(inter))
+    assert np.all(Hg - sr.H <= 1e-12 * sr.scale), (name, np.max((Hg - sr.H) / sr.scale))
+    fo = (sr.F - Uprev[inter]) / dt                     # f at the oracle's choice
+    _, _, fg = hamiltonian(p, inter, pg, U, dt, p.fields(inter))
+    assert np.abs(Fg - (Uprev[inter] + dt * fg)).max() <= 1e-12 * max(1.0, np.abs(sr.F).max())
+    assert np.abs(Fg[decisive] - sr.F[decisive]).max(initial=0.0) <= 1e-12 * max(1.0, np.abs(sr.F).max())
+    assert abs(st["R_max"] - sr.R.max()) <= 1e-11 * max(1.0, sr.scale.max() * dt)
+    del fo
+
+
+def _gpu_march(p, n_steps=None, **kw):
+    torch = require_gpu()
+    g, fields = setup(p)
+    U = to_dev(p.g(p.all_idx()), torch)
+    U2 = torch.empty_like(U)
+    pol = torch.zeros(p.N, dtype=torch.uint8, device="cuda")
+    n_steps = n_steps or p.n_steps
+    stats = []
+    for s in range(1, n_steps + 1):
+        t = s * p.dt
+        fb, fc = p.f_tables(t)
+        g.set_source(fb, fc)
+        psi = to_dev(p.psi(t, p.boundary_idx()), torch)
+        st = g.step(p.dt, U, U2, pol, psi, **kw)
+        stats.append(st)
+        U, U2 = U2, U
+    torch.cuda.synchronize()
+    return U.cpu().numpy(), pol.cpu().numpy(), stats
+
+
+@pytest.mark.parametrize("name,mk,steps", [
+    ("cfg0_full_march", lambda: bj_config(0), None),
+    ("probA_41", lambda: problem_A(41), None),
+    ("probB_41", lambda: problem_B(41), None),
+    ("cfg2_129_2steps", lambda: bj_config(2, n=129), 2),
+    ("cfg3_17_2steps", lambda: bj_config(3, n=17), 2),
+])
+def test_step_parity(name, mk, steps):
+    p = mk()
+    Ug, polg, stats = _gpu_march(p, steps)
+    Uo = p.g(p.all_idx())
+    for s in range(1, (steps or p.n_steps) + 1):
+        Uo, polo, _ = howard_step(p, Uo, s * p.dt, p.dt)
+    scale = max(1.0, np.abs(Uo).max())
+    err = np.abs(Ug - Uo).max() / scale
+    assert err <= 1e-8, (name, err, stats[-1])
+    for st in stats:
+        assert st["final_rres"] <= 1e-12
+
+
+def test_step_parity_cfg1_first_step():
+    p = bj_config(1)
+    Ug, polg, stats = _gpu_march(p, 1)
+    Uo, polo, _ = howard_step(p, p.g(p.all_idx()), p.dt, p.dt)
+    err = np.abs(Ug - Uo).max() / max(1.0, np.abs(Uo).max())
+    assert err <= 1e-8, (err, stats)
+
+
+def test_solve_parity_fixed_policy():
+    """Policy evaluation alone: GPU BiCGSTAB+GMG vs SuperLU on the same A^pi, F^pi."""
+    torch = require_gpu()
+    p = bj_config(2, n=129)
+    g, fields = setup(p)
+    dt = p.dt
+    U0 = p.g(p.all_idx())
+    sr = control_search(p, U0, U0, dt, dt)
+    inter = Geometry.of(p).interior_idx()
+    pol = np.zeros(p.N, dtype=np.int64)
+    pol[inter] = sr.policy
+    psi = np.zeros(p.N)
+    b = p.boundary_idx()
+    psi[b] = U0[b]
+    sysm = assemble(p, pol, dt, dt, U0, psi)
+    X, _ = solve(sysm)
+    Fd = torch.zeros(p.N, dtype=torch.float64, device="cuda")
+    Fd[torch.from_numpy(inter).cuda()] = torch.from_numpy(sr.F).cuda()
+    pold = to_dev(pol.astype(np.uint8), torch)
+    x = to_dev(U0, torch)
+    g.mg_setup(dt, pold)
+    st = g.solve(dt, pold, Fd, x)
+    xg = x.cpu().numpy()
+    assert st["rres"] <= 1e-12
+    assert np.abs(xg[inter] - X).max() <= 1e-8 * max(1.0, np.abs(X).max())
+    # unpreconditioned BiCGSTAB reaches the same solution (MG only changes the iteration count)
+    x2 = to_dev(U0, torch)
+    st2 = g.solve(dt, pold, Fd, x2, use_mg=0, krylov_maxit=20000)
+    assert np.abs(x2.cpu().numpy()[inter] - X).max() <= 1e-8 * max(1.0, np.abs(X).max())
+    assert st["iters"] < st2["iters"]
+
+
+def test_host_pointer_step_matches_device():
+    """e2e path: hjb_step with host (numpy) buffers gives bitwise the same result."""
+    torch = require_gpu()
+    p = bj_config(0)
+    g, fields = setup(p)
+    U0 = p.g(p.all_idx())
+    psi = p.psi(p.dt, p.boundary_idx())
+    Ud = torch.empty(p.N, dtype=torch.float64, device="cuda")
+    g.step(p.dt, to_dev(U0, torch), Ud, None, to_dev(psi, torch))
+    Uh = np.zeros(p.N)
+    polh = np.zeros(p.N, dtype=np.uint8)
+    g.step(p.dt, U0.copy(), Uh, polh, psi.copy())
+    assert np.array_equal(Uh, Ud.cpu().numpy())
+
+
+def test_edge_cases():
+    torch = require_gpu()
+    # single control -> exactly one policy evaluation
+    p = bj_config(0, K=1)
+    _, _, stats = _gpu_march(p, 1)
+    assert stats[0]["pi_iters"] == 1 and stats[0]["changed"][1] == 0
+    # smallest grid: one interior node (no multigrid possible below)
+    p = bj_config(0, n=3)
+    Ug, _, _ = _gpu_march(p, 1, use_mg=0)
+    Uo, _, _ = howard_step(p, p.g(p.all_idx()), p.dt, p.dt)
+    assert np.abs(Ug - Uo).max() <= 1e-12
+    # n != 2^l + 1 -> multigrid unsupported, the error is reported, not a crash
+    from paper_1605_04821_b200 import HJBError
+    p = bj_config(2, n=100, K=7)
+    g, _ = setup(p)
+    with pytest.raises(HJBError):
+        g.mg_setup(p.dt, torch.zeros(p.N, dtype=torch.uint8, device="cuda"))
+    # invalid arguments are rejected with a code
+    from paper_1605_04821_b200 import HJBGrid
+    with pytest.raises(HJBError):
+        HJBGrid(4, 1, 1, 0, 9, -1.0, 1.0)
+    with pytest.raises(HJBError):
+        HJBGrid(2, 1, 300, 0, 9, -1.0, 1.0)
