@@ -1,0 +1,390 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path: implicit semi-Lagrangian HJB steps (arXiv:1605.04821) on B200.
+
+One "step" = one implicit Euler step t_{n-1} -> t_n solved by policy iteration through the C-ABI
+(`hjb_step`: control search + GMG-preconditioned BiCGSTAB per policy iteration), i.e. every row
+of SURVEY.md §8(a) once.  Metric (BASELINE.json): unknowns*steps/s = N_I * K / time.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg4] [--impl b200|reference]
+
+Prints ONE JSON line (rank 0).  Timing: W untimed warm-up steps, then exactly K steps bracketed by
+a barrier + cuda synchronize on both sides, each step timed with CUDA events on the library's
+stream (L2 flushed before every timed step by writing a 256 MiB buffer, outside the events),
+max over ranks.  `roofline` is the dominant kernel class's algorithmic bytes / its summed
+event-timed device time over the timed region (library instrumentation, hjb_profile_*).
+`e2e` repeats the timed steps through the same C-ABI call with pinned HOST buffers (host<->device
+copies inside the timed region).  `cpu_baseline` (rank 0, N=1) times the CPU oracle on a bounded
+sample (one full oracle step of the same coefficient model on a reduced grid).
+`--impl reference` times that oracle alone (the CPU reference arm of this tier).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "implicit SL steps: unknowns·steps/s, fraction of HBM/FP64 roofline, 1/2/4/8 B200"
+UNIT = "unknowns·steps/s"
+CONFIG_IDX = {"cfg0": 0, "cfg1": 1, "cfg2": 2, "cfg3": 3, "cfg4": 4}
+DEFAULT_CONFIG = "cfg4"
+ORACLE_SAMPLE_N = 129          # cpu_baseline / reference-arm sample grid (same coefficient model)
+HBM_FALLBACK_GBS = 6650.0      # B200_PROFILING.md fallback, used only without MEASURED_PEAKS.json
+FP64_NOMINAL_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # 148 SMs x 64 DFMA/clk x 2 x 1.965 GHz
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIG_IDX))
+    ap.add_argument("--n", type=int, default=None, help="override grid size (diagnostics only)")
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-time-kernels", action="store_true",
+                    help="do not event-time kernel classes (roofline then null)")
+    ap.add_argument("--json-out", default=None)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            return json.load(f), "measured"
+    return {"hbm_gbs": HBM_FALLBACK_GBS}, "fallback"
+
+
+def fp64_peak():
+    """Measured fp64 FMA peak (profiles/fp64_peak.json, tools/fp64_peak.cu) else nominal."""
+    path = os.path.join(ROOT, "profiles", "fp64_peak.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["tflops"]), "measured (profiles/fp64_peak.json)"
+    return FP64_NOMINAL_TFLOPS, "nominal 148 SMs x 64 DFMA/clk x 2 x 1.965 GHz"
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={gpu_index}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        time.sleep(0.25)
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.p.kill()
+        self.f.flush()
+        self.f.seek(0)
+        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            r = [c.strip() for c in r]
+            if len(r) < 9:
+                continue
+            try:
+                sm.append(float(r[1]))
+                smax.append(float(r[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, r[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- CPU oracle
+def oracle_sample(cfg_idx: int, n: int = ORACLE_SAMPLE_N):
+    """One full oracle implicit step (policy iteration, SuperLU solves) of the same coefficient model
+    on an n^d grid, single-threaded.  Returns (unknowns*steps/s, seconds, description)."""
+    from threadpoolctl import threadpool_limits
+
+    from oracle.howard import howard_step
+    from synth import bj_config
+    p = bj_config(cfg_idx, n=n if cfg_idx != 3 else min(n, 17))
+    U0 = p.g(p.all_idx())
+    with threadpool_limits(limits=1):
+        t0 = time.perf_counter()
+        howard_step(p, U0, p.dt, p.dt)
+        el = time.perf_counter() - t0
+    desc = (f"one oracle implicit step (Howard + SuperLU, 1 thread) of the {p.name} coefficient model "
+            f"on {p.n}^{p.d} ({p.N_interior} unknowns, K={p.K}, dt={p.dt:g})")
+    return p.N_interior / el, el, desc
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if world > 1 and rank != 0:
+        return
+    cfg = CONFIG_IDX[args.config]
+    for _ in range(args.warmup):
+        oracle_sample(cfg, n=17 if cfg != 3 else 9)
+    vals, secs = [], []
+    desc = ""
+    for _ in range(args.steps):
+        v, s, desc = oracle_sample(cfg)
+        vals.append(v)
+        secs.append(s)
+    tot = sum(secs)
+    from synth import bj_config
+    p = bj_config(cfg, n=ORACLE_SAMPLE_N if cfg != 3 else 17)
+    value = p.N_interior * args.steps / tot
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": f"{args.config} coefficient model, oracle sample on {p.n}^{p.d}"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    emit(line, args)
+
+
+def emit(line, args):
+    s = json.dumps(line)
+    print(s, flush=True)
+    if args.json_out:
+        with open(args.json_out, "w") as f:
+            f.write(s + "\n")
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def run_b200(args):
+    import numpy as np
+    import torch
+
+    from paper_1605_04821_b200 import build as libbuild
+    rank, world, local = dist_env()
+    if world != args.gpus and "WORLD_SIZE" in os.environ:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (there is no CPU fallback)")
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    libbuild.build()
+    from synth import bj_config
+    from synth.device import grid_for, initial_values, packed_psi
+
+    cfg = CONFIG_IDX[args.config]
+    p = bj_config(cfg, n=args.n)
+    if world > 1:
+        raise SystemExit("multi-GPU slab decomposition: see DESIGN.md §7 (not in this build)")
+    dev = torch.device("cuda", local)
+    g, fields = grid_for(p, device=local)
+    lay = g.layout()
+    nI = lay["n_interior"]
+    U = initial_values(p, device=dev).contiguous()
+    U2 = torch.empty_like(U)
+    pol = torch.zeros(p.N, dtype=torch.uint8, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # 256 MiB > 126 MB L2
+    stream = torch.cuda.current_stream(dev)
+    total = args.warmup + args.steps
+    # per-step inputs (problem data, generated before the timed region)
+    psis = [packed_psi(p, s * p.dt, device=dev) for s in range(1, total + 1)]
+    srcs = [p.f_tables(s * p.dt) for s in range(1, total + 1)]
+
+    def do_step(s, Uin, Uout, polbuf, psi):
+        fb, fc = srcs[s - 1]
+        g.set_source(fb, fc)
+        return g.step(p.dt, Uin, Uout, polbuf, psi)
+
+    stats = []
+    for s in range(1, args.warmup + 1):
+        do_step(s, U, U2, pol, psis[s - 1])
+        U, U2 = U2, U
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    g.profile_reset(time_kernels=not args.no_time_kernels)
+    clk = ClockSampler(local)
+    torch.cuda.synchronize()
+    wall0 = time.perf_counter()
+    for i, s in enumerate(range(args.warmup + 1, total + 1)):
+        flush.zero_()
+        ev[i][0].record(stream)
+        stats.append(do_step(s, U, U2, pol, psis[s - 1]))
+        ev[i][1].record(stream)
+        U, U2 = U2, U
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - wall0
+    clocks = clk.stop()
+    prof = g.profile_read()
+    ms_steps = [a.elapsed_time(b) for a, b in ev]
+    ms_total = sum(ms_steps)
+    value = nI * args.steps / (ms_total / 1e3)
+    # solution sanity vs the manufactured solution (not a parity claim; parity is in tests/)
+    t_end = total * p.dt
+    err = (U - p.u_exact(t_end, torch.arange(p.N, device=dev))).abs().max().item()
+
+    # --------------------------------------------------------------- roofline (dominant class)
+    peaks, peak_src = measured_peaks()
+    cls = prof["classes"]
+    timed = {k: v for k, v in cls.items() if v["ms"] > 0}
+    roof = None
+    roof_search = None
+    if timed:
+        dom = max(timed, key=lambda k: timed[k]["ms"])
+        c = timed[dom]
+        per_launch_ms = c["ms"] / max(1, c["launches"])
+        if dom == "search":
+            pk, src = fp64_peak()
+            ach = c["flops"] / (c["ms"] / 1e3) / 1e12
+            roof = {"bound": "alu", "kernel": dom, "achieved": ach, "peak": pk, "unit": "TFLOP/s",
+                    "frac": ach / pk, "traffic": traffic_for(dom, args.config, c),
+                    "peak_source": src, "launch_ms": per_launch_ms}
+        else:
+            ach = c["bytes"] / (c["ms"] / 1e3) / 1e9
+            pk = float(peaks["hbm_gbs"])
+            roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": pk, "unit": "GB/s",
+                    "frac": ach / pk, "traffic": traffic_for(dom, args.config, c),
+                    "peak_source": f"{peak_src} copy bandwidth (MEASURED_PEAKS.json)",
+                    "launch_ms": per_launch_ms,
+                    "algorithmic_bytes_per_launch": c["bytes"] / max(1, c["launches"])}
+        if "search" in timed and dom != "search":
+            c = timed["search"]
+            pk, src = fp64_peak()
+            ach = c["flops"] / (c["ms"] / 1e3) / 1e12
+            roof_search = {"bound": "alu", "achieved": ach, "peak": pk, "unit": "TFLOP/s",
+                           "frac": ach / pk, "peak_source": src,
+                           "launch_ms": c["ms"] / max(1, c["launches"])}
+    shares = {k: round(v["ms"] / ms_total, 4) for k, v in cls.items() if v["ms"] > 0}
+    hbm_frac = {k: (v["bytes"] / (v["ms"] / 1e3) / 1e9) / float(peaks["hbm_gbs"])
+                for k, v in cls.items() if v["ms"] > 0 and k != "search"}
+
+    # --------------------------------------------------------------- e2e through host buffers
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(g, p, args, U, stream, srcs, psis, nI, dev)
+
+    pis = [st["pi_iters"] for st in stats]
+    kr = [st["krylov_iters_total"] for st in stats]
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_total / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload_name(args.config, p), "n": p.n, "d": p.d, "K": p.K,
+                   "unknowns": nI, "dt": p.dt, "steps_from_t": args.warmup * p.dt,
+                   "parallelism": f"slab{world}", "l2": "256 MiB L2 flush before every timed step; "
+                   "working set > L2"},
+        "roofline": roof, "roofline_search": roof_search,
+        "hbm_frac_by_class": hbm_frac, "time_share_by_class": shares,
+        "mg_cycles_per_pi": (2 * sum(kr) / max(1, sum(pis))),
+        "krylov_iters_per_pi": sum(kr) / max(1, sum(pis)), "pi_iters_per_step": sum(pis) / len(pis),
+        "levels": stats[-1]["n_levels"], "final_rres": max(st["final_rres"] for st in stats),
+        "max_err_vs_ustar": err, "wall_s_timed": wall,
+        "gpu_launches": int(prof["total_launches"]), "clocks": clocks, "e2e": e2e,
+    }
+    if not args.no_cpu_baseline and rank == 0 and world == 1:
+        v, s, desc = oracle_sample(cfg)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc,
+                                "seconds": s, "host_cpus": os.cpu_count()}
+    if rank == 0:
+        emit(line, args)
+    g.close()
+
+
+def workload_name(cfg, p):
+    return {"cfg0": "BASELINE configs[0]", "cfg1": "BASELINE configs[1]", "cfg2": "BASELINE configs[2]",
+            "cfg3": "BASELINE configs[3]", "cfg4": "BASELINE configs[4] (largest grid, 1 GPU)"}[cfg] + \
+        f": d={p.d}, {p.n}^{p.d} grid, K={p.K}"
+
+
+def traffic_for(cls, config, c):
+    """DRAM bytes per launch of this class from a committed ncu --set full summary
+    (profiles/ncu_traffic.json: bytes per node of the captured launch x this run's nodes/launch)."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        d = json.load(f)
+    e = d.get(config, {}).get(cls)
+    if not e:
+        return None
+    return e["dram_bytes_per_node"] * c["nodes"] / max(1, c["launches"])
+
+
+def run_e2e(g, p, args, U_dev, stream, srcs, psis, nI, dev):
+    """The same steps through hjb_step with pinned HOST buffers: each step copies U_prev, the policy
+    and psi host->device and U + policy device->host inside the timed region (inside the call)."""
+    import torch
+    N = p.N
+    Uh_prev = torch.empty(N, dtype=torch.float64, pin_memory=True)
+    Uh = torch.empty(N, dtype=torch.float64, pin_memory=True)
+    polh = torch.zeros(N, dtype=torch.uint8, pin_memory=True)
+    Uh_prev.copy_(U_dev.cpu())
+    psih = [x.cpu().pin_memory() for x in psis]
+    Uh_np, Uhp_np, pol_np = Uh.numpy(), Uh_prev.numpy(), polh.numpy()
+    psi_np = [x.numpy() for x in psih]
+    base = args.warmup + args.steps
+    n_e2e = args.steps
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    t0 = time.perf_counter()
+    for i in range(n_e2e):
+        s = (base + i) % len(srcs) + 1
+        fb, fc = srcs[s - 1]
+        g.set_source(fb, fc)
+        g.step(p.dt, Uhp_np, Uh_np, pol_np, psi_np[s - 1])
+        Uhp_np, Uh_np = Uh_np, Uhp_np
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    ms = ev0.elapsed_time(ev1)
+    nb = psis[0].numel()
+    return {"value": nI * n_e2e / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": 8 * N + N + 8 * nb,
+            "d2h_bytes_per_step": 8 * N + N, "steps": n_e2e, "wall_s": wall,
+            "path": "hjb_step C-ABI with pinned host U_prev/U/policy/psi"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -214,6 +214,39 @@ typedef struct {
 hjb_status hjb_step(hjb_grid_t g, double dt, const double* U_prev, double* U, uint8_t* policy,
                     const double* psi_packed, const hjb_solve_params* p, hjb_step_stats* out);
 
+/* ------------------------------------------------------------------- instrumentation
+ * Every kernel launch of the library is counted per class.  With time_kernels != 0 each launch
+ * is also bracketed by CUDA events on the grid's stream and its device time summed per class
+ * (the events add ~2 us of host work per launch; off by default).  `bytes` is the ALGORITHMIC
+ * HBM traffic of the launches (the per-node formulas of DESIGN.md §6 times the nodes each launch
+ * processed), `flops` the algorithmic fp64 operations, so that bytes/ms and
+ * flops/ms are roofline numerators.  Counters are per handle; reset clears them.              */
+typedef enum {
+  HJB_KC_SEARCH = 0,    /* control search (policy improvement)                               */
+  HJB_KC_APPLY = 1,     /* y = A x on the fine level (Krylov operator, hjb_apply)            */
+  HJB_KC_RESID = 2,     /* r = b - A x (all levels)                                          */
+  HJB_KC_SMOOTH = 3,    /* damped-Jacobi sweeps (all levels)                                 */
+  HJB_KC_TRANSFER = 4,  /* restriction, prolongation, policy/field injection                 */
+  HJB_KC_COARSE = 5,    /* coarsest-level dense assemble / invert / solve                    */
+  HJB_KC_VECTOR = 6,    /* BiCGSTAB vector updates with fused dot products, norms, copies    */
+  HJB_KC_REDUCE = 7,    /* fixed-order reduction of block partials + Krylov scalar update    */
+  HJB_KC_BOUNDARY = 8,  /* Dirichlet data scatter                                            */
+  HJB_KC_COUNT = 9
+} hjb_kernel_class;
+
+typedef struct {
+  int64_t launches[HJB_KC_COUNT];
+  double ms[HJB_KC_COUNT];
+  double bytes[HJB_KC_COUNT];
+  double flops[HJB_KC_COUNT];
+  double nodes[HJB_KC_COUNT];
+  int64_t total_launches;
+  int32_t timed;            /* 1 if ms[] was collected */
+} hjb_profile;
+
+hjb_status hjb_profile_reset(hjb_grid_t g, int32_t time_kernels);
+hjb_status hjb_profile_read(hjb_grid_t g, hjb_profile* out);   /* synchronises the stream */
+
 #ifdef __cplusplus
 }
 #endif

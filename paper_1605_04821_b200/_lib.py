@@ -17,7 +17,11 @@ STATUS = {0: "HJB_OK", 1: "HJB_ERR_INVALID_ARG", 2: "HJB_ERR_UNSUPPORTED", 3: "H
 EXPORTS = ["hjb_last_error", "hjb_version", "hjb_grid_create", "hjb_grid_query", "hjb_grid_destroy",
            "hjb_set_coeffs", "hjb_set_source", "hjb_policy_update", "hjb_apply",
            "hjb_mg_params_default", "hjb_mg_setup", "hjb_mg_apply", "hjb_solve_params_default",
-           "hjb_solve", "hjb_step"]
+           "hjb_solve", "hjb_step", "hjb_profile_reset", "hjb_profile_read"]
+
+KERNEL_CLASSES = ["search", "apply", "resid", "smooth", "transfer", "coarse", "vector", "reduce",
+                  "boundary"]
+HJB_KC_COUNT = len(KERNEL_CLASSES)
 
 
 class GridDesc(C.Structure):
@@ -75,6 +79,19 @@ class StepStats(C.Structure):
                     n_levels=self.n_levels)
 
 
+class Profile(C.Structure):
+    _fields_ = [("launches", C.c_int64 * HJB_KC_COUNT), ("ms", C.c_double * HJB_KC_COUNT),
+                ("bytes", C.c_double * HJB_KC_COUNT), ("flops", C.c_double * HJB_KC_COUNT),
+                ("nodes", C.c_double * HJB_KC_COUNT), ("total_launches", C.c_int64),
+                ("timed", C.c_int32)]
+
+    def as_dict(self):
+        per = {k: dict(launches=self.launches[i], ms=self.ms[i], bytes=self.bytes[i],
+                       flops=self.flops[i], nodes=self.nodes[i])
+               for i, k in enumerate(KERNEL_CLASSES)}
+        return dict(classes=per, total_launches=self.total_launches, timed=bool(self.timed))
+
+
 _lib = None
 
 
@@ -104,6 +121,8 @@ def load(path: str = LIB_PATH):
         "hjb_solve_params_default": (None, [i32, C.POINTER(SolveParams)]),
         "hjb_solve": (i32, [vp, d, vp, vp, vp, C.POINTER(SolveParams), C.POINTER(SolveStats)]),
         "hjb_step": (i32, [vp, d, vp, vp, vp, vp, C.POINTER(SolveParams), C.POINTER(StepStats)]),
+        "hjb_profile_reset": (i32, [vp, i32]),
+        "hjb_profile_read": (i32, [vp, C.POINTER(Profile)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

@@ -148,3 +148,12 @@ class HJBGrid:
         if raise_on_error:
             check(code)
         return out
+
+    # ------------------------------------------------------------------ instrumentation
+    def profile_reset(self, time_kernels: bool = False):
+        check(self.lib.hjb_profile_reset(self.h, 1 if time_kernels else 0))
+
+    def profile_read(self) -> dict:
+        pr = _lib.Profile()
+        check(self.lib.hjb_profile_read(self.h, C.byref(pr)))
+        return pr.as_dict()

@@ -87,7 +87,49 @@ struct hjb_grid {
   const uint8_t* mg_pol0 = nullptr;
   double mg_dt = 0.0;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  // instrumentation (hjb_profile_*)
+  static constexpr int kSlots = 256;
+  bool prof_timing = false;
+  cudaEvent_t pev[2 * kSlots] = {};
+  int pcls[kSlots] = {};
+  int npend = 0;
+  hjb_profile prof{};
+  int nplanes0 = 0;  // per-node coefficient planes read by the operator (sigma/b/c fields)
 };
+
+// ---------------------------------------------------------------------------- instrumentation
+static void prof_drain(hjb_grid* g) {
+  if (g->npend == 0) return;
+  cudaEventSynchronize(g->pev[2 * g->npend - 1]);
+  for (int i = 0; i < g->npend; ++i) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, g->pev[2 * i], g->pev[2 * i + 1]) == cudaSuccess) g->prof.ms[g->pcls[i]] += ms;
+  }
+  g->npend = 0;
+}
+static void prof_pre(hjb_grid* g, int) {
+  if (!g->prof_timing) return;
+  if (g->npend == hjb_grid::kSlots) prof_drain(g);
+  cudaEventRecord(g->pev[2 * g->npend], g->st);
+}
+static void prof_post(hjb_grid* g, int cls, double nodes, double bytes, double flops) {
+  g->prof.launches[cls] += 1;
+  g->prof.total_launches += 1;
+  g->prof.nodes[cls] += nodes;
+  g->prof.bytes[cls] += bytes;
+  g->prof.flops[cls] += flops;
+  if (!g->prof_timing) return;
+  cudaEventRecord(g->pev[2 * g->npend + 1], g->st);
+  g->pcls[g->npend] = cls;
+  g->npend += 1;
+}
+// LAUNCH(class, nodes, algorithmic bytes, algorithmic flops, kernel<<<...>>>(...))
+#define LAUNCH(CLS, NODES, BYTES, FLOPS, ...)                              \
+  do {                                                                     \
+    prof_pre(g, CLS);                                                      \
+    __VA_ARGS__;                                                           \
+    prof_post(g, CLS, (double)(NODES), (double)(BYTES), (double)(FLOPS));  \
+  } while (0)
 
 // ---------------------------------------------------------------------------- small helpers
 static int nblocks(int64_t work) {
@@ -138,7 +180,8 @@ static LevelDev make_level(int D, int64_t n, double lo, double hi, double k, dou
 
 static double host_finalize(hjb_grid* g, int nblk, unsigned maxmask, int which, hjb_status* err,
                             double* second = nullptr) {
-  k_finalize<<<1, 1024, 0, g->st>>>(g->partial, nblk, g->red, maxmask, g->S, which);
+  LAUNCH(HJB_KC_REDUCE, nblk, 16.0 * nblk, 2.0 * nblk,
+         k_finalize<<<1, 1024, 0, g->st>>>(g->partial, nblk, g->red, maxmask, g->S, which));
   cudaMemcpyAsync(g->hred, g->red, 2 * sizeof(double), cudaMemcpyDeviceToHost, g->st);
   cudaError_t e = cudaStreamSynchronize(g->st);
   if (e != cudaSuccess) {
@@ -157,7 +200,13 @@ static void launch_operator(hjb_grid* g, const LevelDev& L, const CoefDev& C, in
                             const double* u) {
   const int nb = nblocks(L.n_own);
   cudaStream_t st = g->st;
-#define OPL(M, ND) k_operator<D, M, ND><<<nb, kThreads, 0, st>>>(L, C, dt, omega, pol, x, b, y, u, g->partial)
+  const int cls = mode == OP_APPLY ? HJB_KC_APPLY : (mode == OP_RESID ? HJB_KC_RESID : HJB_KC_SMOOTH);
+  const double nodes = (double)L.n_own;
+  const double bpn = 1.0 + 8.0 + (mode != OP_JACOBI0 ? 8.0 : 0.0) + (mode != OP_APPLY ? 8.0 : 0.0) +
+                     (ndot >= 1 ? 8.0 : 0.0) + 8.0 * g->nplanes0;
+  const double fpn = (2.0 * g->P + 1.0) * (1 << D) * 2.0 + 4.0 + 2.0 * ndot;
+#define OPL(M, ND) LAUNCH(cls, nodes, nodes * bpn, nodes * fpn, \
+    k_operator<D, M, ND><<<nb, kThreads, 0, st>>>(L, C, dt, omega, pol, x, b, y, u, g->partial))
   if (mode == OP_APPLY) {
     if (ndot == 0) OPL(OP_APPLY, 0);
     else if (ndot == 1) OPL(OP_APPLY, 1);
@@ -236,6 +285,8 @@ extern "C" hjb_status hjb_grid_destroy(hjb_grid_t g) {
   cudaFreeHost(g->hred);
   for (auto& e : g->ev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : g->pev)
+    if (e) cudaEventDestroy(e);
   delete g;
   return HJB_OK;
 }
@@ -295,6 +346,7 @@ extern "C" hjb_status hjb_grid_create(const hjb_grid_desc* d, hjb_grid_t* out) {
     return fail(HJB_ERR_OOM, "pinned alloc");
   }
   for (auto& e : g->ev) cudaEventCreate(&e);
+  for (auto& e : g->pev) cudaEventCreate(&e);
   cudaError_t e = cudaStreamSynchronize(g->st);
   if (e != cudaSuccess) {
     hjb_grid_destroy(g);
@@ -365,6 +417,8 @@ extern "C" hjb_status hjb_set_coeffs(hjb_grid_t g, const hjb_coeffs* c) {
   g->C0.K = g->K;
   g->C0.P = g->P;
   g->C0.Q = g->Q;
+  g->nplanes0 = (c->sigma_scale ? g->P : 0) + (c->sigma_node ? g->P * g->D : 0) + (c->b_scale ? 1 : 0) +
+                (c->b_node ? g->D : 0) + (c->c_node ? 1 : 0);
   g->have_coeffs = true;
   g->mg_ready = false;
   return HJB_OK;
@@ -386,8 +440,13 @@ extern "C" hjb_status hjb_set_source(hjb_grid_t g, const double* f_basis, const 
 static hjb_status policy_update_dev(hjb_grid* g, double dt, const double* U, const double* Uprev, uint8_t* pol,
                                     double* F, hjb_pi_stats* out) {
   const int nb = nblocks(g->L0.n_own);
-  if (g->D == 2) k_search<2><<<nb, kThreads, 0, g->st>>>(g->L0, g->C0, dt, U, Uprev, pol, F, g->partial);
-  else k_search<3><<<nb, kThreads, 0, g->st>>>(g->L0, g->C0, dt, U, Uprev, pol, F, g->partial);
+  const double nodes = (double)g->L0.n_own;
+  const double bpn = 8.0 + 8.0 + 1.0 + 1.0 + 8.0 + 8.0 * g->Q + 8.0 * g->nplanes0;
+  const double fpn = g->K * ((2.0 * g->P + 1.0) * (1 << g->D) * 2.0 + 2.0 * g->Q + 4.0);
+  if (g->D == 2) LAUNCH(HJB_KC_SEARCH, nodes, nodes * bpn, nodes * fpn,
+                        k_search<2><<<nb, kThreads, 0, g->st>>>(g->L0, g->C0, dt, U, Uprev, pol, F, g->partial));
+  else LAUNCH(HJB_KC_SEARCH, nodes, nodes * bpn, nodes * fpn,
+              k_search<3><<<nb, kThreads, 0, g->st>>>(g->L0, g->C0, dt, U, Uprev, pol, F, g->partial));
   CKL();
   hjb_status err;
   double changed = 0.0;
@@ -512,7 +571,7 @@ static hjb_status inject_all(hjb_grid* g) {
     Level& lc = g->levels[i];
     const uint8_t* pf = (i == 1) ? g->mg_pol0 : lf.pol;
     const int nb = nblocks(lc.elems);
-    k_inject_u8<D><<<nb, kThreads, 0, g->st>>>(lf.L, lc.L, pf, lc.pol);
+    LAUNCH(HJB_KC_TRANSFER, lc.elems, 2.0 * lc.elems, 0, k_inject_u8<D><<<nb, kThreads, 0, g->st>>>(lf.L, lc.L, pf, lc.pol));
     struct FP { const double* f; double* c; int np; };
     const FP fps[] = {{lf.C.sigma_scale, (double*)lc.C.sigma_scale, g->P},
                       {lf.C.sigma_node, (double*)lc.C.sigma_node, g->P * D},
@@ -520,18 +579,21 @@ static hjb_status inject_all(hjb_grid* g) {
                       {lf.C.b_node, (double*)lc.C.b_node, D},
                       {lf.C.c_node, (double*)lc.C.c_node, 1}};
     for (const FP& f : fps)
-      if (f.f) k_inject_f64<D><<<nb, kThreads, 0, g->st>>>(lf.L, lc.L, f.f, lf.C.ld, f.c, lc.C.ld, f.np);
+      if (f.f)
+        LAUNCH(HJB_KC_TRANSFER, lc.elems, 16.0 * f.np * lc.elems, 0,
+               k_inject_f64<D><<<nb, kThreads, 0, g->st>>>(lf.L, lc.L, f.f, lf.C.ld, f.c, lc.C.ld, f.np));
     CKL();
   }
   Level& lc = g->levels.back();
   const int64_t Nc = lc.L.n_own;
   const uint8_t* pc = (g->levels.size() == 1) ? g->mg_pol0 : lc.pol;
   CK(cudaMemsetAsync(lc.Ainv, 0, (size_t)Nc * Nc * sizeof(double), g->st));
-  k_coarse_assemble<D><<<(int)((Nc + 127) / 128), 128, 0, g->st>>>(lc.L, lc.C, g->mg_dt, pc, lc.Ainv);
+  LAUNCH(HJB_KC_COARSE, Nc, 8.0 * Nc * Nc, 0,
+         k_coarse_assemble<D><<<(int)((Nc + 127) / 128), 128, 0, g->st>>>(lc.L, lc.C, g->mg_dt, pc, lc.Ainv));
   CKL();
   const size_t smem = (size_t)Nc * Nc * sizeof(double);
   if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_coarse_invert, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_coarse_invert<<<1, 1024, smem, g->st>>>(lc.Ainv, (int)Nc);
+  LAUNCH(HJB_KC_COARSE, Nc, 16.0 * Nc * Nc, 2.0 * Nc * Nc * Nc, k_coarse_invert<<<1, 1024, smem, g->st>>>(lc.Ainv, (int)Nc));
   CKL();
   return HJB_OK;
 }
@@ -567,7 +629,8 @@ static hjb_status vcycle(hjb_grid* g, size_t l, const double* b, double* out) {
   cudaStream_t st = g->st;
   if (l + 1 == g->levels.size()) {
     const int Nc = (int)L.n_own;
-    k_coarse_solve<D><<<1, 256, Nc * sizeof(double), st>>>(L, lv.Ainv, b, out);
+    LAUNCH(HJB_KC_COARSE, Nc, 8.0 * Nc * Nc + 16.0 * Nc, 2.0 * Nc * Nc,
+           k_coarse_solve<D><<<1, 256, Nc * sizeof(double), st>>>(L, lv.Ainv, b, out));
     CKL();
     return HJB_OK;
   }
@@ -582,10 +645,12 @@ static hjb_status vcycle(hjb_grid* g, size_t l, const double* b, double* out) {
   }
   launch_operator<D>(g, L, lv.C, OP_RESID, 0, dt, 0.0, pol, bufs[cur], b, lv.res, nullptr);
   Level& lc = g->levels[l + 1];
-  k_restrict<D><<<nblocks(lc.L.n_own), kThreads, 0, st>>>(L, lc.L, lv.res, lc.b);
+  LAUNCH(HJB_KC_TRANSFER, L.n_own, 8.0 * (L.n_own + lc.L.n_own), 18.0 * lc.L.n_own,
+         k_restrict<D><<<nblocks(lc.L.n_own), kThreads, 0, st>>>(L, lc.L, lv.res, lc.b));
   CKL();
   TRY(vcycle<D>(g, l + 1, lc.b, lc.x));
-  k_prolong_add<D><<<nblocks(L.n_own), kThreads, 0, st>>>(L, lc.L, lc.x, bufs[cur]);
+  LAUNCH(HJB_KC_TRANSFER, L.n_own, 16.0 * L.n_own + 8.0 * lc.L.n_own, 4.0 * L.n_own,
+         k_prolong_add<D><<<nblocks(L.n_own), kThreads, 0, st>>>(L, lc.L, lc.x, bufs[cur]));
   for (int k = 0; k < npost; ++k) {
     launch_operator<D>(g, L, lv.C, OP_JACOBI, 0, dt, om, pol, bufs[cur], b, bufs[1 - cur], nullptr);
     cur = 1 - cur;
@@ -597,8 +662,9 @@ static hjb_status vcycle(hjb_grid* g, size_t l, const double* b, double* out) {
 
 static hjb_status precond(hjb_grid* g, bool use_mg, const double* b, double* x) {
   if (!use_mg) {
-    if (g->D == 2) k_copy_interior<2><<<nblocks(g->L0.n_own), kThreads, 0, g->st>>>(g->L0, b, x);
-    else k_copy_interior<3><<<nblocks(g->L0.n_own), kThreads, 0, g->st>>>(g->L0, b, x);
+    const double nn = (double)g->L0.n_own;
+    if (g->D == 2) LAUNCH(HJB_KC_VECTOR, nn, 16.0 * nn, 0, k_copy_interior<2><<<nblocks(g->L0.n_own), kThreads, 0, g->st>>>(g->L0, b, x));
+    else LAUNCH(HJB_KC_VECTOR, nn, 16.0 * nn, 0, k_copy_interior<3><<<nblocks(g->L0.n_own), kThreads, 0, g->st>>>(g->L0, b, x));
     CKL();
     return HJB_OK;
   }
@@ -616,7 +682,8 @@ extern "C" hjb_status hjb_mg_apply(hjb_grid_t g, const double* b, double* x) {
 template <int D>
 static hjb_status norms_dev(hjb_grid* g, const double* v, double* n2, double* ninf) {
   const int nb = nblocks(g->L0.n_own);
-  k_norms<D><<<nb, kThreads, 0, g->st>>>(g->L0, v, g->partial);
+  LAUNCH(HJB_KC_VECTOR, g->L0.n_own, 8.0 * g->L0.n_own, 3.0 * g->L0.n_own,
+         k_norms<D><<<nb, kThreads, 0, g->st>>>(g->L0, v, g->partial));
   CKL();
   hjb_status err;
   *n2 = std::sqrt(host_finalize(g, nb, 0x2u, SC_NONE, &err, ninf));
@@ -643,7 +710,8 @@ static hjb_status bicgstab(hjb_grid* g, double dt, const uint8_t* pol, const dou
   for (int restart = 0; restart < 4 && !converged; ++restart) {
     // r = F - A x ; rhat = r ; p = r
     launch_operator<D>(g, L, C, OP_RESID, 0, dt, 0.0, pol, x, F, g->r, nullptr);
-    k_bicg_init<D><<<nb, kThreads, 0, st>>>(L, g->r, g->rhat, g->p, g->partial);
+    LAUNCH(HJB_KC_VECTOR, L.n_own, 24.0 * L.n_own, 2.0 * L.n_own,
+           k_bicg_init<D><<<nb, kThreads, 0, st>>>(L, g->r, g->rhat, g->p, g->partial));
     CKL();
     rr = host_finalize(g, nb, 0u, SC_INIT, &err);
     if (err != HJB_OK) return err;
@@ -652,16 +720,20 @@ static hjb_status bicgstab(hjb_grid* g, double dt, const uint8_t* pol, const dou
     bool restart_needed = false;
     int inner = 0;
     while (it < sp->krylov_maxit) {
-      if (inner > 0) k_bicg_p<D><<<nb, kThreads, 0, st>>>(L, g->S, g->r, g->p, g->v);
+      if (inner > 0)
+        LAUNCH(HJB_KC_VECTOR, L.n_own, 32.0 * L.n_own, 4.0 * L.n_own,
+               k_bicg_p<D><<<nb, kThreads, 0, st>>>(L, g->S, g->r, g->p, g->v));
       TRY(precond(g, mg, g->p, g->phat));
       launch_operator<D>(g, L, C, OP_APPLY, 1, dt, 0.0, pol, g->phat, nullptr, g->v, g->rhat);
-      k_finalize<<<1, 1024, 0, st>>>(g->partial, nb, g->red, 0u, g->S, SC_AFTER_V);
-      k_bicg_s<D><<<nb, kThreads, 0, st>>>(L, g->S, g->r, g->v, g->s, g->partial);
+      LAUNCH(HJB_KC_REDUCE, nb, 16.0 * nb, 2.0 * nb, k_finalize<<<1, 1024, 0, st>>>(g->partial, nb, g->red, 0u, g->S, SC_AFTER_V));
+      LAUNCH(HJB_KC_VECTOR, L.n_own, 24.0 * L.n_own, 4.0 * L.n_own,
+             k_bicg_s<D><<<nb, kThreads, 0, st>>>(L, g->S, g->r, g->v, g->s, g->partial));
       TRY(precond(g, mg, g->s, g->shat));
       launch_operator<D>(g, L, C, OP_APPLY, 2, dt, 0.0, pol, g->shat, nullptr, g->t, g->s);
-      k_finalize<<<1, 1024, 0, st>>>(g->partial, nb, g->red, 0u, g->S, SC_AFTER_T);
-      k_bicg_x<D><<<nb, kThreads, 0, st>>>(L, g->S, x, g->phat, g->shat, g->s, g->t, g->r, g->rhat, g->partial);
-      k_finalize<<<1, 1024, 0, st>>>(g->partial, nb, g->red, 0u, g->S, SC_AFTER_R);
+      LAUNCH(HJB_KC_REDUCE, nb, 16.0 * nb, 2.0 * nb, k_finalize<<<1, 1024, 0, st>>>(g->partial, nb, g->red, 0u, g->S, SC_AFTER_T));
+      LAUNCH(HJB_KC_VECTOR, L.n_own, 64.0 * L.n_own, 10.0 * L.n_own,
+             k_bicg_x<D><<<nb, kThreads, 0, st>>>(L, g->S, x, g->phat, g->shat, g->s, g->t, g->r, g->rhat, g->partial));
+      LAUNCH(HJB_KC_REDUCE, nb, 16.0 * nb, 2.0 * nb, k_finalize<<<1, 1024, 0, st>>>(g->partial, nb, g->red, 0u, g->S, SC_AFTER_R));
       CKL();
       CK(cudaMemcpyAsync(g->hS, g->S, sizeof(KScal), cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
@@ -746,8 +818,9 @@ extern "C" hjb_status hjb_step(hjb_grid_t g, double dt, const double* U_prev, do
   if (dU != dprev) CK(cudaMemcpyAsync(dU, dprev, vb, cudaMemcpyDeviceToDevice, st));
   if (dpsi) {
     const int nbb = (int)std::min<int64_t>((g->n_boundary + 255) / 256, 4096);
-    if (g->D == 2) k_scatter_psi<2><<<nbb, 256, 0, st>>>(g->L0, g->n_boundary, dpsi, dU);
-    else k_scatter_psi<3><<<nbb, 256, 0, st>>>(g->L0, g->n_boundary, dpsi, dU);
+    const double nbd = (double)g->n_boundary;
+    if (g->D == 2) LAUNCH(HJB_KC_BOUNDARY, nbd, 16.0 * nbd, 0, k_scatter_psi<2><<<nbb, 256, 0, st>>>(g->L0, g->n_boundary, dpsi, dU));
+    else LAUNCH(HJB_KC_BOUNDARY, nbd, 16.0 * nbd, 0, k_scatter_psi<3><<<nbb, 256, 0, st>>>(g->L0, g->n_boundary, dpsi, dU));
     CKL();
   }
   hjb_step_stats S{};
@@ -790,4 +863,24 @@ extern "C" hjb_status hjb_step(hjb_grid_t g, double dt, const double* U_prev, do
   CK(cudaStreamSynchronize(st));
   if (out) *out = S;
   return result;
+}
+
+// ---------------------------------------------------------------------------- API: instrumentation
+extern "C" hjb_status hjb_profile_reset(hjb_grid_t g, int32_t time_kernels) {
+  if (!g) return fail(HJB_ERR_INVALID_ARG, "null handle");
+  CK(cudaSetDevice(g->desc.device));
+  prof_drain(g);
+  g->prof = hjb_profile{};
+  g->prof_timing = time_kernels != 0;
+  g->prof.timed = g->prof_timing ? 1 : 0;
+  return HJB_OK;
+}
+
+extern "C" hjb_status hjb_profile_read(hjb_grid_t g, hjb_profile* out) {
+  if (!g || !out) return fail(HJB_ERR_INVALID_ARG, "null handle/out");
+  CK(cudaSetDevice(g->desc.device));
+  prof_drain(g);
+  CK(cudaStreamSynchronize(g->st));
+  *out = g->prof;
+  return HJB_OK;
 }
