@@ -179,6 +179,12 @@ typedef struct {
   double tol_pi;             /* policy-iteration stop: R <= tol_pi (1e-10) */
   int32_t max_pi;            /* 50 */
   hjb_mg_params mg;
+  double pi_forcing;         /* inexact policy iteration (hjb_step only): while the policy still
+                                changes, each policy evaluation stops at ||r||_2 <= max(krylov_rtol
+                                ||F||_2, pi_forcing ||r_0||_2); a policy found stable after an
+                                inexact evaluation is re-evaluated exactly before the step ends, so
+                                the fixed point is unchanged (DESIGN.md §3 reading xxii).
+                                0 = exact evaluation every iteration (the paper's Howard loop). */
 } hjb_solve_params;
 
 typedef struct {

@@ -55,7 +55,8 @@ class MgParams(C.Structure):
 
 class SolveParams(C.Structure):
     _fields_ = [("krylov_rtol", C.c_double), ("krylov_maxit", C.c_int32), ("use_mg", C.c_int32),
-                ("tol_pi", C.c_double), ("max_pi", C.c_int32), ("mg", MgParams)]
+                ("tol_pi", C.c_double), ("max_pi", C.c_int32), ("mg", MgParams),
+                ("pi_forcing", C.c_double)]
 
 
 class SolveStats(C.Structure):

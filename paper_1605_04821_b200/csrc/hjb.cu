@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <map>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -41,7 +42,7 @@ static hjb_status fail(hjb_status s, const std::string& msg) {
     if (s_ != HJB_OK) return s_;   \
   } while (0)
 
-static constexpr int kMaxBlocks = 148 * 8;  // grid-stride: 8 resident 256-thread CTAs per SM
+static constexpr int kMaxBlocks = 148 * 16;  // partial-sum slots: 16 resident 128-thread CTAs per SM
 
 struct Level {
   LevelDev L{};
@@ -95,6 +96,8 @@ struct hjb_grid {
   int npend = 0;
   hjb_profile prof{};
   int nplanes0 = 0;  // per-node coefficient planes read by the operator (sigma/b/c fields)
+  int sms = 148;
+  int nblk_last = 1;  // CTAs of the last dims() launch (partials to reduce)
 };
 
 // ---------------------------------------------------------------------------- instrumentation
@@ -132,9 +135,27 @@ static void prof_post(hjb_grid* g, int cls, double nodes, double bytes, double f
   } while (0)
 
 // ---------------------------------------------------------------------------- small helpers
-static int nblocks(int64_t work) {
-  int64_t b = (work + kThreads - 1) / kThreads;
-  return (int)std::max<int64_t>(1, std::min<int64_t>(b, kMaxBlocks));
+// 2D launch over the owned interior of level L: x covers an x1 line, y strides over lines.  All
+// CTAs are made co-resident (occupancy x SMs) so the lines in flight form one band that moves
+// through the grid and the +-reach rows it gathers from stay in L2.
+static int occupancy_of(const void* fn) {
+  static std::map<const void*, int> cache;
+  auto it = cache.find(fn);
+  if (it != cache.end()) return it->second;
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kTX, 0) != cudaSuccess || occ < 1) occ = 1;
+  cache[fn] = occ;
+  return occ;
+}
+static dim3 dims(hjb_grid* g, const LevelDev& L, const void* fn) {
+  const int gx = std::max(1, (L.nI + kTX - 1) / kTX);
+  const int64_t cap = std::min<int64_t>((int64_t)occupancy_of(fn) * g->sms, kMaxBlocks);
+  const int gy = (int)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(L.nrows, 65535), cap / gx));
+  g->nblk_last = gx * gy;
+  return dim3(gx, gy);
+}
+static int nblocks1d(int64_t work) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, kMaxBlocks));
 }
 
 static bool is_device_ptr(const void* p) {
@@ -156,6 +177,8 @@ static LevelDev make_level(int D, int64_t n, double lo, double hi, double k, dou
   LevelDev L{};
   L.n = (int)n;
   L.nI = (int)(n - 2);
+  L.nrows = 1;
+  for (int d = 0; d < D - 1; ++d) L.nrows *= (int)(n - 2);
   L.row_elems = 1;
   for (int d = 0; d < D - 1; ++d) L.row_elems *= n;
   // single rank: owned interior rows 1..n-2 of the slowest axis, local array = whole grid
@@ -167,12 +190,10 @@ static LevelDev make_level(int D, int64_t n, double lo, double hi, double k, dou
   int64_t own = 1;
   for (int d = 0; d < D; ++d) own *= (n - 2);
   L.n_own = own;
-  L.lo = lo;
-  L.hi = hi;
   L.h = (hi - lo) / (double)(n - 1);
-  L.inv_h = 1.0 / L.h;
-  L.k = k;
-  L.k2 = k2;
+  L.nm1 = (double)(n - 1);
+  L.kh = k / L.h;
+  L.k2h = k2 / L.h;
   L.inv_2k2 = 1.0 / (2.0 * k2);
   L.inv_k2 = 1.0 / k2;
   return L;
@@ -198,7 +219,6 @@ template <int D>
 static void launch_operator(hjb_grid* g, const LevelDev& L, const CoefDev& C, int mode, int ndot, double dt,
                             double omega, const uint8_t* pol, const double* x, const double* b, double* y,
                             const double* u) {
-  const int nb = nblocks(L.n_own);
   cudaStream_t st = g->st;
   const int cls = mode == OP_APPLY ? HJB_KC_APPLY : (mode == OP_RESID ? HJB_KC_RESID : HJB_KC_SMOOTH);
   const double nodes = (double)L.n_own;
@@ -206,7 +226,7 @@ static void launch_operator(hjb_grid* g, const LevelDev& L, const CoefDev& C, in
                      (ndot >= 1 ? 8.0 : 0.0) + 8.0 * g->nplanes0;
   const double fpn = (2.0 * g->P + 1.0) * (1 << D) * 2.0 + 4.0 + 2.0 * ndot;
 #define OPL(M, ND) LAUNCH(cls, nodes, nodes * bpn, nodes * fpn, \
-    k_operator<D, M, ND><<<nb, kThreads, 0, st>>>(L, C, dt, omega, pol, x, b, y, u, g->partial))
+    k_operator<D, M, ND><<<dims(g, L, (const void*)k_operator<D, M, ND>), kTX, 0, st>>>(L, C, dt, omega, pol, x, b, y, u, g->partial))
   if (mode == OP_APPLY) {
     if (ndot == 0) OPL(OP_APPLY, 0);
     else if (ndot == 1) OPL(OP_APPLY, 1);
@@ -250,6 +270,7 @@ extern "C" void hjb_solve_params_default(int32_t dim, hjb_solve_params* o) {
   o->tol_pi = 1e-10;
   o->max_pi = 50;
   hjb_mg_params_default(dim, &o->mg);
+  o->pi_forcing = 0.0;
 }
 
 // ---------------------------------------------------------------------------- API: grid
@@ -304,7 +325,9 @@ extern "C" hjb_status hjb_grid_create(const hjb_grid_desc* d, hjb_grid_t* out) {
     return fail(HJB_ERR_UNSUPPORTED, "nranks > 1: slab decomposition is not enabled in this build");
   int64_t tot = 1;
   for (int i = 0; i < d->dim; ++i) tot *= d->n;
-  if ((d->n - 2) > (1LL << 30) || tot > (1LL << 40)) return fail(HJB_ERR_INVALID_ARG, "grid too large");
+  // local arrays are indexed with 32-bit offsets; one x1 line must fit the partial-sum slots
+  if (tot >= (1LL << 31) || (d->n - 2) > (int64_t)kTX * kMaxBlocks)
+    return fail(HJB_ERR_INVALID_ARG, "grid too large for one rank (local arrays must hold < 2^31 nodes)");
   CK(cudaSetDevice(d->device));
   hjb_grid* g = new hjb_grid();
   g->desc = *d;
@@ -318,6 +341,8 @@ extern "C" hjb_status hjb_grid_create(const hjb_grid_desc* d, hjb_grid_t* out) {
   g->h = (d->hi - d->lo) / (double)(d->n - 1);
   g->k = std::sqrt(g->h);  // k = sqrt(dx)
   g->st = (cudaStream_t)d->stream;
+  cudaDeviceGetAttribute(&g->sms, cudaDevAttrMultiProcessorCount, d->device);
+  if (g->sms < 1) g->sms = 148;
   g->L0 = make_level(g->D, g->n, g->lo, g->hi, g->k, g->h, 0, 1);
   g->N = g->L0.local_rows * g->L0.row_elems;
   g->n_interior = g->L0.n_own;
@@ -439,18 +464,17 @@ extern "C" hjb_status hjb_set_source(hjb_grid_t g, const double* f_basis, const 
 // ---------------------------------------------------------------------------- policy improvement
 static hjb_status policy_update_dev(hjb_grid* g, double dt, const double* U, const double* Uprev, uint8_t* pol,
                                     double* F, hjb_pi_stats* out) {
-  const int nb = nblocks(g->L0.n_own);
   const double nodes = (double)g->L0.n_own;
   const double bpn = 8.0 + 8.0 + 1.0 + 1.0 + 8.0 + 8.0 * g->Q + 8.0 * g->nplanes0;
   const double fpn = g->K * ((2.0 * g->P + 1.0) * (1 << g->D) * 2.0 + 2.0 * g->Q + 4.0);
   if (g->D == 2) LAUNCH(HJB_KC_SEARCH, nodes, nodes * bpn, nodes * fpn,
-                        k_search<2><<<nb, kThreads, 0, g->st>>>(g->L0, g->C0, dt, U, Uprev, pol, F, g->partial));
+                        k_search<2><<<dims(g, g->L0, (const void*)k_search<2>), kTX, 0, g->st>>>(g->L0, g->C0, dt, U, Uprev, pol, F, g->partial));
   else LAUNCH(HJB_KC_SEARCH, nodes, nodes * bpn, nodes * fpn,
-              k_search<3><<<nb, kThreads, 0, g->st>>>(g->L0, g->C0, dt, U, Uprev, pol, F, g->partial));
+              k_search<3><<<dims(g, g->L0, (const void*)k_search<3>), kTX, 0, g->st>>>(g->L0, g->C0, dt, U, Uprev, pol, F, g->partial));
   CKL();
   hjb_status err;
   double changed = 0.0;
-  const double R = host_finalize(g, nb, 0x1u, SC_NONE, &err, &changed);
+  const double R = host_finalize(g, g->nblk_last, 0x1u, SC_NONE, &err, &changed);
   if (err != HJB_OK) return err;
   if (out) {
     out->R_max = R;
@@ -570,8 +594,8 @@ static hjb_status inject_all(hjb_grid* g) {
     Level& lf = g->levels[i - 1];
     Level& lc = g->levels[i];
     const uint8_t* pf = (i == 1) ? g->mg_pol0 : lf.pol;
-    const int nb = nblocks(lc.elems);
-    LAUNCH(HJB_KC_TRANSFER, lc.elems, 2.0 * lc.elems, 0, k_inject_u8<D><<<nb, kThreads, 0, g->st>>>(lf.L, lc.L, pf, lc.pol));
+    const int nb = nblocks1d(lc.elems);
+    LAUNCH(HJB_KC_TRANSFER, lc.elems, 2.0 * lc.elems, 0, k_inject_u8<D><<<nb, 256, 0, g->st>>>(lf.L, lc.L, pf, lc.pol));
     struct FP { const double* f; double* c; int np; };
     const FP fps[] = {{lf.C.sigma_scale, (double*)lc.C.sigma_scale, g->P},
                       {lf.C.sigma_node, (double*)lc.C.sigma_node, g->P * D},
@@ -581,7 +605,7 @@ static hjb_status inject_all(hjb_grid* g) {
     for (const FP& f : fps)
       if (f.f)
         LAUNCH(HJB_KC_TRANSFER, lc.elems, 16.0 * f.np * lc.elems, 0,
-               k_inject_f64<D><<<nb, kThreads, 0, g->st>>>(lf.L, lc.L, f.f, lf.C.ld, f.c, lc.C.ld, f.np));
+               k_inject_f64<D><<<nb, 256, 0, g->st>>>(lf.L, lc.L, f.f, lf.C.ld, f.c, lc.C.ld, f.np));
     CKL();
   }
   Level& lc = g->levels.back();
@@ -646,11 +670,11 @@ static hjb_status vcycle(hjb_grid* g, size_t l, const double* b, double* out) {
   launch_operator<D>(g, L, lv.C, OP_RESID, 0, dt, 0.0, pol, bufs[cur], b, lv.res, nullptr);
   Level& lc = g->levels[l + 1];
   LAUNCH(HJB_KC_TRANSFER, L.n_own, 8.0 * (L.n_own + lc.L.n_own), 18.0 * lc.L.n_own,
-         k_restrict<D><<<nblocks(lc.L.n_own), kThreads, 0, st>>>(L, lc.L, lv.res, lc.b));
+         k_restrict<D><<<dims(g, lc.L, (const void*)k_restrict<D>), kTX, 0, st>>>(L, lc.L, lv.res, lc.b));
   CKL();
   TRY(vcycle<D>(g, l + 1, lc.b, lc.x));
   LAUNCH(HJB_KC_TRANSFER, L.n_own, 16.0 * L.n_own + 8.0 * lc.L.n_own, 4.0 * L.n_own,
-         k_prolong_add<D><<<nblocks(L.n_own), kThreads, 0, st>>>(L, lc.L, lc.x, bufs[cur]));
+         k_prolong_add<D><<<dims(g, L, (const void*)k_prolong_add<D>), kTX, 0, st>>>(L, lc.L, lc.x, bufs[cur]));
   for (int k = 0; k < npost; ++k) {
     launch_operator<D>(g, L, lv.C, OP_JACOBI, 0, dt, om, pol, bufs[cur], b, bufs[1 - cur], nullptr);
     cur = 1 - cur;
@@ -663,8 +687,8 @@ static hjb_status vcycle(hjb_grid* g, size_t l, const double* b, double* out) {
 static hjb_status precond(hjb_grid* g, bool use_mg, const double* b, double* x) {
   if (!use_mg) {
     const double nn = (double)g->L0.n_own;
-    if (g->D == 2) LAUNCH(HJB_KC_VECTOR, nn, 16.0 * nn, 0, k_copy_interior<2><<<nblocks(g->L0.n_own), kThreads, 0, g->st>>>(g->L0, b, x));
-    else LAUNCH(HJB_KC_VECTOR, nn, 16.0 * nn, 0, k_copy_interior<3><<<nblocks(g->L0.n_own), kThreads, 0, g->st>>>(g->L0, b, x));
+    if (g->D == 2) LAUNCH(HJB_KC_VECTOR, nn, 16.0 * nn, 0, k_copy_interior<2><<<dims(g, g->L0, (const void*)k_copy_interior<2>), kTX, 0, g->st>>>(g->L0, b, x));
+    else LAUNCH(HJB_KC_VECTOR, nn, 16.0 * nn, 0, k_copy_interior<3><<<dims(g, g->L0, (const void*)k_copy_interior<3>), kTX, 0, g->st>>>(g->L0, b, x));
     CKL();
     return HJB_OK;
   }
@@ -681,9 +705,9 @@ extern "C" hjb_status hjb_mg_apply(hjb_grid_t g, const double* b, double* x) {
 // ---------------------------------------------------------------------------- BiCGSTAB
 template <int D>
 static hjb_status norms_dev(hjb_grid* g, const double* v, double* n2, double* ninf) {
-  const int nb = nblocks(g->L0.n_own);
   LAUNCH(HJB_KC_VECTOR, g->L0.n_own, 8.0 * g->L0.n_own, 3.0 * g->L0.n_own,
-         k_norms<D><<<nb, kThreads, 0, g->st>>>(g->L0, v, g->partial));
+         k_norms<D><<<dims(g, g->L0, (const void*)k_norms<D>), kTX, 0, g->st>>>(g->L0, v, g->partial));
+  const int nb = g->nblk_last;
   CKL();
   hjb_status err;
   *n2 = std::sqrt(host_finalize(g, nb, 0x2u, SC_NONE, &err, ninf));
@@ -691,18 +715,18 @@ static hjb_status norms_dev(hjb_grid* g, const double* v, double* n2, double* ni
 }
 
 template <int D>
+// eta > 0: inexact policy evaluation, stop at ||r||_2 <= max(rtol ||F||_2, eta ||r_0||_2)
 static hjb_status bicgstab(hjb_grid* g, double dt, const uint8_t* pol, const double* F, double* x,
-                           const hjb_solve_params* sp, hjb_solve_stats* out) {
+                           const hjb_solve_params* sp, hjb_solve_stats* out, double eta = 0.0) {
   const LevelDev& L = g->L0;
   const CoefDev& C = g->C0;
-  const int nb = nblocks(L.n_own);
   cudaStream_t st = g->st;
   const bool mg = sp->use_mg != 0;
   if (mg && (!g->mg_ready || g->mg_pol0 != pol || g->mg_dt != dt))
     return fail(HJB_ERR_STATE, "hjb_mg_setup must be called with the same policy and dt before solving");
   double bn2, bninf;
   TRY(norms_dev<D>(g, F, &bn2, &bninf));
-  const double tol = sp->krylov_rtol * bn2;
+  double tol = sp->krylov_rtol * bn2;
   int it = 0;
   hjb_status err = HJB_OK;
   double rr = 0.0;
@@ -711,29 +735,30 @@ static hjb_status bicgstab(hjb_grid* g, double dt, const uint8_t* pol, const dou
     // r = F - A x ; rhat = r ; p = r
     launch_operator<D>(g, L, C, OP_RESID, 0, dt, 0.0, pol, x, F, g->r, nullptr);
     LAUNCH(HJB_KC_VECTOR, L.n_own, 24.0 * L.n_own, 2.0 * L.n_own,
-           k_bicg_init<D><<<nb, kThreads, 0, st>>>(L, g->r, g->rhat, g->p, g->partial));
+           k_bicg_init<D><<<dims(g, L, (const void*)k_bicg_init<D>), kTX, 0, st>>>(L, g->r, g->rhat, g->p, g->partial));
     CKL();
-    rr = host_finalize(g, nb, 0u, SC_INIT, &err);
+    rr = host_finalize(g, g->nblk_last, 0u, SC_INIT, &err);
     if (err != HJB_OK) return err;
     if (!std::isfinite(rr)) return fail(HJB_ERR_NONFINITE, "non-finite residual");
+    if (restart == 0 && eta > 0.0) tol = std::max(tol, eta * std::sqrt(rr));
     if (std::sqrt(rr) <= tol) { converged = true; break; }
     bool restart_needed = false;
     int inner = 0;
     while (it < sp->krylov_maxit) {
       if (inner > 0)
         LAUNCH(HJB_KC_VECTOR, L.n_own, 32.0 * L.n_own, 4.0 * L.n_own,
-               k_bicg_p<D><<<nb, kThreads, 0, st>>>(L, g->S, g->r, g->p, g->v));
+               k_bicg_p<D><<<dims(g, L, (const void*)k_bicg_p<D>), kTX, 0, st>>>(L, g->S, g->r, g->p, g->v));
       TRY(precond(g, mg, g->p, g->phat));
       launch_operator<D>(g, L, C, OP_APPLY, 1, dt, 0.0, pol, g->phat, nullptr, g->v, g->rhat);
-      LAUNCH(HJB_KC_REDUCE, nb, 16.0 * nb, 2.0 * nb, k_finalize<<<1, 1024, 0, st>>>(g->partial, nb, g->red, 0u, g->S, SC_AFTER_V));
+      { const int nb = g->nblk_last; LAUNCH(HJB_KC_REDUCE, nb, 16.0 * nb, 2.0 * nb, k_finalize<<<1, 1024, 0, st>>>(g->partial, nb, g->red, 0u, g->S, SC_AFTER_V)); }
       LAUNCH(HJB_KC_VECTOR, L.n_own, 24.0 * L.n_own, 4.0 * L.n_own,
-             k_bicg_s<D><<<nb, kThreads, 0, st>>>(L, g->S, g->r, g->v, g->s, g->partial));
+             k_bicg_s<D><<<dims(g, L, (const void*)k_bicg_s<D>), kTX, 0, st>>>(L, g->S, g->r, g->v, g->s, g->partial));
       TRY(precond(g, mg, g->s, g->shat));
       launch_operator<D>(g, L, C, OP_APPLY, 2, dt, 0.0, pol, g->shat, nullptr, g->t, g->s);
-      LAUNCH(HJB_KC_REDUCE, nb, 16.0 * nb, 2.0 * nb, k_finalize<<<1, 1024, 0, st>>>(g->partial, nb, g->red, 0u, g->S, SC_AFTER_T));
+      { const int nb = g->nblk_last; LAUNCH(HJB_KC_REDUCE, nb, 16.0 * nb, 2.0 * nb, k_finalize<<<1, 1024, 0, st>>>(g->partial, nb, g->red, 0u, g->S, SC_AFTER_T)); }
       LAUNCH(HJB_KC_VECTOR, L.n_own, 64.0 * L.n_own, 10.0 * L.n_own,
-             k_bicg_x<D><<<nb, kThreads, 0, st>>>(L, g->S, x, g->phat, g->shat, g->s, g->t, g->r, g->rhat, g->partial));
-      LAUNCH(HJB_KC_REDUCE, nb, 16.0 * nb, 2.0 * nb, k_finalize<<<1, 1024, 0, st>>>(g->partial, nb, g->red, 0u, g->S, SC_AFTER_R));
+             k_bicg_x<D><<<dims(g, L, (const void*)k_bicg_x<D>), kTX, 0, st>>>(L, g->S, x, g->phat, g->shat, g->s, g->t, g->r, g->rhat, g->partial));
+      { const int nb = g->nblk_last; LAUNCH(HJB_KC_REDUCE, nb, 16.0 * nb, 2.0 * nb, k_finalize<<<1, 1024, 0, st>>>(g->partial, nb, g->red, 0u, g->S, SC_AFTER_R)); }
       CKL();
       CK(cudaMemcpyAsync(g->hS, g->S, sizeof(KScal), cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
@@ -826,6 +851,7 @@ extern "C" hjb_status hjb_step(hjb_grid_t g, double dt, const double* U_prev, do
   hjb_step_stats S{};
   float ms;
   hjb_status result = HJB_OK;
+  bool last_exact = true;  // the last policy evaluation reached krylov_rtol
   for (int it = 1; it <= sp->max_pi; ++it) {
     hjb_pi_stats pis{};
     cudaEventRecord(g->ev[0], st);
@@ -838,13 +864,20 @@ extern "C" hjb_status hjb_step(hjb_grid_t g, double dt, const double* U_prev, do
     S.changed[slot] = pis.changed;
     S.R[slot] = pis.R_max;
     S.final_R = pis.R_max;
-    if (it > 1 && (pis.changed == 0 || pis.R_max <= sp->tol_pi)) break;
+    // stop: nonlinear residual certificate (any iterate), or a stable policy whose evaluation was exact
+    if (it > 1 && (pis.R_max <= sp->tol_pi || (pis.changed == 0 && last_exact))) break;
     if (it == sp->max_pi) { result = fail(HJB_ERR_NOT_CONVERGED, "policy iteration hit max_pi"); break; }
+    const bool settled = (it > 1 && pis.changed == 0);  // only reached after an inexact solve
     cudaEventRecord(g->ev[0], st);
-    if (sp->use_mg) TRY(hjb_mg_setup(g, dt, dpol, &sp->mg));
+    if (sp->use_mg && !(settled && g->mg_ready && g->mg_pol0 == dpol && g->mg_dt == dt))
+      TRY(hjb_mg_setup(g, dt, dpol, &sp->mg));
     cudaEventRecord(g->ev[1], st);
     hjb_solve_stats ss{};
-    hjb_status s = g->D == 2 ? bicgstab<2>(g, dt, dpol, g->F, dU, sp, &ss) : bicgstab<3>(g, dt, dpol, g->F, dU, sp, &ss);
+    // inexact Howard: while the policy still changes, evaluate it only to eta * ||r_0||
+    const double eta = settled ? 0.0 : sp->pi_forcing;
+    hjb_status s = g->D == 2 ? bicgstab<2>(g, dt, dpol, g->F, dU, sp, &ss, eta)
+                             : bicgstab<3>(g, dt, dpol, g->F, dU, sp, &ss, eta);
+    last_exact = (ss.rres <= sp->krylov_rtol);
     cudaEventRecord(g->ev[2], st);
     cudaEventSynchronize(g->ev[2]);
     cudaEventElapsedTime(&ms, g->ev[0], g->ev[1]);

@@ -1,4 +1,4 @@
-// hjb_device.cuh -- sm_100a device code for the implicit LISL/HJB hot path.
+// hjb_device.cuh -- sm_100a device code for the implicit LISL/HJB hot path (fp64).
 //
 // Scheme (arXiv:1605.04821): Scheme 2 steps y+-_p = +-k sigma_p, y_{P+1} = k^2 b (PAPER.md:95-96,
 // k = sqrt(h)), truncated to the box with mu = largest value in (0,1] keeping the segment in
@@ -8,17 +8,23 @@
 //     (A x)_j = x_j - dt [ sum_e w_e (I x(z_e) - x_j) + c_j x_j ],  w_e = {A,B}/(2k^2), 1/(mu_d k^2)
 // and its diagonal D_j = 1 + dt (sum_e w_e - sum_e w_e w_j(z_e) - c_j).
 //
+// Geometry is done in GRID UNITS: a node is its integer multi-index i, a step y becomes the offset
+// o = y/h in cells, an endpoint is t = i + mu o and its cell is floor(t) (clamped to n-2) with
+// fraction s = t - floor(t).  This is the oracle's physical-coordinate formula (z - lo)/h divided
+// through by h; the two differ only by rounding (~1e-16 relative in s), and every decision on the
+// way (inside/outside, cell choice) is continuous in the result (SURVEY hard part 4).
+//
 // Everything is recomputed on the fly per (node, control): no per-policy matrix is stored.
-// Thread mapping: one thread per interior node, consecutive threads = consecutive x1 (coalesced
-// gathers: for x-independent sigma the endpoints of a warp are consecutive nodes), grid-stride over
-// the owned interior in row order so the +-reach rows in flight stay L2-resident.
+// Thread mapping: a 2D launch, threads along x1 (coalesced; for x-independent sigma the endpoints
+// of a warp are consecutive nodes), blocks striding over interior rows so the +-reach rows in
+// flight form a band that stays L2-resident.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
 
 namespace hjb {
 
-constexpr int kThreads = 256;
+constexpr int kTX = 128;   // threads per block (along x1)
 constexpr int kMaxP = 3;
 constexpr int kMaxQ = 16;
 
@@ -26,14 +32,15 @@ constexpr int kMaxQ = 16;
 struct LevelDev {
   int n;               // nodes per dimension on this level
   int nI;              // n - 2 interior nodes per dimension
+  int nrows;           // owned interior lines along x1 (n_own / nI)
   int64_t row_elems;   // n^(D-1)
   int64_t local_row0;  // global slowest-axis row of local row 0
   int64_t local_rows;  // rows held in a local array
   int64_t row_first;   // first owned interior row (global, slowest axis)
   int64_t n_own;       // owned interior nodes
-  double lo, hi, h, inv_h;
-  double k;            // SL diffusion step scale (k = sqrt(h_fine) by default)
-  double k2;           // drift step scale and denominator (= h on the fine level, exactly)
+  double h, nm1;       // mesh width; n - 1
+  double kh;           // diffusion step in cells: k / h (k = sqrt(h_fine) by default)
+  double k2h;          // drift step in cells: k^2 / h
   double inv_2k2, inv_k2;
 };
 
@@ -55,38 +62,46 @@ struct CoefDev {
 };
 
 template <int D>
-struct NodeCtx {
+struct Node {
   int i[D];          // global multi-index
-  double x[D];       // coordinates
-  int64_t loc;       // local linear offset
+  double fi[D];      // i as double
+  double dist[D];    // min(i, n-1-i): an offset |o| <= dist keeps both i+o and i-o in the box
+  int loc;           // local linear offset (local arrays hold < 2^31 elements)
   double sc[kMaxP];  // sigma scale per column
   double sn[kMaxP][D];
   double bs, bn[D], cn;
 };
 
-// interior flat index t -> node
+// interior line `row` (0..nrows), column `col` (0..nI) -> node
 template <int D>
-__device__ __forceinline__ void node_from_interior(const LevelDev& L, int64_t t, NodeCtx<D>& nd) {
-  const int64_t nI = L.nI;
+__device__ __forceinline__ void node_at(const LevelDev& L, int col, int row, Node<D>& nd) {
+  nd.i[0] = 1 + col;
   if (D == 2) {
-    int64_t r = t / nI;
-    nd.i[0] = 1 + (int)(t - r * nI);
-    nd.i[1] = (int)(L.row_first + r);
-    nd.loc = (int64_t)(nd.i[1] - L.local_row0) * L.n + nd.i[0];
+    nd.i[1] = (int)L.row_first + row;
+    nd.loc = (nd.i[1] - (int)L.local_row0) * L.n + nd.i[0];
   } else {
-    int64_t r = t / nI;
-    nd.i[0] = 1 + (int)(t - r * nI);
-    int64_t r2 = r / nI;
-    nd.i[1] = 1 + (int)(r - r2 * nI);
-    nd.i[2] = (int)(L.row_first + r2);
-    nd.loc = ((int64_t)(nd.i[2] - L.local_row0) * L.n + nd.i[1]) * L.n + nd.i[0];
+    const int r2 = row / L.nI;
+    nd.i[1] = 1 + (row - r2 * L.nI);
+    nd.i[D - 1] = (int)L.row_first + r2;
+    nd.loc = ((nd.i[D - 1] - (int)L.local_row0) * L.n + nd.i[1]) * L.n + nd.i[0];
   }
 #pragma unroll
-  for (int d = 0; d < D; ++d) nd.x[d] = L.lo + (double)nd.i[d] * L.h;
+  for (int d = 0; d < D; ++d) {
+    nd.fi[d] = (double)nd.i[d];
+    const int m = min(nd.i[d], L.n - 1 - nd.i[d]);
+    nd.dist[d] = (double)m;
+  }
 }
 
 template <int D>
-__device__ __forceinline__ void load_fields(const CoefDev& C, NodeCtx<D>& nd) {
+__device__ __forceinline__ int interior_offset(const LevelDev& L, int col, int row) {
+  if (D == 2) return ((int)L.row_first + row - (int)L.local_row0) * L.n + 1 + col;
+  const int r2 = row / L.nI;
+  return (((int)L.row_first + r2 - (int)L.local_row0) * L.n + 1 + (row - r2 * L.nI)) * L.n + 1 + col;
+}
+
+template <int D>
+__device__ __forceinline__ void load_fields(const CoefDev& C, Node<D>& nd) {
   const int64_t j = nd.loc;
 #pragma unroll
   for (int p = 0; p < kMaxP; ++p) {
@@ -107,67 +122,82 @@ __device__ __forceinline__ void load_fields(const CoefDev& C, NodeCtx<D>& nd) {
   nd.cn = C.c_node ? __ldg(C.c_node + j) : 0.0;
 }
 
-// ----------------------------------------------------------------------------- truncation
-// mu = largest value in (0,1] with x + [0,mu] y inside [lo,hi]^D;
-// bd = binding dimension (-1 if untruncated).
+// ----------------------------------------------------------------------------- cells
+// floor split of t = i + o for an UNTRUNCATED offset: c = i + floor(o), s = o - floor(o), via
+// round-to-nearest by the 1.5*2^52 magic constant (no fp64<->int conversion instructions).
+struct Split {
+  int c;
+  double s;
+};
+__device__ __forceinline__ void split_pm(double o, int i, int nm2, Split& p, Split& m) {
+  const double magic = 6755399441055744.0;  // 1.5 * 2^52
+  const double big = o + magic;
+  const int r = __double2loint(big);          // rint(o) as an integer
+  const double rf = big - magic;              // rint(o)
+  const double f = o - rf;                    // in [-0.5, 0.5]
+  // +o: floor = r - (f < 0)
+  const bool neg = f < 0.0;
+  p.c = i + r - (neg ? 1 : 0);
+  p.s = neg ? f + 1.0 : f;
+  // -o: rint(-o) = -r, fraction -f; floor = -r - (-f < 0)
+  const bool pos = f > 0.0;
+  m.c = i - r - (pos ? 1 : 0);
+  m.s = pos ? 1.0 - f : -f;
+  if (p.c > nm2) { p.c = nm2; p.s = 1.0; }  // endpoint exactly on the upper face
+  if (m.c > nm2) { m.c = nm2; m.s = 1.0; }
+}
+
+// general (possibly truncated) endpoint t = i + mu o, binding coordinate snapped onto the face
 template <int D>
-__device__ __forceinline__ double ray_mu(const LevelDev& L, const double* x, const double* y, int& bd) {
+__device__ __forceinline__ void cell_general(const LevelDev& L, const Node<D>& nd, const double* o, double mu,
+                                             int bd, int* c, double* s) {
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    double t = fma(mu, o[d], nd.fi[d]);
+    t = fmin(fmax(t, 0.0), L.nm1);
+    if (d == bd) t = (o[d] > 0.0) ? L.nm1 : 0.0;
+    double fl = floor(t);
+    int ci = (int)fl;
+    if (ci > L.n - 2) { ci = L.n - 2; fl = (double)ci; }
+    c[d] = ci;
+    s[d] = t - fl;
+  }
+}
+
+// truncation of the ray i + [0,1] o: mu = largest value in (0,1] keeping it in [0, n-1]^D
+// (PAPER.md:224, 291-293); bd = binding dimension (-1 if untruncated).
+template <int D>
+__device__ __forceinline__ double ray_mu(const LevelDev& L, const Node<D>& nd, const double* o, int& bd) {
   double mu = 1.0;
   bd = -1;
 #pragma unroll
   for (int d = 0; d < D; ++d) {
-    const double z = x[d] + y[d];
-    if (z > L.hi) {
-      const double t = (L.hi - x[d]) / y[d];
+    const double room_hi = L.nm1 - nd.fi[d];
+    if (o[d] > room_hi) {
+      const double t = room_hi / o[d];
       if (t < mu) { mu = t; bd = d; }
-    } else if (z < L.lo) {
-      const double t = (L.lo - x[d]) / y[d];
+    } else if (o[d] < -nd.fi[d]) {
+      const double t = -nd.fi[d] / o[d];
       if (t < mu) { mu = t; bd = d; }
     }
   }
   return mu;
 }
 
-// endpoint z = x + s*mu*y with the binding coordinate put exactly on the face (reading: snap)
-template <int D>
-__device__ __forceinline__ void endpoint(const LevelDev& L, const double* x, const double* y, double smu,
-                                         int bd, double* z) {
-#pragma unroll
-  for (int d = 0; d < D; ++d) {
-    double v = fma(smu, y[d], x[d]);
-    v = fmin(fmax(v, L.lo), L.hi);
-    if (d == bd) v = (smu * y[d] > 0.0) ? L.hi : L.lo;
-    z[d] = v;
-  }
-}
-
 // ----------------------------------------------------------------------------- interpolation
-// cell of z: c = clamp(floor((z-lo)/h), 0, n-2), s = (z-lo)/h - c (reading vii)
-template <int D>
-__device__ __forceinline__ void cell_of(const LevelDev& L, const double* z, int* c, double* s) {
-#pragma unroll
-  for (int d = 0; d < D; ++d) {
-    const double t = (z[d] - L.lo) * L.inv_h;
-    int ci = (int)floor(t);
-    ci = ci < 0 ? 0 : (ci > L.n - 2 ? L.n - 2 : ci);
-    c[d] = ci;
-    s[d] = t - (double)ci;
-  }
-}
-
 template <int D>
 __device__ __forceinline__ double gather_interp(const LevelDev& L, const double* __restrict__ v, const int* c,
                                                 const double* s) {
   if (D == 2) {
-    const double* p = v + ((int64_t)(c[1] - L.local_row0) * L.n + c[0]);
+    const double* p = v + ((c[1] - (int)L.local_row0) * L.n + c[0]);
     const double v00 = __ldg(p), v10 = __ldg(p + 1);
     const double v01 = __ldg(p + L.n), v11 = __ldg(p + L.n + 1);
     const double a = fma(s[0], v10 - v00, v00);
     const double b = fma(s[0], v11 - v01, v01);
     return fma(s[1], b - a, a);
   } else {
-    const int64_t n = L.n, nn = n * n;
-    const double* p = v + (((int64_t)(c[2] - L.local_row0) * n + c[1]) * n + c[0]);
+    const int n = L.n, nn = n * n;
+    const double* p = v + (((c[2] - (int)L.local_row0) * n + c[1]) * n + c[0]);
     const double v000 = __ldg(p), v100 = __ldg(p + 1);
     const double v010 = __ldg(p + n), v110 = __ldg(p + n + 1);
     const double v001 = __ldg(p + nn), v101 = __ldg(p + nn + 1);
@@ -200,70 +230,83 @@ __device__ __forceinline__ double self_weight(const int* i, const int* c, const 
 // wsum = sum_e w_e                (= sum_p (A_p+B_p)/(2k^2) + 1/(mu_d k^2))
 // self = sum_e w_e w_j(z_e)       (only if SELF: l_hat_jj of P:399-401)
 template <int D, bool GATHER, bool SELF>
-__device__ __forceinline__ void row_eval(const LevelDev& L, const CoefDev& C, const NodeCtx<D>& nd, int a,
+__device__ __forceinline__ void row_eval(const LevelDev& L, const CoefDev& C, const Node<D>& nd, int a,
                                          const double* __restrict__ v, double& acc, double& wsum,
                                          double& self) {
   acc = 0.0;
   wsum = 0.0;
   self = 0.0;
-  const double* sd = C.sigma_dir + (int64_t)a * C.P * D;
+  const double* sd = C.sigma_dir + a * C.P * D;
+  const int nm2 = L.n - 2;
 #pragma unroll
   for (int p = 0; p < kMaxP; ++p) {
     if (p >= C.P) break;
-    double y[D];
-    bool nz = false;
+    double o[D];
+    bool nz = false, inside = true;
 #pragma unroll
     for (int d = 0; d < D; ++d) {
-      y[d] = L.k * fma(nd.sc[p], __ldg(sd + p * D + d), nd.sn[p][d]);
-      nz |= (y[d] != 0.0);
+      o[d] = L.kh * fma(nd.sc[p], __ldg(sd + p * D + d), nd.sn[p][d]);
+      nz |= (o[d] != 0.0);
+      inside &= (fabs(o[d]) <= nd.dist[d]);
     }
     if (!nz) continue;  // zero step: its two terms cancel exactly
-    double ym[D];
+    if (inside) {
+      // untruncated pair (A = B = 1): endpoints i +- o
+      int cp[D], cm[D];
+      double sp[D], sm[D];
 #pragma unroll
-    for (int d = 0; d < D; ++d) ym[d] = -y[d];
+      for (int d = 0; d < D; ++d) {
+        Split P_, M_;
+        split_pm(o[d], nd.i[d], nm2, P_, M_);
+        cp[d] = P_.c; sp[d] = P_.s;
+        cm[d] = M_.c; sm[d] = M_.s;
+      }
+      wsum += 2.0 * L.inv_2k2;
+      if (GATHER) acc = fma(L.inv_2k2, gather_interp<D>(L, v, cp, sp) + gather_interp<D>(L, v, cm, sm), acc);
+      if (SELF) self = fma(L.inv_2k2, self_weight<D>(nd.i, cp, sp) + self_weight<D>(nd.i, cm, sm), self);
+      continue;
+    }
+    double om[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) om[d] = -o[d];
     int bp, bm;
-    const double mup = ray_mu<D>(L, nd.x, y, bp);
-    const double mum = ray_mu<D>(L, nd.x, ym, bm);
+    const double mup = ray_mu<D>(L, nd, o, bp);
+    const double mum = ray_mu<D>(L, nd, om, bm);
     double A = 1.0, B = 1.0;
     if (bp >= 0 || bm >= 0) {
       const double sum = mup + mum;
       A = 2.0 / (mup * sum);
       B = 2.0 / (mum * sum);
     }
-    double zp[D], zm[D];
-    endpoint<D>(L, nd.x, y, mup, bp, zp);
-    endpoint<D>(L, nd.x, y, -mum, bm, zm);
     const double wA = A * L.inv_2k2, wB = B * L.inv_2k2;
     wsum += wA + wB;
     int c[D];
     double s[D];
-    cell_of<D>(L, zp, c, s);
+    cell_general<D>(L, nd, o, mup, bp, c, s);
     if (GATHER) acc = fma(wA, gather_interp<D>(L, v, c, s), acc);
     if (SELF) self = fma(wA, self_weight<D>(nd.i, c, s), self);
-    cell_of<D>(L, zm, c, s);
+    cell_general<D>(L, nd, om, mum, bm, c, s);
     if (GATHER) acc = fma(wB, gather_interp<D>(L, v, c, s), acc);
     if (SELF) self = fma(wB, self_weight<D>(nd.i, c, s), self);
   }
   // drift pair: y_{P+1} = k^2 b, both endpoints equal, A = B = 1/mu (total weight 2/(mu 2k^2))
   {
-    const double* bd_ = C.b_dir + (int64_t)a * D;
-    double y[D];
+    const double* bd_ = C.b_dir + a * D;
+    double o[D];
     bool nz = false;
 #pragma unroll
     for (int d = 0; d < D; ++d) {
-      y[d] = L.k2 * fma(nd.bs, __ldg(bd_ + d), nd.bn[d]);
-      nz |= (y[d] != 0.0);
+      o[d] = L.k2h * fma(nd.bs, __ldg(bd_ + d), nd.bn[d]);
+      nz |= (o[d] != 0.0);
     }
     if (nz) {
       int bdim;
-      const double mu = ray_mu<D>(L, nd.x, y, bdim);
-      double z[D];
-      endpoint<D>(L, nd.x, y, mu, bdim, z);
-      const double w = (bdim >= 0) ? L.inv_k2 / mu : L.inv_k2;
-      wsum += w;
+      const double mu = ray_mu<D>(L, nd, o, bdim);
       int c[D];
       double s[D];
-      cell_of<D>(L, z, c, s);
+      cell_general<D>(L, nd, o, mu, bdim, c, s);
+      const double w = (bdim >= 0) ? L.inv_k2 / mu : L.inv_k2;
+      wsum += w;
       if (GATHER) acc = fma(w, gather_interp<D>(L, v, c, s), acc);
       if (SELF) self = fma(w, self_weight<D>(nd.i, c, s), self);
     }
@@ -282,10 +325,13 @@ __device__ __forceinline__ double warp_max(double v) {
   return v;
 }
 
-// block-reduce NV values (sum, or max if MAXMASK bit set) and write partial[blockIdx.x*NV + k]
+__device__ __forceinline__ int block_linear() { return blockIdx.y * gridDim.x + blockIdx.x; }
+
+// block-reduce NV values (sum, or max if MAXMASK bit set) and write partial[block*NV + k]
 template <int NV>
 __device__ __forceinline__ void block_reduce_store(double (&val)[NV], double* partial, unsigned maxmask = 0u) {
-  __shared__ double sm[NV][kThreads / 32];
+  constexpr int NW = kTX / 32;
+  __shared__ double sm[NV][NW];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
@@ -297,9 +343,9 @@ __device__ __forceinline__ void block_reduce_store(double (&val)[NV], double* pa
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
       const bool mx = (maxmask >> k) & 1u;
-      double v = lane < (kThreads / 32) ? sm[k][lane] : (mx ? -INFINITY : 0.0);
+      double v = lane < NW ? sm[k][lane] : (mx ? -INFINITY : 0.0);
       v = mx ? warp_max(v) : warp_sum(v);
-      if (lane == 0) partial[blockIdx.x * NV + k] = v;
+      if (lane == 0) partial[block_linear() * NV + k] = v;
     }
   }
 }

@@ -4,6 +4,11 @@
 
 namespace hjb {
 
+// every owned interior node of level L: (col, row) -> x1 index 1+col, line `row`
+#define FOR_INTERIOR(L)                                                       \
+  for (int row = blockIdx.y; row < (L).nrows; row += gridDim.y)              \
+    for (int col = blockIdx.x * kTX + threadIdx.x; col < (L).nI; col += gridDim.x * kTX)
+
 // ================================================================== operator-family kernel
 enum OpMode : int {
   OP_APPLY = 0,    // y = A x                    (+ optional dots with y)
@@ -14,7 +19,7 @@ enum OpMode : int {
 
 // NDOT: 0, 1 -> partial[0] = sum y*u ; 2 -> partial[0] = sum y*u, partial[1] = sum y*y
 template <int D, int MODE, int NDOT>
-__global__ void __launch_bounds__(kThreads) k_operator(LevelDev L, CoefDev C, double dt, double omega,
+__global__ void __launch_bounds__(kTX) k_operator(LevelDev L, CoefDev C, double dt, double omega,
                                                       const uint8_t* __restrict__ pol,
                                                       const double* __restrict__ x,
                                                       const double* __restrict__ b, double* __restrict__ y,
@@ -22,10 +27,9 @@ __global__ void __launch_bounds__(kThreads) k_operator(LevelDev L, CoefDev C, do
   constexpr bool GATHER = (MODE != OP_JACOBI0);
   constexpr bool SELF = (MODE == OP_JACOBI || MODE == OP_JACOBI0);
   double dots[2] = {0.0, 0.0};
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < L.n_own; t += stride) {
-    NodeCtx<D> nd;
-    node_from_interior<D>(L, t, nd);
+  FOR_INTERIOR(L) {
+    Node<D> nd;
+    node_at<D>(L, col, row, nd);
     load_fields<D>(C, nd);
     const int a = pol[nd.loc];
     double acc, wsum, self;
@@ -58,16 +62,15 @@ __global__ void __launch_bounds__(kThreads) k_operator(LevelDev L, CoefDev C, do
 // For every owned interior node: H^a = acc_a - wsum_a U_j + c^a U_j + f^a for all a (lowest-index
 // argmin), policy/F outputs, partials: [max R, changed count].
 template <int D>
-__global__ void __launch_bounds__(kThreads) k_search(LevelDev L, CoefDev C, double dt,
+__global__ void __launch_bounds__(kTX) k_search(LevelDev L, CoefDev C, double dt,
                                                     const double* __restrict__ U,
                                                     const double* __restrict__ Uprev,
                                                     uint8_t* __restrict__ pol, double* __restrict__ F,
                                                     double* partial) {
   double red[2] = {0.0, 0.0};
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < L.n_own; t += stride) {
-    NodeCtx<D> nd;
-    node_from_interior<D>(L, t, nd);
+  FOR_INTERIOR(L) {
+    Node<D> nd;
+    node_at<D>(L, col, row, nd);
     load_fields<D>(C, nd);
     double feat[kMaxQ];
 #pragma unroll
@@ -165,29 +168,14 @@ __global__ void __launch_bounds__(1024) k_finalize(const double* __restrict__ pa
   }
 }
 
-// interior-node iteration helper for vector kernels
-template <int D>
-__device__ __forceinline__ int64_t interior_loc(const LevelDev& L, int64_t t) {
-  const int64_t nI = L.nI;
-  if (D == 2) {
-    const int64_t r = t / nI;
-    return (L.row_first + r - L.local_row0) * L.n + 1 + (t - r * nI);
-  } else {
-    const int64_t r = t / nI;
-    const int64_t r2 = r / nI;
-    return ((L.row_first + r2 - L.local_row0) * L.n + 1 + (r - r2 * nI)) * L.n + 1 + (t - r * nI);
-  }
-}
-
 // r_hat = r, p = r ; partial: (r,r)
 template <int D>
-__global__ void __launch_bounds__(kThreads) k_bicg_init(LevelDev L, const double* __restrict__ r,
+__global__ void __launch_bounds__(kTX) k_bicg_init(LevelDev L, const double* __restrict__ r,
                                                        double* __restrict__ rhat, double* __restrict__ p,
                                                        double* partial) {
   double red[2] = {0.0, 0.0};
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < L.n_own; t += stride) {
-    const int64_t j = interior_loc<D>(L, t);
+  FOR_INTERIOR(L) {
+    const int j = interior_offset<D>(L, col, row);
     const double v = r[j];
     rhat[j] = v;
     p[j] = v;
@@ -198,28 +186,26 @@ __global__ void __launch_bounds__(kThreads) k_bicg_init(LevelDev L, const double
 
 // p = r + beta (p - omega v),  beta = (rho/rho_old)(alpha/omega)
 template <int D>
-__global__ void __launch_bounds__(kThreads) k_bicg_p(LevelDev L, const KScal* __restrict__ S,
+__global__ void __launch_bounds__(kTX) k_bicg_p(LevelDev L, const KScal* __restrict__ S,
                                                     const double* __restrict__ r, double* __restrict__ p,
                                                     const double* __restrict__ v) {
   const double beta = (S->rho / S->rho_old) * (S->alpha / S->omega);
   const double om = S->omega;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < L.n_own; t += stride) {
-    const int64_t j = interior_loc<D>(L, t);
+  FOR_INTERIOR(L) {
+    const int j = interior_offset<D>(L, col, row);
     p[j] = fma(beta, fma(-om, v[j], p[j]), r[j]);
   }
 }
 
 // s = r - alpha v ; partial (s,s)
 template <int D>
-__global__ void __launch_bounds__(kThreads) k_bicg_s(LevelDev L, const KScal* __restrict__ S,
+__global__ void __launch_bounds__(kTX) k_bicg_s(LevelDev L, const KScal* __restrict__ S,
                                                     const double* __restrict__ r, const double* __restrict__ v,
                                                     double* __restrict__ s, double* partial) {
   const double al = S->alpha;
   double red[2] = {0.0, 0.0};
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < L.n_own; t += stride) {
-    const int64_t j = interior_loc<D>(L, t);
+  FOR_INTERIOR(L) {
+    const int j = interior_offset<D>(L, col, row);
     const double sv = fma(-al, v[j], r[j]);
     s[j] = sv;
     red[0] = fma(sv, sv, red[0]);
@@ -229,7 +215,7 @@ __global__ void __launch_bounds__(kThreads) k_bicg_s(LevelDev L, const KScal* __
 
 // x += alpha phat + omega shat ; r = s - omega t ; partials (rhat, r), (r, r)
 template <int D>
-__global__ void __launch_bounds__(kThreads) k_bicg_x(LevelDev L, const KScal* __restrict__ S,
+__global__ void __launch_bounds__(kTX) k_bicg_x(LevelDev L, const KScal* __restrict__ S,
                                                     double* __restrict__ x, const double* __restrict__ phat,
                                                     const double* __restrict__ shat,
                                                     const double* __restrict__ s, const double* __restrict__ tv,
@@ -237,9 +223,8 @@ __global__ void __launch_bounds__(kThreads) k_bicg_x(LevelDev L, const KScal* __
                                                     double* partial) {
   const double al = S->alpha, om = S->omega;
   double red[2] = {0.0, 0.0};
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < L.n_own; t += stride) {
-    const int64_t j = interior_loc<D>(L, t);
+  FOR_INTERIOR(L) {
+    const int j = interior_offset<D>(L, col, row);
     x[j] = fma(om, shat[j], fma(al, phat[j], x[j]));
     const double rv = fma(-om, tv[j], s[j]);
     r[j] = rv;
@@ -251,11 +236,10 @@ __global__ void __launch_bounds__(kThreads) k_bicg_x(LevelDev L, const KScal* __
 
 // squared 2-norm and max-norm partials of a vector over owned interior nodes
 template <int D>
-__global__ void __launch_bounds__(kThreads) k_norms(LevelDev L, const double* __restrict__ v, double* partial) {
+__global__ void __launch_bounds__(kTX) k_norms(LevelDev L, const double* __restrict__ v, double* partial) {
   double red[2] = {0.0, 0.0};
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < L.n_own; t += stride) {
-    const double a = v[interior_loc<D>(L, t)];
+  FOR_INTERIOR(L) {
+    const double a = v[interior_offset<D>(L, col, row)];
     red[0] = fma(a, a, red[0]);
     red[1] = fmax(red[1], (a == a) ? fabs(a) : INFINITY);
   }
@@ -263,11 +247,10 @@ __global__ void __launch_bounds__(kThreads) k_norms(LevelDev L, const double* __
 }
 
 template <int D>
-__global__ void __launch_bounds__(kThreads) k_copy_interior(LevelDev L, const double* __restrict__ a,
+__global__ void __launch_bounds__(kTX) k_copy_interior(LevelDev L, const double* __restrict__ a,
                                                            double* __restrict__ b) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < L.n_own; t += stride) {
-    const int64_t j = interior_loc<D>(L, t);
+  FOR_INTERIOR(L) {
+    const int j = interior_offset<D>(L, col, row);
     b[j] = a[j];
   }
 }
@@ -309,12 +292,11 @@ __global__ void k_scatter_psi(LevelDev L, int64_t nb, const double* __restrict__
 // ================================================================== multigrid transfers
 // full weighting r_f -> b_c at coarse interior nodes (weights 1/4,1/2,1/4 per dim)
 template <int D>
-__global__ void __launch_bounds__(kThreads) k_restrict(LevelDev Lf, LevelDev Lc, const double* __restrict__ rf,
+__global__ void __launch_bounds__(kTX) k_restrict(LevelDev Lf, LevelDev Lc, const double* __restrict__ rf,
                                                       double* __restrict__ bc) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < Lc.n_own; t += stride) {
-    NodeCtx<D> nd;
-    node_from_interior<D>(Lc, t, nd);
+  FOR_INTERIOR(Lc) {
+    Node<D> nd;
+    node_at<D>(Lc, col, row, nd);
     double acc = 0.0;
     if (D == 2) {
       const int64_t base = (int64_t)(2 * nd.i[1] - Lf.local_row0) * Lf.n + 2 * nd.i[0];
@@ -350,12 +332,11 @@ __global__ void __launch_bounds__(kThreads) k_restrict(LevelDev Lf, LevelDev Lc,
 
 // x_f += P e_c (multilinear prolongation) at fine interior nodes
 template <int D>
-__global__ void __launch_bounds__(kThreads) k_prolong_add(LevelDev Lf, LevelDev Lc, const double* __restrict__ ec,
+__global__ void __launch_bounds__(kTX) k_prolong_add(LevelDev Lf, LevelDev Lc, const double* __restrict__ ec,
                                                          double* __restrict__ xf) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < Lf.n_own; t += stride) {
-    NodeCtx<D> nd;
-    node_from_interior<D>(Lf, t, nd);
+  FOR_INTERIOR(Lf) {
+    Node<D> nd;
+    node_at<D>(Lf, col, row, nd);
     int c0[D], c1[D];
     double w1[D];
 #pragma unroll
@@ -427,28 +408,35 @@ __global__ void k_inject_f64(LevelDev Lf, LevelDev Lc, const double* __restrict_
 }
 
 // ================================================================== coarsest level (dense)
-// assemble the dense interior matrix of the coarsest level: A[j][i] (row-major, Nc x Nc)
+// interior node t (0..n_own) of a single-rank level -> (col, row)
+template <int D>
+__device__ __forceinline__ void coarse_node(const LevelDev& L, int t, Node<D>& nd) {
+  const int row = t / L.nI;
+  node_at<D>(L, t - row * L.nI, row, nd);
+}
+
+// assemble the dense interior matrix of the coarsest level: A[j][i] (row-major, Nc x Nc), the same
+// truncated Scheme-2 row as row_eval (general path for every endpoint)
 template <int D>
 __global__ void k_coarse_assemble(LevelDev L, CoefDev C, double dt, const uint8_t* __restrict__ pol,
                                   double* __restrict__ A) {
-  const int64_t Nc = L.n_own;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < Nc; t += (int64_t)gridDim.x * blockDim.x) {
-    NodeCtx<D> nd;
-    node_from_interior<D>(L, t, nd);
+  const int Nc = (int)L.n_own;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < Nc; t += gridDim.x * blockDim.x) {
+    Node<D> nd;
+    coarse_node<D>(L, t, nd);
     load_fields<D>(C, nd);
     const int a = pol[nd.loc];
-    double* row = A + t * Nc;
+    double* row = A + (int64_t)t * Nc;
     double wsum = 0.0;
     const int nI = L.nI;
-    // visit every endpoint tap: emulate row_eval with explicit taps
-    auto add_tap = [&](const double* z, double w) {
+    auto add_tap = [&](const double* o, double mu, int bd, double w) {
       int c[D];
       double s[D];
-      cell_of<D>(L, z, c, s);
+      cell_general<D>(L, nd, o, mu, bd, c, s);
 #pragma unroll
       for (int m = 0; m < (1 << D); ++m) {
         double ww = w;
-        int64_t col = 0;
+        int col = 0;
         bool interior = true;
 #pragma unroll
         for (int d = D - 1; d >= 0; --d) {
@@ -461,49 +449,44 @@ __global__ void k_coarse_assemble(LevelDev L, CoefDev C, double dt, const uint8_
         if (interior && ww != 0.0) row[col] -= dt * ww;
       }
     };
-    const double* sd = C.sigma_dir + (int64_t)a * C.P * D;
+    const double* sd = C.sigma_dir + a * C.P * D;
     for (int p = 0; p < C.P; ++p) {
-      double y[D], ym[D];
+      double o[D], om[D];
       bool nz = false;
 #pragma unroll
       for (int d = 0; d < D; ++d) {
-        y[d] = L.k * fma(nd.sc[p], sd[p * D + d], nd.sn[p][d]);
-        ym[d] = -y[d];
-        nz |= (y[d] != 0.0);
+        o[d] = L.kh * fma(nd.sc[p], sd[p * D + d], nd.sn[p][d]);
+        om[d] = -o[d];
+        nz |= (o[d] != 0.0);
       }
       if (!nz) continue;
       int bp, bm;
-      const double mup = ray_mu<D>(L, nd.x, y, bp);
-      const double mum = ray_mu<D>(L, nd.x, ym, bm);
+      const double mup = ray_mu<D>(L, nd, o, bp);
+      const double mum = ray_mu<D>(L, nd, om, bm);
       double Aw = 1.0, Bw = 1.0;
       if (bp >= 0 || bm >= 0) {
         const double sum = mup + mum;
         Aw = 2.0 / (mup * sum);
         Bw = 2.0 / (mum * sum);
       }
-      double zp[D], zm[D];
-      endpoint<D>(L, nd.x, y, mup, bp, zp);
-      endpoint<D>(L, nd.x, y, -mum, bm, zm);
       wsum += (Aw + Bw) * L.inv_2k2;
-      add_tap(zp, Aw * L.inv_2k2);
-      add_tap(zm, Bw * L.inv_2k2);
+      add_tap(o, mup, bp, Aw * L.inv_2k2);
+      add_tap(om, mum, bm, Bw * L.inv_2k2);
     }
     {
-      double y[D];
+      double o[D];
       bool nz = false;
 #pragma unroll
       for (int d = 0; d < D; ++d) {
-        y[d] = L.k2 * fma(nd.bs, C.b_dir[a * D + d], nd.bn[d]);
-        nz |= (y[d] != 0.0);
+        o[d] = L.k2h * fma(nd.bs, C.b_dir[a * D + d], nd.bn[d]);
+        nz |= (o[d] != 0.0);
       }
       if (nz) {
         int bdim;
-        const double mu = ray_mu<D>(L, nd.x, y, bdim);
-        double z[D];
-        endpoint<D>(L, nd.x, y, mu, bdim, z);
+        const double mu = ray_mu<D>(L, nd, o, bdim);
         const double w = (bdim >= 0) ? L.inv_k2 / mu : L.inv_k2;
         wsum += w;
-        add_tap(z, w);
+        add_tap(o, mu, bdim, w);
       }
     }
     const double c = nd.cn + C.c_ctrl[a];
@@ -545,13 +528,17 @@ __global__ void k_coarse_solve(LevelDev L, const double* __restrict__ Ainv, cons
                                double* __restrict__ x) {
   extern __shared__ double bs[];
   const int Nc = (int)L.n_own;
-  for (int t = threadIdx.x; t < Nc; t += blockDim.x) bs[t] = b[interior_loc<D>(L, t)];
+  for (int t = threadIdx.x; t < Nc; t += blockDim.x) {
+    const int row = t / L.nI;
+    bs[t] = b[interior_offset<D>(L, t - row * L.nI, row)];
+  }
   __syncthreads();
   for (int t = threadIdx.x; t < Nc; t += blockDim.x) {
     double acc = 0.0;
-    const double* row = Ainv + (int64_t)t * Nc;
-    for (int i = 0; i < Nc; ++i) acc = fma(row[i], bs[i], acc);
-    x[interior_loc<D>(L, t)] = acc;
+    const double* rowp = Ainv + (int64_t)t * Nc;
+    for (int i = 0; i < Nc; ++i) acc = fma(rowp[i], bs[i], acc);
+    const int row = t / L.nI;
+    x[interior_offset<D>(L, t - row * L.nI, row)] = acc;
   }
 }
 

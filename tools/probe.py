@@ -14,6 +14,8 @@ ap.add_argument("--steps", type=int, default=2)
 ap.add_argument("--nu", type=int, default=2)
 ap.add_argument("--omega", type=float, default=1.0)
 ap.add_argument("--kmode", type=int, default=0)
+ap.add_argument("--eta", type=float, default=0.0)
+ap.add_argument("--profile", action="store_true")
 args = ap.parse_args()
 p = bj_config(args.cfg, n=args.n, K=args.K)
 t0 = time.time()
@@ -27,9 +29,17 @@ for s in range(1, args.steps + 1):
     fb, fc = p.f_tables(t); g.set_source(fb, fc)
     psi = packed_psi(p, t)
     torch.cuda.synchronize(); t1 = time.time()
-    st = g.step(p.dt, U, U2, pol, psi, mg=dict(nu_pre=args.nu, nu_post=args.nu, omega=args.omega, coarse_k_mode=args.kmode), raise_on_error=False)
+    if args.profile: g.profile_reset(True)
+    st = g.step(p.dt, U, U2, pol, psi, mg=dict(nu_pre=args.nu, nu_post=args.nu, omega=args.omega, coarse_k_mode=args.kmode), raise_on_error=False, pi_forcing=args.eta)
     torch.cuda.synchronize(); el = time.time() - t1
     U, U2 = U2, U
     err = (U - p.u_exact(t, torch.arange(p.N, device="cuda"))).abs().max().item()
     print(json.dumps(dict(step=s, wall_s=round(el, 4), err_vs_ustar=err, **st)), flush=True)
     print(f"  unknowns*steps/s = {p.N_interior/el:.3e}", flush=True)
+    if args.profile:
+        pr = g.profile_read()
+        for k, v in pr["classes"].items():
+            if v["launches"]:
+                gbs = v["bytes"] / max(v["ms"], 1e-9) / 1e6
+                print(f"  {k:9s} launches={v['launches']:6d} ms={v['ms']:10.3f} GB/s={gbs:8.1f} "
+                      f"TF/s={v['flops'] / max(v['ms'], 1e-9) / 1e9:7.3f}", flush=True)
