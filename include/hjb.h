@@ -93,6 +93,29 @@ typedef struct {
   double h, k;          /* mesh width and SL step k = sqrt(h)                   */
 } hjb_layout;
 
+/* Slab decomposition (host-only, no GPU needed; the same functions hjb_grid_create uses).
+ * The n-2 interior rows of the slowest axis are split into nranks contiguous blocks,
+ * rank r owning interior rows [1 + floor(r (n-2)/R), 1 + floor((r+1)(n-2)/R)).  Local arrays
+ * hold the owned rows plus `halo` rows on each side, clipped to [0, n): the Dirichlet rows 0 and
+ * n-1 live in the halo region of the first/last rank.  Every rank must own >= halo rows (so a halo
+ * comes from one neighbour), else HJB_ERR_INVALID_ARG.  halo must be >= floor(max |offset| of a
+ * stencil endpoint along the slowest axis, in cells) + 1 (the interpolation cell of an endpoint at
+ * row i + o spans rows floor(i+o) .. floor(i+o)+1); hjb_set_coeffs checks this on the device.
+ * nranks == 1: one slab, halo ignored (0).                                                      */
+hjb_status hjb_partition(int32_t dim, int64_t n, int32_t nranks, int32_t rank, int64_t halo,
+                         hjb_layout* out);
+
+typedef struct {
+  int32_t peer;        /* neighbour rank                                                       */
+  int64_t send_row;    /* first GLOBAL row sent to peer (owned rows of this rank)              */
+  int64_t recv_row;    /* first GLOBAL row received from peer (lands in this rank's halo)      */
+  int64_t rows;        /* rows per message (= halo)                                           */
+} hjb_halo_msg;
+
+/* The halo messages of `rank` (0, 1 or 2: to rank-1 and rank+1), in that order. */
+hjb_status hjb_halo_plan(int32_t dim, int64_t n, int32_t nranks, int32_t rank, int64_t halo,
+                         hjb_halo_msg out[2], int32_t* count);
+
 /* Create a grid handle; allocates the Krylov workspace (about 10 grid arrays). */
 hjb_status hjb_grid_create(const hjb_grid_desc* desc, hjb_grid_t* out);
 hjb_status hjb_grid_query(hjb_grid_t g, hjb_layout* out);

@@ -17,7 +17,8 @@ STATUS = {0: "HJB_OK", 1: "HJB_ERR_INVALID_ARG", 2: "HJB_ERR_UNSUPPORTED", 3: "H
 EXPORTS = ["hjb_last_error", "hjb_version", "hjb_grid_create", "hjb_grid_query", "hjb_grid_destroy",
            "hjb_set_coeffs", "hjb_set_source", "hjb_policy_update", "hjb_apply",
            "hjb_mg_params_default", "hjb_mg_setup", "hjb_mg_apply", "hjb_solve_params_default",
-           "hjb_solve", "hjb_step", "hjb_profile_reset", "hjb_profile_read"]
+           "hjb_solve", "hjb_step", "hjb_profile_reset", "hjb_profile_read",
+           "hjb_partition", "hjb_halo_plan"]
 
 KERNEL_CLASSES = ["search", "apply", "resid", "smooth", "transfer", "coarse", "vector", "reduce",
                   "boundary"]
@@ -36,6 +37,10 @@ class Layout(C.Structure):
                 ("halo", C.c_int64), ("local_row0", C.c_int64), ("local_rows", C.c_int64),
                 ("local_elems", C.c_int64), ("n_interior", C.c_int64), ("n_boundary", C.c_int64),
                 ("n_levels", C.c_int32), ("h", C.c_double), ("k", C.c_double)]
+
+
+class HaloMsg(C.Structure):
+    _fields_ = [("peer", C.c_int32), ("send_row", C.c_int64), ("recv_row", C.c_int64), ("rows", C.c_int64)]
 
 
 class Coeffs(C.Structure):
@@ -124,6 +129,8 @@ def load(path: str = LIB_PATH):
         "hjb_step": (i32, [vp, d, vp, vp, vp, vp, C.POINTER(SolveParams), C.POINTER(StepStats)]),
         "hjb_profile_reset": (i32, [vp, i32]),
         "hjb_profile_read": (i32, [vp, C.POINTER(Profile)]),
+        "hjb_partition": (i32, [i32, i64, i32, i32, i64, C.POINTER(Layout)]),
+        "hjb_halo_plan": (i32, [i32, i64, i32, i32, i64, HaloMsg * 2, C.POINTER(i32)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -142,3 +149,18 @@ class HJBError(RuntimeError):
 def check(code: int):
     if code != 0:
         raise HJBError(code, load().hjb_last_error().decode(errors="replace"))
+
+
+def partition(dim: int, n: int, nranks: int, rank: int, halo: int) -> dict:
+    """Host-only slab layout of `rank` (hjb_partition); raises HJBError on invalid input."""
+    lay = Layout()
+    check(load().hjb_partition(dim, n, nranks, rank, halo, C.byref(lay)))
+    return {f: getattr(lay, f) for f, _ in lay._fields_}
+
+
+def halo_plan(dim: int, n: int, nranks: int, rank: int, halo: int) -> list:
+    """Host-only halo messages of `rank` (hjb_halo_plan)."""
+    msgs = (HaloMsg * 2)()
+    cnt = C.c_int32()
+    check(load().hjb_halo_plan(dim, n, nranks, rank, halo, msgs, C.byref(cnt)))
+    return [dict(peer=m.peer, send_row=m.send_row, recv_row=m.recv_row, rows=m.rows) for m in msgs[:cnt.value]]

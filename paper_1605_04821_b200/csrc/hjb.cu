@@ -382,6 +382,64 @@ extern "C" hjb_status hjb_grid_create(const hjb_grid_desc* d, hjb_grid_t* out) {
   return HJB_OK;
 }
 
+// ---------------------------------------------------------------------------- API: partition
+static int64_t ipow(int64_t b, int e) {
+  int64_t r = 1;
+  for (int i = 0; i < e; ++i) r *= b;
+  return r;
+}
+
+extern "C" hjb_status hjb_partition(int32_t dim, int64_t n, int32_t nranks, int32_t rank, int64_t halo,
+                                    hjb_layout* o) {
+  if (!o) return fail(HJB_ERR_INVALID_ARG, "null out");
+  if (dim != 2 && dim != 3) return fail(HJB_ERR_INVALID_ARG, "dim must be 2 or 3");
+  if (n < 3) return fail(HJB_ERR_INVALID_ARG, "n must be >= 3");
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(HJB_ERR_INVALID_ARG, "bad rank/nranks");
+  const int64_t nI = n - 2;
+  if (nranks == 1) halo = 0;
+  else if (halo < 1) return fail(HJB_ERR_INVALID_ARG, "halo must be >= 1 when nranks > 1");
+  const int64_t r0 = 1 + (rank * nI) / nranks, r1 = 1 + ((rank + 1) * nI) / nranks;
+  for (int q = 0; q < nranks; ++q) {
+    const int64_t own = (((int64_t)q + 1) * nI) / nranks - ((int64_t)q * nI) / nranks;
+    if (own < std::max<int64_t>(1, halo))
+      return fail(HJB_ERR_INVALID_ARG, "too many ranks: every rank must own >= halo interior rows");
+  }
+  const int64_t lr0 = nranks == 1 ? 0 : std::max<int64_t>(0, r0 - halo);
+  const int64_t lr1 = nranks == 1 ? n : std::min<int64_t>(n, r1 + halo);
+  o->n = n;
+  o->row_elems = ipow(n, dim - 1);
+  o->row0 = r0;
+  o->row1 = r1;
+  o->halo = halo;
+  o->local_row0 = lr0;
+  o->local_rows = lr1 - lr0;
+  o->local_elems = o->local_rows * o->row_elems;
+  o->n_interior = (r1 - r0) * ipow(nI, dim - 1);
+  o->n_boundary = ipow(n, dim) - ipow(nI, dim);
+  o->n_levels = 0;
+  o->h = 0.0;
+  o->k = 0.0;
+  return HJB_OK;
+}
+
+extern "C" hjb_status hjb_halo_plan(int32_t dim, int64_t n, int32_t nranks, int32_t rank, int64_t halo,
+                                    hjb_halo_msg out[2], int32_t* count) {
+  if (!out || !count) return fail(HJB_ERR_INVALID_ARG, "null out");
+  hjb_layout me;
+  TRY(hjb_partition(dim, n, nranks, rank, halo, &me));
+  *count = 0;
+  if (nranks == 1) return HJB_OK;
+  if (rank > 0) {  // lower neighbour: send my first `halo` owned rows, receive its last ones
+    out[*count] = hjb_halo_msg{rank - 1, me.row0, me.row0 - halo, halo};
+    ++*count;
+  }
+  if (rank + 1 < nranks) {  // upper neighbour: send my last `halo` owned rows, receive its first ones
+    out[*count] = hjb_halo_msg{rank + 1, me.row1 - halo, me.row1, halo};
+    ++*count;
+  }
+  return HJB_OK;
+}
+
 extern "C" hjb_status hjb_grid_query(hjb_grid_t g, hjb_layout* o) {
   if (!g || !o) return fail(HJB_ERR_INVALID_ARG, "null handle/out");
   o->n = g->n;

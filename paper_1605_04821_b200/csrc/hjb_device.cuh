@@ -147,6 +147,17 @@ __device__ __forceinline__ void split_pm(double o, int i, int nm2, Split& p, Spl
   if (m.c > nm2) { m.c = nm2; m.s = 1.0; }
 }
 
+__device__ __forceinline__ void split_p(double o, int i, int nm2, Split& p) {
+  const double magic = 6755399441055744.0;
+  const double big = o + magic;
+  const int r = __double2loint(big);
+  const double f = o - (big - magic);
+  const bool neg = f < 0.0;
+  p.c = i + r - (neg ? 1 : 0);
+  p.s = neg ? f + 1.0 : f;
+  if (p.c > nm2) { p.c = nm2; p.s = 1.0; }
+}
+
 // general (possibly truncated) endpoint t = i + mu o, binding coordinate snapped onto the face
 template <int D>
 __device__ __forceinline__ void cell_general(const LevelDev& L, const Node<D>& nd, const double* o, double mu,
@@ -293,13 +304,26 @@ __device__ __forceinline__ void row_eval(const LevelDev& L, const CoefDev& C, co
   {
     const double* bd_ = C.b_dir + a * D;
     double o[D];
-    bool nz = false;
+    bool nz = false, inside = true;
 #pragma unroll
     for (int d = 0; d < D; ++d) {
       o[d] = L.k2h * fma(nd.bs, __ldg(bd_ + d), nd.bn[d]);
       nz |= (o[d] != 0.0);
+      inside &= (fabs(o[d]) <= nd.dist[d]);
     }
-    if (nz) {
+    if (nz && inside) {  // untruncated drift endpoint (mu = 1)
+      int c[D];
+      double s[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        Split P_;
+        split_p(o[d], nd.i[d], nm2, P_);
+        c[d] = P_.c; s[d] = P_.s;
+      }
+      wsum += L.inv_k2;
+      if (GATHER) acc = fma(L.inv_k2, gather_interp<D>(L, v, c, s), acc);
+      if (SELF) self = fma(L.inv_k2, self_weight<D>(nd.i, c, s), self);
+    } else if (nz) {
       int bdim;
       const double mu = ray_mu<D>(L, nd, o, bdim);
       int c[D];

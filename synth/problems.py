@@ -149,6 +149,22 @@ class Problem:
             return self._psi(t, idx, _xp_of(idx))
         return self._u_exact(t, idx, _xp_of(idx))
 
+    def halo_rows(self, k_scale: float = 1.0) -> int:
+        """Halo rows a slab needs: floor(max |offset| along the slowest axis, in cells) + 1 (an
+        endpoint at i + o reads rows floor(i+o) and floor(i+o)+1), from the problem data (the
+        library re-checks it on the device in hjb_set_coeffs)."""
+        f = self.fields(self.all_idx()) if self.N <= (1 << 22) else self.fields(
+            np.arange(0, self.N, max(1, self.N // (1 << 20)), dtype=np.int64))
+        ax = self.d - 1
+        sc = np.abs(np.asarray(f["sigma_scale"])).max(axis=1) if "sigma_scale" in f else np.ones(self.P)
+        sn = np.abs(np.asarray(f["sigma_node"])[:, ax]).max(axis=1) if "sigma_node" in f else np.zeros(self.P)
+        bs = np.abs(np.asarray(f["b_scale"])).max() if "b_scale" in f else 1.0
+        bn = np.abs(np.asarray(f["b_node"])[ax]).max() if "b_node" in f else 0.0
+        kh = k_scale * math.sqrt(self.h) / self.h
+        reach = max(kh * (sc[p] * np.abs(self.sigma_dir[:, p, ax]).max() + sn[p]) for p in range(self.P))
+        reach = max(reach, bs * np.abs(self.b_dir[:, ax]).max() + bn)
+        return int(math.floor(reach * (1 + 1e-12))) + 1
+
     def control_tables(self):
         return (np.ascontiguousarray(self.sigma_dir, dtype=np.float64),
                 np.ascontiguousarray(self.b_dir, dtype=np.float64),

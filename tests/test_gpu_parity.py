@@ -126,6 +126,24 @@ def test_step_parity(name, mk, steps):
         assert st["final_rres"] <= 1e-12
 
 
+@pytest.mark.parametrize("name,mk,steps", [
+    ("cfg0_inexact", lambda: bj_config(0), 3),
+    ("cfg2_129_inexact", lambda: bj_config(2, n=129), 2),
+    ("cfg3_17_inexact", lambda: bj_config(3, n=17), 1),
+])
+def test_step_parity_inexact_policy_evaluation(name, mk, steps):
+    """pi_forcing > 0 (reading xxii): early policy evaluations are inexact, the fixed point is not."""
+    p = mk()
+    Ug, _, stats = _gpu_march(p, steps, pi_forcing=1e-2)
+    Uo = p.g(p.all_idx())
+    for s in range(1, steps + 1):
+        Uo, _, _ = howard_step(p, Uo, s * p.dt, p.dt)
+    err = np.abs(Ug - Uo).max() / max(1.0, np.abs(Uo).max())
+    assert err <= 1e-8, (name, err, stats[-1])
+    for st in stats:
+        assert st["final_rres"] <= 1e-12 or st["final_R"] <= 1e-10
+
+
 def test_step_parity_cfg1_first_step():
     p = bj_config(1)
     Ug, polg, stats = _gpu_march(p, 1)
