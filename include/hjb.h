@@ -73,11 +73,21 @@ typedef struct {
   int64_t n;           /* nodes per dimension incl. boundary, >= 3                            */
   double lo, hi;       /* Omega = [lo,hi]^d                                                   */
   int32_t rank;        /* slab decomposition along the slowest axis: this rank ...           */
-  int32_t nranks;      /* ... of nranks (1 in this release; >1 returns HJB_ERR_UNSUPPORTED)  */
-  const void* nccl_id; /* reserved: ncclUniqueId when nranks > 1                              */
+  int32_t nranks;      /* ... of nranks (see hjb_partition)                                  */
+  const void* nccl_id; /* nranks > 1: 128 bytes, the ncclUniqueId (comm = HJB_COMM_NCCL, created
+                          by rank 0 and broadcast by the caller) or any group key shared by the
+                          ranks (comm = HJB_COMM_THREADS)                                      */
   void* stream;        /* cudaStream_t                                                        */
   int32_t device;      /* CUDA device ordinal                                                 */
+  int64_t halo;        /* nranks > 1: halo rows per side (>= floor(max reach in rows) + 1)   */
+  int32_t comm;        /* HJB_COMM_NCCL (default) or HJB_COMM_THREADS                         */
 } hjb_grid_desc;
+
+/* Communication backends for nranks > 1.  With nranks > 1 EVERY call on a grid is collective:
+ * all ranks must make the same calls in the same order.                                       */
+#define HJB_COMM_NCCL 0     /* one process per GPU, NCCL over NVLink/NVSwitch (production)    */
+#define HJB_COMM_THREADS 1  /* TEST-ONLY: ranks are host threads of one process on one device;
+                               halos by device copies ordered with CUDA events               */
 
 typedef struct {
   int64_t n;            /* nodes per dimension                                                */
@@ -116,7 +126,12 @@ typedef struct {
 hjb_status hjb_halo_plan(int32_t dim, int64_t n, int32_t nranks, int32_t rank, int64_t halo,
                          hjb_halo_msg out[2], int32_t* count);
 
-/* Create a grid handle; allocates the Krylov workspace (about 10 grid arrays). */
+/* A fresh ncclUniqueId (128 bytes) for nranks > 1 with HJB_COMM_NCCL: rank 0 calls this and the
+ * caller broadcasts the bytes to every rank (e.g. torch.distributed.broadcast_object_list).     */
+hjb_status hjb_comm_unique_id(void* out128);
+
+/* Create a grid handle; allocates the Krylov workspace (about 10 grid arrays).  With nranks > 1
+ * this is collective (it initialises the communicator).                                        */
 hjb_status hjb_grid_create(const hjb_grid_desc* desc, hjb_grid_t* out);
 hjb_status hjb_grid_query(hjb_grid_t g, hjb_layout* out);
 hjb_status hjb_grid_destroy(hjb_grid_t g);
@@ -184,6 +199,9 @@ typedef struct {
   int32_t coarse_k_mode;     /* 0: coarse levels keep the fine SL step k (default);
                                 1: k_l = sqrt(h_l) (the scheme's own rule on each level)      */
   int32_t max_levels;        /* cap on levels (default 32)                                     */
+  int32_t gather_n;          /* nranks > 1: levels with n <= gather_n (or slabs thinner than
+                                their halo) are replicated on every rank after an all-gather
+                                (default 129 in 2D, 33 in 3D; BASELINE cfg4 "129^2 on one GPU") */
 } hjb_mg_params;
 
 void hjb_mg_params_default(int32_t dim, hjb_mg_params* out);
@@ -253,14 +271,15 @@ hjb_status hjb_step(hjb_grid_t g, double dt, const double* U_prev, double* U, ui
 typedef enum {
   HJB_KC_SEARCH = 0,    /* control search (policy improvement)                               */
   HJB_KC_APPLY = 1,     /* y = A x on the fine level (Krylov operator, hjb_apply)            */
-  HJB_KC_RESID = 2,     /* r = b - A x (all levels)                                          */
-  HJB_KC_SMOOTH = 3,    /* damped-Jacobi sweeps (all levels)                                 */
+  HJB_KC_RESID = 2,     /* r = b - A x on the fine level                                     */
+  HJB_KC_SMOOTH = 3,    /* damped-Jacobi sweeps on the fine level                            */
   HJB_KC_TRANSFER = 4,  /* restriction, prolongation, policy/field injection                 */
   HJB_KC_COARSE = 5,    /* coarsest-level dense assemble / invert / solve                    */
   HJB_KC_VECTOR = 6,    /* BiCGSTAB vector updates with fused dot products, norms, copies    */
   HJB_KC_REDUCE = 7,    /* fixed-order reduction of block partials + Krylov scalar update    */
-  HJB_KC_BOUNDARY = 8,  /* Dirichlet data scatter                                            */
-  HJB_KC_COUNT = 9
+  HJB_KC_BOUNDARY = 8,  /* Dirichlet data scatter, halo check                                */
+  HJB_KC_MG_COARSE = 9, /* residual / Jacobi sweeps on coarse multigrid levels               */
+  HJB_KC_COUNT = 10
 } hjb_kernel_class;
 
 typedef struct {

@@ -18,10 +18,12 @@ EXPORTS = ["hjb_last_error", "hjb_version", "hjb_grid_create", "hjb_grid_query",
            "hjb_set_coeffs", "hjb_set_source", "hjb_policy_update", "hjb_apply",
            "hjb_mg_params_default", "hjb_mg_setup", "hjb_mg_apply", "hjb_solve_params_default",
            "hjb_solve", "hjb_step", "hjb_profile_reset", "hjb_profile_read",
-           "hjb_partition", "hjb_halo_plan"]
+           "hjb_partition", "hjb_halo_plan", "hjb_comm_unique_id"]
+
+HJB_COMM_NCCL, HJB_COMM_THREADS = 0, 1
 
 KERNEL_CLASSES = ["search", "apply", "resid", "smooth", "transfer", "coarse", "vector", "reduce",
-                  "boundary"]
+                  "boundary", "mg_coarse"]
 HJB_KC_COUNT = len(KERNEL_CLASSES)
 
 
@@ -29,7 +31,7 @@ class GridDesc(C.Structure):
     _fields_ = [("dim", C.c_int32), ("P", C.c_int32), ("K", C.c_int32), ("Q", C.c_int32),
                 ("n", C.c_int64), ("lo", C.c_double), ("hi", C.c_double),
                 ("rank", C.c_int32), ("nranks", C.c_int32), ("nccl_id", C.c_void_p),
-                ("stream", C.c_void_p), ("device", C.c_int32)]
+                ("stream", C.c_void_p), ("device", C.c_int32), ("halo", C.c_int64), ("comm", C.c_int32)]
 
 
 class Layout(C.Structure):
@@ -55,7 +57,8 @@ class PiStats(C.Structure):
 
 class MgParams(C.Structure):
     _fields_ = [("nu_pre", C.c_int32), ("nu_post", C.c_int32), ("omega", C.c_double),
-                ("coarse_max_n", C.c_int32), ("coarse_k_mode", C.c_int32), ("max_levels", C.c_int32)]
+                ("coarse_max_n", C.c_int32), ("coarse_k_mode", C.c_int32), ("max_levels", C.c_int32),
+                ("gather_n", C.c_int32)]
 
 
 class SolveParams(C.Structure):
@@ -130,6 +133,7 @@ def load(path: str = LIB_PATH):
         "hjb_profile_reset": (i32, [vp, i32]),
         "hjb_profile_read": (i32, [vp, C.POINTER(Profile)]),
         "hjb_partition": (i32, [i32, i64, i32, i32, i64, C.POINTER(Layout)]),
+        "hjb_comm_unique_id": (i32, [vp]),
         "hjb_halo_plan": (i32, [i32, i64, i32, i32, i64, HaloMsg * 2, C.POINTER(i32)]),
     }
     for name, (res, args) in sig.items():
@@ -164,3 +168,10 @@ def halo_plan(dim: int, n: int, nranks: int, rank: int, halo: int) -> list:
     cnt = C.c_int32()
     check(load().hjb_halo_plan(dim, n, nranks, rank, halo, msgs, C.byref(cnt)))
     return [dict(peer=m.peer, send_row=m.send_row, recv_row=m.recv_row, rows=m.rows) for m in msgs[:cnt.value]]
+
+
+def comm_unique_id() -> bytes:
+    """128-byte ncclUniqueId (rank 0 creates it, the caller broadcasts it)."""
+    buf = C.create_string_buffer(128)
+    check(load().hjb_comm_unique_id(buf))
+    return buf.raw

@@ -36,7 +36,12 @@ class HJBGrid:
     """Handle on one grid (one rank).  Arrays passed in must follow `layout` (see hjb.h)."""
 
     def __init__(self, dim: int, P: int, K: int, Q: int, n: int, lo: float, hi: float,
-                 device: int = 0, stream=None):
+                 device: int = 0, stream=None, rank: int = 0, nranks: int = 1, halo: int = 0,
+                 comm: str = "nccl", comm_id: bytes = None):
+        """nranks > 1: slab `rank` of a decomposed grid (hjb_partition).  comm = "nccl" (one process
+        per GPU; comm_id = the 128-byte id from comm_unique_id() on rank 0, broadcast by the caller)
+        or "threads" (TEST-ONLY: ranks are threads of one process; comm_id = any shared 128-byte key).
+        Every call is then collective."""
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("HJBGrid needs a CUDA device (B200); there is no CPU fallback")
@@ -45,11 +50,19 @@ class HJBGrid:
         if stream is None:
             stream = torch.cuda.current_stream(device)
         self._stream = stream
-        d = _lib.GridDesc(dim=dim, P=P, K=K, Q=Q, n=n, lo=lo, hi=hi, rank=0, nranks=1,
-                          nccl_id=None, stream=stream.cuda_stream, device=device)
+        self._id = None
+        if nranks > 1:
+            if comm_id is None or len(comm_id) != 128:
+                raise ValueError("nranks > 1 needs a 128-byte comm_id")
+            self._id = C.create_string_buffer(bytes(comm_id), 128)
+        d = _lib.GridDesc(dim=dim, P=P, K=K, Q=Q, n=n, lo=lo, hi=hi, rank=rank, nranks=nranks,
+                          nccl_id=C.cast(self._id, C.c_void_p) if self._id is not None else None,
+                          stream=stream.cuda_stream, device=device, halo=halo,
+                          comm=_lib.HJB_COMM_THREADS if comm == "threads" else _lib.HJB_COMM_NCCL)
         h = C.c_void_p()
         check(self.lib.hjb_grid_create(C.byref(d), C.byref(h)))
         self.h = h
+        self.rank, self.nranks = rank, nranks
         self.dim, self.P, self.K, self.Q, self.n = dim, P, K, Q, n
         self._keep = {}
 

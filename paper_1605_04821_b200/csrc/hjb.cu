@@ -1,18 +1,21 @@
-// hjb.cu -- C-ABI of libhjb (include/hjb.h): handle management, coefficient upload, and the
-// host orchestration of policy iteration / BiCGSTAB / geometric multigrid.  All arithmetic on
-// grid data runs in the kernels of hjb_kernels.cuh; the host only sequences launches and reads a
-// few scalars (Krylov convergence, policy-iteration stopping) through pinned memory.
+// hjb.cu -- C-ABI of libhjb (include/hjb.h): handle management, coefficient upload, slab
+// decomposition, and the host orchestration of policy iteration / BiCGSTAB / geometric multigrid.
+// All arithmetic on grid data runs in the kernels of hjb_kernels.cuh; the host only sequences
+// launches, halo exchanges and all-gathers (hjb_comm.h), and reads a few scalars (Krylov
+// convergence, policy-iteration stopping) through pinned memory.
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cmath>
-#include <map>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <memory>
 #include <string>
 #include <vector>
 
 #include "hjb.h"
+#include "hjb_comm.h"
 #include "hjb_kernels.cuh"
 
 using namespace hjb;
@@ -44,17 +47,23 @@ static hjb_status fail(hjb_status s, const std::string& msg) {
 
 static constexpr int kMaxBlocks = 148 * 16;  // partial-sum slots: 16 resident 128-thread CTAs per SM
 
+// One multigrid level.  Level 0 is the fine grid.  "Slab" levels are decomposed like the fine grid
+// (owned rows [r0, r1) of the slowest axis + H halo rows); "replicated" levels (at and below the
+// gather level, nranks > 1 only) hold the full grid on every rank and are computed redundantly.
 struct Level {
   LevelDev L{};
-  int64_t elems = 0;          // local elements of a grid array on this level
-  double* tmp = nullptr;      // smoother ping-pong
-  double* res = nullptr;      // residual before restriction
-  double* x = nullptr;        // coarse levels: correction
-  double* b = nullptr;        // coarse levels: restricted rhs
-  uint8_t* pol = nullptr;     // coarse levels: injected policy
-  double* fields = nullptr;   // coarse levels: injected field planes
+  int64_t elems = 0;              // local elements of a grid array on this level
+  bool replicated = false;
+  int64_t H = 0;                  // halo rows (slab levels, nranks > 1)
+  std::vector<int64_t> r0s, r1s;  // slab levels: owned rows of every rank
+  double* tmp = nullptr;          // smoother ping-pong
+  double* res = nullptr;          // residual before restriction
+  double* x = nullptr;            // coarse levels: correction
+  double* b = nullptr;            // coarse levels: restricted rhs
+  uint8_t* pol = nullptr;         // coarse levels: injected policy
+  double* fields = nullptr;       // coarse levels: injected field planes
   CoefDev C{};
-  double* Ainv = nullptr;     // coarsest level dense inverse
+  double* Ainv = nullptr;         // coarsest level dense inverse
 };
 
 struct hjb_grid {
@@ -63,24 +72,35 @@ struct hjb_grid {
   int64_t n = 0;
   double lo = 0, hi = 1, h = 0, k = 0;
   cudaStream_t st = nullptr;
+  hjb_layout lay{};               // this rank's slab
+  int R = 1, rank = 0;
+  std::unique_ptr<Comm> comm;
+  std::vector<int64_t> r0s, r1s;  // fine owned rows of every rank
   LevelDev L0{};
   int64_t N = 0, n_interior = 0, n_boundary = 0;
   // coefficients
   double* d_tab = nullptr;  // sigma_dir | b_dir | c_ctrl | f_basis | f_ctrl
   CoefDev C0{};
   bool have_coeffs = false;
+  double reach_diff = 0.0, reach_drift = 0.0;  // max |offset| along the slowest axis, cells (level 0)
   // Krylov workspace
   double *r = nullptr, *rhat = nullptr, *p = nullptr, *v = nullptr, *s = nullptr, *t = nullptr;
   double *phat = nullptr, *shat = nullptr, *F = nullptr;
   double* partial = nullptr;
-  double* red = nullptr;
+  double* red = nullptr;      // [0..1] result, [2..3] this rank's partial result
+  double* red_all = nullptr;  // [nranks][2] gathered
   KScal* S = nullptr;
-  KScal* hS = nullptr;     // pinned mirror
-  double* hred = nullptr;  // pinned mirror of red
+  KScal* hS = nullptr;        // pinned mirror
+  double* hred = nullptr;     // pinned mirror of red
   uint8_t* pol_int = nullptr;
+  double* scratch = nullptr;  // const-input copy for halo exchange (nranks > 1)
   // staging for host pointers
   double *stage_prev = nullptr, *stage_U = nullptr, *stage_psi = nullptr;
   uint8_t* stage_pol = nullptr;
+  // gather-level staging (nranks > 1)
+  void* gsend = nullptr;
+  void* grecv = nullptr;
+  size_t gbytes = 0;
   // multigrid
   std::vector<Level> levels;
   hjb_mg_params mgp{};
@@ -150,7 +170,8 @@ static int occupancy_of(const void* fn) {
 static dim3 dims(hjb_grid* g, const LevelDev& L, const void* fn) {
   const int gx = std::max(1, (L.nI + kTX - 1) / kTX);
   const int64_t cap = std::min<int64_t>((int64_t)occupancy_of(fn) * g->sms, kMaxBlocks);
-  const int gy = (int)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(L.nrows, 65535), cap / gx));
+  const int64_t rows = std::min<int64_t>(std::max(L.nrows, 1), 65535);
+  const int gy = (int)std::max<int64_t>(1, std::min<int64_t>(rows, cap / gx));
   g->nblk_last = gx * gy;
   return dim3(gx, gy);
 }
@@ -173,23 +194,24 @@ static hjb_status dalloc(void** p, size_t bytes) {
   return HJB_OK;
 }
 
-static LevelDev make_level(int D, int64_t n, double lo, double hi, double k, double k2, int rank, int nranks) {
+static int64_t ipow(int64_t b, int e) {
+  int64_t r = 1;
+  for (int i = 0; i < e; ++i) r *= b;
+  return r;
+}
+
+// level geometry: owned interior rows [r0, r1) of the slowest axis, local rows [lr0, lr1)
+static LevelDev make_level(int D, int64_t n, double lo, double hi, double k, double k2, int64_t r0, int64_t r1,
+                           int64_t lr0, int64_t lr1) {
   LevelDev L{};
   L.n = (int)n;
   L.nI = (int)(n - 2);
-  L.nrows = 1;
-  for (int d = 0; d < D - 1; ++d) L.nrows *= (int)(n - 2);
-  L.row_elems = 1;
-  for (int d = 0; d < D - 1; ++d) L.row_elems *= n;
-  // single rank: owned interior rows 1..n-2 of the slowest axis, local array = whole grid
-  (void)rank;
-  (void)nranks;
-  L.local_row0 = 0;
-  L.local_rows = n;
-  L.row_first = 1;
-  int64_t own = 1;
-  for (int d = 0; d < D; ++d) own *= (n - 2);
-  L.n_own = own;
+  L.nrows = (int)((r1 - r0) * ipow(n - 2, D - 2));
+  L.row_elems = ipow(n, D - 1);
+  L.local_row0 = lr0;
+  L.local_rows = lr1 - lr0;
+  L.row_first = r0;
+  L.n_own = (int64_t)L.nrows * L.nI;
   L.h = (hi - lo) / (double)(n - 1);
   L.nm1 = (double)(n - 1);
   L.kh = k / L.h;
@@ -198,29 +220,102 @@ static LevelDev make_level(int D, int64_t n, double lo, double hi, double k, dou
   L.inv_k2 = 1.0 / k2;
   return L;
 }
+static LevelDev full_level(int D, int64_t n, double lo, double hi, double k, double k2) {
+  return make_level(D, n, lo, hi, k, k2, 1, n - 1, 0, n);
+}
+
+// ---------------------------------------------------------------------------- communication
+// halo exchange of `rows` rows each side of a slab-level array x (no-op for one rank / replicated)
+static hjb_status halo_exchange(hjb_grid* g, const Level& lv, double* x, int64_t rows) {
+  if (g->R == 1 || lv.replicated || rows <= 0) return HJB_OK;
+  const int64_t re = lv.L.row_elems, lr0 = lv.L.local_row0;
+  const int64_t r0 = lv.r0s[g->rank], r1 = lv.r1s[g->rank];
+  Msg m[2];
+  int nm = 0;
+  const size_t bytes = (size_t)(rows * re) * sizeof(double);
+  if (g->rank > 0) m[nm++] = Msg{g->rank - 1, x + (r0 - lr0) * re, x + (r0 - rows - lr0) * re, bytes};
+  if (g->rank + 1 < g->R) m[nm++] = Msg{g->rank + 1, x + (r1 - rows - lr0) * re, x + (r1 - lr0) * re, bytes};
+  std::string err;
+  if (g->comm->exchange(g->st, m, nm, &err) != cudaSuccess)
+    return fail(g->desc.comm == HJB_COMM_NCCL ? HJB_ERR_NCCL : HJB_ERR_CUDA, "halo exchange: " + err);
+  return HJB_OK;
+}
+
+// reduce the block partials of the last dims() launch to red[0..1] on the device (several ranks:
+// per-rank results all-gathered and combined in rank order), then the BiCGSTAB scalar update
+static hjb_status reduce_dev(hjb_grid* g, int nblk, unsigned maxmask, int which) {
+  if (g->R == 1) {
+    LAUNCH(HJB_KC_REDUCE, nblk, 16.0 * nblk, 2.0 * nblk,
+           k_finalize<<<1, 1024, 0, g->st>>>(g->partial, nblk, g->red, maxmask, g->S, which));
+    CKL();
+    return HJB_OK;
+  }
+  LAUNCH(HJB_KC_REDUCE, nblk, 16.0 * nblk, 2.0 * nblk,
+         k_finalize<<<1, 1024, 0, g->st>>>(g->partial, nblk, g->red + 2, maxmask, g->S, SC_NONE));
+  CKL();
+  std::string err;
+  if (g->comm->allgather(g->st, g->red + 2, g->red_all, 2 * sizeof(double), &err) != cudaSuccess)
+    return fail(HJB_ERR_NCCL, "allgather: " + err);
+  LAUNCH(HJB_KC_REDUCE, g->R, 16.0 * g->R, 2.0 * g->R,
+         k_combine<<<1, 32, 0, g->st>>>(g->red_all, g->R, g->red, maxmask, g->S, which));
+  CKL();
+  return HJB_OK;
+}
 
 static double host_finalize(hjb_grid* g, int nblk, unsigned maxmask, int which, hjb_status* err,
                             double* second = nullptr) {
-  LAUNCH(HJB_KC_REDUCE, nblk, 16.0 * nblk, 2.0 * nblk,
-         k_finalize<<<1, 1024, 0, g->st>>>(g->partial, nblk, g->red, maxmask, g->S, which));
+  *err = reduce_dev(g, nblk, maxmask, which);
+  if (*err != HJB_OK) return NAN;
   cudaMemcpyAsync(g->hred, g->red, 2 * sizeof(double), cudaMemcpyDeviceToHost, g->st);
   cudaError_t e = cudaStreamSynchronize(g->st);
   if (e != cudaSuccess) {
     *err = fail(HJB_ERR_CUDA, std::string("sync: ") + cudaGetErrorString(e));
     return NAN;
   }
-  *err = HJB_OK;
   if (second) *second = g->hred[1];
   return g->hred[0];
+}
+
+// copy rows [J0_q, J1_q) of a full-grid array from every rank to every rank (gather level)
+static hjb_status gather_rows(hjb_grid* g, void* full, size_t elem, int64_t row_elems,
+                              const std::vector<int64_t>& J0, const std::vector<int64_t>& J1) {
+  int64_t maxr = 0;
+  for (int q = 0; q < g->R; ++q) maxr = std::max(maxr, J1[q] - J0[q]);
+  const size_t chunk = (size_t)(maxr * row_elems) * elem;
+  if (chunk == 0) return HJB_OK;
+  if (chunk > g->gbytes) {
+    cudaFree(g->gsend);
+    cudaFree(g->grecv);
+    g->gsend = g->grecv = nullptr;
+    TRY(dalloc(&g->gsend, chunk));
+    TRY(dalloc(&g->grecv, chunk * g->R));
+    g->gbytes = chunk;
+  }
+  const int me = g->rank;
+  const size_t mine = (size_t)((J1[me] - J0[me]) * row_elems) * elem;
+  if (mine)
+    CK(cudaMemcpyAsync(g->gsend, (char*)full + (size_t)(J0[me] * row_elems) * elem, mine,
+                       cudaMemcpyDeviceToDevice, g->st));
+  std::string err;
+  if (g->comm->allgather(g->st, g->gsend, g->grecv, chunk, &err) != cudaSuccess)
+    return fail(HJB_ERR_NCCL, "gather level: " + err);
+  for (int q = 0; q < g->R; ++q) {
+    const size_t b = (size_t)((J1[q] - J0[q]) * row_elems) * elem;
+    if (q != me && b)
+      CK(cudaMemcpyAsync((char*)full + (size_t)(J0[q] * row_elems) * elem, (char*)g->grecv + q * chunk, b,
+                         cudaMemcpyDeviceToDevice, g->st));
+  }
+  return HJB_OK;
 }
 
 // ---------------------------------------------------------------------------- dimension dispatch
 template <int D>
 static void launch_operator(hjb_grid* g, const LevelDev& L, const CoefDev& C, int mode, int ndot, double dt,
                             double omega, const uint8_t* pol, const double* x, const double* b, double* y,
-                            const double* u) {
+                            const double* u, bool fine = true) {
   cudaStream_t st = g->st;
-  const int cls = mode == OP_APPLY ? HJB_KC_APPLY : (mode == OP_RESID ? HJB_KC_RESID : HJB_KC_SMOOTH);
+  const int cls = !fine ? HJB_KC_MG_COARSE
+                        : (mode == OP_APPLY ? HJB_KC_APPLY : (mode == OP_RESID ? HJB_KC_RESID : HJB_KC_SMOOTH));
   const double nodes = (double)L.n_own;
   const double bpn = 1.0 + 8.0 + (mode != OP_JACOBI0 ? 8.0 : 0.0) + (mode != OP_APPLY ? 8.0 : 0.0) +
                      (ndot >= 1 ? 8.0 : 0.0) + 8.0 * g->nplanes0;
@@ -242,12 +337,6 @@ static void launch_operator(hjb_grid* g, const LevelDev& L, const CoefDev& C, in
 #undef OPL
 }
 
-static void op(hjb_grid* g, const LevelDev& L, const CoefDev& C, int mode, int ndot, double dt, double omega,
-               const uint8_t* pol, const double* x, const double* b, double* y, const double* u) {
-  if (g->D == 2) launch_operator<2>(g, L, C, mode, ndot, dt, omega, pol, x, b, y, u);
-  else launch_operator<3>(g, L, C, mode, ndot, dt, omega, pol, x, b, y, u);
-}
-
 // ---------------------------------------------------------------------------- API: misc
 extern "C" const char* hjb_last_error(void) { return g_err.c_str(); }
 extern "C" int32_t hjb_version(void) { return HJB_VERSION; }
@@ -260,6 +349,7 @@ extern "C" void hjb_mg_params_default(int32_t dim, hjb_mg_params* o) {
   o->coarse_max_n = (dim == 3) ? 5 : 9;
   o->coarse_k_mode = 0;
   o->max_levels = 32;
+  o->gather_n = (dim == 3) ? 33 : 129;
 }
 
 extern "C" void hjb_solve_params_default(int32_t dim, hjb_solve_params* o) {
@@ -273,122 +363,7 @@ extern "C" void hjb_solve_params_default(int32_t dim, hjb_solve_params* o) {
   o->pi_forcing = 0.0;
 }
 
-// ---------------------------------------------------------------------------- API: grid
-static void free_levels(hjb_grid* g) {
-  for (size_t i = 0; i < g->levels.size(); ++i) {
-    Level& l = g->levels[i];
-    cudaFree(l.tmp);
-    cudaFree(l.res);
-    if (i > 0) {
-      cudaFree(l.x);
-      cudaFree(l.b);
-      cudaFree(l.pol);
-      cudaFree(l.fields);
-    }
-    cudaFree(l.Ainv);
-  }
-  g->levels.clear();
-  g->mg_ready = false;
-}
-
-extern "C" hjb_status hjb_grid_destroy(hjb_grid_t g) {
-  if (!g) return fail(HJB_ERR_INVALID_ARG, "null handle");
-  cudaSetDevice(g->desc.device);
-  if (g->st) cudaStreamSynchronize(g->st);
-  free_levels(g);
-  double* bufs[] = {g->d_tab, g->r, g->rhat, g->p, g->v, g->s, g->t, g->phat, g->shat, g->F,
-                    g->partial, g->red, g->stage_prev, g->stage_U, g->stage_psi};
-  for (double* b : bufs) cudaFree(b);
-  cudaFree(g->S);
-  cudaFree(g->pol_int);
-  cudaFree(g->stage_pol);
-  cudaFreeHost(g->hS);
-  cudaFreeHost(g->hred);
-  for (auto& e : g->ev)
-    if (e) cudaEventDestroy(e);
-  for (auto& e : g->pev)
-    if (e) cudaEventDestroy(e);
-  delete g;
-  return HJB_OK;
-}
-
-extern "C" hjb_status hjb_grid_create(const hjb_grid_desc* d, hjb_grid_t* out) {
-  if (!d || !out) return fail(HJB_ERR_INVALID_ARG, "null desc/out");
-  *out = nullptr;
-  if (d->dim != 2 && d->dim != 3) return fail(HJB_ERR_INVALID_ARG, "dim must be 2 or 3");
-  if (d->P < 1 || d->P > d->dim) return fail(HJB_ERR_INVALID_ARG, "P must be in [1, dim]");
-  if (d->K < 1 || d->K > HJB_MAX_K) return fail(HJB_ERR_INVALID_ARG, "K must be in [1,255]");
-  if (d->Q < 0 || d->Q > HJB_MAX_Q) return fail(HJB_ERR_INVALID_ARG, "Q must be in [0,16]");
-  if (d->n < 3) return fail(HJB_ERR_INVALID_ARG, "n must be >= 3");
-  if (!(d->hi > d->lo)) return fail(HJB_ERR_INVALID_ARG, "hi must be > lo");
-  if (d->nranks != 1 || d->rank != 0)
-    return fail(HJB_ERR_UNSUPPORTED, "nranks > 1: slab decomposition is not enabled in this build");
-  int64_t tot = 1;
-  for (int i = 0; i < d->dim; ++i) tot *= d->n;
-  // local arrays are indexed with 32-bit offsets; one x1 line must fit the partial-sum slots
-  if (tot >= (1LL << 31) || (d->n - 2) > (int64_t)kTX * kMaxBlocks)
-    return fail(HJB_ERR_INVALID_ARG, "grid too large for one rank (local arrays must hold < 2^31 nodes)");
-  CK(cudaSetDevice(d->device));
-  hjb_grid* g = new hjb_grid();
-  g->desc = *d;
-  g->D = d->dim;
-  g->P = d->P;
-  g->K = d->K;
-  g->Q = d->Q;
-  g->n = d->n;
-  g->lo = d->lo;
-  g->hi = d->hi;
-  g->h = (d->hi - d->lo) / (double)(d->n - 1);
-  g->k = std::sqrt(g->h);  // k = sqrt(dx)  (PAPER.md:76)
-  g->st = (cudaStream_t)d->stream;
-  cudaDeviceGetAttribute(&g->sms, cudaDevAttrMultiProcessorCount, d->device);
-  if (g->sms < 1) g->sms = 148;
-  g->L0 = make_level(g->D, g->n, g->lo, g->hi, g->k, g->h, 0, 1);
-  g->N = g->L0.local_rows * g->L0.row_elems;
-  g->n_interior = g->L0.n_own;
-  g->n_boundary = tot - g->n_interior;
-  const size_t vb = (size_t)g->N * sizeof(double);
-  double** vecs[] = {&g->r, &g->rhat, &g->p, &g->v, &g->s, &g->t, &g->phat, &g->shat, &g->F};
-  hjb_status s = HJB_OK;
-  for (double** pv : vecs) {
-    if ((s = dalloc((void**)pv, vb)) != HJB_OK) {
-      hjb_grid_destroy(g);
-      return s;
-    }
-    cudaMemsetAsync(*pv, 0, vb, g->st);
-  }
-  if ((s = dalloc((void**)&g->partial, (size_t)kMaxBlocks * 2 * sizeof(double))) != HJB_OK ||
-      (s = dalloc((void**)&g->red, 4 * sizeof(double))) != HJB_OK ||
-      (s = dalloc((void**)&g->S, sizeof(KScal))) != HJB_OK ||
-      (s = dalloc((void**)&g->pol_int, (size_t)g->N)) != HJB_OK) {
-    hjb_grid_destroy(g);
-    return s;
-  }
-  cudaMemsetAsync(g->pol_int, 0, (size_t)g->N, g->st);
-  if (cudaMallocHost((void**)&g->hS, sizeof(KScal)) != cudaSuccess ||
-      cudaMallocHost((void**)&g->hred, 4 * sizeof(double)) != cudaSuccess) {
-    hjb_grid_destroy(g);
-    return fail(HJB_ERR_OOM, "pinned alloc");
-  }
-  for (auto& e : g->ev) cudaEventCreate(&e);
-  for (auto& e : g->pev) cudaEventCreate(&e);
-  cudaError_t e = cudaStreamSynchronize(g->st);
-  if (e != cudaSuccess) {
-    hjb_grid_destroy(g);
-    return fail(HJB_ERR_CUDA, cudaGetErrorString(e));
-  }
-  hjb_mg_params_default(g->D, &g->mgp);
-  *out = g;
-  return HJB_OK;
-}
-
 // ---------------------------------------------------------------------------- API: partition
-static int64_t ipow(int64_t b, int e) {
-  int64_t r = 1;
-  for (int i = 0; i < e; ++i) r *= b;
-  return r;
-}
-
 extern "C" hjb_status hjb_partition(int32_t dim, int64_t n, int32_t nranks, int32_t rank, int64_t halo,
                                     hjb_layout* o) {
   if (!o) return fail(HJB_ERR_INVALID_ARG, "null out");
@@ -440,18 +415,161 @@ extern "C" hjb_status hjb_halo_plan(int32_t dim, int64_t n, int32_t nranks, int3
   return HJB_OK;
 }
 
+extern "C" hjb_status hjb_comm_unique_id(void* out128) {
+  if (!out128) return fail(HJB_ERR_INVALID_ARG, "null out");
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return fail(HJB_ERR_NCCL, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+  std::memcpy(out128, &id, sizeof(id));
+  return HJB_OK;
+}
+
+// ---------------------------------------------------------------------------- API: grid
+static void free_levels(hjb_grid* g) {
+  for (size_t i = 0; i < g->levels.size(); ++i) {
+    Level& l = g->levels[i];
+    cudaFree(l.tmp);
+    cudaFree(l.res);
+    if (i > 0) {
+      cudaFree(l.x);
+      cudaFree(l.b);
+      cudaFree(l.pol);
+      cudaFree(l.fields);
+    }
+    cudaFree(l.Ainv);
+  }
+  g->levels.clear();
+  g->mg_ready = false;
+}
+
+extern "C" hjb_status hjb_grid_destroy(hjb_grid_t g) {
+  if (!g) return fail(HJB_ERR_INVALID_ARG, "null handle");
+  cudaSetDevice(g->desc.device);
+  if (g->st) cudaStreamSynchronize(g->st);
+  free_levels(g);
+  double* bufs[] = {g->d_tab, g->r, g->rhat, g->p, g->v, g->s, g->t, g->phat, g->shat, g->F,
+                    g->partial, g->red, g->red_all, g->scratch, g->stage_prev, g->stage_U, g->stage_psi};
+  for (double* b : bufs) cudaFree(b);
+  cudaFree(g->gsend);
+  cudaFree(g->grecv);
+  cudaFree(g->S);
+  cudaFree(g->pol_int);
+  cudaFree(g->stage_pol);
+  cudaFreeHost(g->hS);
+  cudaFreeHost(g->hred);
+  for (auto& e : g->ev)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : g->pev)
+    if (e) cudaEventDestroy(e);
+  g->comm.reset();
+  delete g;
+  return HJB_OK;
+}
+
+extern "C" hjb_status hjb_grid_create(const hjb_grid_desc* d, hjb_grid_t* out) {
+  if (!d || !out) return fail(HJB_ERR_INVALID_ARG, "null desc/out");
+  *out = nullptr;
+  if (d->dim != 2 && d->dim != 3) return fail(HJB_ERR_INVALID_ARG, "dim must be 2 or 3");
+  if (d->P < 1 || d->P > d->dim) return fail(HJB_ERR_INVALID_ARG, "P must be in [1, dim]");
+  if (d->K < 1 || d->K > HJB_MAX_K) return fail(HJB_ERR_INVALID_ARG, "K must be in [1,255]");
+  if (d->Q < 0 || d->Q > HJB_MAX_Q) return fail(HJB_ERR_INVALID_ARG, "Q must be in [0,16]");
+  if (d->n < 3) return fail(HJB_ERR_INVALID_ARG, "n must be >= 3");
+  if (!(d->hi > d->lo)) return fail(HJB_ERR_INVALID_ARG, "hi must be > lo");
+  if (d->nranks < 1 || d->rank < 0 || d->rank >= d->nranks) return fail(HJB_ERR_INVALID_ARG, "bad rank/nranks");
+  if (d->nranks > 1 && !d->nccl_id) return fail(HJB_ERR_INVALID_ARG, "nranks > 1 needs nccl_id (128 bytes)");
+  if (d->nranks > 1 && d->comm != HJB_COMM_NCCL && d->comm != HJB_COMM_THREADS)
+    return fail(HJB_ERR_INVALID_ARG, "unknown comm backend");
+  hjb_layout lay;
+  TRY(hjb_partition(d->dim, d->n, d->nranks, d->rank, d->halo, &lay));
+  // local arrays are indexed with 32-bit offsets; one x1 line must fit the partial-sum slots
+  if (lay.local_elems >= (1LL << 31) || (d->n - 2) > (int64_t)kTX * kMaxBlocks)
+    return fail(HJB_ERR_INVALID_ARG, "grid too large for one rank (local arrays must hold < 2^31 nodes)");
+  CK(cudaSetDevice(d->device));
+  hjb_grid* g = new hjb_grid();
+  g->desc = *d;
+  g->D = d->dim;
+  g->P = d->P;
+  g->K = d->K;
+  g->Q = d->Q;
+  g->n = d->n;
+  g->lo = d->lo;
+  g->hi = d->hi;
+  g->h = (d->hi - d->lo) / (double)(d->n - 1);
+  g->k = std::sqrt(g->h);  // k = sqrt(dx)  (PAPER.md:76)
+  g->st = (cudaStream_t)d->stream;
+  g->R = d->nranks;
+  g->rank = d->rank;
+  g->lay = lay;
+  cudaDeviceGetAttribute(&g->sms, cudaDevAttrMultiProcessorCount, d->device);
+  if (g->sms < 1) g->sms = 148;
+  for (int q = 0; q < g->R; ++q) {
+    hjb_layout lq;
+    hjb_partition(d->dim, d->n, d->nranks, q, d->halo, &lq);
+    g->r0s.push_back(lq.row0);
+    g->r1s.push_back(lq.row1);
+  }
+  g->L0 = make_level(g->D, g->n, g->lo, g->hi, g->k, g->h, lay.row0, lay.row1, lay.local_row0,
+                     lay.local_row0 + lay.local_rows);
+  g->N = lay.local_elems;
+  g->n_interior = lay.n_interior;
+  g->n_boundary = lay.n_boundary;
+  if (g->R > 1) {
+    std::string err;
+    bool ok;
+    if (d->comm == HJB_COMM_THREADS) {
+      auto* c = new ThreadComm();
+      g->comm.reset(c);
+      ok = ThreadComm::init(c, d->nccl_id, d->rank, d->nranks, &err);
+    } else {
+      auto* c = new NcclComm();
+      g->comm.reset(c);
+      ok = NcclComm::init(c, d->nccl_id, d->rank, d->nranks, &err);
+    }
+    if (!ok) {
+      hjb_grid_destroy(g);
+      return fail(HJB_ERR_NCCL, err);
+    }
+  }
+  const size_t vb = (size_t)g->N * sizeof(double);
+  double** vecs[] = {&g->r, &g->rhat, &g->p, &g->v, &g->s, &g->t, &g->phat, &g->shat, &g->F};
+  hjb_status s = HJB_OK;
+  for (double** pv : vecs) {
+    if ((s = dalloc((void**)pv, vb)) != HJB_OK) {
+      hjb_grid_destroy(g);
+      return s;
+    }
+    cudaMemsetAsync(*pv, 0, vb, g->st);
+  }
+  if ((s = dalloc((void**)&g->partial, (size_t)kMaxBlocks * 2 * sizeof(double))) != HJB_OK ||
+      (s = dalloc((void**)&g->red, 4 * sizeof(double))) != HJB_OK ||
+      (s = dalloc((void**)&g->red_all, (size_t)2 * g->R * sizeof(double))) != HJB_OK ||
+      (s = dalloc((void**)&g->S, sizeof(KScal))) != HJB_OK ||
+      (s = dalloc((void**)&g->pol_int, (size_t)g->N)) != HJB_OK) {
+    hjb_grid_destroy(g);
+    return s;
+  }
+  cudaMemsetAsync(g->pol_int, 0, (size_t)g->N, g->st);
+  if (cudaMallocHost((void**)&g->hS, sizeof(KScal)) != cudaSuccess ||
+      cudaMallocHost((void**)&g->hred, 4 * sizeof(double)) != cudaSuccess) {
+    hjb_grid_destroy(g);
+    return fail(HJB_ERR_OOM, "pinned alloc");
+  }
+  for (auto& e : g->ev) cudaEventCreate(&e);
+  for (auto& e : g->pev) cudaEventCreate(&e);
+  cudaError_t e = cudaStreamSynchronize(g->st);
+  if (e != cudaSuccess) {
+    hjb_grid_destroy(g);
+    return fail(HJB_ERR_CUDA, cudaGetErrorString(e));
+  }
+  hjb_mg_params_default(g->D, &g->mgp);
+  *out = g;
+  return HJB_OK;
+}
+
 extern "C" hjb_status hjb_grid_query(hjb_grid_t g, hjb_layout* o) {
   if (!g || !o) return fail(HJB_ERR_INVALID_ARG, "null handle/out");
-  o->n = g->n;
-  o->row_elems = g->L0.row_elems;
-  o->row0 = 0;
-  o->row1 = g->n;
-  o->halo = 0;
-  o->local_row0 = g->L0.local_row0;
-  o->local_rows = g->L0.local_rows;
-  o->local_elems = g->N;
-  o->n_interior = g->n_interior;
-  o->n_boundary = g->n_boundary;
+  *o = g->lay;
   o->n_levels = (int32_t)g->levels.size();
   o->h = g->h;
   o->k = g->k;
@@ -504,6 +622,28 @@ extern "C" hjb_status hjb_set_coeffs(hjb_grid_t g, const hjb_coeffs* c) {
                 (c->b_node ? g->D : 0) + (c->c_node ? 1 : 0);
   g->have_coeffs = true;
   g->mg_ready = false;
+  if (g->R > 1) {  // the halo must cover the widest stencil (hjb_partition)
+    const double nodes = (double)g->L0.n_own;
+    if (g->D == 2)
+      LAUNCH(HJB_KC_BOUNDARY, nodes, nodes * 8.0 * (1 + g->nplanes0), 0,
+             k_reach<2><<<dims(g, g->L0, (const void*)k_reach<2>), kTX, 0, g->st>>>(g->L0, g->C0, g->partial));
+    else
+      LAUNCH(HJB_KC_BOUNDARY, nodes, nodes * 8.0 * (1 + g->nplanes0), 0,
+             k_reach<3><<<dims(g, g->L0, (const void*)k_reach<3>), kTX, 0, g->st>>>(g->L0, g->C0, g->partial));
+    CKL();
+    hjb_status err;
+    double rb = 0.0;
+    const double rd = host_finalize(g, g->nblk_last, 0x3u, SC_NONE, &err, &rb);
+    if (err != HJB_OK) return err;
+    g->reach_diff = rd;
+    g->reach_drift = rb;
+    const int64_t need = (int64_t)std::floor(std::max(rd, rb) * (1.0 + 1e-12)) + 1;
+    if (need > g->lay.halo) {
+      g->have_coeffs = false;
+      return fail(HJB_ERR_INVALID_ARG, "halo too small for these coefficients: need " + std::to_string(need) +
+                                           " rows, grid has " + std::to_string(g->lay.halo));
+    }
+  }
   return HJB_OK;
 }
 
@@ -519,16 +659,42 @@ extern "C" hjb_status hjb_set_source(hjb_grid_t g, const double* f_basis, const 
   return HJB_OK;
 }
 
+// the fine level as a Level (before hjb_mg_setup built the hierarchy)
+static const Level& fine_level(hjb_grid* g, Level& tmp) {
+  if (!g->levels.empty()) return g->levels[0];
+  tmp.L = g->L0;
+  tmp.replicated = false;
+  tmp.H = g->lay.halo;
+  tmp.r0s = g->r0s;
+  tmp.r1s = g->r1s;
+  return tmp;
+}
+
+// a const caller array whose halo rows must be filled: copy into scratch first (nranks > 1)
+static hjb_status halo_input(hjb_grid* g, const double* x, const double** out) {
+  *out = x;
+  if (g->R == 1) return HJB_OK;
+  if (!g->scratch) TRY(dalloc((void**)&g->scratch, (size_t)g->N * sizeof(double)));
+  CK(cudaMemcpyAsync(g->scratch, x, (size_t)g->N * sizeof(double), cudaMemcpyDeviceToDevice, g->st));
+  Level tmp;
+  TRY(halo_exchange(g, fine_level(g, tmp), g->scratch, g->lay.halo));
+  *out = g->scratch;
+  return HJB_OK;
+}
+
 // ---------------------------------------------------------------------------- policy improvement
+// U's halo rows must already be exchanged
 static hjb_status policy_update_dev(hjb_grid* g, double dt, const double* U, const double* Uprev, uint8_t* pol,
                                     double* F, hjb_pi_stats* out) {
   const double nodes = (double)g->L0.n_own;
   const double bpn = 8.0 + 8.0 + 1.0 + 1.0 + 8.0 + 8.0 * g->Q + 8.0 * g->nplanes0;
   const double fpn = g->K * ((2.0 * g->P + 1.0) * (1 << g->D) * 2.0 + 2.0 * g->Q + 4.0);
-  if (g->D == 2) LAUNCH(HJB_KC_SEARCH, nodes, nodes * bpn, nodes * fpn,
-                        k_search<2><<<dims(g, g->L0, (const void*)k_search<2>), kTX, 0, g->st>>>(g->L0, g->C0, dt, U, Uprev, pol, F, g->partial));
-  else LAUNCH(HJB_KC_SEARCH, nodes, nodes * bpn, nodes * fpn,
-              k_search<3><<<dims(g, g->L0, (const void*)k_search<3>), kTX, 0, g->st>>>(g->L0, g->C0, dt, U, Uprev, pol, F, g->partial));
+  if (g->D == 2)
+    LAUNCH(HJB_KC_SEARCH, nodes, nodes * bpn, nodes * fpn,
+           k_search<2><<<dims(g, g->L0, (const void*)k_search<2>), kTX, 0, g->st>>>(g->L0, g->C0, dt, U, Uprev, pol, F, g->partial));
+  else
+    LAUNCH(HJB_KC_SEARCH, nodes, nodes * bpn, nodes * fpn,
+           k_search<3><<<dims(g, g->L0, (const void*)k_search<3>), kTX, 0, g->st>>>(g->L0, g->C0, dt, U, Uprev, pol, F, g->partial));
   CKL();
   hjb_status err;
   double changed = 0.0;
@@ -553,7 +719,9 @@ extern "C" hjb_status hjb_policy_update(hjb_grid_t g, double dt, const double* U
   if (!g || !U || !U_prev || !policy || !F) return fail(HJB_ERR_INVALID_ARG, "null argument");
   TRY(check_dt(g, dt));
   CK(cudaSetDevice(g->desc.device));
-  return policy_update_dev(g, dt, U, U_prev, policy, F, out);
+  const double* Ux;
+  TRY(halo_input(g, U, &Ux));
+  return policy_update_dev(g, dt, Ux, U_prev, policy, F, out);
 }
 
 // ---------------------------------------------------------------------------- apply
@@ -561,27 +729,38 @@ extern "C" hjb_status hjb_apply(hjb_grid_t g, double dt, const uint8_t* policy, 
   if (!g || !policy || !x || !y) return fail(HJB_ERR_INVALID_ARG, "null argument");
   TRY(check_dt(g, dt));
   CK(cudaSetDevice(g->desc.device));
-  if (x != y) CK(cudaMemcpyAsync(y, x, (size_t)g->N * sizeof(double), cudaMemcpyDeviceToDevice, g->st));
-  else return fail(HJB_ERR_INVALID_ARG, "x and y must not alias");
-  op(g, g->L0, g->C0, OP_APPLY, 0, dt, 0.0, policy, x, nullptr, y, nullptr);
+  if (x == y) return fail(HJB_ERR_INVALID_ARG, "x and y must not alias");
+  CK(cudaMemcpyAsync(y, x, (size_t)g->N * sizeof(double), cudaMemcpyDeviceToDevice, g->st));
+  const double* xx;
+  TRY(halo_input(g, x, &xx));
+  if (g->D == 2) launch_operator<2>(g, g->L0, g->C0, OP_APPLY, 0, dt, 0.0, policy, xx, nullptr, y, nullptr);
+  else launch_operator<3>(g, g->L0, g->C0, OP_APPLY, 0, dt, 0.0, policy, xx, nullptr, y, nullptr);
   CKL();
   return HJB_OK;
 }
 
 // ---------------------------------------------------------------------------- multigrid
+static int64_t level_halo(hjb_grid* g, const LevelDev& L) {
+  // reach in this level's cells scales with kh, k2h relative to the fine level (same fields)
+  const double rd = g->reach_diff * (L.kh / g->L0.kh), rb = g->reach_drift * (L.k2h / g->L0.k2h);
+  return (int64_t)std::floor(std::max(rd, rb) * (1.0 + 1e-12)) + 1;
+}
+
 static hjb_status build_levels(hjb_grid* g, const hjb_mg_params* mp) {
   free_levels(g);
   const int D = g->D;
   int64_t n = g->n;
-  g->levels.push_back(Level());
-  g->levels[0].L = g->L0;
-  g->levels[0].elems = g->N;
-  g->levels[0].C = g->C0;
-  auto interior_count = [&](int64_t nn) {
-    int64_t c = 1;
-    for (int d = 0; d < D; ++d) c *= (nn - 2);
-    return c;
-  };
+  {
+    Level l0;
+    l0.L = g->L0;
+    l0.elems = g->N;
+    l0.C = g->C0;
+    l0.H = g->lay.halo;
+    l0.r0s = g->r0s;
+    l0.r1s = g->r1s;
+    g->levels.push_back(l0);
+  }
+  auto interior_count = [&](int64_t nn) { return ipow(nn - 2, D); };
   while ((int)g->levels.size() < mp->max_levels) {
     const bool small = interior_count(n) <= 160 && n <= std::max<int64_t>(mp->coarse_max_n, 3);
     if (small) break;
@@ -592,12 +771,35 @@ static hjb_status build_levels(hjb_grid* g, const hjb_mg_params* mp) {
       }
       break;
     }
+    const Level& lf = g->levels.back();
     const int64_t nc = (n - 1) / 2 + 1;
     Level l;
     const double hc = (g->hi - g->lo) / (double)(nc - 1);
     const double kc = (mp->coarse_k_mode == 1) ? std::sqrt(hc) : g->k;
     const double k2c = (mp->coarse_k_mode == 1) ? hc : g->h;
-    l.L = make_level(D, nc, g->lo, g->hi, kc, k2c, 0, 1);
+    l.L = full_level(D, nc, g->lo, g->hi, kc, k2c);
+    l.replicated = (g->R > 1) && lf.replicated;
+    if (g->R > 1 && !lf.replicated) {
+      // coarse row J is owned by the rank owning fine row 2J: J in [ceil(r0/2), ceil(r1/2))
+      std::vector<int64_t> c0(g->R), c1(g->R);
+      for (int q = 0; q < g->R; ++q) {
+        c0[q] = (lf.r0s[q] + 1) / 2;
+        c1[q] = (lf.r1s[q] + 1) / 2;
+      }
+      const int64_t H = level_halo(g, l.L);
+      bool thin = nc <= mp->gather_n;
+      for (int q = 0; q < g->R; ++q) thin |= (c1[q] - c0[q]) < std::max<int64_t>(H, 1);
+      if (thin) {
+        l.replicated = true;
+      } else {
+        l.r0s = c0;
+        l.r1s = c1;
+        l.H = H;
+        const int64_t r0 = c0[g->rank], r1 = c1[g->rank];
+        l.L = make_level(D, nc, g->lo, g->hi, kc, k2c, r0, r1, std::max<int64_t>(0, r0 - H),
+                         std::min<int64_t>(nc, r1 + H));
+      }
+    }
     l.elems = l.L.local_rows * l.L.row_elems;
     g->levels.push_back(l);
     n = nc;
@@ -605,6 +807,10 @@ static hjb_status build_levels(hjb_grid* g, const hjb_mg_params* mp) {
   if (interior_count(g->levels.back().L.n) > 160) {
     free_levels(g);
     return fail(HJB_ERR_UNSUPPORTED, "coarsest level too large for the dense solve (needs n = 2^l + 1)");
+  }
+  if (g->R > 1 && (g->levels.size() == 1 || !g->levels.back().replicated)) {
+    free_levels(g);
+    return fail(HJB_ERR_UNSUPPORTED, "multigrid on several ranks: the coarsest level must be gathered");
   }
   // field planes present on the fine level (f_feat is not needed below level 0)
   int nplanes = 0;
@@ -627,7 +833,10 @@ static hjb_status build_levels(hjb_grid* g, const hjb_mg_params* mp) {
       CK(cudaMemsetAsync(l.x, 0, vb, g->st));
       CK(cudaMemsetAsync(l.b, 0, vb, g->st));
       CK(cudaMemsetAsync(l.pol, 0, (size_t)l.elems, g->st));
-      if (nplanes > 0) TRY(dalloc((void**)&l.fields, (size_t)nplanes * vb));
+      if (nplanes > 0) {
+        TRY(dalloc((void**)&l.fields, (size_t)nplanes * vb));
+        CK(cudaMemsetAsync(l.fields, 0, (size_t)nplanes * vb, g->st));
+      }
       CoefDev C = g->C0;
       C.ld = l.elems;
       C.f_feat = nullptr;
@@ -646,6 +855,16 @@ static hjb_status build_levels(hjb_grid* g, const hjb_mg_params* mp) {
   return HJB_OK;
 }
 
+// coarse rows of the first replicated level computed by each rank (from its last slab level)
+static void transition_rows(hjb_grid* g, const Level& lf, std::vector<int64_t>& J0, std::vector<int64_t>& J1) {
+  J0.resize(g->R);
+  J1.resize(g->R);
+  for (int q = 0; q < g->R; ++q) {
+    J0[q] = (lf.r0s[q] + 1) / 2;
+    J1[q] = (lf.r1s[q] + 1) / 2;
+  }
+}
+
 template <int D>
 static hjb_status inject_all(hjb_grid* g) {
   for (size_t i = 1; i < g->levels.size(); ++i) {
@@ -653,7 +872,12 @@ static hjb_status inject_all(hjb_grid* g) {
     Level& lc = g->levels[i];
     const uint8_t* pf = (i == 1) ? g->mg_pol0 : lf.pol;
     const int nb = nblocks1d(lc.elems);
-    LAUNCH(HJB_KC_TRANSFER, lc.elems, 2.0 * lc.elems, 0, k_inject_u8<D><<<nb, 256, 0, g->st>>>(lf.L, lc.L, pf, lc.pol));
+    // fine rows whose policy / field values are valid on this rank
+    const bool fslab = g->R > 1 && !lf.replicated;
+    const int64_t fr_lo = fslab ? lf.r0s[g->rank] : 0;
+    const int64_t fr_hi = fslab ? lf.r1s[g->rank] : lf.L.n;
+    LAUNCH(HJB_KC_TRANSFER, lc.elems, 2.0 * lc.elems, 0,
+           k_inject_u8<D><<<nb, 256, 0, g->st>>>(lf.L, lc.L, pf, lc.pol, fr_lo, fr_hi));
     struct FP { const double* f; double* c; int np; };
     const FP fps[] = {{lf.C.sigma_scale, (double*)lc.C.sigma_scale, g->P},
                       {lf.C.sigma_node, (double*)lc.C.sigma_node, g->P * D},
@@ -663,8 +887,17 @@ static hjb_status inject_all(hjb_grid* g) {
     for (const FP& f : fps)
       if (f.f)
         LAUNCH(HJB_KC_TRANSFER, lc.elems, 16.0 * f.np * lc.elems, 0,
-               k_inject_f64<D><<<nb, 256, 0, g->st>>>(lf.L, lc.L, f.f, lf.C.ld, f.c, lc.C.ld, f.np));
+               k_inject_f64<D><<<nb, 256, 0, g->st>>>(lf.L, lc.L, f.f, lf.C.ld, f.c, lc.C.ld, f.np, fr_lo, fr_hi));
     CKL();
+    if (lc.replicated && fslab) {  // gather level: every rank gets the full coarse data
+      std::vector<int64_t> J0, J1;
+      transition_rows(g, lf, J0, J1);
+      const int64_t re = lc.L.row_elems;
+      TRY(gather_rows(g, lc.pol, 1, re, J0, J1));
+      for (const FP& f : fps)
+        if (f.f)
+          for (int k = 0; k < f.np; ++k) TRY(gather_rows(g, f.c + (size_t)k * lc.C.ld, 8, re, J0, J1));
+    }
   }
   Level& lc = g->levels.back();
   const int64_t Nc = lc.L.n_own;
@@ -692,8 +925,7 @@ extern "C" hjb_status hjb_mg_setup(hjb_grid_t g, double dt, const uint8_t* polic
   const bool rebuild = g->levels.empty() || std::memcmp(&g->mgp, p, sizeof(hjb_mg_params)) != 0 ||
                        g->levels[0].C.ld != g->C0.ld;
   if (rebuild) TRY(build_levels(g, p));
-  g->levels[0].C = g->C0;
-  // refresh field pointers of level 0 (set_coeffs may have changed them)
+  g->levels[0].C = g->C0;  // refresh field pointers of level 0 (set_coeffs may have changed them)
   g->mg_pol0 = policy;
   g->mg_dt = dt;
   if (g->D == 2) TRY(inject_all<2>(g));
@@ -709,6 +941,7 @@ static hjb_status vcycle(hjb_grid* g, size_t l, const double* b, double* out) {
   const uint8_t* pol = (l == 0) ? g->mg_pol0 : lv.pol;
   const LevelDev& L = lv.L;
   cudaStream_t st = g->st;
+  const bool fine = (l == 0);
   if (l + 1 == g->levels.size()) {
     const int Nc = (int)L.n_own;
     LAUNCH(HJB_KC_COARSE, Nc, 8.0 * Nc * Nc + 16.0 * Nc, 2.0 * Nc * Nc,
@@ -720,21 +953,41 @@ static hjb_status vcycle(hjb_grid* g, size_t l, const double* b, double* out) {
   const int npre = g->mgp.nu_pre, npost = g->mgp.nu_post;
   double* bufs[2] = {out, lv.tmp};
   int cur = ((npre - 1 + npost) % 2 == 0) ? 0 : 1;  // so the last sweep lands in `out`
-  launch_operator<D>(g, L, lv.C, OP_JACOBI0, 0, dt, om, pol, nullptr, b, bufs[cur], nullptr);
+  launch_operator<D>(g, L, lv.C, OP_JACOBI0, 0, dt, om, pol, nullptr, b, bufs[cur], nullptr, fine);
   for (int k = 1; k < npre; ++k) {
-    launch_operator<D>(g, L, lv.C, OP_JACOBI, 0, dt, om, pol, bufs[cur], b, bufs[1 - cur], nullptr);
+    TRY(halo_exchange(g, lv, bufs[cur], lv.H));
+    launch_operator<D>(g, L, lv.C, OP_JACOBI, 0, dt, om, pol, bufs[cur], b, bufs[1 - cur], nullptr, fine);
     cur = 1 - cur;
   }
-  launch_operator<D>(g, L, lv.C, OP_RESID, 0, dt, 0.0, pol, bufs[cur], b, lv.res, nullptr);
+  TRY(halo_exchange(g, lv, bufs[cur], lv.H));
+  launch_operator<D>(g, L, lv.C, OP_RESID, 0, dt, 0.0, pol, bufs[cur], b, lv.res, nullptr, fine);
   Level& lc = g->levels[l + 1];
-  LAUNCH(HJB_KC_TRANSFER, L.n_own, 8.0 * (L.n_own + lc.L.n_own), 18.0 * lc.L.n_own,
-         k_restrict<D><<<dims(g, lc.L, (const void*)k_restrict<D>), kTX, 0, st>>>(L, lc.L, lv.res, lc.b));
-  CKL();
+  TRY(halo_exchange(g, lv, lv.res, 1));
+  if (lc.replicated && !lv.replicated) {
+    // gather level: restrict my coarse rows into the full coarse array, then all-gather them
+    std::vector<int64_t> J0, J1;
+    transition_rows(g, lv, J0, J1);
+    LevelDev view = lc.L;
+    view.row_first = J0[g->rank];
+    view.nrows = (int)((J1[g->rank] - J0[g->rank]) * ipow(lc.L.n - 2, D - 2));
+    view.n_own = (int64_t)view.nrows * view.nI;
+    if (view.nrows > 0)
+      LAUNCH(HJB_KC_TRANSFER, L.n_own, 8.0 * (L.n_own + view.n_own), 18.0 * view.n_own,
+             k_restrict<D><<<dims(g, view, (const void*)k_restrict<D>), kTX, 0, st>>>(L, view, lv.res, lc.b));
+    CKL();
+    TRY(gather_rows(g, lc.b, 8, lc.L.row_elems, J0, J1));
+  } else {
+    LAUNCH(HJB_KC_TRANSFER, L.n_own, 8.0 * (L.n_own + lc.L.n_own), 18.0 * lc.L.n_own,
+           k_restrict<D><<<dims(g, lc.L, (const void*)k_restrict<D>), kTX, 0, st>>>(L, lc.L, lv.res, lc.b));
+    CKL();
+  }
   TRY(vcycle<D>(g, l + 1, lc.b, lc.x));
+  TRY(halo_exchange(g, lc, lc.x, 1));
   LAUNCH(HJB_KC_TRANSFER, L.n_own, 16.0 * L.n_own + 8.0 * lc.L.n_own, 4.0 * L.n_own,
          k_prolong_add<D><<<dims(g, L, (const void*)k_prolong_add<D>), kTX, 0, st>>>(L, lc.L, lc.x, bufs[cur]));
   for (int k = 0; k < npost; ++k) {
-    launch_operator<D>(g, L, lv.C, OP_JACOBI, 0, dt, om, pol, bufs[cur], b, bufs[1 - cur], nullptr);
+    TRY(halo_exchange(g, lv, bufs[cur], lv.H));
+    launch_operator<D>(g, L, lv.C, OP_JACOBI, 0, dt, om, pol, bufs[cur], b, bufs[1 - cur], nullptr, fine);
     cur = 1 - cur;
   }
   CKL();
@@ -745,8 +998,12 @@ static hjb_status vcycle(hjb_grid* g, size_t l, const double* b, double* out) {
 static hjb_status precond(hjb_grid* g, bool use_mg, const double* b, double* x) {
   if (!use_mg) {
     const double nn = (double)g->L0.n_own;
-    if (g->D == 2) LAUNCH(HJB_KC_VECTOR, nn, 16.0 * nn, 0, k_copy_interior<2><<<dims(g, g->L0, (const void*)k_copy_interior<2>), kTX, 0, g->st>>>(g->L0, b, x));
-    else LAUNCH(HJB_KC_VECTOR, nn, 16.0 * nn, 0, k_copy_interior<3><<<dims(g, g->L0, (const void*)k_copy_interior<3>), kTX, 0, g->st>>>(g->L0, b, x));
+    if (g->D == 2)
+      LAUNCH(HJB_KC_VECTOR, nn, 16.0 * nn, 0,
+             k_copy_interior<2><<<dims(g, g->L0, (const void*)k_copy_interior<2>), kTX, 0, g->st>>>(g->L0, b, x));
+    else
+      LAUNCH(HJB_KC_VECTOR, nn, 16.0 * nn, 0,
+             k_copy_interior<3><<<dims(g, g->L0, (const void*)k_copy_interior<3>), kTX, 0, g->st>>>(g->L0, b, x));
     CKL();
     return HJB_OK;
   }
@@ -772,13 +1029,17 @@ static hjb_status norms_dev(hjb_grid* g, const double* v, double* n2, double* ni
   return err;
 }
 
+// eta > 0: inexact policy evaluation, stop at ||r||_2 <= max(rtol ||F||_2, eta ||r_0||_2).
+// x's halo rows are exchanged here (x is the caller's in/out array).
 template <int D>
-// eta > 0: inexact policy evaluation, stop at ||r||_2 <= max(rtol ||F||_2, eta ||r_0||_2)
 static hjb_status bicgstab(hjb_grid* g, double dt, const uint8_t* pol, const double* F, double* x,
                            const hjb_solve_params* sp, hjb_solve_stats* out, double eta = 0.0) {
   const LevelDev& L = g->L0;
   const CoefDev& C = g->C0;
   cudaStream_t st = g->st;
+  Level tmpl;
+  const Level& lv0 = fine_level(g, tmpl);
+  const int64_t H = g->lay.halo;
   const bool mg = sp->use_mg != 0;
   if (mg && (!g->mg_ready || g->mg_pol0 != pol || g->mg_dt != dt))
     return fail(HJB_ERR_STATE, "hjb_mg_setup must be called with the same policy and dt before solving");
@@ -791,6 +1052,7 @@ static hjb_status bicgstab(hjb_grid* g, double dt, const uint8_t* pol, const dou
   bool converged = false;
   for (int restart = 0; restart < 4 && !converged; ++restart) {
     // r = F - A x ; rhat = r ; p = r
+    TRY(halo_exchange(g, lv0, x, H));
     launch_operator<D>(g, L, C, OP_RESID, 0, dt, 0.0, pol, x, F, g->r, nullptr);
     LAUNCH(HJB_KC_VECTOR, L.n_own, 24.0 * L.n_own, 2.0 * L.n_own,
            k_bicg_init<D><<<dims(g, L, (const void*)k_bicg_init<D>), kTX, 0, st>>>(L, g->r, g->rhat, g->p, g->partial));
@@ -800,24 +1062,25 @@ static hjb_status bicgstab(hjb_grid* g, double dt, const uint8_t* pol, const dou
     if (!std::isfinite(rr)) return fail(HJB_ERR_NONFINITE, "non-finite residual");
     if (restart == 0 && eta > 0.0) tol = std::max(tol, eta * std::sqrt(rr));
     if (std::sqrt(rr) <= tol) { converged = true; break; }
-    bool restart_needed = false;
     int inner = 0;
     while (it < sp->krylov_maxit) {
       if (inner > 0)
         LAUNCH(HJB_KC_VECTOR, L.n_own, 32.0 * L.n_own, 4.0 * L.n_own,
                k_bicg_p<D><<<dims(g, L, (const void*)k_bicg_p<D>), kTX, 0, st>>>(L, g->S, g->r, g->p, g->v));
       TRY(precond(g, mg, g->p, g->phat));
+      TRY(halo_exchange(g, lv0, g->phat, H));
       launch_operator<D>(g, L, C, OP_APPLY, 1, dt, 0.0, pol, g->phat, nullptr, g->v, g->rhat);
-      { const int nb = g->nblk_last; LAUNCH(HJB_KC_REDUCE, nb, 16.0 * nb, 2.0 * nb, k_finalize<<<1, 1024, 0, st>>>(g->partial, nb, g->red, 0u, g->S, SC_AFTER_V)); }
+      TRY(reduce_dev(g, g->nblk_last, 0u, SC_AFTER_V));
       LAUNCH(HJB_KC_VECTOR, L.n_own, 24.0 * L.n_own, 4.0 * L.n_own,
              k_bicg_s<D><<<dims(g, L, (const void*)k_bicg_s<D>), kTX, 0, st>>>(L, g->S, g->r, g->v, g->s, g->partial));
       TRY(precond(g, mg, g->s, g->shat));
+      TRY(halo_exchange(g, lv0, g->shat, H));
       launch_operator<D>(g, L, C, OP_APPLY, 2, dt, 0.0, pol, g->shat, nullptr, g->t, g->s);
-      { const int nb = g->nblk_last; LAUNCH(HJB_KC_REDUCE, nb, 16.0 * nb, 2.0 * nb, k_finalize<<<1, 1024, 0, st>>>(g->partial, nb, g->red, 0u, g->S, SC_AFTER_T)); }
+      TRY(reduce_dev(g, g->nblk_last, 0u, SC_AFTER_T));
       LAUNCH(HJB_KC_VECTOR, L.n_own, 64.0 * L.n_own, 10.0 * L.n_own,
-             k_bicg_x<D><<<dims(g, L, (const void*)k_bicg_x<D>), kTX, 0, st>>>(L, g->S, x, g->phat, g->shat, g->s, g->t, g->r, g->rhat, g->partial));
-      { const int nb = g->nblk_last; LAUNCH(HJB_KC_REDUCE, nb, 16.0 * nb, 2.0 * nb, k_finalize<<<1, 1024, 0, st>>>(g->partial, nb, g->red, 0u, g->S, SC_AFTER_R)); }
-      CKL();
+             k_bicg_x<D><<<dims(g, L, (const void*)k_bicg_x<D>), kTX, 0, st>>>(L, g->S, x, g->phat, g->shat, g->s,
+                                                                               g->t, g->r, g->rhat, g->partial));
+      TRY(reduce_dev(g, g->nblk_last, 0u, SC_AFTER_R));
       CK(cudaMemcpyAsync(g->hS, g->S, sizeof(KScal), cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
       ++it;
@@ -825,9 +1088,10 @@ static hjb_status bicgstab(hjb_grid* g, double dt, const uint8_t* pol, const dou
       rr = g->hS->rr;
       if (!std::isfinite(rr)) return fail(HJB_ERR_NONFINITE, "non-finite residual in BiCGSTAB");
       if (std::sqrt(rr) <= tol) break;
-      if (g->hS->breakdown) { restart_needed = true; break; }
+      if (g->hS->breakdown) break;  // restart from the current iterate
     }
     // true residual check (recursive residual drifts, SURVEY hard part 5)
+    TRY(halo_exchange(g, lv0, x, H));
     launch_operator<D>(g, L, C, OP_RESID, 0, dt, 0.0, pol, x, F, g->r, nullptr);
     double tr2, trinf;
     TRY(norms_dev<D>(g, g->r, &tr2, &trinf));
@@ -838,7 +1102,6 @@ static hjb_status bicgstab(hjb_grid* g, double dt, const uint8_t* pol, const dou
     }
     if (tr2 <= tol) { converged = true; break; }
     if (it >= sp->krylov_maxit) break;
-    (void)restart_needed;
   }
   if (out && converged && it == 0) {
     out->iters = 0;
@@ -902,10 +1165,14 @@ extern "C" hjb_status hjb_step(hjb_grid_t g, double dt, const double* U_prev, do
   if (dpsi) {
     const int nbb = (int)std::min<int64_t>((g->n_boundary + 255) / 256, 4096);
     const double nbd = (double)g->n_boundary;
-    if (g->D == 2) LAUNCH(HJB_KC_BOUNDARY, nbd, 16.0 * nbd, 0, k_scatter_psi<2><<<nbb, 256, 0, st>>>(g->L0, g->n_boundary, dpsi, dU));
-    else LAUNCH(HJB_KC_BOUNDARY, nbd, 16.0 * nbd, 0, k_scatter_psi<3><<<nbb, 256, 0, st>>>(g->L0, g->n_boundary, dpsi, dU));
+    if (g->D == 2)
+      LAUNCH(HJB_KC_BOUNDARY, nbd, 16.0 * nbd, 0, k_scatter_psi<2><<<nbb, 256, 0, st>>>(g->L0, g->n_boundary, dpsi, dU));
+    else
+      LAUNCH(HJB_KC_BOUNDARY, nbd, 16.0 * nbd, 0, k_scatter_psi<3><<<nbb, 256, 0, st>>>(g->L0, g->n_boundary, dpsi, dU));
     CKL();
   }
+  Level tmpl;
+  const Level& lv0 = fine_level(g, tmpl);
   hjb_step_stats S{};
   float ms;
   hjb_status result = HJB_OK;
@@ -913,6 +1180,7 @@ extern "C" hjb_status hjb_step(hjb_grid_t g, double dt, const double* U_prev, do
   for (int it = 1; it <= sp->max_pi; ++it) {
     hjb_pi_stats pis{};
     cudaEventRecord(g->ev[0], st);
+    TRY(halo_exchange(g, lv0, dU, g->lay.halo));
     TRY(policy_update_dev(g, dt, dU, dprev, dpol, g->F, &pis));
     cudaEventRecord(g->ev[1], st);
     cudaEventSynchronize(g->ev[1]);

@@ -168,6 +168,44 @@ __global__ void __launch_bounds__(1024) k_finalize(const double* __restrict__ pa
   }
 }
 
+// multi-rank: combine the per-rank reductions gathered as all[q][2] (fixed rank order: bitwise
+// repeatable for a given rank count), then the BiCGSTAB scalar update `which`
+__global__ void k_combine(const double* __restrict__ all, int nranks, double* out, unsigned maxmask, KScal* S,
+                          int which) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double red[2];
+  for (int k = 0; k < 2; ++k) {
+    const bool mx = (maxmask >> k) & 1u;
+    double v = mx ? -INFINITY : 0.0;
+    for (int q = 0; q < nranks; ++q) v = mx ? fmax(v, all[2 * q + k]) : v + all[2 * q + k];
+    red[k] = v;
+  }
+  out[0] = red[0];
+  out[1] = red[1];
+  if (which != SC_NONE) scal_update(S, red, which);
+}
+
+// largest stencil offset along the slowest axis in cells over owned nodes and all controls:
+// partial [max diffusion |o|, max drift |o|]  (halo check of hjb_set_coeffs)
+template <int D>
+__global__ void __launch_bounds__(kTX) k_reach(LevelDev L, CoefDev C, double* partial) {
+  double red[2] = {0.0, 0.0};
+  FOR_INTERIOR(L) {
+    Node<D> nd;
+    node_at<D>(L, col, row, nd);
+    load_fields<D>(C, nd);
+    for (int a = 0; a < C.K; ++a) {
+      for (int p = 0; p < C.P; ++p) {
+        const double o = L.kh * fma(nd.sc[p], __ldg(C.sigma_dir + (a * C.P + p) * D + D - 1), nd.sn[p][D - 1]);
+        red[0] = fmax(red[0], fabs(o));
+      }
+      const double ob = L.k2h * fma(nd.bs, __ldg(C.b_dir + a * D + D - 1), nd.bn[D - 1]);
+      red[1] = fmax(red[1], fabs(ob));
+    }
+  }
+  block_reduce_store<2>(red, partial, 0x3u);
+}
+
 // r_hat = r, p = r ; partial: (r,r)
 template <int D>
 __global__ void __launch_bounds__(kTX) k_bicg_init(LevelDev L, const double* __restrict__ r,
@@ -368,9 +406,11 @@ __global__ void __launch_bounds__(kTX) k_prolong_add(LevelDev Lf, LevelDev Lc, c
   }
 }
 
-// inject the policy from level f to level c (coarse node J <- fine node 2J), all local coarse nodes
+// inject the policy from level f to level c (coarse node J <- fine node 2J), every local coarse node
+// whose fine node lies in the fine rows [fr_lo, fr_hi) (the rows whose values are valid there)
 template <int D>
-__global__ void k_inject_u8(LevelDev Lf, LevelDev Lc, const uint8_t* __restrict__ pf, uint8_t* __restrict__ pc) {
+__global__ void k_inject_u8(LevelDev Lf, LevelDev Lc, const uint8_t* __restrict__ pf, uint8_t* __restrict__ pc,
+                            int64_t fr_lo, int64_t fr_hi) {
   const int64_t nloc = Lc.local_rows * Lc.row_elems;
   const int64_t nc = Lc.n, nf = Lf.n;
   for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nloc; q += (int64_t)gridDim.x * blockDim.x) {
@@ -378,7 +418,9 @@ __global__ void k_inject_u8(LevelDev Lf, LevelDev Lc, const uint8_t* __restrict_
     int64_t r = q;
 #pragma unroll
     for (int d = 0; d < D - 1; ++d) { i[d] = r % nc; r /= nc; }
-    const int64_t fr = 2 * (r + Lc.local_row0) - Lf.local_row0;
+    const int64_t gfr = 2 * (r + Lc.local_row0);
+    if (gfr < fr_lo || gfr >= fr_hi) continue;
+    const int64_t fr = gfr - Lf.local_row0;
     if (fr < 0 || fr >= Lf.local_rows) continue;
     int64_t loc = fr;
 #pragma unroll
@@ -390,7 +432,7 @@ __global__ void k_inject_u8(LevelDev Lf, LevelDev Lc, const uint8_t* __restrict_
 // inject nplanes fp64 field planes (plane strides ldf / ldc)
 template <int D>
 __global__ void k_inject_f64(LevelDev Lf, LevelDev Lc, const double* __restrict__ ff, int64_t ldf,
-                             double* __restrict__ fc, int64_t ldc, int nplanes) {
+                             double* __restrict__ fc, int64_t ldc, int nplanes, int64_t fr_lo, int64_t fr_hi) {
   const int64_t nloc = Lc.local_rows * Lc.row_elems;
   const int64_t nc = Lc.n, nf = Lf.n;
   for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nloc; q += (int64_t)gridDim.x * blockDim.x) {
@@ -398,7 +440,9 @@ __global__ void k_inject_f64(LevelDev Lf, LevelDev Lc, const double* __restrict_
     int64_t r = q;
 #pragma unroll
     for (int d = 0; d < D - 1; ++d) { i[d] = r % nc; r /= nc; }
-    const int64_t fr = 2 * (r + Lc.local_row0) - Lf.local_row0;
+    const int64_t gfr = 2 * (r + Lc.local_row0);
+    if (gfr < fr_lo || gfr >= fr_hi) continue;
+    const int64_t fr = gfr - Lf.local_row0;
     if (fr < 0 || fr >= Lf.local_rows) continue;
     int64_t loc = fr;
 #pragma unroll
