@@ -320,8 +320,15 @@ static void launch_operator(hjb_grid* g, const LevelDev& L, const CoefDev& C, in
   const double bpn = 1.0 + 8.0 + (mode != OP_JACOBI0 ? 8.0 : 0.0) + (mode != OP_APPLY ? 8.0 : 0.0) +
                      (ndot >= 1 ? 8.0 : 0.0) + 8.0 * g->nplanes0;
   const double fpn = (2.0 * g->P + 1.0) * (1 << D) * 2.0 + 4.0 + 2.0 * ndot;
-#define OPL(M, ND) LAUNCH(cls, nodes, nodes * bpn, nodes * fpn, \
-    k_operator<D, M, ND><<<dims(g, L, (const void*)k_operator<D, M, ND>), kTX, 0, st>>>(L, C, dt, omega, pol, x, b, y, u, g->partial))
+#define OPL(M, ND)                                                                                            \
+  do {                                                                                                      \
+    if (g->P == 1) LAUNCH(cls, nodes, nodes * bpn, nodes * fpn,                                              \
+        k_operator<D, 1, M, ND><<<dims(g, L, (const void*)k_operator<D, 1, M, ND>), kTX, 0, st>>>(L, C, dt, omega, pol, x, b, y, u, g->partial)); \
+    else if (g->P == 2) LAUNCH(cls, nodes, nodes * bpn, nodes * fpn,                                         \
+        k_operator<D, 2, M, ND><<<dims(g, L, (const void*)k_operator<D, 2, M, ND>), kTX, 0, st>>>(L, C, dt, omega, pol, x, b, y, u, g->partial)); \
+    else LAUNCH(cls, nodes, nodes * bpn, nodes * fpn,                                                        \
+        k_operator<D, (D > 2 ? 3 : 2), M, ND><<<dims(g, L, (const void*)k_operator<D, (D > 2 ? 3 : 2), M, ND>), kTX, 0, st>>>(L, C, dt, omega, pol, x, b, y, u, g->partial)); \
+  } while (0)
   if (mode == OP_APPLY) {
     if (ndot == 0) OPL(OP_APPLY, 0);
     else if (ndot == 1) OPL(OP_APPLY, 1);
@@ -689,12 +696,18 @@ static hjb_status policy_update_dev(hjb_grid* g, double dt, const double* U, con
   const double nodes = (double)g->L0.n_own;
   const double bpn = 8.0 + 8.0 + 1.0 + 1.0 + 8.0 + 8.0 * g->Q + 8.0 * g->nplanes0;
   const double fpn = g->K * ((2.0 * g->P + 1.0) * (1 << g->D) * 2.0 + 2.0 * g->Q + 4.0);
-  if (g->D == 2)
-    LAUNCH(HJB_KC_SEARCH, nodes, nodes * bpn, nodes * fpn,
-           k_search<2><<<dims(g, g->L0, (const void*)k_search<2>), kTX, 0, g->st>>>(g->L0, g->C0, dt, U, Uprev, pol, F, g->partial));
-  else
-    LAUNCH(HJB_KC_SEARCH, nodes, nodes * bpn, nodes * fpn,
-           k_search<3><<<dims(g, g->L0, (const void*)k_search<3>), kTX, 0, g->st>>>(g->L0, g->C0, dt, U, Uprev, pol, F, g->partial));
+#define SRCH(DD, PP)                                                                                          \
+  LAUNCH(HJB_KC_SEARCH, nodes, nodes * bpn, nodes * fpn,                                                    \
+         k_search<DD, PP><<<dims(g, g->L0, (const void*)k_search<DD, PP>), kTX, 0, g->st>>>(g->L0, g->C0, dt, U, Uprev, pol, F, g->partial))
+  if (g->D == 2) {
+    if (g->P == 1) SRCH(2, 1);
+    else SRCH(2, 2);
+  } else {
+    if (g->P == 1) SRCH(3, 1);
+    else if (g->P == 2) SRCH(3, 2);
+    else SRCH(3, 3);
+  }
+#undef SRCH
   CKL();
   hjb_status err;
   double changed = 0.0;

@@ -337,6 +337,135 @@ __device__ __forceinline__ void row_eval(const LevelDev& L, const CoefDev& C, co
   }
 }
 
+// ----------------------------------------------------------------------------- two-phase row
+// The hot kernels evaluate a row in two phases: (1) the geometry of ALL 2P+1 endpoints (fp64, no
+// memory traffic beyond the control tables), (2) all 2^d (2P+1) gathers issued back to back, so
+// their L2 latencies overlap instead of serialising endpoint by endpoint.
+template <int D>
+struct Tap {
+  int c[D];      // cell (lowest corner), global multi-index
+  double s[D];   // fractions in the cell
+  double w;      // weight w_e (0 for a skipped zero step)
+};
+
+template <int D>
+__device__ __forceinline__ int tap_base(const LevelDev& L, const Tap<D>& t) {
+  if (D == 2) return (t.c[1] - (int)L.local_row0) * L.n + t.c[0];
+  return ((t.c[2] - (int)L.local_row0) * L.n + t.c[1]) * L.n + t.c[0];
+}
+
+template <int D>
+__device__ __forceinline__ double tap_value(const LevelDev& L, const double* __restrict__ v, const Tap<D>& t) {
+  const double* p = v + tap_base<D>(L, t);
+  if (D == 2) {
+    const double v00 = __ldg(p), v10 = __ldg(p + 1);
+    const double v01 = __ldg(p + L.n), v11 = __ldg(p + L.n + 1);
+    const double a = fma(t.s[0], v10 - v00, v00);
+    const double b = fma(t.s[0], v11 - v01, v01);
+    return fma(t.s[1], b - a, a);
+  } else {
+    const int n = L.n, nn = n * n;
+    const double v000 = __ldg(p), v100 = __ldg(p + 1);
+    const double v010 = __ldg(p + n), v110 = __ldg(p + n + 1);
+    const double v001 = __ldg(p + nn), v101 = __ldg(p + nn + 1);
+    const double v011 = __ldg(p + nn + n), v111 = __ldg(p + nn + n + 1);
+    const double a0 = fma(t.s[0], v100 - v000, v000);
+    const double b0 = fma(t.s[0], v110 - v010, v010);
+    const double a1 = fma(t.s[0], v101 - v001, v001);
+    const double b1 = fma(t.s[0], v111 - v011, v011);
+    const double p0 = fma(t.s[1], b0 - a0, a0);
+    const double p1 = fma(t.s[1], b1 - a1, a1);
+    return fma(t.s[2], p1 - p0, p0);
+  }
+}
+
+// endpoints of control a at node nd: taps[2p] = +sigma_p, taps[2p+1] = -sigma_p, taps[2P] = drift.
+// Returns wsum = sum_e w_e.
+template <int D, int P>
+__device__ __forceinline__ double row_geometry(const LevelDev& L, const CoefDev& C, const Node<D>& nd, int a,
+                                               Tap<D>* taps) {
+  double wsum = 0.0;
+  const double* sd = C.sigma_dir + a * P * D;
+  const int nm2 = L.n - 2;
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    double o[D];
+    bool nz = false, inside = true;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      o[d] = L.kh * fma(nd.sc[p], __ldg(sd + p * D + d), nd.sn[p][d]);
+      nz |= (o[d] != 0.0);
+      inside &= (fabs(o[d]) <= nd.dist[d]);
+    }
+    Tap<D>& tp = taps[2 * p];
+    Tap<D>& tm = taps[2 * p + 1];
+    if (inside) {  // untruncated pair (A = B = 1); a zero step gets weight 0 (its terms cancel)
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        Split P_, M_;
+        split_pm(o[d], nd.i[d], nm2, P_, M_);
+        tp.c[d] = P_.c; tp.s[d] = P_.s;
+        tm.c[d] = M_.c; tm.s[d] = M_.s;
+      }
+      const double w = nz ? L.inv_2k2 : 0.0;
+      tp.w = w;
+      tm.w = w;
+      wsum += 2.0 * w;
+    } else {
+      double om[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) om[d] = -o[d];
+      int bp, bm;
+      const double mup = ray_mu<D>(L, nd, o, bp);
+      const double mum = ray_mu<D>(L, nd, om, bm);
+      double A = 1.0, B = 1.0;
+      if (bp >= 0 || bm >= 0) {
+        const double sum = mup + mum;
+        A = 2.0 / (mup * sum);
+        B = 2.0 / (mum * sum);
+      }
+      tp.w = A * L.inv_2k2;
+      tm.w = B * L.inv_2k2;
+      wsum += tp.w + tm.w;
+      cell_general<D>(L, nd, o, mup, bp, tp.c, tp.s);
+      cell_general<D>(L, nd, om, mum, bm, tm.c, tm.s);
+    }
+  }
+  {  // drift pair: y_{P+1} = k^2 b, both endpoints equal, A = B = 1/mu (total weight 2/(mu 2k^2))
+    const double* bd_ = C.b_dir + a * D;
+    double o[D];
+    bool nz = false, inside = true;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      o[d] = L.k2h * fma(nd.bs, __ldg(bd_ + d), nd.bn[d]);
+      nz |= (o[d] != 0.0);
+      inside &= (fabs(o[d]) <= nd.dist[d]);
+    }
+    Tap<D>& t = taps[2 * P];
+    if (inside) {
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        Split P_;
+        split_p(o[d], nd.i[d], nm2, P_);
+        t.c[d] = P_.c; t.s[d] = P_.s;
+      }
+      t.w = nz ? L.inv_k2 : 0.0;
+    } else {
+      int bdim;
+      const double mu = ray_mu<D>(L, nd, o, bdim);
+      cell_general<D>(L, nd, o, mu, bdim, t.c, t.s);
+      t.w = (bdim >= 0) ? L.inv_k2 / mu : L.inv_k2;
+    }
+    wsum += t.w;
+  }
+  return wsum;
+}
+
+template <int D>
+__device__ __forceinline__ double tap_self(const Node<D>& nd, const Tap<D>& t) {
+  return t.w * self_weight<D>(nd.i, t.c, t.s);
+}
+
 // ----------------------------------------------------------------------------- reductions
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

@@ -18,22 +18,35 @@ enum OpMode : int {
 };
 
 // NDOT: 0, 1 -> partial[0] = sum y*u ; 2 -> partial[0] = sum y*u, partial[1] = sum y*y
-template <int D, int MODE, int NDOT>
+template <int D, int P, int MODE, int NDOT>
 __global__ void __launch_bounds__(kTX) k_operator(LevelDev L, CoefDev C, double dt, double omega,
-                                                      const uint8_t* __restrict__ pol,
-                                                      const double* __restrict__ x,
-                                                      const double* __restrict__ b, double* __restrict__ y,
-                                                      const double* __restrict__ u, double* partial) {
+                                                  const uint8_t* __restrict__ pol,
+                                                  const double* __restrict__ x,
+                                                  const double* __restrict__ b, double* __restrict__ y,
+                                                  const double* __restrict__ u, double* partial) {
   constexpr bool GATHER = (MODE != OP_JACOBI0);
   constexpr bool SELF = (MODE == OP_JACOBI || MODE == OP_JACOBI0);
+  constexpr int E = 2 * P + 1;
   double dots[2] = {0.0, 0.0};
   FOR_INTERIOR(L) {
     Node<D> nd;
     node_at<D>(L, col, row, nd);
     load_fields<D>(C, nd);
     const int a = pol[nd.loc];
-    double acc, wsum, self;
-    row_eval<D, GATHER, SELF>(L, C, nd, a, x, acc, wsum, self);
+    Tap<D> taps[E];
+    const double wsum = row_geometry<D, P>(L, C, nd, a, taps);
+    double acc = 0.0, self = 0.0;
+    if (GATHER) {
+      double vals[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) vals[e] = tap_value<D>(L, x, taps[e]);
+#pragma unroll
+      for (int e = 0; e < E; ++e) acc = fma(taps[e].w, vals[e], acc);
+    }
+    if (SELF) {
+#pragma unroll
+      for (int e = 0; e < E; ++e) self += tap_self<D>(nd, taps[e]);
+    }
     const double c = nd.cn + __ldg(C.c_ctrl + a);
     double out;
     if (MODE == OP_JACOBI0) {
@@ -61,12 +74,13 @@ __global__ void __launch_bounds__(kTX) k_operator(LevelDev L, CoefDev C, double 
 // ================================================================== control search
 // For every owned interior node: H^a = acc_a - wsum_a U_j + c^a U_j + f^a for all a (lowest-index
 // argmin), policy/F outputs, partials: [max R, changed count].
-template <int D>
+template <int D, int P>
 __global__ void __launch_bounds__(kTX) k_search(LevelDev L, CoefDev C, double dt,
-                                                    const double* __restrict__ U,
-                                                    const double* __restrict__ Uprev,
-                                                    uint8_t* __restrict__ pol, double* __restrict__ F,
-                                                    double* partial) {
+                                                const double* __restrict__ U,
+                                                const double* __restrict__ Uprev,
+                                                uint8_t* __restrict__ pol, double* __restrict__ F,
+                                                double* partial) {
+  constexpr int E = 2 * P + 1;
   double red[2] = {0.0, 0.0};
   FOR_INTERIOR(L) {
     Node<D> nd;
@@ -79,10 +93,16 @@ __global__ void __launch_bounds__(kTX) k_search(LevelDev L, CoefDev C, double dt
     double best = INFINITY, fbest = 0.0;
     int arg = 0;
     for (int a = 0; a < C.K; ++a) {
-      double acc, wsum, self;
-      row_eval<D, true, false>(L, C, nd, a, U, acc, wsum, self);
+      Tap<D> taps[E];
+      const double wsum = row_geometry<D, P>(L, C, nd, a, taps);
+      double vals[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) vals[e] = tap_value<D>(L, U, taps[e]);
+      double acc = 0.0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) acc = fma(taps[e].w, vals[e], acc);
       double f = __ldg(C.f_ctrl + a);
-      const double* fb = C.f_basis + (int64_t)a * C.Q;
+      const double* fb = C.f_basis + a * C.Q;
 #pragma unroll
       for (int q = 0; q < kMaxQ; ++q)
         if (q < C.Q) f = fma(__ldg(fb + q), feat[q], f);

@@ -8,5 +8,5 @@ timeout 600 python tools/opbench.py --cfg 4 --reps 10 > $O/opbench4_cfg4.log 2>&
 timeout 300 python tools/opbench.py --cfg 2 --reps 20 > $O/opbench4_cfg2.log 2>&1; echo "exit $?" >> $O/opbench4_cfg2.log
 CMD="python tools/opbench.py --cfg 4 --reps 2 --only apply"
 timeout 600 $CMD > $O/plain4.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_operator -s 2 -c 2 -o $O/prof4_apply_cfg4 $CMD > $O/ncu4.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_operator -s 2 -c 1 -o $O/prof4_apply_cfg4 $CMD > $O/ncu4.log 2>&1
 echo "ncu exit $?" >> $O/ncu4.log
