@@ -199,24 +199,43 @@ def run_b200(args):
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA device (there is no CPU fallback)")
     torch.cuda.set_device(local)
+    dist = None
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    libbuild.build()
+    if rank == 0:
+        libbuild.build()
+    if dist is not None:
+        dist.barrier()
+    from paper_1605_04821_b200 import _lib
     from synth import bj_config
     from synth.device import grid_for, initial_values, packed_psi
 
     cfg = CONFIG_IDX[args.config]
     p = bj_config(cfg, n=args.n)
-    if world > 1:
-        raise SystemExit("multi-GPU slab decomposition: see DESIGN.md §7 (not in this build)")
     dev = torch.device("cuda", local)
-    g, fields = grid_for(p, device=local)
+    comm_id = None
+    if dist is not None:                      # slab decomposition over the ranks (NCCL)
+        obj = [_lib.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        comm_id = obj[0]
+    g, fields = grid_for(p, device=local, rank=rank, nranks=world, comm="nccl", comm_id=comm_id)
     lay = g.layout()
-    nI = lay["n_interior"]
-    U = initial_values(p, device=dev).contiguous()
+    nI = p.N_interior                          # whole-job unknowns (all ranks)
+    U = initial_values(p, device=dev, lay=lay).contiguous()
     U2 = torch.empty_like(U)
-    pol = torch.zeros(p.N, dtype=torch.uint8, device=dev)
+    pol = torch.zeros(lay["local_elems"], dtype=torch.uint8, device=dev)
+
+    def bar():
+        if dist is not None:
+            dist.barrier()
+
+    def allmax(v):
+        if dist is None:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.item()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # 256 MiB > 126 MB L2
     stream = torch.cuda.current_stream(dev)
     total = args.warmup + args.steps
@@ -238,6 +257,7 @@ def run_b200(args):
           for _ in range(args.steps)]
     g.profile_reset(time_kernels=not args.no_time_kernels)
     clk = ClockSampler(local)
+    bar()
     torch.cuda.synchronize()
     wall0 = time.perf_counter()
     for i, s in enumerate(range(args.warmup + 1, total + 1)):
@@ -247,15 +267,21 @@ def run_b200(args):
         ev[i][1].record(stream)
         U, U2 = U2, U
     torch.cuda.synchronize()
+    bar()
     wall = time.perf_counter() - wall0
     clocks = clk.stop()
     prof = g.profile_read()
     ms_steps = [a.elapsed_time(b) for a, b in ev]
-    ms_total = sum(ms_steps)
+    ms_total = allmax(sum(ms_steps))          # device time, max over ranks
     value = nI * args.steps / (ms_total / 1e3)
     # solution sanity vs the manufactured solution (not a parity claim; parity is in tests/)
     t_end = total * p.dt
-    err = (U - p.u_exact(t_end, torch.arange(p.N, device=dev))).abs().max().item()
+    from synth.device import local_index
+    li = local_index(p, lay, device=dev)
+    own = ~p.is_boundary(li)
+    r_own = (li // lay["row_elems"] >= lay["row0"]) & (li // lay["row_elems"] < lay["row1"])
+    diff = (U - p.u_exact(t_end, li)).abs()
+    err = allmax(diff[own & r_own].max().item() if world > 1 else diff.max().item())
 
     # --------------------------------------------------------------- roofline (dominant class)
     peaks, peak_src = measured_peaks()
@@ -295,7 +321,7 @@ def run_b200(args):
     # --------------------------------------------------------------- e2e through host buffers
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(g, p, args, U, stream, srcs, psis, nI, dev)
+        e2e = run_e2e(g, p, args, U, stream, srcs, psis, nI, dev, lay, bar, allmax)
 
     pis = [st["pi_iters"] for st in stats]
     kr = [st["krylov_iters_total"] for st in stats]
@@ -344,11 +370,11 @@ def traffic_for(cls, config, c):
     return e["dram_bytes_per_node"] * c["nodes"] / max(1, c["launches"])
 
 
-def run_e2e(g, p, args, U_dev, stream, srcs, psis, nI, dev):
+def run_e2e(g, p, args, U_dev, stream, srcs, psis, nI, dev, lay, bar, allmax):
     """The same steps through hjb_step with pinned HOST buffers: each step copies U_prev, the policy
     and psi host->device and U + policy device->host inside the timed region (inside the call)."""
     import torch
-    N = p.N
+    N = lay["local_elems"]
     Uh_prev = torch.empty(N, dtype=torch.float64, pin_memory=True)
     Uh = torch.empty(N, dtype=torch.float64, pin_memory=True)
     polh = torch.zeros(N, dtype=torch.uint8, pin_memory=True)
@@ -358,6 +384,7 @@ def run_e2e(g, p, args, U_dev, stream, srcs, psis, nI, dev):
     psi_np = [x.numpy() for x in psih]
     base = args.warmup + args.steps
     n_e2e = args.steps
+    bar()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
@@ -370,8 +397,9 @@ def run_e2e(g, p, args, U_dev, stream, srcs, psis, nI, dev):
         Uhp_np, Uh_np = Uh_np, Uhp_np
     ev1.record(stream)
     torch.cuda.synchronize()
+    bar()
     wall = time.perf_counter() - t0
-    ms = ev0.elapsed_time(ev1)
+    ms = allmax(ev0.elapsed_time(ev1))
     nb = psis[0].numel()
     return {"value": nI * n_e2e / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": 8 * N + N + 8 * nb,
             "d2h_bytes_per_step": 8 * N + N, "steps": n_e2e, "wall_s": wall,

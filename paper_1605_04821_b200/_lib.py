@@ -104,11 +104,13 @@ class Profile(C.Structure):
 _lib = None
 
 
-def load(path: str = LIB_PATH):
+def load(path: str = None):
     """Load libhjb.so.  Raises (loudly) if it is missing: there is no fallback."""
     global _lib
     if _lib is not None:
         return _lib
+    # HJB_LIB selects an alternative in-tree build (kernel A/B experiments, tools/)
+    path = path or os.environ.get("HJB_LIB") or LIB_PATH
     if not os.path.exists(path):
         raise RuntimeError(f"libhjb.so not found at {path}: build it with "
                            "`python -m paper_1605_04821_b200.build` (no CPU fallback exists)")

@@ -122,6 +122,50 @@ __device__ __forceinline__ void load_fields(const CoefDev& C, Node<D>& nd) {
   nd.cn = C.c_node ? __ldg(C.c_node + j) : 0.0;
 }
 
+// per-node streamed inputs of the operator kernels, loaded one line ahead (software pipelining:
+// the next line's loads are in flight while this line's gathers run)
+template <int D, int P>
+struct NodeIn {
+  double sc[P], sn[P][D], bs, bn[D], cn;
+  double xj, bj;
+  int a;
+};
+
+template <int D, int P, bool XJ, bool BJ>
+__device__ __forceinline__ void fetch_node(const LevelDev& L, const CoefDev& C, const uint8_t* __restrict__ pol,
+                                           const double* __restrict__ x, const double* __restrict__ b, int col,
+                                           int row, NodeIn<D, P>& in) {
+  const int j = interior_offset<D>(L, col, row);
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    in.sc[p] = C.sigma_scale ? __ldg(C.sigma_scale + p * C.ld + j) : 1.0;
+#pragma unroll
+    for (int d = 0; d < D; ++d) in.sn[p][d] = C.sigma_node ? __ldg(C.sigma_node + (p * D + d) * C.ld + j) : 0.0;
+  }
+  in.bs = C.b_scale ? __ldg(C.b_scale + j) : 1.0;
+#pragma unroll
+  for (int d = 0; d < D; ++d) in.bn[d] = C.b_node ? __ldg(C.b_node + d * C.ld + j) : 0.0;
+  in.cn = C.c_node ? __ldg(C.c_node + j) : 0.0;
+  in.a = __ldg(pol + j);
+  in.xj = XJ ? __ldg(x + j) : 0.0;
+  in.bj = BJ ? __ldg(b + j) : 0.0;
+}
+
+template <int D, int P>
+__device__ __forceinline__ void node_from(const LevelDev& L, int col, int row, const NodeIn<D, P>& in, Node<D>& nd) {
+  node_at<D>(L, col, row, nd);
+#pragma unroll
+  for (int p = 0; p < kMaxP; ++p) {
+    nd.sc[p] = p < P ? in.sc[p < P ? p : 0] : 1.0;
+#pragma unroll
+    for (int d = 0; d < D; ++d) nd.sn[p][d] = p < P ? in.sn[p < P ? p : 0][d] : 0.0;
+  }
+  nd.bs = in.bs;
+#pragma unroll
+  for (int d = 0; d < D; ++d) nd.bn[d] = in.bn[d];
+  nd.cn = in.cn;
+}
+
 // ----------------------------------------------------------------------------- cells
 // floor split of t = i + o for an UNTRUNCATED offset: c = i + floor(o), s = o - floor(o), via
 // round-to-nearest by the 1.5*2^52 magic constant (no fp64<->int conversion instructions).

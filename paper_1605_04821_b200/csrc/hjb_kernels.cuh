@@ -18,8 +18,14 @@ enum OpMode : int {
 };
 
 // NDOT: 0, 1 -> partial[0] = sum y*u ; 2 -> partial[0] = sum y*u, partial[1] = sum y*y
+#ifndef HJB_OP_MINB
+#define HJB_OP_MINB 1
+#endif
+#ifndef HJB_SEARCH_MINB
+#define HJB_SEARCH_MINB 1
+#endif
 template <int D, int P, int MODE, int NDOT>
-__global__ void __launch_bounds__(kTX) k_operator(LevelDev L, CoefDev C, double dt, double omega,
+__global__ void __launch_bounds__(kTX, HJB_OP_MINB) k_operator(LevelDev L, CoefDev C, double dt, double omega,
                                                   const uint8_t* __restrict__ pol,
                                                   const double* __restrict__ x,
                                                   const double* __restrict__ b, double* __restrict__ y,
@@ -27,46 +33,58 @@ __global__ void __launch_bounds__(kTX) k_operator(LevelDev L, CoefDev C, double 
   constexpr bool GATHER = (MODE != OP_JACOBI0);
   constexpr bool SELF = (MODE == OP_JACOBI || MODE == OP_JACOBI0);
   constexpr int E = 2 * P + 1;
+  constexpr bool XJ = (MODE != OP_JACOBI0);
+  constexpr bool BJ = (MODE != OP_APPLY);
   double dots[2] = {0.0, 0.0};
-  FOR_INTERIOR(L) {
-    Node<D> nd;
-    node_at<D>(L, col, row, nd);
-    load_fields<D>(C, nd);
-    const int a = pol[nd.loc];
-    Tap<D> taps[E];
-    const double wsum = row_geometry<D, P>(L, C, nd, a, taps);
-    double acc = 0.0, self = 0.0;
-    if (GATHER) {
-      double vals[E];
+  const int col = blockIdx.x * kTX + threadIdx.x;
+  const bool active = col < L.nI;
+  NodeIn<D, P> in{};
+  int row = blockIdx.y;
+  if (active && row < L.nrows) fetch_node<D, P, XJ, BJ>(L, C, pol, x, b, col, row, in);
+  for (; row < L.nrows; row += gridDim.y) {
+    NodeIn<D, P> nx{};
+    const int rn = row + gridDim.y;
+    if (active && rn < L.nrows) fetch_node<D, P, XJ, BJ>(L, C, pol, x, b, col, rn, nx);
+    if (active) {
+      Node<D> nd;
+      node_from<D, P>(L, col, row, in, nd);
+      const int a = in.a;
+      Tap<D> taps[E];
+      const double wsum = row_geometry<D, P>(L, C, nd, a, taps);
+      double acc = 0.0, self = 0.0;
+      if (GATHER) {
+        double vals[E];
 #pragma unroll
-      for (int e = 0; e < E; ++e) vals[e] = tap_value<D>(L, x, taps[e]);
+        for (int e = 0; e < E; ++e) vals[e] = tap_value<D>(L, x, taps[e]);
 #pragma unroll
-      for (int e = 0; e < E; ++e) acc = fma(taps[e].w, vals[e], acc);
-    }
-    if (SELF) {
-#pragma unroll
-      for (int e = 0; e < E; ++e) self += tap_self<D>(nd, taps[e]);
-    }
-    const double c = nd.cn + __ldg(C.c_ctrl + a);
-    double out;
-    if (MODE == OP_JACOBI0) {
-      const double diag = 1.0 + dt * (wsum - self - c);
-      out = omega * __ldg(b + nd.loc) / diag;
-    } else {
-      const double xj = __ldg(x + nd.loc);
-      const double Ax = xj - dt * (acc - wsum * xj + c * xj);
-      if (MODE == OP_APPLY) {
-        out = Ax;
-      } else if (MODE == OP_RESID) {
-        out = __ldg(b + nd.loc) - Ax;
-      } else {
-        const double diag = 1.0 + dt * (wsum - self - c);
-        out = xj + omega * (__ldg(b + nd.loc) - Ax) / diag;
+        for (int e = 0; e < E; ++e) acc = fma(taps[e].w, vals[e], acc);
       }
+      if (SELF) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) self += tap_self<D>(nd, taps[e]);
+      }
+      const double c = nd.cn + __ldg(C.c_ctrl + a);
+      double out;
+      if (MODE == OP_JACOBI0) {
+        const double diag = 1.0 + dt * (wsum - self - c);
+        out = omega * in.bj / diag;
+      } else {
+        const double xj = in.xj;
+        const double Ax = xj - dt * (acc - wsum * xj + c * xj);
+        if (MODE == OP_APPLY) {
+          out = Ax;
+        } else if (MODE == OP_RESID) {
+          out = in.bj - Ax;
+        } else {
+          const double diag = 1.0 + dt * (wsum - self - c);
+          out = xj + omega * (in.bj - Ax) / diag;
+        }
+      }
+      y[nd.loc] = out;
+      if (NDOT >= 1) dots[0] = fma(out, __ldg(u + nd.loc), dots[0]);
+      if (NDOT >= 2) dots[1] = fma(out, out, dots[1]);
     }
-    y[nd.loc] = out;
-    if (NDOT >= 1) dots[0] = fma(out, __ldg(u + nd.loc), dots[0]);
-    if (NDOT >= 2) dots[1] = fma(out, out, dots[1]);
+    in = nx;
   }
   if (NDOT > 0) block_reduce_store<2>(dots, partial);
 }
@@ -75,7 +93,7 @@ __global__ void __launch_bounds__(kTX) k_operator(LevelDev L, CoefDev C, double 
 // For every owned interior node: H^a = acc_a - wsum_a U_j + c^a U_j + f^a for all a (lowest-index
 // argmin), policy/F outputs, partials: [max R, changed count].
 template <int D, int P>
-__global__ void __launch_bounds__(kTX) k_search(LevelDev L, CoefDev C, double dt,
+__global__ void __launch_bounds__(kTX, HJB_SEARCH_MINB) k_search(LevelDev L, CoefDev C, double dt,
                                                 const double* __restrict__ U,
                                                 const double* __restrict__ Uprev,
                                                 uint8_t* __restrict__ pol, double* __restrict__ F,
