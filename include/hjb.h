@@ -225,7 +225,8 @@ typedef struct {
                                 ||F||_2, pi_forcing ||r_0||_2); a policy found stable after an
                                 inexact evaluation is re-evaluated exactly before the step ends, so
                                 the fixed point is unchanged (DESIGN.md §3 reading xxii).
-                                0 = exact evaluation every iteration (the paper's Howard loop). */
+                                0 = exact evaluation every iteration (the paper's Howard loop);
+                                default 0.1.                                                    */
 } hjb_solve_params;
 
 typedef struct {

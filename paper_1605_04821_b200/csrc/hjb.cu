@@ -367,7 +367,7 @@ extern "C" void hjb_solve_params_default(int32_t dim, hjb_solve_params* o) {
   o->tol_pi = 1e-10;
   o->max_pi = 50;
   hjb_mg_params_default(dim, &o->mg);
-  o->pi_forcing = 0.0;
+  o->pi_forcing = 0.1;
 }
 
 // ---------------------------------------------------------------------------- API: partition

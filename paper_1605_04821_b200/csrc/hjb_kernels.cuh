@@ -99,6 +99,11 @@ __global__ void __launch_bounds__(kTX, HJB_SEARCH_MINB) k_search(LevelDev L, Coe
                                                 uint8_t* __restrict__ pol, double* __restrict__ F,
                                                 double* partial) {
   constexpr int E = 2 * P + 1;
+#ifndef HJB_SEARCH_UNROLL2
+  constexpr bool UNROLL2 = (D == 2);
+#else
+  constexpr bool UNROLL2 = HJB_SEARCH_UNROLL2 && (D == 2);
+#endif
   double red[2] = {0.0, 0.0};
   FOR_INTERIOR(L) {
     Node<D> nd;
@@ -110,7 +115,43 @@ __global__ void __launch_bounds__(kTX, HJB_SEARCH_MINB) k_search(LevelDev L, Coe
     const double Uj = __ldg(U + nd.loc);
     double best = INFINITY, fbest = 0.0;
     int arg = 0;
-    for (int a = 0; a < C.K; ++a) {
+    // H^a_j = sum_e w_e I U(z_e) - wsum U_j + c^a_j U_j + f^a_j
+    auto tail = [&](int a, double acc, double wsum, double& f) {
+      f = __ldg(C.f_ctrl + a);
+      const double* fb = C.f_basis + a * C.Q;
+#pragma unroll
+      for (int q = 0; q < kMaxQ; ++q)
+        if (q < C.Q) f = fma(__ldg(fb + q), feat[q], f);
+      const double c = nd.cn + __ldg(C.c_ctrl + a);
+      return (acc - wsum * Uj) + c * Uj + f;
+    };
+    int a = 0;
+    if (UNROLL2) {
+      // two controls per pass: both geometries, then all 2 (2P+1) 2^d gathers in flight together
+      for (; a + 1 < C.K; a += 2) {
+        Tap<D> t0[E], t1[E];
+        const double w0 = row_geometry<D, P>(L, C, nd, a, t0);
+        const double w1 = row_geometry<D, P>(L, C, nd, a + 1, t1);
+        double v0[E], v1[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          v0[e] = tap_value<D>(L, U, t0[e]);
+          v1[e] = tap_value<D>(L, U, t1[e]);
+        }
+        double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          acc0 = fma(t0[e].w, v0[e], acc0);
+          acc1 = fma(t1[e].w, v1[e], acc1);
+        }
+        double f0, f1;
+        const double H0 = tail(a, acc0, w0, f0);
+        const double H1 = tail(a + 1, acc1, w1, f1);
+        if (H0 < best) { best = H0; arg = a; fbest = f0; }      // strict: lowest index wins ties
+        if (H1 < best) { best = H1; arg = a + 1; fbest = f1; }
+      }
+    }
+    for (; a < C.K; ++a) {
       Tap<D> taps[E];
       const double wsum = row_geometry<D, P>(L, C, nd, a, taps);
       double vals[E];
@@ -119,13 +160,8 @@ __global__ void __launch_bounds__(kTX, HJB_SEARCH_MINB) k_search(LevelDev L, Coe
       double acc = 0.0;
 #pragma unroll
       for (int e = 0; e < E; ++e) acc = fma(taps[e].w, vals[e], acc);
-      double f = __ldg(C.f_ctrl + a);
-      const double* fb = C.f_basis + a * C.Q;
-#pragma unroll
-      for (int q = 0; q < kMaxQ; ++q)
-        if (q < C.Q) f = fma(__ldg(fb + q), feat[q], f);
-      const double c = nd.cn + __ldg(C.c_ctrl + a);
-      const double H = (acc - wsum * Uj) + c * Uj + f;
+      double f;
+      const double H = tail(a, acc, wsum, f);
       if (H < best) {  // strict: lowest index wins exact ties (reading iv)
         best = H;
         arg = a;

@@ -114,8 +114,9 @@ def _gpu_march(p, n_steps=None, **kw):
     ("cfg3_17_2steps", lambda: bj_config(3, n=17), 2),
 ])
 def test_step_parity(name, mk, steps):
+    """The paper's Howard loop: every policy evaluation solved to 1e-12 (pi_forcing = 0)."""
     p = mk()
-    Ug, polg, stats = _gpu_march(p, steps)
+    Ug, polg, stats = _gpu_march(p, steps, pi_forcing=0.0)
     Uo = p.g(p.all_idx())
     for s in range(1, (steps or p.n_steps) + 1):
         Uo, polo, _ = howard_step(p, Uo, s * p.dt, p.dt)
@@ -146,7 +147,7 @@ def test_step_parity_inexact_policy_evaluation(name, mk, steps):
 
 def test_step_parity_cfg1_first_step():
     p = bj_config(1)
-    Ug, polg, stats = _gpu_march(p, 1)
+    Ug, polg, stats = _gpu_march(p, 1)          # library defaults (inexact early evaluations)
     Uo, polo, _ = howard_step(p, p.g(p.all_idx()), p.dt, p.dt)
     err = np.abs(Ug - Uo).max() / max(1.0, np.abs(Uo).max())
     assert err <= 1e-8, (err, stats)
