@@ -244,9 +244,12 @@ def run_b200(args):
     srcs = [p.f_tables(s * p.dt) for s in range(1, total + 1)]
 
     def do_step(s, Uin, Uout, polbuf, psi):
+        # initial iterate: linear extrapolation 2 U^{n-1} - U^{n-2} once two steps exist (Uout holds
+        # U^{n-2}: ping-pong buffers); the fixed point does not depend on it (DESIGN.md xxiv)
         fb, fc = srcs[s - 1]
         g.set_source(fb, fc)
-        return g.step(p.dt, Uin, Uout, polbuf, psi)
+        return g.step(p.dt, Uin, Uout, polbuf, psi, guess=(_lib.HJB_GUESS_EXTRAPOLATE if s >= 2
+                                                           else _lib.HJB_GUESS_PREV))
 
     stats = []
     for s in range(1, args.warmup + 1):
@@ -389,11 +392,13 @@ def run_e2e(g, p, args, U_dev, stream, srcs, psis, nI, dev, lay, bar, allmax):
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
     t0 = time.perf_counter()
+    from paper_1605_04821_b200 import _lib
     for i in range(n_e2e):
         s = (base + i) % len(srcs) + 1
         fb, fc = srcs[s - 1]
         g.set_source(fb, fc)
-        g.step(p.dt, Uhp_np, Uh_np, pol_np, psi_np[s - 1])
+        g.step(p.dt, Uhp_np, Uh_np, pol_np, psi_np[s - 1],
+               guess=_lib.HJB_GUESS_EXTRAPOLATE if i >= 1 else _lib.HJB_GUESS_PREV)
         Uhp_np, Uh_np = Uh_np, Uhp_np
     ev1.record(stream)
     torch.cuda.synchronize()

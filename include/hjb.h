@@ -227,7 +227,17 @@ typedef struct {
                                 the fixed point is unchanged (DESIGN.md §3 reading xxii).
                                 0 = exact evaluation every iteration (the paper's Howard loop);
                                 default 0.1.                                                    */
+  int32_t guess;             /* hjb_step's initial iterate (the fixed point does not depend on it):
+                                HJB_GUESS_PREV (default): U_prev, as the paper's time march;
+                                HJB_GUESS_GIVEN: U as passed by the caller;
+                                HJB_GUESS_EXTRAPOLATE: U holds U^{n-2} on entry and the iterate is
+                                2 U_prev - U^{n-2} (linear extrapolation in time, DESIGN.md xxiv).
+                                Boundary entries are always set to psi(t_n) (if given).         */
 } hjb_solve_params;
+
+#define HJB_GUESS_PREV 0
+#define HJB_GUESS_GIVEN 1
+#define HJB_GUESS_EXTRAPOLATE 2
 
 typedef struct {
   int32_t iters;             /* BiCGSTAB iterations */
@@ -241,8 +251,9 @@ hjb_status hjb_solve(hjb_grid_t g, double dt, const uint8_t* policy, const doubl
 
 /* ---------------------------------------------------------------------------- step
  * One implicit Euler step t_{n-1} -> t_n = t_{n-1} + dt by policy iteration:
- *   U <- U_prev with boundary entries psi(t_n) (psi_packed: the n_boundary boundary values in
- *   lexicographic order; NULL keeps U's boundary entries), then repeat
+ *   U <- initial iterate (hjb_solve_params.guess; default U_prev) with boundary entries psi(t_n)
+ *   (psi_packed: the n_boundary boundary values in lexicographic order; NULL keeps U's boundary
+ *   entries), then repeat
  *     policy improvement (hjb_policy_update) -> stop if it > 1 and (changed == 0 or R <= tol_pi)
  *     -> mg setup -> BiCGSTAB solve of A^pi U = F^pi from the current U.
  * The initial policy is the greedy policy at U_prev (reading iii).  f must already be

@@ -368,6 +368,7 @@ extern "C" void hjb_solve_params_default(int32_t dim, hjb_solve_params* o) {
   o->max_pi = 50;
   hjb_mg_params_default(dim, &o->mg);
   o->pi_forcing = 0.1;
+  o->guess = HJB_GUESS_PREV;
 }
 
 // ---------------------------------------------------------------------------- API: partition
@@ -1159,9 +1160,13 @@ extern "C" hjb_status hjb_step(hjb_grid_t g, double dt, const double* U_prev, do
     CK(cudaMemcpyAsync(g->stage_prev, U_prev, vb, cudaMemcpyHostToDevice, st));
     dprev = g->stage_prev;
   }
+  if (sp->guess < HJB_GUESS_PREV || sp->guess > HJB_GUESS_EXTRAPOLATE)
+    return fail(HJB_ERR_INVALID_ARG, "unknown initial-guess mode");
+  const int guess = (U == U_prev) ? HJB_GUESS_PREV : sp->guess;
   if (h_U) {
     if (!g->stage_U) TRY(dalloc((void**)&g->stage_U, vb));
     dU = g->stage_U;
+    if (guess != HJB_GUESS_PREV) CK(cudaMemcpyAsync(dU, U, vb, cudaMemcpyHostToDevice, st));
   }
   if (h_pol) {
     if (!g->stage_pol) TRY(dalloc((void**)&g->stage_pol, (size_t)g->N));
@@ -1173,8 +1178,20 @@ extern "C" hjb_status hjb_step(hjb_grid_t g, double dt, const double* U_prev, do
     CK(cudaMemcpyAsync(g->stage_psi, psi, (size_t)g->n_boundary * sizeof(double), cudaMemcpyHostToDevice, st));
     dpsi = g->stage_psi;
   }
-  // a1: U <- U_prev with boundary psi(t_n)
-  if (dU != dprev) CK(cudaMemcpyAsync(dU, dprev, vb, cudaMemcpyDeviceToDevice, st));
+  // a1: initial iterate (U_prev, the caller's guess, or the linear extrapolation 2 U_prev - U^{n-2}),
+  // then boundary entries psi(t_n)
+  if (guess == HJB_GUESS_PREV && dU != dprev) {
+    CK(cudaMemcpyAsync(dU, dprev, vb, cudaMemcpyDeviceToDevice, st));
+  } else if (guess == HJB_GUESS_EXTRAPOLATE) {
+    const double nn = (double)g->L0.n_own;
+    if (g->D == 2)
+      LAUNCH(HJB_KC_VECTOR, nn, 24.0 * nn, 2.0 * nn,
+             k_extrapolate<2><<<dims(g, g->L0, (const void*)k_extrapolate<2>), kTX, 0, st>>>(g->L0, dprev, dU));
+    else
+      LAUNCH(HJB_KC_VECTOR, nn, 24.0 * nn, 2.0 * nn,
+             k_extrapolate<3><<<dims(g, g->L0, (const void*)k_extrapolate<3>), kTX, 0, st>>>(g->L0, dprev, dU));
+    CKL();
+  }
   if (dpsi) {
     const int nbb = (int)std::min<int64_t>((g->n_boundary + 255) / 256, 4096);
     const double nbd = (double)g->n_boundary;

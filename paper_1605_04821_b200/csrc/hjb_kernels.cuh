@@ -358,6 +358,16 @@ __global__ void __launch_bounds__(kTX) k_norms(LevelDev L, const double* __restr
   block_reduce_store<2>(red, partial, 0x2u);
 }
 
+// initial guess U <- 2 U_prev - U  (U holds U^{n-2} on entry: linear extrapolation in time)
+template <int D>
+__global__ void __launch_bounds__(kTX) k_extrapolate(LevelDev L, const double* __restrict__ up,
+                                                     double* __restrict__ u) {
+  FOR_INTERIOR(L) {
+    const int j = interior_offset<D>(L, col, row);
+    u[j] = fma(2.0, up[j], -u[j]);
+  }
+}
+
 template <int D>
 __global__ void __launch_bounds__(kTX) k_copy_interior(LevelDev L, const double* __restrict__ a,
                                                            double* __restrict__ b) {

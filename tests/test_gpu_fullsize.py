@@ -56,8 +56,14 @@ def test_fullsize_apply_sampled(cfg):
     cols, vals, _ = lhat_rows(geo, geo.node_x(idx), sig, b)
     xa = np.abs(xh)
     scale = xa[idx] + p.dt * (np.sum(vals * (xa[cols] + xa[idx][:, None]), axis=1) + np.abs(c) * xa[idx])
+    # NS: "operator apply <= 1e-12 relative in max-norm"
+    assert np.abs(yg - yo).max() <= 1e-12 * np.abs(yo).max()
+    # row-wise (reading xvi): the rounding scale of a row plus the oracle's own coordinate rounding:
+    # it forms z = lo + i h + mu y and (z - lo)/h in physical units, which carries an absolute error
+    # of ~(n-1) eps cells in the fraction s at large n (the grid-unit GPU path has ~|o| eps)
+    tol = 1e-12 + 4.0 * (p.n - 1) * np.finfo(float).eps
     err = np.abs(yg - yo) / scale
-    assert err.max() <= 1e-12, err.max()
+    assert err.max() <= tol, (err.max(), tol)
 
 
 @pytest.mark.parametrize("cfg", [2, 4])

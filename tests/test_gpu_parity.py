@@ -145,6 +145,35 @@ def test_step_parity_inexact_policy_evaluation(name, mk, steps):
         assert st["final_rres"] <= 1e-12 or st["final_R"] <= 1e-10
 
 
+@pytest.mark.parametrize("name,mk,steps", [
+    ("cfg0_extrap", lambda: bj_config(0), 4),
+    ("cfg2_129_extrap", lambda: bj_config(2, n=129), 3),
+])
+def test_step_parity_extrapolated_guess(name, mk, steps):
+    """guess = HJB_GUESS_EXTRAPOLATE (2 U^{n-1} - U^{n-2} from the second step on, reading xxiv):
+    a different initial iterate, the same discrete solution."""
+    from paper_1605_04821_b200 import _lib
+    torch = require_gpu()
+    p = mk()
+    g, _ = setup(p)
+    U = to_dev(p.g(p.all_idx()), torch)
+    U2 = torch.empty_like(U)
+    pol = torch.zeros(p.N, dtype=torch.uint8, device="cuda")
+    Uo = p.g(p.all_idx())
+    pis = []
+    for s in range(1, steps + 1):
+        t = s * p.dt
+        fb, fc = p.f_tables(t)
+        g.set_source(fb, fc)
+        st = g.step(p.dt, U, U2, pol, to_dev(p.psi(t, p.boundary_idx()), torch),
+                    guess=_lib.HJB_GUESS_EXTRAPOLATE if s >= 2 else _lib.HJB_GUESS_PREV)
+        pis.append(st["pi_iters"])
+        U, U2 = U2, U
+        Uo, _, _ = howard_step(p, Uo, t, p.dt)
+        err = np.abs(U.cpu().numpy() - Uo).max() / max(1.0, np.abs(Uo).max())
+        assert err <= 1e-8, (name, s, err, st)
+
+
 def test_step_parity_cfg1_first_step():
     p = bj_config(1)
     Ug, polg, stats = _gpu_march(p, 1)          # library defaults (inexact early evaluations)
