@@ -240,8 +240,9 @@ def run_b200(args):
     stream = torch.cuda.current_stream(dev)
     total = args.warmup + args.steps
     # per-step inputs (problem data, generated before the timed region)
-    psis = [packed_psi(p, s * p.dt, device=dev) for s in range(1, total + 1)]
-    srcs = [p.f_tables(s * p.dt) for s in range(1, total + 1)]
+    n_all = total + (0 if args.no_e2e else args.steps)   # the e2e steps continue the same march
+    psis = [packed_psi(p, s * p.dt, device=dev) for s in range(1, n_all + 1)]
+    srcs = [p.f_tables(s * p.dt) for s in range(1, n_all + 1)]
 
     def do_step(s, Uin, Uout, polbuf, psi):
         # initial iterate: linear extrapolation 2 U^{n-1} - U^{n-2} once two steps exist (Uout holds
@@ -324,7 +325,7 @@ def run_b200(args):
     # --------------------------------------------------------------- e2e through host buffers
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(g, p, args, U, stream, srcs, psis, nI, dev, lay, bar, allmax)
+        e2e = run_e2e(g, p, args, U, U2, stream, srcs, psis, nI, dev, lay, bar, allmax)
 
     pis = [st["pi_iters"] for st in stats]
     kr = [st["krylov_iters_total"] for st in stats]
@@ -373,7 +374,7 @@ def traffic_for(cls, config, c):
     return e["dram_bytes_per_node"] * c["nodes"] / max(1, c["launches"])
 
 
-def run_e2e(g, p, args, U_dev, stream, srcs, psis, nI, dev, lay, bar, allmax):
+def run_e2e(g, p, args, U_dev, U2_dev, stream, srcs, psis, nI, dev, lay, bar, allmax):
     """The same steps through hjb_step with pinned HOST buffers: each step copies U_prev, the policy
     and psi host->device and U + policy device->host inside the timed region (inside the call)."""
     import torch
@@ -381,11 +382,14 @@ def run_e2e(g, p, args, U_dev, stream, srcs, psis, nI, dev, lay, bar, allmax):
     Uh_prev = torch.empty(N, dtype=torch.float64, pin_memory=True)
     Uh = torch.empty(N, dtype=torch.float64, pin_memory=True)
     polh = torch.zeros(N, dtype=torch.uint8, pin_memory=True)
-    Uh_prev.copy_(U_dev.cpu())
+    Uh_prev.copy_(U_dev.cpu())       # U^{n-1}
+    Uh.copy_(U2_dev.cpu())           # U^{n-2}: the march continues with the extrapolated guess
     psih = [x.cpu().pin_memory() for x in psis]
     Uh_np, Uhp_np, pol_np = Uh.numpy(), Uh_prev.numpy(), polh.numpy()
     psi_np = [x.numpy() for x in psih]
     base = args.warmup + args.steps
+    if args.steps + args.warmup < 2:
+        raise SystemExit("e2e needs two previous steps (use --no-e2e)")
     n_e2e = args.steps
     bar()
     torch.cuda.synchronize()
@@ -394,11 +398,10 @@ def run_e2e(g, p, args, U_dev, stream, srcs, psis, nI, dev, lay, bar, allmax):
     t0 = time.perf_counter()
     from paper_1605_04821_b200 import _lib
     for i in range(n_e2e):
-        s = (base + i) % len(srcs) + 1
+        s = base + i + 1
         fb, fc = srcs[s - 1]
         g.set_source(fb, fc)
-        g.step(p.dt, Uhp_np, Uh_np, pol_np, psi_np[s - 1],
-               guess=_lib.HJB_GUESS_EXTRAPOLATE if i >= 1 else _lib.HJB_GUESS_PREV)
+        g.step(p.dt, Uhp_np, Uh_np, pol_np, psi_np[s - 1], guess=_lib.HJB_GUESS_EXTRAPOLATE)
         Uhp_np, Uh_np = Uh_np, Uhp_np
     ev1.record(stream)
     torch.cuda.synchronize()

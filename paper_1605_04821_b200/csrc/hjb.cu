@@ -163,14 +163,17 @@ static int occupancy_of(const void* fn) {
   auto it = cache.find(fn);
   if (it != cache.end()) return it->second;
   int occ = 0;
+#ifdef HJB_L1MAX
+  cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 0);  // maximal L1
+#endif
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kTX, 0) != cudaSuccess || occ < 1) occ = 1;
   cache[fn] = occ;
   return occ;
 }
 static dim3 dims(hjb_grid* g, const LevelDev& L, const void* fn) {
-  const int gx = std::max(1, (L.nI + kTX - 1) / kTX);
+  const int gx = std::max(1, (L.nI + kBX - 1) / kBX);
   const int64_t cap = std::min<int64_t>((int64_t)occupancy_of(fn) * g->sms, kMaxBlocks);
-  const int64_t rows = std::min<int64_t>(std::max(L.nrows, 1), 65535);
+  const int64_t rows = std::min<int64_t>(std::max((L.nrows + kBY - 1) / kBY, 1), 65535);
   const int gy = (int)std::max<int64_t>(1, std::min<int64_t>(rows, cap / gx));
   g->nblk_last = gx * gy;
   return dim3(gx, gy);
@@ -323,11 +326,11 @@ static void launch_operator(hjb_grid* g, const LevelDev& L, const CoefDev& C, in
 #define OPL(M, ND)                                                                                            \
   do {                                                                                                      \
     if (g->P == 1) LAUNCH(cls, nodes, nodes * bpn, nodes * fpn,                                              \
-        k_operator<D, 1, M, ND><<<dims(g, L, (const void*)k_operator<D, 1, M, ND>), kTX, 0, st>>>(L, C, dt, omega, pol, x, b, y, u, g->partial)); \
+        k_operator<D, 1, M, ND><<<dims(g, L, (const void*)k_operator<D, 1, M, ND>), dim3(kBX, kBY), 0, st>>>(L, C, dt, omega, pol, x, b, y, u, g->partial)); \
     else if (g->P == 2) LAUNCH(cls, nodes, nodes * bpn, nodes * fpn,                                         \
-        k_operator<D, 2, M, ND><<<dims(g, L, (const void*)k_operator<D, 2, M, ND>), kTX, 0, st>>>(L, C, dt, omega, pol, x, b, y, u, g->partial)); \
+        k_operator<D, 2, M, ND><<<dims(g, L, (const void*)k_operator<D, 2, M, ND>), dim3(kBX, kBY), 0, st>>>(L, C, dt, omega, pol, x, b, y, u, g->partial)); \
     else LAUNCH(cls, nodes, nodes * bpn, nodes * fpn,                                                        \
-        k_operator<D, (D > 2 ? 3 : 2), M, ND><<<dims(g, L, (const void*)k_operator<D, (D > 2 ? 3 : 2), M, ND>), kTX, 0, st>>>(L, C, dt, omega, pol, x, b, y, u, g->partial)); \
+        k_operator<D, (D > 2 ? 3 : 2), M, ND><<<dims(g, L, (const void*)k_operator<D, (D > 2 ? 3 : 2), M, ND>), dim3(kBX, kBY), 0, st>>>(L, C, dt, omega, pol, x, b, y, u, g->partial)); \
   } while (0)
   if (mode == OP_APPLY) {
     if (ndot == 0) OPL(OP_APPLY, 0);
@@ -491,7 +494,7 @@ extern "C" hjb_status hjb_grid_create(const hjb_grid_desc* d, hjb_grid_t* out) {
   hjb_layout lay;
   TRY(hjb_partition(d->dim, d->n, d->nranks, d->rank, d->halo, &lay));
   // local arrays are indexed with 32-bit offsets; one x1 line must fit the partial-sum slots
-  if (lay.local_elems >= (1LL << 31) || (d->n - 2) > (int64_t)kTX * kMaxBlocks)
+  if (lay.local_elems >= (1LL << 31) || (d->n - 2) > (int64_t)kBX * kMaxBlocks)
     return fail(HJB_ERR_INVALID_ARG, "grid too large for one rank (local arrays must hold < 2^31 nodes)");
   CK(cudaSetDevice(d->device));
   hjb_grid* g = new hjb_grid();
@@ -634,10 +637,10 @@ extern "C" hjb_status hjb_set_coeffs(hjb_grid_t g, const hjb_coeffs* c) {
     const double nodes = (double)g->L0.n_own;
     if (g->D == 2)
       LAUNCH(HJB_KC_BOUNDARY, nodes, nodes * 8.0 * (1 + g->nplanes0), 0,
-             k_reach<2><<<dims(g, g->L0, (const void*)k_reach<2>), kTX, 0, g->st>>>(g->L0, g->C0, g->partial));
+             k_reach<2><<<dims(g, g->L0, (const void*)k_reach<2>), dim3(kBX, kBY), 0, g->st>>>(g->L0, g->C0, g->partial));
     else
       LAUNCH(HJB_KC_BOUNDARY, nodes, nodes * 8.0 * (1 + g->nplanes0), 0,
-             k_reach<3><<<dims(g, g->L0, (const void*)k_reach<3>), kTX, 0, g->st>>>(g->L0, g->C0, g->partial));
+             k_reach<3><<<dims(g, g->L0, (const void*)k_reach<3>), dim3(kBX, kBY), 0, g->st>>>(g->L0, g->C0, g->partial));
     CKL();
     hjb_status err;
     double rb = 0.0;
@@ -699,7 +702,7 @@ static hjb_status policy_update_dev(hjb_grid* g, double dt, const double* U, con
   const double fpn = g->K * ((2.0 * g->P + 1.0) * (1 << g->D) * 2.0 + 2.0 * g->Q + 4.0);
 #define SRCH(DD, PP)                                                                                          \
   LAUNCH(HJB_KC_SEARCH, nodes, nodes * bpn, nodes * fpn,                                                    \
-         k_search<DD, PP><<<dims(g, g->L0, (const void*)k_search<DD, PP>), kTX, 0, g->st>>>(g->L0, g->C0, dt, U, Uprev, pol, F, g->partial))
+         k_search<DD, PP><<<dims(g, g->L0, (const void*)k_search<DD, PP>), dim3(kBX, kBY), 0, g->st>>>(g->L0, g->C0, dt, U, Uprev, pol, F, g->partial))
   if (g->D == 2) {
     if (g->P == 1) SRCH(2, 1);
     else SRCH(2, 2);
@@ -987,18 +990,18 @@ static hjb_status vcycle(hjb_grid* g, size_t l, const double* b, double* out) {
     view.n_own = (int64_t)view.nrows * view.nI;
     if (view.nrows > 0)
       LAUNCH(HJB_KC_TRANSFER, L.n_own, 8.0 * (L.n_own + view.n_own), 18.0 * view.n_own,
-             k_restrict<D><<<dims(g, view, (const void*)k_restrict<D>), kTX, 0, st>>>(L, view, lv.res, lc.b));
+             k_restrict<D><<<dims(g, view, (const void*)k_restrict<D>), dim3(kBX, kBY), 0, st>>>(L, view, lv.res, lc.b));
     CKL();
     TRY(gather_rows(g, lc.b, 8, lc.L.row_elems, J0, J1));
   } else {
     LAUNCH(HJB_KC_TRANSFER, L.n_own, 8.0 * (L.n_own + lc.L.n_own), 18.0 * lc.L.n_own,
-           k_restrict<D><<<dims(g, lc.L, (const void*)k_restrict<D>), kTX, 0, st>>>(L, lc.L, lv.res, lc.b));
+           k_restrict<D><<<dims(g, lc.L, (const void*)k_restrict<D>), dim3(kBX, kBY), 0, st>>>(L, lc.L, lv.res, lc.b));
     CKL();
   }
   TRY(vcycle<D>(g, l + 1, lc.b, lc.x));
   TRY(halo_exchange(g, lc, lc.x, 1));
   LAUNCH(HJB_KC_TRANSFER, L.n_own, 16.0 * L.n_own + 8.0 * lc.L.n_own, 4.0 * L.n_own,
-         k_prolong_add<D><<<dims(g, L, (const void*)k_prolong_add<D>), kTX, 0, st>>>(L, lc.L, lc.x, bufs[cur]));
+         k_prolong_add<D><<<dims(g, L, (const void*)k_prolong_add<D>), dim3(kBX, kBY), 0, st>>>(L, lc.L, lc.x, bufs[cur]));
   for (int k = 0; k < npost; ++k) {
     TRY(halo_exchange(g, lv, bufs[cur], lv.H));
     launch_operator<D>(g, L, lv.C, OP_JACOBI, 0, dt, om, pol, bufs[cur], b, bufs[1 - cur], nullptr, fine);
@@ -1014,10 +1017,10 @@ static hjb_status precond(hjb_grid* g, bool use_mg, const double* b, double* x) 
     const double nn = (double)g->L0.n_own;
     if (g->D == 2)
       LAUNCH(HJB_KC_VECTOR, nn, 16.0 * nn, 0,
-             k_copy_interior<2><<<dims(g, g->L0, (const void*)k_copy_interior<2>), kTX, 0, g->st>>>(g->L0, b, x));
+             k_copy_interior<2><<<dims(g, g->L0, (const void*)k_copy_interior<2>), dim3(kBX, kBY), 0, g->st>>>(g->L0, b, x));
     else
       LAUNCH(HJB_KC_VECTOR, nn, 16.0 * nn, 0,
-             k_copy_interior<3><<<dims(g, g->L0, (const void*)k_copy_interior<3>), kTX, 0, g->st>>>(g->L0, b, x));
+             k_copy_interior<3><<<dims(g, g->L0, (const void*)k_copy_interior<3>), dim3(kBX, kBY), 0, g->st>>>(g->L0, b, x));
     CKL();
     return HJB_OK;
   }
@@ -1035,7 +1038,7 @@ extern "C" hjb_status hjb_mg_apply(hjb_grid_t g, const double* b, double* x) {
 template <int D>
 static hjb_status norms_dev(hjb_grid* g, const double* v, double* n2, double* ninf) {
   LAUNCH(HJB_KC_VECTOR, g->L0.n_own, 8.0 * g->L0.n_own, 3.0 * g->L0.n_own,
-         k_norms<D><<<dims(g, g->L0, (const void*)k_norms<D>), kTX, 0, g->st>>>(g->L0, v, g->partial));
+         k_norms<D><<<dims(g, g->L0, (const void*)k_norms<D>), dim3(kBX, kBY), 0, g->st>>>(g->L0, v, g->partial));
   const int nb = g->nblk_last;
   CKL();
   hjb_status err;
@@ -1069,7 +1072,7 @@ static hjb_status bicgstab(hjb_grid* g, double dt, const uint8_t* pol, const dou
     TRY(halo_exchange(g, lv0, x, H));
     launch_operator<D>(g, L, C, OP_RESID, 0, dt, 0.0, pol, x, F, g->r, nullptr);
     LAUNCH(HJB_KC_VECTOR, L.n_own, 24.0 * L.n_own, 2.0 * L.n_own,
-           k_bicg_init<D><<<dims(g, L, (const void*)k_bicg_init<D>), kTX, 0, st>>>(L, g->r, g->rhat, g->p, g->partial));
+           k_bicg_init<D><<<dims(g, L, (const void*)k_bicg_init<D>), dim3(kBX, kBY), 0, st>>>(L, g->r, g->rhat, g->p, g->partial));
     CKL();
     rr = host_finalize(g, g->nblk_last, 0u, SC_INIT, &err);
     if (err != HJB_OK) return err;
@@ -1080,19 +1083,19 @@ static hjb_status bicgstab(hjb_grid* g, double dt, const uint8_t* pol, const dou
     while (it < sp->krylov_maxit) {
       if (inner > 0)
         LAUNCH(HJB_KC_VECTOR, L.n_own, 32.0 * L.n_own, 4.0 * L.n_own,
-               k_bicg_p<D><<<dims(g, L, (const void*)k_bicg_p<D>), kTX, 0, st>>>(L, g->S, g->r, g->p, g->v));
+               k_bicg_p<D><<<dims(g, L, (const void*)k_bicg_p<D>), dim3(kBX, kBY), 0, st>>>(L, g->S, g->r, g->p, g->v));
       TRY(precond(g, mg, g->p, g->phat));
       TRY(halo_exchange(g, lv0, g->phat, H));
       launch_operator<D>(g, L, C, OP_APPLY, 1, dt, 0.0, pol, g->phat, nullptr, g->v, g->rhat);
       TRY(reduce_dev(g, g->nblk_last, 0u, SC_AFTER_V));
       LAUNCH(HJB_KC_VECTOR, L.n_own, 24.0 * L.n_own, 4.0 * L.n_own,
-             k_bicg_s<D><<<dims(g, L, (const void*)k_bicg_s<D>), kTX, 0, st>>>(L, g->S, g->r, g->v, g->s, g->partial));
+             k_bicg_s<D><<<dims(g, L, (const void*)k_bicg_s<D>), dim3(kBX, kBY), 0, st>>>(L, g->S, g->r, g->v, g->s, g->partial));
       TRY(precond(g, mg, g->s, g->shat));
       TRY(halo_exchange(g, lv0, g->shat, H));
       launch_operator<D>(g, L, C, OP_APPLY, 2, dt, 0.0, pol, g->shat, nullptr, g->t, g->s);
       TRY(reduce_dev(g, g->nblk_last, 0u, SC_AFTER_T));
       LAUNCH(HJB_KC_VECTOR, L.n_own, 64.0 * L.n_own, 10.0 * L.n_own,
-             k_bicg_x<D><<<dims(g, L, (const void*)k_bicg_x<D>), kTX, 0, st>>>(L, g->S, x, g->phat, g->shat, g->s,
+             k_bicg_x<D><<<dims(g, L, (const void*)k_bicg_x<D>), dim3(kBX, kBY), 0, st>>>(L, g->S, x, g->phat, g->shat, g->s,
                                                                                g->t, g->r, g->rhat, g->partial));
       TRY(reduce_dev(g, g->nblk_last, 0u, SC_AFTER_R));
       CK(cudaMemcpyAsync(g->hS, g->S, sizeof(KScal), cudaMemcpyDeviceToHost, st));
@@ -1186,10 +1189,10 @@ extern "C" hjb_status hjb_step(hjb_grid_t g, double dt, const double* U_prev, do
     const double nn = (double)g->L0.n_own;
     if (g->D == 2)
       LAUNCH(HJB_KC_VECTOR, nn, 24.0 * nn, 2.0 * nn,
-             k_extrapolate<2><<<dims(g, g->L0, (const void*)k_extrapolate<2>), kTX, 0, st>>>(g->L0, dprev, dU));
+             k_extrapolate<2><<<dims(g, g->L0, (const void*)k_extrapolate<2>), dim3(kBX, kBY), 0, st>>>(g->L0, dprev, dU));
     else
       LAUNCH(HJB_KC_VECTOR, nn, 24.0 * nn, 2.0 * nn,
-             k_extrapolate<3><<<dims(g, g->L0, (const void*)k_extrapolate<3>), kTX, 0, st>>>(g->L0, dprev, dU));
+             k_extrapolate<3><<<dims(g, g->L0, (const void*)k_extrapolate<3>), dim3(kBX, kBY), 0, st>>>(g->L0, dprev, dU));
     CKL();
   }
   if (dpsi) {
@@ -1230,7 +1233,7 @@ extern "C" hjb_status hjb_step(hjb_grid_t g, double dt, const double* U_prev, do
     cudaEventRecord(g->ev[1], st);
     hjb_solve_stats ss{};
     // inexact Howard: while the policy still changes, evaluate it only to eta * ||r_0||
-    const double eta = settled ? 0.0 : sp->pi_forcing;
+    const double eta = (settled || g->K == 1) ? 0.0 : sp->pi_forcing;  // K = 1: the policy is final
     hjb_status s = g->D == 2 ? bicgstab<2>(g, dt, dpol, g->F, dU, sp, &ss, eta)
                              : bicgstab<3>(g, dt, dpol, g->F, dU, sp, &ss, eta);
     last_exact = (ss.rres <= sp->krylov_rtol);

@@ -24,7 +24,12 @@
 
 namespace hjb {
 
-constexpr int kTX = 128;   // threads per block (along x1)
+constexpr int kTX = 128;   // threads per block of the 2D grid kernels
+#ifndef HJB_BX
+#define HJB_BX 128
+#endif
+constexpr int kBX = HJB_BX;        // block extent along x1 (consecutive nodes per row)
+constexpr int kBY = kTX / kBX;     // interior lines per block
 constexpr int kMaxP = 3;
 constexpr int kMaxQ = 16;
 
@@ -529,7 +534,8 @@ template <int NV>
 __device__ __forceinline__ void block_reduce_store(double (&val)[NV], double* partial, unsigned maxmask = 0u) {
   constexpr int NW = kTX / 32;
   __shared__ double sm[NV][NW];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+  const int lane = tid & 31, wid = tid >> 5;
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
     double v = ((maxmask >> k) & 1u) ? warp_max(val[k]) : warp_sum(val[k]);

@@ -6,8 +6,8 @@ namespace hjb {
 
 // every owned interior node of level L: (col, row) -> x1 index 1+col, line `row`
 #define FOR_INTERIOR(L)                                                       \
-  for (int row = blockIdx.y; row < (L).nrows; row += gridDim.y)              \
-    for (int col = blockIdx.x * kTX + threadIdx.x; col < (L).nI; col += gridDim.x * kTX)
+  for (int row = blockIdx.y * kBY + threadIdx.y; row < (L).nrows; row += gridDim.y * kBY) \
+    for (int col = blockIdx.x * kBX + threadIdx.x; col < (L).nI; col += gridDim.x * kBX)
 
 // ================================================================== operator-family kernel
 enum OpMode : int {
@@ -36,14 +36,15 @@ __global__ void __launch_bounds__(kTX, HJB_OP_MINB) k_operator(LevelDev L, CoefD
   constexpr bool XJ = (MODE != OP_JACOBI0);
   constexpr bool BJ = (MODE != OP_APPLY);
   double dots[2] = {0.0, 0.0};
-  const int col = blockIdx.x * kTX + threadIdx.x;
+  const int col = blockIdx.x * kBX + threadIdx.x;
   const bool active = col < L.nI;
   NodeIn<D, P> in{};
-  int row = blockIdx.y;
+  int row = blockIdx.y * kBY + threadIdx.y;
+  const int rstride = gridDim.y * kBY;
   if (active && row < L.nrows) fetch_node<D, P, XJ, BJ>(L, C, pol, x, b, col, row, in);
-  for (; row < L.nrows; row += gridDim.y) {
+  for (; row < L.nrows; row += rstride) {
     NodeIn<D, P> nx{};
-    const int rn = row + gridDim.y;
+    const int rn = row + rstride;
     if (active && rn < L.nrows) fetch_node<D, P, XJ, BJ>(L, C, pol, x, b, col, rn, nx);
     if (active) {
       Node<D> nd;
