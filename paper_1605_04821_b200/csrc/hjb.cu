@@ -170,10 +170,11 @@ static int occupancy_of(const void* fn) {
   cache[fn] = occ;
   return occ;
 }
-static dim3 dims(hjb_grid* g, const LevelDev& L, const void* fn) {
-  const int gx = std::max(1, (L.nI + kBX - 1) / kBX);
+static dim3 dims(hjb_grid* g, const LevelDev& L, const void* fn, int bx = kBX) {
+  const int by = kTX / bx;
+  const int gx = std::max(1, (L.nI + bx - 1) / bx);
   const int64_t cap = std::min<int64_t>((int64_t)occupancy_of(fn) * g->sms, kMaxBlocks);
-  const int64_t rows = std::min<int64_t>(std::max((L.nrows + kBY - 1) / kBY, 1), 65535);
+  const int64_t rows = std::min<int64_t>(std::max((L.nrows + by - 1) / by, 1), 65535);
   const int gy = (int)std::max<int64_t>(1, std::min<int64_t>(rows, cap / gx));
   g->nblk_last = gx * gy;
   return dim3(gx, gy);
@@ -221,6 +222,8 @@ static LevelDev make_level(int D, int64_t n, double lo, double hi, double k, dou
   L.k2h = k2 / L.h;
   L.inv_2k2 = 1.0 / (2.0 * k2);
   L.inv_k2 = 1.0 / k2;
+  L.pf_rows = 0;
+  L.local_elems = (int)(L.local_rows * L.row_elems);
   return L;
 }
 static LevelDev full_level(int D, int64_t n, double lo, double hi, double k, double k2) {
@@ -309,6 +312,16 @@ static hjb_status gather_rows(hjb_grid* g, void* full, size_t elem, int64_t row_
                          cudaMemcpyDeviceToDevice, g->st));
   }
   return HJB_OK;
+}
+
+// L2 prefetch distance of a level: its widest reach in rows + 2 (HJB_NO_PREFETCH: off)
+static int prefetch_rows(hjb_grid* g, const LevelDev& L) {
+#ifdef HJB_NO_PREFETCH
+  return 0;
+#else
+  const double rd = g->reach_diff * (L.kh / g->L0.kh), rb = g->reach_drift * (L.k2h / g->L0.k2h);
+  return (int)std::floor(std::max(rd, rb)) + 2;
+#endif
 }
 
 // ---------------------------------------------------------------------------- dimension dispatch
@@ -494,7 +507,7 @@ extern "C" hjb_status hjb_grid_create(const hjb_grid_desc* d, hjb_grid_t* out) {
   hjb_layout lay;
   TRY(hjb_partition(d->dim, d->n, d->nranks, d->rank, d->halo, &lay));
   // local arrays are indexed with 32-bit offsets; one x1 line must fit the partial-sum slots
-  if (lay.local_elems >= (1LL << 31) || (d->n - 2) > (int64_t)kBX * kMaxBlocks)
+  if (lay.local_elems >= (1LL << 31) || (d->n - 2) > (int64_t)std::min(kBX, kSBX) * kMaxBlocks)
     return fail(HJB_ERR_INVALID_ARG, "grid too large for one rank (local arrays must hold < 2^31 nodes)");
   CK(cudaSetDevice(d->device));
   hjb_grid* g = new hjb_grid();
@@ -633,7 +646,7 @@ extern "C" hjb_status hjb_set_coeffs(hjb_grid_t g, const hjb_coeffs* c) {
                 (c->b_node ? g->D : 0) + (c->c_node ? 1 : 0);
   g->have_coeffs = true;
   g->mg_ready = false;
-  if (g->R > 1) {  // the halo must cover the widest stencil (hjb_partition)
+  {  // widest stencil offset: halo check (several ranks) and the L2 prefetch distance
     const double nodes = (double)g->L0.n_own;
     if (g->D == 2)
       LAUNCH(HJB_KC_BOUNDARY, nodes, nodes * 8.0 * (1 + g->nplanes0), 0,
@@ -649,7 +662,8 @@ extern "C" hjb_status hjb_set_coeffs(hjb_grid_t g, const hjb_coeffs* c) {
     g->reach_diff = rd;
     g->reach_drift = rb;
     const int64_t need = (int64_t)std::floor(std::max(rd, rb) * (1.0 + 1e-12)) + 1;
-    if (need > g->lay.halo) {
+    g->L0.pf_rows = prefetch_rows(g, g->L0);
+    if (g->R > 1 && need > g->lay.halo) {
       g->have_coeffs = false;
       return fail(HJB_ERR_INVALID_ARG, "halo too small for these coefficients: need " + std::to_string(need) +
                                            " rows, grid has " + std::to_string(g->lay.halo));
@@ -702,7 +716,7 @@ static hjb_status policy_update_dev(hjb_grid* g, double dt, const double* U, con
   const double fpn = g->K * ((2.0 * g->P + 1.0) * (1 << g->D) * 2.0 + 2.0 * g->Q + 4.0);
 #define SRCH(DD, PP)                                                                                          \
   LAUNCH(HJB_KC_SEARCH, nodes, nodes * bpn, nodes * fpn,                                                    \
-         k_search<DD, PP><<<dims(g, g->L0, (const void*)k_search<DD, PP>), dim3(kBX, kBY), 0, g->st>>>(g->L0, g->C0, dt, U, Uprev, pol, F, g->partial))
+         k_search<DD, PP><<<dims(g, g->L0, (const void*)k_search<DD, PP>, kSBX), dim3(kSBX, kSBY), 0, g->st>>>(g->L0, g->C0, dt, U, Uprev, pol, F, g->partial))
   if (g->D == 2) {
     if (g->P == 1) SRCH(2, 1);
     else SRCH(2, 2);
@@ -943,6 +957,8 @@ extern "C" hjb_status hjb_mg_setup(hjb_grid_t g, double dt, const uint8_t* polic
                        g->levels[0].C.ld != g->C0.ld;
   if (rebuild) TRY(build_levels(g, p));
   g->levels[0].C = g->C0;  // refresh field pointers of level 0 (set_coeffs may have changed them)
+  g->levels[0].L.pf_rows = g->L0.pf_rows;
+  for (size_t i = 1; i < g->levels.size(); ++i) g->levels[i].L.pf_rows = prefetch_rows(g, g->levels[i].L);
   g->mg_pol0 = policy;
   g->mg_dt = dt;
   if (g->D == 2) TRY(inject_all<2>(g));

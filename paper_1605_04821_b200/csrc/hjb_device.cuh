@@ -30,6 +30,11 @@ constexpr int kTX = 128;   // threads per block of the 2D grid kernels
 #endif
 constexpr int kBX = HJB_BX;        // block extent along x1 (consecutive nodes per row)
 constexpr int kBY = kTX / kBX;     // interior lines per block
+#ifndef HJB_SBX
+#define HJB_SBX 32
+#endif
+constexpr int kSBX = HJB_SBX;      // control search: 32 x 4 blocks (4 adjacent lines share the
+constexpr int kSBY = kTX / kSBX;   // same control's gather rows -> L1 reuse across warps)
 constexpr int kMaxP = 3;
 constexpr int kMaxQ = 16;
 
@@ -47,7 +52,17 @@ struct LevelDev {
   double kh;           // diffusion step in cells: k / h (k = sqrt(h_fine) by default)
   double k2h;          // drift step in cells: k^2 / h
   double inv_2k2, inv_k2;
+  int pf_rows;         // L2 prefetch distance along the slowest axis (max reach + 2; 0 = off)
+  int local_elems;     // local_rows * row_elems
 };
+
+// L2 prefetch of the grid line `pf_rows` slowest-axis rows ahead of node j: the leading edge of
+// the gather band, which would otherwise miss L2 (one line per 16 lanes)
+__device__ __forceinline__ void prefetch_ahead(const LevelDev& L, const double* v, int j, int col) {
+  if (L.pf_rows <= 0 || (col & 15) != 0) return;
+  const long long a = (long long)j + (long long)L.pf_rows * L.row_elems;
+  if (a < L.local_elems) asm volatile("prefetch.global.L2 [%0];" ::"l"(v + a));
+}
 
 // ----------------------------------------------------------------------------- coefficients
 struct CoefDev {

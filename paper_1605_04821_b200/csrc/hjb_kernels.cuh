@@ -4,6 +4,11 @@
 
 namespace hjb {
 
+// every owned interior node of level L with (BX x BY) blocks
+#define FOR_INTERIOR_B(L, BX, BY)                                                            \
+  for (int row = blockIdx.y * (BY) + threadIdx.y; row < (L).nrows; row += gridDim.y * (BY)) \
+    for (int col = blockIdx.x * (BX) + threadIdx.x; col < (L).nI; col += gridDim.x * (BX))
+
 // every owned interior node of level L: (col, row) -> x1 index 1+col, line `row`
 #define FOR_INTERIOR(L)                                                       \
   for (int row = blockIdx.y * kBY + threadIdx.y; row < (L).nrows; row += gridDim.y * kBY) \
@@ -49,6 +54,7 @@ __global__ void __launch_bounds__(kTX, HJB_OP_MINB) k_operator(LevelDev L, CoefD
     if (active) {
       Node<D> nd;
       node_from<D, P>(L, col, row, in, nd);
+      if (GATHER) prefetch_ahead(L, x, nd.loc, col);
       const int a = in.a;
       Tap<D> taps[E];
       const double wsum = row_geometry<D, P>(L, C, nd, a, taps);
@@ -106,10 +112,11 @@ __global__ void __launch_bounds__(kTX, HJB_SEARCH_MINB) k_search(LevelDev L, Coe
   constexpr bool UNROLL2 = HJB_SEARCH_UNROLL2 && (D == 2);
 #endif
   double red[2] = {0.0, 0.0};
-  FOR_INTERIOR(L) {
+  FOR_INTERIOR_B(L, kSBX, kSBY) {
     Node<D> nd;
     node_at<D>(L, col, row, nd);
     load_fields<D>(C, nd);
+    prefetch_ahead(L, U, nd.loc, col);
     double feat[kMaxQ];
 #pragma unroll
     for (int q = 0; q < kMaxQ; ++q) feat[q] = (q < C.Q) ? __ldg(C.f_feat + q * C.ld + nd.loc) : 0.0;
