@@ -158,22 +158,24 @@ static void prof_post(hjb_grid* g, int cls, double nodes, double bytes, double f
 // 2D launch over the owned interior of level L: x covers an x1 line, y strides over lines.  All
 // CTAs are made co-resident (occupancy x SMs) so the lines in flight form one band that moves
 // through the grid and the +-reach rows it gathers from stay in L2.
-static int occupancy_of(const void* fn) {
-  static std::map<const void*, int> cache;
-  auto it = cache.find(fn);
+static int occupancy_of(const void* fn, size_t smem = 0) {
+  static std::map<std::pair<const void*, size_t>, int> cache;
+  const auto key = std::make_pair(fn, smem);
+  auto it = cache.find(key);
   if (it != cache.end()) return it->second;
   int occ = 0;
 #ifdef HJB_L1MAX
   cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 0);  // maximal L1
 #endif
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kTX, 0) != cudaSuccess || occ < 1) occ = 1;
-  cache[fn] = occ;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kTX, smem) != cudaSuccess || occ < 1) occ = 1;
+  cache[key] = occ;
   return occ;
 }
-static dim3 dims(hjb_grid* g, const LevelDev& L, const void* fn, int bx = kBX) {
+static dim3 dims(hjb_grid* g, const LevelDev& L, const void* fn, int bx = kBX, size_t smem = 0) {
   const int by = kTX / bx;
   const int gx = std::max(1, (L.nI + bx - 1) / bx);
-  const int64_t cap = std::min<int64_t>((int64_t)occupancy_of(fn) * g->sms, kMaxBlocks);
+  const int64_t cap = std::min<int64_t>((int64_t)occupancy_of(fn, smem) * g->sms, kMaxBlocks);
   const int64_t rows = std::min<int64_t>(std::max((L.nrows + by - 1) / by, 1), 65535);
   const int gy = (int)std::max<int64_t>(1, std::min<int64_t>(rows, cap / gx));
   g->nblk_last = gx * gy;
@@ -336,14 +338,15 @@ static void launch_operator(hjb_grid* g, const LevelDev& L, const CoefDev& C, in
   const double bpn = 1.0 + 8.0 + (mode != OP_JACOBI0 ? 8.0 : 0.0) + (mode != OP_APPLY ? 8.0 : 0.0) +
                      (ndot >= 1 ? 8.0 : 0.0) + 8.0 * g->nplanes0;
   const double fpn = (2.0 * g->P + 1.0) * (1 << D) * 2.0 + 4.0 + 2.0 * ndot;
+  const size_t tsm = (size_t)g->K * (g->P * D + D + 1) * sizeof(double);  // control tables in smem
 #define OPL(M, ND)                                                                                            \
   do {                                                                                                      \
     if (g->P == 1) LAUNCH(cls, nodes, nodes * bpn, nodes * fpn,                                              \
-        k_operator<D, 1, M, ND><<<dims(g, L, (const void*)k_operator<D, 1, M, ND>), dim3(kBX, kBY), 0, st>>>(L, C, dt, omega, pol, x, b, y, u, g->partial)); \
+        k_operator<D, 1, M, ND><<<dims(g, L, (const void*)k_operator<D, 1, M, ND>, kBX, tsm), dim3(kBX, kBY), tsm, st>>>(L, C, dt, omega, pol, x, b, y, u, g->partial)); \
     else if (g->P == 2) LAUNCH(cls, nodes, nodes * bpn, nodes * fpn,                                         \
-        k_operator<D, 2, M, ND><<<dims(g, L, (const void*)k_operator<D, 2, M, ND>), dim3(kBX, kBY), 0, st>>>(L, C, dt, omega, pol, x, b, y, u, g->partial)); \
+        k_operator<D, 2, M, ND><<<dims(g, L, (const void*)k_operator<D, 2, M, ND>, kBX, tsm), dim3(kBX, kBY), tsm, st>>>(L, C, dt, omega, pol, x, b, y, u, g->partial)); \
     else LAUNCH(cls, nodes, nodes * bpn, nodes * fpn,                                                        \
-        k_operator<D, (D > 2 ? 3 : 2), M, ND><<<dims(g, L, (const void*)k_operator<D, (D > 2 ? 3 : 2), M, ND>), dim3(kBX, kBY), 0, st>>>(L, C, dt, omega, pol, x, b, y, u, g->partial)); \
+        k_operator<D, (D > 2 ? 3 : 2), M, ND><<<dims(g, L, (const void*)k_operator<D, (D > 2 ? 3 : 2), M, ND>, kBX, tsm), dim3(kBX, kBY), tsm, st>>>(L, C, dt, omega, pol, x, b, y, u, g->partial)); \
   } while (0)
   if (mode == OP_APPLY) {
     if (ndot == 0) OPL(OP_APPLY, 0);
@@ -714,9 +717,10 @@ static hjb_status policy_update_dev(hjb_grid* g, double dt, const double* U, con
   const double nodes = (double)g->L0.n_own;
   const double bpn = 8.0 + 8.0 + 1.0 + 1.0 + 8.0 + 8.0 * g->Q + 8.0 * g->nplanes0;
   const double fpn = g->K * ((2.0 * g->P + 1.0) * (1 << g->D) * 2.0 + 2.0 * g->Q + 4.0);
+  const size_t tsm = (size_t)g->K * (g->P * g->D + g->D + 2 + g->Q) * sizeof(double);
 #define SRCH(DD, PP)                                                                                          \
   LAUNCH(HJB_KC_SEARCH, nodes, nodes * bpn, nodes * fpn,                                                    \
-         k_search<DD, PP><<<dims(g, g->L0, (const void*)k_search<DD, PP>, kSBX), dim3(kSBX, kSBY), 0, g->st>>>(g->L0, g->C0, dt, U, Uprev, pol, F, g->partial))
+         k_search<DD, PP><<<dims(g, g->L0, (const void*)k_search<DD, PP>, kSBX, tsm), dim3(kSBX, kSBY), tsm, g->st>>>(g->L0, g->C0, dt, U, Uprev, pol, F, g->partial))
   if (g->D == 2) {
     if (g->P == 1) SRCH(2, 1);
     else SRCH(2, 2);

@@ -446,10 +446,9 @@ __device__ __forceinline__ double tap_value(const LevelDev& L, const double* __r
 // endpoints of control a at node nd: taps[2p] = +sigma_p, taps[2p+1] = -sigma_p, taps[2P] = drift.
 // Returns wsum = sum_e w_e.
 template <int D, int P>
-__device__ __forceinline__ double row_geometry(const LevelDev& L, const CoefDev& C, const Node<D>& nd, int a,
-                                               Tap<D>* taps) {
+__device__ __forceinline__ double row_geometry(const LevelDev& L, const double* sd, const double* bd_,
+                                               const Node<D>& nd, Tap<D>* taps) {
   double wsum = 0.0;
-  const double* sd = C.sigma_dir + a * P * D;
   const int nm2 = L.n - 2;
 #pragma unroll
   for (int p = 0; p < P; ++p) {
@@ -457,7 +456,7 @@ __device__ __forceinline__ double row_geometry(const LevelDev& L, const CoefDev&
     bool nz = false, inside = true;
 #pragma unroll
     for (int d = 0; d < D; ++d) {
-      o[d] = L.kh * fma(nd.sc[p], __ldg(sd + p * D + d), nd.sn[p][d]);
+      o[d] = L.kh * fma(nd.sc[p], sd[p * D + d], nd.sn[p][d]);
       nz |= (o[d] != 0.0);
       inside &= (fabs(o[d]) <= nd.dist[d]);
     }
@@ -496,12 +495,11 @@ __device__ __forceinline__ double row_geometry(const LevelDev& L, const CoefDev&
     }
   }
   {  // drift pair: y_{P+1} = k^2 b, both endpoints equal, A = B = 1/mu (total weight 2/(mu 2k^2))
-    const double* bd_ = C.b_dir + a * D;
     double o[D];
     bool nz = false, inside = true;
 #pragma unroll
     for (int d = 0; d < D; ++d) {
-      o[d] = L.k2h * fma(nd.bs, __ldg(bd_ + d), nd.bn[d]);
+      o[d] = L.k2h * fma(nd.bs, bd_[d], nd.bn[d]);
       nz |= (o[d] != 0.0);
       inside &= (fabs(o[d]) <= nd.dist[d]);
     }
@@ -523,6 +521,95 @@ __device__ __forceinline__ double row_geometry(const LevelDev& L, const CoefDev&
     wsum += t.w;
   }
   return wsum;
+}
+
+// ---- fast path: every endpoint strictly inside the box (no truncation; A = B = 1, mu_d = 1).
+// Offsets o (cells) of the 2P diffusion steps and the drift step, as the general path forms them.
+template <int D, int P>
+__device__ __forceinline__ void row_offsets(const LevelDev& L, const double* sd, const double* bd,
+                                            const Node<D>& nd, double (&o)[P + 1][D]) {
+#pragma unroll
+  for (int p = 0; p < P; ++p)
+#pragma unroll
+    for (int d = 0; d < D; ++d) o[p][d] = L.kh * fma(nd.sc[p], sd[p * D + d], nd.sn[p][d]);
+#pragma unroll
+  for (int d = 0; d < D; ++d) o[P][d] = L.k2h * fma(nd.bs, bd[d], nd.bn[d]);
+}
+
+// |o| < dist strictly: i +- o lies in the open box, so no endpoint is truncated and every cell
+// index stays within [0, n-2] without clamping
+template <int D, int P>
+__device__ __forceinline__ bool offsets_inside(const Node<D>& nd, const double (&o)[P + 1][D]) {
+  bool in = true;
+#pragma unroll
+  for (int p = 0; p <= P; ++p)
+#pragma unroll
+    for (int d = 0; d < D; ++d) in &= fabs(o[p][d]) < nd.dist[d];
+  return in;
+}
+
+// cells and fractions of all endpoints from one floor per (step, dimension): +o -> (i + fl, o - fl),
+// -o -> (i - fl - [s != 0], 1 - s or 0); zero steps get weight 0 (their two terms cancel)
+template <int D, int P>
+__device__ __forceinline__ double row_geometry_fast(const LevelDev& L, const Node<D>& nd,
+                                                    const double (&o)[P + 1][D], Tap<D>* taps) {
+  double wsum = 0.0;
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    bool nz = false;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const double fl = floor(o[p][d]);
+      const int fi = (int)fl;
+      const double sp = o[p][d] - fl;
+      const bool frac = sp != 0.0;
+      taps[2 * p].c[d] = nd.i[d] + fi;
+      taps[2 * p].s[d] = sp;
+      taps[2 * p + 1].c[d] = nd.i[d] - fi - (frac ? 1 : 0);
+      taps[2 * p + 1].s[d] = frac ? 1.0 - sp : 0.0;
+      nz |= (o[p][d] != 0.0);
+    }
+    const double w = nz ? L.inv_2k2 : 0.0;
+    taps[2 * p].w = w;
+    taps[2 * p + 1].w = w;
+    wsum += 2.0 * w;
+  }
+  bool nz = false;
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    const double fl = floor(o[P][d]);
+    taps[2 * P].c[d] = nd.i[d] + (int)fl;
+    taps[2 * P].s[d] = o[P][d] - fl;
+    nz |= (o[P][d] != 0.0);
+  }
+  taps[2 * P].w = nz ? L.inv_k2 : 0.0;
+  return wsum + taps[2 * P].w;
+}
+
+// geometry of control a (table rows sd, bd) at node nd: fast path when the whole warp is untruncated
+template <int D, int P>
+__device__ __forceinline__ double row_taps(const LevelDev& L, const double* sd, const double* bd,
+                                           const Node<D>& nd, Tap<D>* taps) {
+  double o[P + 1][D];
+  row_offsets<D, P>(L, sd, bd, nd, o);
+  if (__all_sync(__activemask(), offsets_inside<D, P>(nd, o))) return row_geometry_fast<D, P>(L, nd, o, taps);
+  return row_geometry<D, P>(L, sd, bd, nd, taps);
+}
+
+// the control tables in shared memory: sigma_dir [K][P][D] | b_dir [K][D] | c_ctrl [K]
+// (| f_ctrl [K] | f_basis [K][Q] with SRC)
+template <int D, int P, bool SRC>
+__device__ __forceinline__ void stage_tables(const CoefDev& C, double* tab) {
+  const int nsd = C.K * P * D, nbd = C.K * D;
+  const int tid = threadIdx.y * blockDim.x + threadIdx.x, nt = blockDim.x * blockDim.y;
+  for (int e = tid; e < nsd; e += nt) tab[e] = __ldg(C.sigma_dir + e);
+  for (int e = tid; e < nbd; e += nt) tab[nsd + e] = __ldg(C.b_dir + e);
+  for (int e = tid; e < C.K; e += nt) tab[nsd + nbd + e] = __ldg(C.c_ctrl + e);
+  if (SRC) {
+    for (int e = tid; e < C.K; e += nt) tab[nsd + nbd + C.K + e] = __ldg(C.f_ctrl + e);
+    for (int e = tid; e < C.K * C.Q; e += nt) tab[nsd + nbd + 2 * C.K + e] = __ldg(C.f_basis + e);
+  }
+  __syncthreads();
 }
 
 template <int D>

@@ -40,24 +40,35 @@ __global__ void __launch_bounds__(kTX, HJB_OP_MINB) k_operator(LevelDev L, CoefD
   constexpr int E = 2 * P + 1;
   constexpr bool XJ = (MODE != OP_JACOBI0);
   constexpr bool BJ = (MODE != OP_APPLY);
+  extern __shared__ double tab[];
+  stage_tables<D, P, false>(C, tab);
+  const double* tsd = tab;
+  const double* tbd = tab + C.K * P * D;
+  const double* tcc = tbd + C.K * D;
   double dots[2] = {0.0, 0.0};
   const int col = blockIdx.x * kBX + threadIdx.x;
   const bool active = col < L.nI;
-  NodeIn<D, P> in{};
+#ifdef HJB_OP_NOPIPE
+  constexpr bool PIPE = false;
+#else
+  constexpr bool PIPE = true;   // software pipelining of the streamed per-node inputs
+#endif
+  NodeIn<D, P> in;
   int row = blockIdx.y * kBY + threadIdx.y;
   const int rstride = gridDim.y * kBY;
-  if (active && row < L.nrows) fetch_node<D, P, XJ, BJ>(L, C, pol, x, b, col, row, in);
+  if (PIPE && active && row < L.nrows) fetch_node<D, P, XJ, BJ>(L, C, pol, x, b, col, row, in);
   for (; row < L.nrows; row += rstride) {
-    NodeIn<D, P> nx{};
+    NodeIn<D, P> nx;
     const int rn = row + rstride;
-    if (active && rn < L.nrows) fetch_node<D, P, XJ, BJ>(L, C, pol, x, b, col, rn, nx);
+    if (PIPE && active && rn < L.nrows) fetch_node<D, P, XJ, BJ>(L, C, pol, x, b, col, rn, nx);
+    if (!PIPE && active) fetch_node<D, P, XJ, BJ>(L, C, pol, x, b, col, row, in);
     if (active) {
       Node<D> nd;
       node_from<D, P>(L, col, row, in, nd);
       if (GATHER) prefetch_ahead(L, x, nd.loc, col);
       const int a = in.a;
       Tap<D> taps[E];
-      const double wsum = row_geometry<D, P>(L, C, nd, a, taps);
+      const double wsum = row_taps<D, P>(L, tsd + a * P * D, tbd + a * D, nd, taps);
       double acc = 0.0, self = 0.0;
       if (GATHER) {
         double vals[E];
@@ -70,7 +81,7 @@ __global__ void __launch_bounds__(kTX, HJB_OP_MINB) k_operator(LevelDev L, CoefD
 #pragma unroll
         for (int e = 0; e < E; ++e) self += tap_self<D>(nd, taps[e]);
       }
-      const double c = nd.cn + __ldg(C.c_ctrl + a);
+      const double c = nd.cn + tcc[a];
       double out;
       if (MODE == OP_JACOBI0) {
         const double diag = 1.0 + dt * (wsum - self - c);
@@ -91,7 +102,7 @@ __global__ void __launch_bounds__(kTX, HJB_OP_MINB) k_operator(LevelDev L, CoefD
       if (NDOT >= 1) dots[0] = fma(out, __ldg(u + nd.loc), dots[0]);
       if (NDOT >= 2) dots[1] = fma(out, out, dots[1]);
     }
-    in = nx;
+    if (PIPE) in = nx;
   }
   if (NDOT > 0) block_reduce_store<2>(dots, partial);
 }
@@ -107,10 +118,17 @@ __global__ void __launch_bounds__(kTX, HJB_SEARCH_MINB) k_search(LevelDev L, Coe
                                                 double* partial) {
   constexpr int E = 2 * P + 1;
 #ifndef HJB_SEARCH_UNROLL2
-  constexpr bool UNROLL2 = (D == 2);
+  constexpr bool UNROLL2 = false;
 #else
   constexpr bool UNROLL2 = HJB_SEARCH_UNROLL2 && (D == 2);
 #endif
+  extern __shared__ double tab[];
+  stage_tables<D, P, true>(C, tab);
+  const double* tsd = tab;
+  const double* tbd = tab + C.K * P * D;
+  const double* tcc = tbd + C.K * D;
+  const double* tfc = tcc + C.K;
+  const double* tfb = tfc + C.K;
   double red[2] = {0.0, 0.0};
   FOR_INTERIOR_B(L, kSBX, kSBY) {
     Node<D> nd;
@@ -125,12 +143,12 @@ __global__ void __launch_bounds__(kTX, HJB_SEARCH_MINB) k_search(LevelDev L, Coe
     int arg = 0;
     // H^a_j = sum_e w_e I U(z_e) - wsum U_j + c^a_j U_j + f^a_j
     auto tail = [&](int a, double acc, double wsum, double& f) {
-      f = __ldg(C.f_ctrl + a);
-      const double* fb = C.f_basis + a * C.Q;
+      f = tfc[a];
+      const double* fb = tfb + a * C.Q;
 #pragma unroll
       for (int q = 0; q < kMaxQ; ++q)
-        if (q < C.Q) f = fma(__ldg(fb + q), feat[q], f);
-      const double c = nd.cn + __ldg(C.c_ctrl + a);
+        if (q < C.Q) f = fma(fb[q], feat[q], f);
+      const double c = nd.cn + tcc[a];
       return (acc - wsum * Uj) + c * Uj + f;
     };
     int a = 0;
@@ -138,8 +156,8 @@ __global__ void __launch_bounds__(kTX, HJB_SEARCH_MINB) k_search(LevelDev L, Coe
       // two controls per pass: both geometries, then all 2 (2P+1) 2^d gathers in flight together
       for (; a + 1 < C.K; a += 2) {
         Tap<D> t0[E], t1[E];
-        const double w0 = row_geometry<D, P>(L, C, nd, a, t0);
-        const double w1 = row_geometry<D, P>(L, C, nd, a + 1, t1);
+        const double w0 = row_taps<D, P>(L, tsd + a * P * D, tbd + a * D, nd, t0);
+        const double w1 = row_taps<D, P>(L, tsd + (a + 1) * P * D, tbd + (a + 1) * D, nd, t1);
         double v0[E], v1[E];
 #pragma unroll
         for (int e = 0; e < E; ++e) {
@@ -161,7 +179,7 @@ __global__ void __launch_bounds__(kTX, HJB_SEARCH_MINB) k_search(LevelDev L, Coe
     }
     for (; a < C.K; ++a) {
       Tap<D> taps[E];
-      const double wsum = row_geometry<D, P>(L, C, nd, a, taps);
+      const double wsum = row_taps<D, P>(L, tsd + a * P * D, tbd + a * D, nd, taps);
       double vals[E];
 #pragma unroll
       for (int e = 0; e < E; ++e) vals[e] = tap_value<D>(L, U, taps[e]);

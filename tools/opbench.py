@@ -21,6 +21,7 @@ ap.add_argument("--cfg", type=int, default=4)
 ap.add_argument("--n", type=int, default=None)
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--only", default="apply,vcycle,search")
+ap.add_argument("--policy", default="greedy", choices=["greedy", "zero", "random"])
 args = ap.parse_args()
 peaks = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                     "MEASURED_PEAKS.json"))) if os.path.exists("MEASURED_PEAKS.json") else {"hbm_gbs": 6454.0}
@@ -32,6 +33,10 @@ x = random_vector(p, idx=torch.arange(p.N, device="cuda")).contiguous()
 pol = torch.zeros(p.N, dtype=torch.uint8, device="cuda")
 F = torch.zeros(p.N, dtype=torch.float64, device="cuda")
 g.policy_update(p.dt, U0, U0, pol, F)          # a realistic (smooth) policy: greedy at U0
+if args.policy == "zero":
+    pol.zero_()
+elif args.policy == "random":
+    pol.copy_(torch.remainder(torch.arange(p.N, device="cuda") * 2654435761, p.K).to(torch.uint8))
 y = torch.empty_like(x)
 torch.cuda.synchronize()
 print(f"{p.name} n={p.n} K={p.K} N={p.N} setup {time.time() - t0:.1f}s", flush=True)
