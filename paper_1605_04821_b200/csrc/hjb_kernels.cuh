@@ -24,7 +24,7 @@ enum OpMode : int {
 
 // NDOT: 0, 1 -> partial[0] = sum y*u ; 2 -> partial[0] = sum y*u, partial[1] = sum y*y
 #ifndef HJB_OP_MINB
-#define HJB_OP_MINB 1
+#define HJB_OP_MINB 4   // <= 128 registers: 16 resident warps per SM (measured best, profiles/r01_v3)
 #endif
 #ifndef HJB_SEARCH_MINB
 #define HJB_SEARCH_MINB 1
@@ -48,10 +48,10 @@ __global__ void __launch_bounds__(kTX, HJB_OP_MINB) k_operator(LevelDev L, CoefD
   double dots[2] = {0.0, 0.0};
   const int col = blockIdx.x * kBX + threadIdx.x;
   const bool active = col < L.nI;
-#ifdef HJB_OP_NOPIPE
+#ifdef HJB_OP_PIPE
+  constexpr bool PIPE = true;   // software pipelining of the streamed per-node inputs (costs
+#else                           // registers; measured slower, profiles/r01_v3)
   constexpr bool PIPE = false;
-#else
-  constexpr bool PIPE = true;   // software pipelining of the streamed per-node inputs
 #endif
   NodeIn<D, P> in;
   int row = blockIdx.y * kBY + threadIdx.y;
