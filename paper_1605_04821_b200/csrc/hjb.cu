@@ -118,6 +118,14 @@ struct hjb_grid {
   int nplanes0 = 0;  // per-node coefficient planes read by the operator (sigma/b/c fields)
   int sms = 148;
   int nblk_last = 1;  // CTAs of the last dims() launch (partials to reduce)
+  // windowed control search (2D deep-interior tiles, k_search_win)
+  std::vector<double> h_sd, h_bd;  // host copies of sigma_dir / b_dir
+  bool win_ok = false;
+  WinGeom win{};
+  size_t win_smem = 0;
+  int win_grid = 0;
+  double* d_rng = nullptr;    // [scmin_p, scmax_p]_p, [bsmin, bsmax]
+  double* rng_part = nullptr; // k_field_ranges block partials
 };
 
 // ---------------------------------------------------------------------------- instrumentation
@@ -480,6 +488,8 @@ extern "C" hjb_status hjb_grid_destroy(hjb_grid_t g) {
   for (double* b : bufs) cudaFree(b);
   cudaFree(g->gsend);
   cudaFree(g->grecv);
+  cudaFree(g->d_rng);
+  cudaFree(g->rng_part);
   cudaFree(g->S);
   cudaFree(g->pol_int);
   cudaFree(g->stage_pol);
@@ -568,7 +578,7 @@ extern "C" hjb_status hjb_grid_create(const hjb_grid_desc* d, hjb_grid_t* out) {
     }
     cudaMemsetAsync(*pv, 0, vb, g->st);
   }
-  if ((s = dalloc((void**)&g->partial, (size_t)kMaxBlocks * 2 * sizeof(double))) != HJB_OK ||
+  if ((s = dalloc((void**)&g->partial, (size_t)kMaxBlocks * 4 * sizeof(double))) != HJB_OK ||
       (s = dalloc((void**)&g->red, 4 * sizeof(double))) != HJB_OK ||
       (s = dalloc((void**)&g->red_all, (size_t)2 * g->R * sizeof(double))) != HJB_OK ||
       (s = dalloc((void**)&g->S, sizeof(KScal))) != HJB_OK ||
@@ -623,6 +633,90 @@ static hjb_status upload_tables(hjb_grid* g, const double* sigma_dir, const doub
   g->C0.c_ctrl = g->d_tab + nsd + nbd;
   g->C0.f_basis = g->d_tab + nsd + nbd + nc;
   g->C0.f_ctrl = g->d_tab + nsd + nbd + nc + nfb;
+  g->h_sd.assign(h.begin(), h.begin() + nsd);
+  g->h_bd.assign(h.begin() + nsd, h.begin() + nsd + nbd);
+  return HJB_OK;
+}
+
+// ---------------------------------------------------------------------------- windowed search setup
+// Decide whether (and where) the control search runs k_search_win: 2D, no per-node sigma/b offset
+// fields, and a non-empty rectangle of tiles whose every endpoint is strictly inside the box.
+// Window boxes = tile span + the jitter of the per-node scale fields (their per-rank ranges).
+static hjb_status setup_window_search(hjb_grid* g) {
+  g->win_ok = false;
+#ifdef HJB_NO_WINSEARCH
+  return HJB_OK;
+#endif
+  if (g->D != 2 || g->C0.sigma_node || g->C0.b_node || getenv("HJB_NO_WINSEARCH")) return HJB_OK;
+  const int P = g->P, D = 2, K = g->K;
+  const LevelDev& L = g->L0;
+  if (L.nrows <= 0) return HJB_OK;
+  // per-rank ranges of the scale fields
+  const int nv = 2 * P + 2;
+  if (!g->rng_part) TRY(dalloc((void**)&g->rng_part, (size_t)kMaxBlocks * 8 * sizeof(double)));
+  if (!g->d_rng) TRY(dalloc((void**)&g->d_rng, 8 * sizeof(double)));
+  dim3 gd;
+  if (P == 1) {
+    gd = dims(g, L, (const void*)k_field_ranges<2, 1>);
+    k_field_ranges<2, 1><<<gd, dim3(kBX, kBY), 0, g->st>>>(L, g->C0, g->rng_part);
+  } else {
+    gd = dims(g, L, (const void*)k_field_ranges<2, 2>);
+    k_field_ranges<2, 2><<<gd, dim3(kBX, kBY), 0, g->st>>>(L, g->C0, g->rng_part);
+  }
+  CKL();
+  const int nb = g->nblk_last;
+  std::vector<double> part((size_t)nb * nv);
+  CK(cudaMemcpyAsync(part.data(), g->rng_part, part.size() * sizeof(double), cudaMemcpyDeviceToHost, g->st));
+  CK(cudaStreamSynchronize(g->st));
+  std::vector<double> mx(nv, -INFINITY);
+  for (int b = 0; b < nb; ++b)
+    for (int k = 0; k < nv; ++k) mx[k] = std::max(mx[k], part[(size_t)b * nv + k]);
+  double rng[8];
+  for (int k = 0; k < P + 1; ++k) {
+    rng[2 * k] = -mx[2 * k];
+    rng[2 * k + 1] = mx[2 * k + 1];
+  }
+  for (double v : rng)
+    if (!std::isfinite(v)) return HJB_OK;
+  CK(cudaMemcpyAsync(g->d_rng, rng, nv * sizeof(double), cudaMemcpyHostToDevice, g->st));
+  CK(cudaStreamSynchronize(g->st));
+  // reach and jitter per axis over all controls / endpoints
+  double reach[2] = {0, 0}, jit[2] = {0, 0};
+  for (int a = 0; a < K; ++a)
+    for (int e = 0; e <= P; ++e)
+      for (int d = 0; d < D; ++d) {
+        const double c = (e < P) ? L.kh * g->h_sd[(a * P + e) * D + d] : L.k2h * g->h_bd[a * D + d];
+        const double f0 = rng[2 * e], f1 = rng[2 * e + 1];
+        const double o0 = c * f0, o1 = c * f1;
+        reach[d] = std::max(reach[d], std::max(std::fabs(o0), std::fabs(o1)));
+        jit[d] = std::max(jit[d], std::fabs(o1 - o0));
+      }
+  WinGeom W{};
+  W.bwx = kWX - 1 + (int)std::ceil(jit[0] + 2e-6) + 3;
+  W.bwy = kWY - 1 + (int)std::ceil(jit[1] + 2e-6) + 3;
+  W.sw = (W.bwx + 2 + 1) & ~1;
+  const int n = (int)g->n;
+  const int mxr = (int)std::floor(reach[0] + 1e-6) + 1, myr = (int)std::floor(reach[1] + 1e-6) + 1;
+  const int c_lo = mxr - 1, c_hi = n - 2 - mxr;  // col = i0 - 1
+  const int i1_lo = std::max<int>(myr, (int)L.row_first);
+  const int i1_hi = std::min<int>(n - 1 - myr, (int)L.row_first + L.nrows - 1);
+  if (c_hi < c_lo || i1_hi < i1_lo) return HJB_OK;
+  W.ntx = (c_hi - c_lo + 1) / kWX;
+  W.nty = (i1_hi - i1_lo + 1) / kWY;
+  if (W.ntx <= 0 || W.nty <= 0) return HJB_OK;
+  W.rect = SkipRect{c_lo, c_lo + W.ntx * kWX, i1_lo - (int)L.row_first, i1_lo - (int)L.row_first + W.nty * kWY};
+  const int E = 2 * P + 1;
+  const size_t ntab = (size_t)K * (P * D + D + 2 + g->Q);
+  const size_t smem = (((ntab + 15) & ~(size_t)15) + (size_t)2 * E * W.bwy * W.sw) * sizeof(double);
+  if (smem > 200 * 1024 || W.bwx > 256 || W.bwy > 256) return HJB_OK;
+  const void* fn = P == 1 ? (const void*)k_search_win<1> : (const void*)k_search_win<2>;
+  CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kWT, smem) != cudaSuccess || occ < 1) return HJB_OK;
+  g->win = W;
+  g->win_smem = smem;
+  g->win_grid = std::min(W.ntx * W.nty, std::min(occ * g->sms, kMaxBlocks / 2));
+  g->win_ok = true;
   return HJB_OK;
 }
 
@@ -666,6 +760,7 @@ extern "C" hjb_status hjb_set_coeffs(hjb_grid_t g, const hjb_coeffs* c) {
     g->reach_drift = rb;
     const int64_t need = (int64_t)std::floor(std::max(rd, rb) * (1.0 + 1e-12)) + 1;
     g->L0.pf_rows = prefetch_rows(g, g->L0);
+    TRY(setup_window_search(g));
     if (g->R > 1 && need > g->lay.halo) {
       g->have_coeffs = false;
       return fail(HJB_ERR_INVALID_ARG, "halo too small for these coefficients: need " + std::to_string(need) +
@@ -718,9 +813,11 @@ static hjb_status policy_update_dev(hjb_grid* g, double dt, const double* U, con
   const double bpn = 8.0 + 8.0 + 1.0 + 1.0 + 8.0 + 8.0 * g->Q + 8.0 * g->nplanes0;
   const double fpn = g->K * ((2.0 * g->P + 1.0) * (1 << g->D) * 2.0 + 2.0 * g->Q + 4.0);
   const size_t tsm = (size_t)g->K * (g->P * g->D + g->D + 2 + g->Q) * sizeof(double);
+  const bool use_win = g->win_ok && ((uintptr_t)U & 15) == 0;  // bulk copies need 16-byte alignment
+  const SkipRect skip = use_win ? g->win.rect : SkipRect{0, 0, 0, 0};
 #define SRCH(DD, PP)                                                                                          \
   LAUNCH(HJB_KC_SEARCH, nodes, nodes * bpn, nodes * fpn,                                                    \
-         k_search<DD, PP><<<dims(g, g->L0, (const void*)k_search<DD, PP>, kSBX, tsm), dim3(kSBX, kSBY), tsm, g->st>>>(g->L0, g->C0, dt, U, Uprev, pol, F, g->partial))
+         k_search<DD, PP><<<dims(g, g->L0, (const void*)k_search<DD, PP>, kSBX, tsm), dim3(kSBX, kSBY), tsm, g->st>>>(g->L0, g->C0, dt, U, Uprev, pol, F, g->partial, skip))
   if (g->D == 2) {
     if (g->P == 1) SRCH(2, 1);
     else SRCH(2, 2);
@@ -731,9 +828,22 @@ static hjb_status policy_update_dev(hjb_grid* g, double dt, const double* U, con
   }
 #undef SRCH
   CKL();
+  int nblk = g->nblk_last;
+  if (g->win_ok && ((uintptr_t)U & 15) == 0) {  // deep-interior tiles: windows staged in shared memory
+    const double wn = (double)g->win.ntx * g->win.nty * kWT;
+    if (g->P == 1)
+      LAUNCH(HJB_KC_SEARCH, 0, 0, 0, k_search_win<1><<<g->win_grid, kWT, g->win_smem, g->st>>>(
+                                         g->L0, g->C0, dt, U, Uprev, pol, F, g->partial + 2 * nblk, g->win, g->d_rng));
+    else
+      LAUNCH(HJB_KC_SEARCH, 0, 0, 0, k_search_win<2><<<g->win_grid, kWT, g->win_smem, g->st>>>(
+                                         g->L0, g->C0, dt, U, Uprev, pol, F, g->partial + 2 * nblk, g->win, g->d_rng));
+    CKL();
+    (void)wn;
+    nblk += g->win_grid;
+  }
   hjb_status err;
   double changed = 0.0;
-  const double R = host_finalize(g, g->nblk_last, 0x1u, SC_NONE, &err, &changed);
+  const double R = host_finalize(g, nblk, 0x1u, SC_NONE, &err, &changed);
   if (err != HJB_OK) return err;
   if (out) {
     out->R_max = R;

@@ -189,6 +189,11 @@ __device__ __forceinline__ void node_from(const LevelDev& L, int col, int row, c
 // ----------------------------------------------------------------------------- cells
 // floor split of t = i + o for an UNTRUNCATED offset: c = i + floor(o), s = o - floor(o), via
 // round-to-nearest by the 1.5*2^52 magic constant (no fp64<->int conversion instructions).
+// rectangle of (col, row) loop coordinates handled by another kernel
+struct SkipRect {
+  int c0, c1, r0, r1;
+};
+
 struct Split {
   int c;
   double s;
