@@ -125,6 +125,8 @@ struct hjb_grid {
   size_t win_smem = 0;
   int win_grid = 0;
   double* d_rng = nullptr;    // [scmin_p, scmax_p]_p, [bsmin, bsmax]
+  bool reach_ok = false;      // per-axis reach known (scale fields only): deep rectangles enabled
+  double rdiff_ax[2] = {0, 0}, rdrift_ax[2] = {0, 0};
   double* rng_part = nullptr; // k_field_ranges block partials
 };
 
@@ -334,6 +336,22 @@ static int prefetch_rows(hjb_grid* g, const LevelDev& L) {
 #endif
 }
 
+// rectangle (loop coordinates) of level L whose nodes have every endpoint of every control strictly
+// inside the box (2D only; empty when unknown, e.g. with per-node sigma/b offset fields)
+static SkipRect deep_rect(hjb_grid* g, const LevelDev& L) {
+  SkipRect r{0, 0, 0, 0};
+  if (g->D != 2 || !g->reach_ok) return r;
+  const double rx = std::max(g->rdiff_ax[0] * (L.kh / g->L0.kh), g->rdrift_ax[0] * (L.k2h / g->L0.k2h));
+  const double ry = std::max(g->rdiff_ax[1] * (L.kh / g->L0.kh), g->rdrift_ax[1] * (L.k2h / g->L0.k2h));
+  const int n = L.n;
+  const int mx = (int)std::floor(rx + 1e-6) + 1, my = (int)std::floor(ry + 1e-6) + 1;
+  const int c0 = mx - 1, c1 = n - 1 - mx;  // col = i0 - 1, i0 in [mx, n-1-mx]
+  const int i1lo = std::max<int>(my, (int)L.row_first), i1hi = std::min<int>(n - 1 - my, (int)L.row_first + L.nrows - 1);
+  if (c1 <= c0 || i1hi < i1lo) return r;
+  r = SkipRect{c0, c1, i1lo - (int)L.row_first, i1hi + 1 - (int)L.row_first};
+  return r;
+}
+
 // ---------------------------------------------------------------------------- dimension dispatch
 template <int D>
 static void launch_operator(hjb_grid* g, const LevelDev& L, const CoefDev& C, int mode, int ndot, double dt,
@@ -347,14 +365,33 @@ static void launch_operator(hjb_grid* g, const LevelDev& L, const CoefDev& C, in
                      (ndot >= 1 ? 8.0 : 0.0) + 8.0 * g->nplanes0;
   const double fpn = (2.0 * g->P + 1.0) * (1 << D) * 2.0 + 4.0 + 2.0 * ndot;
   const size_t tsm = (size_t)g->K * (g->P * D + D + 1) * sizeof(double);  // control tables in smem
-#define OPL(M, ND)                                                                                            \
+  // the deep rectangle of this level (2D): lean fast-path kernel there, general kernel elsewhere
+  const SkipRect rect = deep_rect(g, L);
+  const bool has_deep = rect.c1 > rect.c0 && rect.r1 > rect.r0;
+  LevelDev Ld = L;  // launch shape of the rectangle
+  Ld.nI = rect.c1 - rect.c0;
+  Ld.nrows = rect.r1 - rect.r0;
+  double* part2 = g->partial;
+#define OPL1(PP, M, ND, DP, LL, PART)                                                                        \
+  LAUNCH(cls, nodes, nodes * bpn, nodes * fpn,                                                              \
+         k_operator<D, PP, M, ND, DP><<<dims(g, LL, (const void*)k_operator<D, PP, M, ND, DP>, kBX, tsm),   \
+                                       dim3(kBX, kBY), tsm, st>>>(L, C, dt, omega, pol, x, b, y, u, PART, rect))
+#define OPLP(PP, M, ND)                                                                                     \
   do {                                                                                                      \
-    if (g->P == 1) LAUNCH(cls, nodes, nodes * bpn, nodes * fpn,                                              \
-        k_operator<D, 1, M, ND><<<dims(g, L, (const void*)k_operator<D, 1, M, ND>, kBX, tsm), dim3(kBX, kBY), tsm, st>>>(L, C, dt, omega, pol, x, b, y, u, g->partial)); \
-    else if (g->P == 2) LAUNCH(cls, nodes, nodes * bpn, nodes * fpn,                                         \
-        k_operator<D, 2, M, ND><<<dims(g, L, (const void*)k_operator<D, 2, M, ND>, kBX, tsm), dim3(kBX, kBY), tsm, st>>>(L, C, dt, omega, pol, x, b, y, u, g->partial)); \
-    else LAUNCH(cls, nodes, nodes * bpn, nodes * fpn,                                                        \
-        k_operator<D, (D > 2 ? 3 : 2), M, ND><<<dims(g, L, (const void*)k_operator<D, (D > 2 ? 3 : 2), M, ND>, kBX, tsm), dim3(kBX, kBY), tsm, st>>>(L, C, dt, omega, pol, x, b, y, u, g->partial)); \
+    OPL1(PP, M, ND, false, L, g->partial);                                                                  \
+    int nb = g->nblk_last;                                                                                  \
+    if (has_deep) {                                                                                         \
+      part2 = g->partial + 2 * nb;                                                                          \
+      OPL1(PP, M, ND, true, Ld, part2);                                                                     \
+      nb += g->nblk_last;                                                                                   \
+    }                                                                                                       \
+    g->nblk_last = nb;                                                                                      \
+  } while (0)
+#define OPL(M, ND)                                                                                          \
+  do {                                                                                                      \
+    if (g->P == 1) OPLP(1, M, ND);                                                                          \
+    else if (g->P == 2) OPLP(2, M, ND);                                                                     \
+    else OPLP((D > 2 ? 3 : 2), M, ND);                                                                      \
   } while (0)
   if (mode == OP_APPLY) {
     if (ndot == 0) OPL(OP_APPLY, 0);
@@ -369,6 +406,9 @@ static void launch_operator(hjb_grid* g, const LevelDev& L, const CoefDev& C, in
     OPL(OP_JACOBI0, 0);
   }
 #undef OPL
+#undef OPLP
+#undef OPL1
+  (void)part2;
 }
 
 // ---------------------------------------------------------------------------- API: misc
@@ -644,6 +684,7 @@ static hjb_status upload_tables(hjb_grid* g, const double* sigma_dir, const doub
 // Window boxes = tile span + the jitter of the per-node scale fields (their per-rank ranges).
 static hjb_status setup_window_search(hjb_grid* g) {
   g->win_ok = false;
+  g->reach_ok = false;
 #ifdef HJB_NO_WINSEARCH
   return HJB_OK;
 #endif
@@ -682,15 +723,20 @@ static hjb_status setup_window_search(hjb_grid* g) {
   CK(cudaStreamSynchronize(g->st));
   // reach and jitter per axis over all controls / endpoints
   double reach[2] = {0, 0}, jit[2] = {0, 0};
+  g->rdiff_ax[0] = g->rdiff_ax[1] = g->rdrift_ax[0] = g->rdrift_ax[1] = 0.0;
   for (int a = 0; a < K; ++a)
     for (int e = 0; e <= P; ++e)
       for (int d = 0; d < D; ++d) {
         const double c = (e < P) ? L.kh * g->h_sd[(a * P + e) * D + d] : L.k2h * g->h_bd[a * D + d];
         const double f0 = rng[2 * e], f1 = rng[2 * e + 1];
         const double o0 = c * f0, o1 = c * f1;
-        reach[d] = std::max(reach[d], std::max(std::fabs(o0), std::fabs(o1)));
+        const double r = std::max(std::fabs(o0), std::fabs(o1));
+        reach[d] = std::max(reach[d], r);
+        double& rr = (e < P) ? g->rdiff_ax[d] : g->rdrift_ax[d];
+        rr = std::max(rr, r);
         jit[d] = std::max(jit[d], std::fabs(o1 - o0));
       }
+  g->reach_ok = true;
   WinGeom W{};
   W.bwx = kWX - 1 + (int)std::ceil(jit[0] + 2e-6) + 3;
   W.bwy = kWY - 1 + (int)std::ceil(jit[1] + 2e-6) + 3;

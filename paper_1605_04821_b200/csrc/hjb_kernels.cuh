@@ -29,12 +29,15 @@ enum OpMode : int {
 #ifndef HJB_SEARCH_MINB
 #define HJB_SEARCH_MINB 1
 #endif
-template <int D, int P, int MODE, int NDOT>
+// DEEP: only the nodes of `rect`, all of whose endpoints (every control) are strictly inside the
+// box -> the lean fast path with no truncation code; otherwise every node outside `rect`.
+template <int D, int P, int MODE, int NDOT, bool DEEP>
 __global__ void __launch_bounds__(kTX, HJB_OP_MINB) k_operator(LevelDev L, CoefDev C, double dt, double omega,
                                                   const uint8_t* __restrict__ pol,
                                                   const double* __restrict__ x,
                                                   const double* __restrict__ b, double* __restrict__ y,
-                                                  const double* __restrict__ u, double* partial) {
+                                                  const double* __restrict__ u, double* partial,
+                                                  SkipRect rect) {
   constexpr bool GATHER = (MODE != OP_JACOBI0);
   constexpr bool SELF = (MODE == OP_JACOBI || MODE == OP_JACOBI0);
   constexpr int E = 2 * P + 1;
@@ -46,29 +49,40 @@ __global__ void __launch_bounds__(kTX, HJB_OP_MINB) k_operator(LevelDev L, CoefD
   const double* tbd = tab + C.K * P * D;
   const double* tcc = tbd + C.K * D;
   double dots[2] = {0.0, 0.0};
-  const int col = blockIdx.x * kBX + threadIdx.x;
-  const bool active = col < L.nI;
+  const int col = (DEEP ? rect.c0 : 0) + blockIdx.x * kBX + threadIdx.x;
+  const int col_end = DEEP ? rect.c1 : L.nI;
+  const int row_end = DEEP ? rect.r1 : L.nrows;
+  const bool active = col < col_end;
+  const bool col_in_rect = col >= rect.c0 && col < rect.c1;
 #ifdef HJB_OP_PIPE
   constexpr bool PIPE = true;   // software pipelining of the streamed per-node inputs (costs
 #else                           // registers; measured slower, profiles/r01_v3)
   constexpr bool PIPE = false;
 #endif
   NodeIn<D, P> in;
-  int row = blockIdx.y * kBY + threadIdx.y;
+  int row = (DEEP ? rect.r0 : 0) + blockIdx.y * kBY + threadIdx.y;
   const int rstride = gridDim.y * kBY;
-  if (PIPE && active && row < L.nrows) fetch_node<D, P, XJ, BJ>(L, C, pol, x, b, col, row, in);
-  for (; row < L.nrows; row += rstride) {
+  if (PIPE && active && row < row_end) fetch_node<D, P, XJ, BJ>(L, C, pol, x, b, col, row, in);
+  for (; row < row_end; row += rstride) {
     NodeIn<D, P> nx;
     const int rn = row + rstride;
-    if (PIPE && active && rn < L.nrows) fetch_node<D, P, XJ, BJ>(L, C, pol, x, b, col, rn, nx);
-    if (!PIPE && active) fetch_node<D, P, XJ, BJ>(L, C, pol, x, b, col, row, in);
-    if (active) {
+    const bool go = active && (DEEP || !(col_in_rect && row >= rect.r0 && row < rect.r1));
+    if (PIPE && active && rn < row_end) fetch_node<D, P, XJ, BJ>(L, C, pol, x, b, col, rn, nx);
+    if (!PIPE && go) fetch_node<D, P, XJ, BJ>(L, C, pol, x, b, col, row, in);
+    if (go) {
       Node<D> nd;
       node_from<D, P>(L, col, row, in, nd);
       if (GATHER) prefetch_ahead(L, x, nd.loc, col);
       const int a = in.a;
       Tap<D> taps[E];
-      const double wsum = row_taps<D, P>(L, tsd + a * P * D, tbd + a * D, nd, taps);
+      double wsum;
+      if (DEEP) {
+        double o[P + 1][D];
+        row_offsets<D, P>(L, tsd + a * P * D, tbd + a * D, nd, o);
+        wsum = row_geometry_fast<D, P>(L, nd, o, taps);
+      } else {
+        wsum = row_taps<D, P>(L, tsd + a * P * D, tbd + a * D, nd, taps);
+      }
       double acc = 0.0, self = 0.0;
       if (GATHER) {
         double vals[E];
