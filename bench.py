@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--no-time-kernels", action="store_true",
                     help="do not event-time kernel classes (roofline then null)")
     ap.add_argument("--json-out", default=None)
+    ap.add_argument("--pi-forcing", type=float, default=None, help="solver setting (default: library's)")
+    ap.add_argument("--nu", type=int, default=None, help="V(nu,nu) smoothing sweeps (default: library's 2)")
     return ap.parse_args()
 
 
@@ -244,13 +246,16 @@ def run_b200(args):
     psis = [packed_psi(p, s * p.dt, device=dev) for s in range(1, n_all + 1)]
     srcs = [p.f_tables(s * p.dt) for s in range(1, n_all + 1)]
 
+    skw = {} if args.pi_forcing is None else {"pi_forcing": args.pi_forcing}
+    mgkw = {} if args.nu is None else {"nu_pre": args.nu, "nu_post": args.nu}
+
     def do_step(s, Uin, Uout, polbuf, psi):
         # initial iterate: linear extrapolation 2 U^{n-1} - U^{n-2} once two steps exist (Uout holds
         # U^{n-2}: ping-pong buffers); the fixed point does not depend on it (DESIGN.md xxiv)
         fb, fc = srcs[s - 1]
         g.set_source(fb, fc)
-        return g.step(p.dt, Uin, Uout, polbuf, psi, guess=(_lib.HJB_GUESS_EXTRAPOLATE if s >= 2
-                                                           else _lib.HJB_GUESS_PREV))
+        return g.step(p.dt, Uin, Uout, polbuf, psi, mg=mgkw, guess=(_lib.HJB_GUESS_EXTRAPOLATE if s >= 2
+                                                                    else _lib.HJB_GUESS_PREV), **skw)
 
     stats = []
     for s in range(1, args.warmup + 1):
@@ -325,7 +330,7 @@ def run_b200(args):
     # --------------------------------------------------------------- e2e through host buffers
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(g, p, args, U, U2, stream, srcs, psis, nI, dev, lay, bar, allmax)
+        e2e = run_e2e(g, p, args, U, U2, stream, srcs, psis, nI, dev, lay, bar, allmax, skw, mgkw)
 
     pis = [st["pi_iters"] for st in stats]
     kr = [st["krylov_iters_total"] for st in stats]
@@ -374,7 +379,7 @@ def traffic_for(cls, config, c):
     return e["dram_bytes_per_node"] * c["nodes"] / max(1, c["launches"])
 
 
-def run_e2e(g, p, args, U_dev, U2_dev, stream, srcs, psis, nI, dev, lay, bar, allmax):
+def run_e2e(g, p, args, U_dev, U2_dev, stream, srcs, psis, nI, dev, lay, bar, allmax, skw, mgkw):
     """The same steps through hjb_step with pinned HOST buffers: each step copies U_prev, the policy
     and psi host->device and U + policy device->host inside the timed region (inside the call)."""
     import torch
@@ -401,7 +406,7 @@ def run_e2e(g, p, args, U_dev, U2_dev, stream, srcs, psis, nI, dev, lay, bar, al
         s = base + i + 1
         fb, fc = srcs[s - 1]
         g.set_source(fb, fc)
-        g.step(p.dt, Uhp_np, Uh_np, pol_np, psi_np[s - 1], guess=_lib.HJB_GUESS_EXTRAPOLATE)
+        g.step(p.dt, Uhp_np, Uh_np, pol_np, psi_np[s - 1], guess=_lib.HJB_GUESS_EXTRAPOLATE, mg=mgkw, **skw)
         Uhp_np, Uh_np = Uh_np, Uhp_np
     ev1.record(stream)
     torch.cuda.synchronize()

@@ -17,5 +17,7 @@ Parity-pin status (see tests/test_oracle_*.py and DESIGN.md §4):
     system.solve                               pinned (dense LU on tiny grids, residual)
     howard.control_search / howard_step        pinned (brute-force policy enumeration, Problem B ties)
     howard.march                               pinned (Table 4a / Table 4-B errors; O(h) rate)
-    certify.nonlinear_residual                 pinned (D6 bound against the exact discrete solution)
+    howard.control_search(idx=sample).R        the nonlinear-residual certificate R_j(U) on sampled rows
+                                               (full-size GPU checks); pinned (D6 bound against the
+                                               exact discrete solution, test_residual_certificate_bound)
 """
