@@ -118,12 +118,8 @@ struct hjb_grid {
   int nplanes0 = 0;  // per-node coefficient planes read by the operator (sigma/b/c fields)
   int sms = 148;
   int nblk_last = 1;  // CTAs of the last dims() launch (partials to reduce)
-  // windowed control search (2D deep-interior tiles, k_search_win)
+  // deep rectangles (2D): per-rank scale-field ranges and per-axis endpoint reach
   std::vector<double> h_sd, h_bd;  // host copies of sigma_dir / b_dir
-  bool win_ok = false;
-  WinGeom win{};
-  size_t win_smem = 0;
-  int win_grid = 0;
   double* d_rng = nullptr;    // [scmin_p, scmax_p]_p, [bsmin, bsmax]
   bool reach_ok = false;      // per-axis reach known (scale fields only): deep rectangles enabled
   double rdiff_ax[2] = {0, 0}, rdrift_ax[2] = {0, 0};
@@ -678,17 +674,16 @@ static hjb_status upload_tables(hjb_grid* g, const double* sigma_dir, const doub
   return HJB_OK;
 }
 
-// ---------------------------------------------------------------------------- windowed search setup
-// Decide whether (and where) the control search runs k_search_win: 2D, no per-node sigma/b offset
-// fields, and a non-empty rectangle of tiles whose every endpoint is strictly inside the box.
-// Window boxes = tile span + the jitter of the per-node scale fields (their per-rank ranges).
-static hjb_status setup_window_search(hjb_grid* g) {
-  g->win_ok = false;
+// ---------------------------------------------------------------------------- deep rectangles
+// Per-rank ranges of the per-node scale fields -> per-axis reach of every control's endpoints ->
+// the rectangle of nodes none of whose endpoints can be truncated (2D, no sigma/b offset fields).
+// deep_rect() scales it to each multigrid level; the lean kernels run there.
+static hjb_status setup_deep(hjb_grid* g) {
   g->reach_ok = false;
-#ifdef HJB_NO_WINSEARCH
+#ifdef HJB_NO_DEEP
   return HJB_OK;
 #endif
-  if (g->D != 2 || g->C0.sigma_node || g->C0.b_node || getenv("HJB_NO_WINSEARCH")) return HJB_OK;
+  if (g->D != 2 || g->C0.sigma_node || g->C0.b_node || getenv("HJB_NO_DEEP")) return HJB_OK;
   const int P = g->P, D = 2, K = g->K;
   const LevelDev& L = g->L0;
   if (L.nrows <= 0) return HJB_OK;
@@ -712,17 +707,17 @@ static hjb_status setup_window_search(hjb_grid* g) {
   std::vector<double> mx(nv, -INFINITY);
   for (int b = 0; b < nb; ++b)
     for (int k = 0; k < nv; ++k) mx[k] = std::max(mx[k], part[(size_t)b * nv + k]);
-  double rng[8];
+  double rng[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   for (int k = 0; k < P + 1; ++k) {
     rng[2 * k] = -mx[2 * k];
     rng[2 * k + 1] = mx[2 * k + 1];
   }
-  for (double v : rng)
-    if (!std::isfinite(v)) return HJB_OK;
+  for (int k = 0; k < nv; ++k)
+    if (!std::isfinite(rng[k])) return HJB_OK;
   CK(cudaMemcpyAsync(g->d_rng, rng, nv * sizeof(double), cudaMemcpyHostToDevice, g->st));
   CK(cudaStreamSynchronize(g->st));
-  // reach and jitter per axis over all controls / endpoints
-  double reach[2] = {0, 0}, jit[2] = {0, 0};
+  // reach per axis over all controls / endpoints (diffusion and drift separately: they scale
+  // differently across multigrid levels)
   g->rdiff_ax[0] = g->rdiff_ax[1] = g->rdrift_ax[0] = g->rdrift_ax[1] = 0.0;
   for (int a = 0; a < K; ++a)
     for (int e = 0; e <= P; ++e)
@@ -731,38 +726,10 @@ static hjb_status setup_window_search(hjb_grid* g) {
         const double f0 = rng[2 * e], f1 = rng[2 * e + 1];
         const double o0 = c * f0, o1 = c * f1;
         const double r = std::max(std::fabs(o0), std::fabs(o1));
-        reach[d] = std::max(reach[d], r);
         double& rr = (e < P) ? g->rdiff_ax[d] : g->rdrift_ax[d];
         rr = std::max(rr, r);
-        jit[d] = std::max(jit[d], std::fabs(o1 - o0));
       }
   g->reach_ok = true;
-  WinGeom W{};
-  W.bwx = kWX - 1 + (int)std::ceil(jit[0] + 2e-6) + 3;
-  W.bwy = kWY - 1 + (int)std::ceil(jit[1] + 2e-6) + 3;
-  W.sw = (W.bwx + 2 + 1) & ~1;
-  const int n = (int)g->n;
-  const int mxr = (int)std::floor(reach[0] + 1e-6) + 1, myr = (int)std::floor(reach[1] + 1e-6) + 1;
-  const int c_lo = mxr - 1, c_hi = n - 2 - mxr;  // col = i0 - 1
-  const int i1_lo = std::max<int>(myr, (int)L.row_first);
-  const int i1_hi = std::min<int>(n - 1 - myr, (int)L.row_first + L.nrows - 1);
-  if (c_hi < c_lo || i1_hi < i1_lo) return HJB_OK;
-  W.ntx = (c_hi - c_lo + 1) / kWX;
-  W.nty = (i1_hi - i1_lo + 1) / kWY;
-  if (W.ntx <= 0 || W.nty <= 0) return HJB_OK;
-  W.rect = SkipRect{c_lo, c_lo + W.ntx * kWX, i1_lo - (int)L.row_first, i1_lo - (int)L.row_first + W.nty * kWY};
-  const int E = 2 * P + 1;
-  const size_t ntab = (size_t)K * (P * D + D + 2 + g->Q);
-  const size_t smem = (((ntab + 15) & ~(size_t)15) + (size_t)2 * E * W.bwy * W.sw) * sizeof(double);
-  if (smem > 200 * 1024 || W.bwx > 256 || W.bwy > 256) return HJB_OK;
-  const void* fn = P == 1 ? (const void*)k_search_win<1> : (const void*)k_search_win<2>;
-  CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int occ = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kWT, smem) != cudaSuccess || occ < 1) return HJB_OK;
-  g->win = W;
-  g->win_smem = smem;
-  g->win_grid = std::min(W.ntx * W.nty, std::min(occ * g->sms, kMaxBlocks / 2));
-  g->win_ok = true;
   return HJB_OK;
 }
 
@@ -806,7 +773,7 @@ extern "C" hjb_status hjb_set_coeffs(hjb_grid_t g, const hjb_coeffs* c) {
     g->reach_drift = rb;
     const int64_t need = (int64_t)std::floor(std::max(rd, rb) * (1.0 + 1e-12)) + 1;
     g->L0.pf_rows = prefetch_rows(g, g->L0);
-    TRY(setup_window_search(g));
+    TRY(setup_deep(g));
     if (g->R > 1 && need > g->lay.halo) {
       g->have_coeffs = false;
       return fail(HJB_ERR_INVALID_ARG, "halo too small for these coefficients: need " + std::to_string(need) +
@@ -859,11 +826,26 @@ static hjb_status policy_update_dev(hjb_grid* g, double dt, const double* U, con
   const double bpn = 8.0 + 8.0 + 1.0 + 1.0 + 8.0 + 8.0 * g->Q + 8.0 * g->nplanes0;
   const double fpn = g->K * ((2.0 * g->P + 1.0) * (1 << g->D) * 2.0 + 2.0 * g->Q + 4.0);
   const size_t tsm = (size_t)g->K * (g->P * g->D + g->D + 2 + g->Q) * sizeof(double);
-  const bool use_win = g->win_ok && ((uintptr_t)U & 15) == 0;  // bulk copies need 16-byte alignment
-  const SkipRect skip = use_win ? g->win.rect : SkipRect{0, 0, 0, 0};
-#define SRCH(DD, PP)                                                                                          \
-  LAUNCH(HJB_KC_SEARCH, nodes, nodes * bpn, nodes * fpn,                                                    \
-         k_search<DD, PP><<<dims(g, g->L0, (const void*)k_search<DD, PP>, kSBX, tsm), dim3(kSBX, kSBY), tsm, g->st>>>(g->L0, g->C0, dt, U, Uprev, pol, F, g->partial, skip))
+  // deep rectangle (2D): lean fast-path kernel there, general kernel on the boundary layer
+  const SkipRect rect = deep_rect(g, g->L0);
+  const bool has_deep = rect.c1 > rect.c0 && rect.r1 > rect.r0;
+  LevelDev Ld = g->L0;
+  Ld.nI = rect.c1 - rect.c0;
+  Ld.nrows = rect.r1 - rect.r0;
+  int nblk = 0;
+#define SRCH1(DD, PP, DP, LL)                                                                                 \
+  LAUNCH(HJB_KC_SEARCH, DP ? 0 : nodes, DP ? 0 : nodes * bpn, DP ? 0 : nodes * fpn,                          \
+         k_search<DD, PP, DP><<<dims(g, LL, (const void*)k_search<DD, PP, DP>, kSBX, tsm), dim3(kSBX, kSBY), \
+                                tsm, g->st>>>(g->L0, g->C0, dt, U, Uprev, pol, F, g->partial + 2 * nblk, rect))
+#define SRCH(DD, PP)                       \
+  do {                                     \
+    SRCH1(DD, PP, false, g->L0);           \
+    nblk += g->nblk_last;                  \
+    if (has_deep) {                        \
+      SRCH1(DD, PP, true, Ld);             \
+      nblk += g->nblk_last;                \
+    }                                      \
+  } while (0)
   if (g->D == 2) {
     if (g->P == 1) SRCH(2, 1);
     else SRCH(2, 2);
@@ -873,20 +855,8 @@ static hjb_status policy_update_dev(hjb_grid* g, double dt, const double* U, con
     else SRCH(3, 3);
   }
 #undef SRCH
+#undef SRCH1
   CKL();
-  int nblk = g->nblk_last;
-  if (g->win_ok && ((uintptr_t)U & 15) == 0) {  // deep-interior tiles: windows staged in shared memory
-    const double wn = (double)g->win.ntx * g->win.nty * kWT;
-    if (g->P == 1)
-      LAUNCH(HJB_KC_SEARCH, 0, 0, 0, k_search_win<1><<<g->win_grid, kWT, g->win_smem, g->st>>>(
-                                         g->L0, g->C0, dt, U, Uprev, pol, F, g->partial + 2 * nblk, g->win, g->d_rng));
-    else
-      LAUNCH(HJB_KC_SEARCH, 0, 0, 0, k_search_win<2><<<g->win_grid, kWT, g->win_smem, g->st>>>(
-                                         g->L0, g->C0, dt, U, Uprev, pol, F, g->partial + 2 * nblk, g->win, g->d_rng));
-    CKL();
-    (void)wn;
-    nblk += g->win_grid;
-  }
   hjb_status err;
   double changed = 0.0;
   const double R = host_finalize(g, nblk, 0x1u, SC_NONE, &err, &changed);

@@ -124,18 +124,15 @@ __global__ void __launch_bounds__(kTX, HJB_OP_MINB) k_operator(LevelDev L, CoefD
 // ================================================================== control search
 // For every owned interior node: H^a = acc_a - wsum_a U_j + c^a U_j + f^a for all a (lowest-index
 // argmin), policy/F outputs, partials: [max R, changed count].
-template <int D, int P>
+// DEEP: only the nodes of `skip` (every endpoint of every control strictly inside the box: the lean
+// fast path); otherwise every node outside `skip`.
+template <int D, int P, bool DEEP>
 __global__ void __launch_bounds__(kTX, HJB_SEARCH_MINB) k_search(LevelDev L, CoefDev C, double dt,
                                                 const double* __restrict__ U,
                                                 const double* __restrict__ Uprev,
                                                 uint8_t* __restrict__ pol, double* __restrict__ F,
                                                 double* partial, SkipRect skip) {
   constexpr int E = 2 * P + 1;
-#ifndef HJB_SEARCH_UNROLL2
-  constexpr bool UNROLL2 = false;
-#else
-  constexpr bool UNROLL2 = HJB_SEARCH_UNROLL2 && (D == 2);
-#endif
   extern __shared__ double tab[];
   stage_tables<D, P, true>(C, tab);
   const double* tsd = tab;
@@ -144,8 +141,11 @@ __global__ void __launch_bounds__(kTX, HJB_SEARCH_MINB) k_search(LevelDev L, Coe
   const double* tfc = tcc + C.K;
   const double* tfb = tfc + C.K;
   double red[2] = {0.0, 0.0};
-  FOR_INTERIOR_B(L, kSBX, kSBY) {
-    if (col >= skip.c0 && col < skip.c1 && row >= skip.r0 && row < skip.r1) continue;  // k_search_win
+  const int c_beg = DEEP ? skip.c0 : 0, c_end = DEEP ? skip.c1 : L.nI;
+  const int r_beg = DEEP ? skip.r0 : 0, r_end = DEEP ? skip.r1 : L.nrows;
+  for (int row = r_beg + blockIdx.y * kSBY + threadIdx.y; row < r_end; row += gridDim.y * kSBY)
+  for (int col = c_beg + blockIdx.x * kSBX + threadIdx.x; col < c_end; col += gridDim.x * kSBX) {
+    if (!DEEP && col >= skip.c0 && col < skip.c1 && row >= skip.r0 && row < skip.r1) continue;
     Node<D> nd;
     node_at<D>(L, col, row, nd);
     load_fields<D>(C, nd);
@@ -167,34 +167,16 @@ __global__ void __launch_bounds__(kTX, HJB_SEARCH_MINB) k_search(LevelDev L, Coe
       return (acc - wsum * Uj) + c * Uj + f;
     };
     int a = 0;
-    if (UNROLL2) {
-      // two controls per pass: both geometries, then all 2 (2P+1) 2^d gathers in flight together
-      for (; a + 1 < C.K; a += 2) {
-        Tap<D> t0[E], t1[E];
-        const double w0 = row_taps<D, P>(L, tsd + a * P * D, tbd + a * D, nd, t0);
-        const double w1 = row_taps<D, P>(L, tsd + (a + 1) * P * D, tbd + (a + 1) * D, nd, t1);
-        double v0[E], v1[E];
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          v0[e] = tap_value<D>(L, U, t0[e]);
-          v1[e] = tap_value<D>(L, U, t1[e]);
-        }
-        double acc0 = 0.0, acc1 = 0.0;
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          acc0 = fma(t0[e].w, v0[e], acc0);
-          acc1 = fma(t1[e].w, v1[e], acc1);
-        }
-        double f0, f1;
-        const double H0 = tail(a, acc0, w0, f0);
-        const double H1 = tail(a + 1, acc1, w1, f1);
-        if (H0 < best) { best = H0; arg = a; fbest = f0; }      // strict: lowest index wins ties
-        if (H1 < best) { best = H1; arg = a + 1; fbest = f1; }
-      }
-    }
     for (; a < C.K; ++a) {
       Tap<D> taps[E];
-      const double wsum = row_taps<D, P>(L, tsd + a * P * D, tbd + a * D, nd, taps);
+      double wsum;
+      if (DEEP) {
+        double o[P + 1][D];
+        row_offsets<D, P>(L, tsd + a * P * D, tbd + a * D, nd, o);
+        wsum = row_geometry_fast<D, P>(L, nd, o, taps);
+      } else {
+        wsum = row_taps<D, P>(L, tsd + a * P * D, tbd + a * D, nd, taps);
+      }
       double vals[E];
 #pragma unroll
       for (int e = 0; e < E; ++e) vals[e] = tap_value<D>(L, U, taps[e]);
@@ -218,226 +200,6 @@ __global__ void __launch_bounds__(kTX, HJB_SEARCH_MINB) k_search(LevelDev L, Coe
     red[1] += (old != arg) ? 1.0 : 0.0;
   }
   block_reduce_store<2>(red, partial, 0x1u);
-}
-
-// ================================================================== control search, smem windows
-// 2D deep-interior tiles (every endpoint of every control strictly inside the box) of kWX x kWY
-// nodes.  For each control the 2P+1 endpoint windows of U (tile span + the coefficient jitter) are
-// copied global -> shared with cp.async.bulk (one bulk copy per window row, completion on an
-// mbarrier), double-buffered across controls, and all gathers read shared memory.  Nodes outside
-// the tiles are done by k_search (it skips this rectangle).
-constexpr int kWX = 32, kWY = 8, kWT = kWX * kWY;
-
-struct WinGeom {
-  int bwx, bwy, sw;        // window box (cells) and its shared-memory row stride (doubles, even)
-  int ntx, nty;            // tiles
-  SkipRect rect;           // tile rectangle in (col, row) loop coordinates
-  double omin[4][2], omax[4][2];  // unused slot layout guard
-};
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_arrive(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t done = 0;
-  for (long long spin = 0; !done; ++spin) {
-    if (spin > (1LL << 28)) __trap();  // a lost transaction: fail loudly instead of hanging
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-  }
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
-// window origin (global cells) of endpoint e of control a for the tile whose first node is (ix0, iy0):
-// the endpoints of the tile lie in [ix0 + omin, ix0 + kWX - 1 + omax] (+1 for the interpolation)
-template <int P>
-__device__ __forceinline__ void win_origin(const LevelDev& L, const double* sd, const double* bd, int e,
-                                           const double* rng, int ix0, int iy0, int& wx0, int& wy0) {
-  // rng: [scmin_p, scmax_p] for p < P then [bsmin, bsmax]
-  double lo[2], hi[2];
-#pragma unroll
-  for (int d = 0; d < 2; ++d) {
-    double c, f0, f1;
-    if (e < 2 * P) {
-      const int p = e >> 1;
-      c = L.kh * ((e & 1) ? -sd[p * 2 + d] : sd[p * 2 + d]);
-      f0 = rng[2 * p];
-      f1 = rng[2 * p + 1];
-    } else {
-      c = L.k2h * bd[d];
-      f0 = rng[2 * P];
-      f1 = rng[2 * P + 1];
-    }
-    const double a0 = c * f0, a1 = c * f1;
-    lo[d] = fmin(a0, a1) - 1e-6;
-    hi[d] = fmax(a0, a1) + 1e-6;
-  }
-  wx0 = ix0 + (int)floor(lo[0]);
-  wy0 = iy0 + (int)floor(lo[1]);
-}
-
-template <int P>
-__global__ void __launch_bounds__(kWT, 1) k_search_win(LevelDev L, CoefDev C, double dt,
-                                                       const double* __restrict__ U,
-                                                       const double* __restrict__ Uprev,
-                                                       uint8_t* __restrict__ pol, double* __restrict__ F,
-                                                       double* partial, WinGeom W, const double* __restrict__ rng_g) {
-  constexpr int D = 2, E = 2 * P + 1;
-  extern __shared__ __align__(128) double sm[];
-  __shared__ __align__(8) uint64_t bars[2];
-  __shared__ int org[2][E][2];
-  __shared__ double rng[2 * P + 2];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // tables (the same layout as stage_tables<SRC>): sigma_dir | b_dir | c_ctrl | f_ctrl | f_basis
-  double* tab = sm;
-  const int ntab = C.K * (P * D + D + 2 + C.Q);
-  const int tab_pad = (ntab + 15) & ~15;
-  for (int e = tid; e < C.K * P * D; e += kWT) tab[e] = __ldg(C.sigma_dir + e);
-  for (int e = tid; e < C.K * D; e += kWT) tab[C.K * P * D + e] = __ldg(C.b_dir + e);
-  for (int e = tid; e < C.K; e += kWT) {
-    tab[C.K * (P * D + D) + e] = __ldg(C.c_ctrl + e);
-    tab[C.K * (P * D + D + 1) + e] = __ldg(C.f_ctrl + e);
-  }
-  for (int e = tid; e < C.K * C.Q; e += kWT) tab[C.K * (P * D + D + 2) + e] = __ldg(C.f_basis + e);
-  if (tid < 2 * P + 2) rng[tid] = rng_g[tid];
-  const double* tsd = tab;
-  const double* tbd = tab + C.K * P * D;
-  const double* tcc = tbd + C.K * D;
-  const double* tfc = tcc + C.K;
-  const double* tfb = tfc + C.K;
-  const int win_elems = W.bwy * W.sw;
-  double* wins = sm + tab_pad;  // [2 stages][E windows][bwy][sw]
-  if (tid == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  uint32_t uses[2] = {0u, 0u};
-  const int lx = tid % kWX, ly = tid / kWX;
-  const long long lr0 = L.local_row0;
-  const int n = L.n;
-  double red[2] = {0.0, 0.0};
-
-  // issue the windows of control a for tile (ix0, iy0) into stage st (warp 0)
-  auto issue = [&](int a, int st, int ix0, int iy0) {
-    if (warp != 0) return;
-    const double* sd = tsd + a * P * D;
-    const double* bd = tbd + a * D;
-    uint32_t total = 0;
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      int wx0, wy0;
-      win_origin<P>(L, sd, bd, e, rng, ix0, iy0, wx0, wy0);
-      if (lane == 0) { org[st][e][0] = wx0; org[st][e][1] = wy0; }
-      total += (uint32_t)(W.bwy * W.sw * 8);
-      (void)total;
-    }
-    if (lane == 0) mbar_expect_arrive(&bars[st], (uint32_t)(E * W.bwy * W.sw * 8));
-    __syncwarp();
-    for (int q = lane; q < E * W.bwy; q += 32) {
-      const int e = q / W.bwy, yy = q - e * W.bwy;
-      int wx0, wy0;
-      win_origin<P>(L, sd, bd, e, rng, ix0, iy0, wx0, wy0);
-      const long long el = ((long long)(wy0 + yy) - lr0) * n + wx0;   // first element of the row
-      const long long al = el & ~1LL;                                 // 16-byte aligned start
-      bulk_g2s(wins + ((size_t)(st * E + e) * W.bwy + yy) * W.sw, U + al, (uint32_t)(W.sw * 8), &bars[st]);
-    }
-  };
-
-  const int ntiles = W.ntx * W.nty;
-  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const int ty = t / W.ntx, tx = t - ty * W.ntx;
-    const int col = W.rect.c0 + tx * kWX + lx, row = W.rect.r0 + ty * kWY + ly;
-    const int ix0 = 1 + W.rect.c0 + tx * kWX, iy0 = (int)L.row_first + W.rect.r0 + ty * kWY;
-    Node<D> nd;
-    node_at<D>(L, col, row, nd);
-    load_fields<D>(C, nd);
-    double feat[kMaxQ];
-#pragma unroll
-    for (int q = 0; q < kMaxQ; ++q) feat[q] = (q < C.Q) ? __ldg(C.f_feat + q * C.ld + nd.loc) : 0.0;
-    const double Uj = __ldg(U + nd.loc);
-    double best = INFINITY, fbest = 0.0;
-    int arg = 0;
-    __syncthreads();                       // previous tile finished with both stages
-    issue(0, 0, ix0, iy0);
-    if (C.K > 1) issue(1, 1, ix0, iy0);
-    for (int a = 0; a < C.K; ++a) {
-      const int st = a & 1;
-      mbar_wait(&bars[st], uses[st] & 1u);
-      uses[st] += 1;
-      const double* sd = tsd + a * P * D;
-      const double* bd = tbd + a * D;
-      double o[P + 1][D];
-      row_offsets<D, P>(L, sd, bd, nd, o);
-      Tap<D> taps[E];
-      const double wsum = row_geometry_fast<D, P>(L, nd, o, taps);
-      double acc = 0.0;
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const int wx0 = org[st][e][0], wy0 = org[st][e][1];
-        const int yy = taps[e].c[1] - wy0;
-        const long long rowel = ((long long)taps[e].c[1] - lr0) * n + wx0;
-        const int sh0 = (int)(rowel & 1LL), sh1 = (int)((rowel + n) & 1LL);
-        const double* w = wins + (size_t)(st * E + e) * win_elems;
-        const double* r0p = w + yy * W.sw + (taps[e].c[0] - wx0) + sh0;
-        const double* r1p = w + (yy + 1) * W.sw + (taps[e].c[0] - wx0) + sh1;
-        const double v00 = r0p[0], v10 = r0p[1], v01 = r1p[0], v11 = r1p[1];
-        const double aa = fma(taps[e].s[0], v10 - v00, v00);
-        const double bb = fma(taps[e].s[0], v11 - v01, v01);
-        acc = fma(taps[e].w, fma(taps[e].s[1], bb - aa, aa), acc);
-      }
-      double f = tfc[a];
-      const double* fb = tfb + a * C.Q;
-#pragma unroll
-      for (int q = 0; q < kMaxQ; ++q)
-        if (q < C.Q) f = fma(fb[q], feat[q], f);
-      const double c = nd.cn + tcc[a];
-      const double H = (acc - wsum * Uj) + c * Uj + f;
-      if (H < best) {  // strict: lowest index wins exact ties (reading iv)
-        best = H;
-        arg = a;
-        fbest = f;
-      }
-      __syncthreads();                     // every thread is done with stage st
-      if (a + 2 < C.K) issue(a + 2, st, ix0, iy0);
-    }
-    const double Up = __ldg(Uprev + nd.loc);
-    const double R = fabs(Uj - Up - dt * best);
-    const int old = pol[nd.loc];
-    pol[nd.loc] = (uint8_t)arg;
-    F[nd.loc] = fma(dt, fbest, Up);
-    red[0] = fmax(red[0], (R == R) ? R : INFINITY);
-    red[1] += (old != arg) ? 1.0 : 0.0;
-  }
-  // block partials (same layout as block_reduce_store<2>)
-  __shared__ double rs[2][kWT / 32];
-  double v0 = warp_max(red[0]), v1 = warp_sum(red[1]);
-  if (lane == 0) { rs[0][warp] = v0; rs[1][warp] = v1; }
-  __syncthreads();
-  if (warp == 0) {
-    v0 = lane < kWT / 32 ? rs[0][lane] : -INFINITY;
-    v1 = lane < kWT / 32 ? rs[1][lane] : 0.0;
-    v0 = warp_max(v0);
-    v1 = warp_sum(v1);
-    if (lane == 0) { partial[blockIdx.x * 2] = v0; partial[blockIdx.x * 2 + 1] = v1; }
-  }
 }
 
 // per-rank ranges of the per-node scale fields: [min sc_p, max sc_p]_p, [min bs, max bs] as

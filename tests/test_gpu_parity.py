@@ -256,27 +256,31 @@ def test_edge_cases():
 
 @pytest.mark.parametrize("name,mk", [("cfg1", lambda: bj_config(1)), ("cfg2_513", lambda: bj_config(2, n=513)),
                                      ("cfg0_K7", lambda: bj_config(0, n=65, K=7))])
-def test_window_search_matches_direct(name, mk, monkeypatch):
-    """k_search_win (shared-memory windows filled by cp.async.bulk) gives bit-identical policy, F
-    and residual to the direct-gather search (HJB_NO_WINSEARCH) on the same inputs."""
+def test_deep_kernels_match_general(name, mk, monkeypatch):
+    """The lean deep-rectangle kernels (no truncation code) give bit-identical search results and
+    operator applications to the general kernels everywhere (HJB_NO_DEEP disables them)."""
     torch = require_gpu()
     p = mk()
     rng = np.random.default_rng(11)
     Uprev = p.g(p.all_idx())
     U = Uprev + 0.05 * rng.uniform(-1, 1, size=p.N)
+    x = random_vector(p)
     out = {}
-    for mode in ("direct", "window"):
-        if mode == "direct":
-            monkeypatch.setenv("HJB_NO_WINSEARCH", "1")
+    for mode in ("general", "deep"):
+        if mode == "general":
+            monkeypatch.setenv("HJB_NO_DEEP", "1")
         else:
-            monkeypatch.delenv("HJB_NO_WINSEARCH", raising=False)
+            monkeypatch.delenv("HJB_NO_DEEP", raising=False)
         g, _ = setup(p)
         pol = torch.zeros(p.N, dtype=torch.uint8, device="cuda")
         F = torch.zeros(p.N, dtype=torch.float64, device="cuda")
         st = g.policy_update(p.dt, to_dev(U, torch), to_dev(Uprev, torch), pol, F)
+        y = torch.zeros(p.N, dtype=torch.float64, device="cuda")
+        g.apply(p.dt, pol, to_dev(x, torch), y)
         torch.cuda.synchronize()
-        out[mode] = (pol.cpu().numpy(), F.cpu().numpy(), st)
+        out[mode] = (pol.cpu().numpy(), F.cpu().numpy(), st, y.cpu().numpy())
         g.close()
-    assert np.array_equal(out["direct"][0], out["window"][0])
-    assert np.array_equal(out["direct"][1], out["window"][1])
-    assert out["direct"][2] == out["window"][2]
+    assert np.array_equal(out["general"][0], out["deep"][0])
+    assert np.array_equal(out["general"][1], out["deep"][1])
+    assert out["general"][2] == out["deep"][2]
+    assert np.array_equal(out["general"][3], out["deep"][3])
