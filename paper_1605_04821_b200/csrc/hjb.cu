@@ -17,6 +17,7 @@
 #include "hjb.h"
 #include "hjb_comm.h"
 #include "hjb_kernels.cuh"
+#include "hjb_tma.cuh"
 
 using namespace hjb;
 
@@ -122,6 +123,10 @@ struct hjb_grid {
   std::vector<double> h_sd, h_bd;  // host copies of sigma_dir / b_dir
   double* d_rng = nullptr;    // [scmin_p, scmax_p]_p, [bsmin, bsmax]
   bool reach_ok = false;      // per-axis reach known (scale fields only): deep rectangles enabled
+  bool tma_ok = false;        // TMA-windowed search tiles (k_search_tma)
+  TmaGeom tma{};
+  size_t tma_smem = 0;
+  int tma_grid = 0;
   double rdiff_ax[2] = {0, 0}, rdrift_ax[2] = {0, 0};
   double* rng_part = nullptr; // k_field_ranges block partials
 };
@@ -614,7 +619,7 @@ extern "C" hjb_status hjb_grid_create(const hjb_grid_desc* d, hjb_grid_t* out) {
     }
     cudaMemsetAsync(*pv, 0, vb, g->st);
   }
-  if ((s = dalloc((void**)&g->partial, (size_t)kMaxBlocks * 4 * sizeof(double))) != HJB_OK ||
+  if ((s = dalloc((void**)&g->partial, (size_t)kMaxBlocks * 8 * sizeof(double))) != HJB_OK ||
       (s = dalloc((void**)&g->red, 4 * sizeof(double))) != HJB_OK ||
       (s = dalloc((void**)&g->red_all, (size_t)2 * g->R * sizeof(double))) != HJB_OK ||
       (s = dalloc((void**)&g->S, sizeof(KScal))) != HJB_OK ||
@@ -674,6 +679,39 @@ static hjb_status upload_tables(hjb_grid* g, const double* sigma_dir, const doub
   return HJB_OK;
 }
 
+// ---------------------------------------------------------------------------- TMA tensor maps
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn tma_encoder() {
+  static EncodeTiledFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+    cudaGetLastError();
+  }
+  return fn;
+}
+
+// {2n, local_rows/2} pair-row view of a level-0 grid array (see hjb_tma.cuh), box bw x bh
+static bool encode_pair_view(hjb_grid* g, const double* U, CUtensorMap* map) {
+  EncodeTiledFn enc = tma_encoder();
+  if (!enc) return false;
+  const cuuint64_t n = (cuuint64_t)g->n;
+  const cuuint64_t dims[2] = {2 * n, (cuuint64_t)(g->L0.local_rows / 2)};
+  const cuuint64_t strides[1] = {2 * n * sizeof(double)};
+  const cuuint32_t box[2] = {(cuuint32_t)g->tma.bw, (cuuint32_t)g->tma.bh};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)U, dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // ---------------------------------------------------------------------------- deep rectangles
 // Per-rank ranges of the per-node scale fields -> per-axis reach of every control's endpoints ->
 // the rectangle of nodes none of whose endpoints can be truncated (2D, no sigma/b offset fields).
@@ -730,6 +768,47 @@ static hjb_status setup_deep(hjb_grid* g) {
         rr = std::max(rr, r);
       }
   g->reach_ok = true;
+  // TMA-windowed search tiles inside the deep rectangle of the fine level (single tensor map view)
+  g->tma_ok = false;
+#ifndef HJB_NO_TMA
+  if (!getenv("HJB_NO_TMA")) {
+    double jit[2] = {0, 0};
+    for (int a = 0; a < K; ++a)
+      for (int e = 0; e <= P; ++e)
+        for (int d = 0; d < D; ++d) {
+          const double c = (e < P) ? L.kh * g->h_sd[(a * P + e) * D + d] : L.k2h * g->h_bd[a * D + d];
+          jit[d] = std::max(jit[d], std::fabs(c * rng[2 * e + 1] - c * rng[2 * e]));
+        }
+    const SkipRect dr = deep_rect(g, L);
+    TmaGeom T{};
+    T.bw = (kWX - 1 + (int)std::ceil(jit[0] + 2e-6) + 3 + 1) & ~1;
+    const int bwy = kWY - 1 + (int)std::ceil(jit[1] + 2e-6) + 3;
+    T.bh = (bwy + 1) / 2 + 1;
+    T.slot = ((T.bw * T.bh + 15) / 16) * 16;
+    T.ntx = (dr.c1 - dr.c0) / kWX;
+    // every pair-row a window needs must exist in the {2n, local_rows/2} view
+    const int reach_y = (int)std::floor(std::max(g->rdiff_ax[1], g->rdrift_ax[1]) + 1e-6) + 2;
+    const int pair_rows = (int)(L.local_rows / 2);
+    int rmax = dr.r1;  // exclusive, loop coordinates
+    while (rmax > dr.r0 && (int)L.row_first + rmax - 1 + reach_y - (int)L.local_row0 >= 2 * pair_rows) --rmax;
+    T.nty = (rmax - dr.r0) / kWY;
+    T.tiles = SkipRect{dr.c0, dr.c0 + T.ntx * kWX, dr.r0, dr.r0 + T.nty * kWY};
+    const int E = 2 * P + 1;
+    const size_t ntab = (size_t)K * (P * D + D + 2 + g->Q);
+    const size_t smem = (((ntab + 15) & ~(size_t)15) + (size_t)2 * E * 2 * T.slot) * sizeof(double);
+    if (T.ntx > 0 && T.nty > 0 && T.bw <= 256 && T.bh <= 256 && smem <= 200 * 1024 && tma_encoder()) {
+      const void* fn = P == 1 ? (const void*)k_search_tma<1> : (const void*)k_search_tma<2>;
+      CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      int occ = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kWT, smem) == cudaSuccess && occ >= 1) {
+        g->tma = T;
+        g->tma_smem = smem;
+        g->tma_grid = std::min(T.ntx * T.nty, std::min(occ * g->sms, kMaxBlocks));
+        g->tma_ok = true;
+      }
+    }
+  }
+#endif
   return HJB_OK;
 }
 
@@ -833,10 +912,13 @@ static hjb_status policy_update_dev(hjb_grid* g, double dt, const double* U, con
   Ld.nI = rect.c1 - rect.c0;
   Ld.nrows = rect.r1 - rect.r0;
   int nblk = 0;
+  CUtensorMap umap;
+  const bool use_tma = has_deep && g->tma_ok && ((uintptr_t)U & 15) == 0 && encode_pair_view(g, U, &umap);
+  const SkipRect tiles = use_tma ? g->tma.tiles : SkipRect{0, 0, 0, 0};
 #define SRCH1(DD, PP, DP, LL)                                                                                 \
   LAUNCH(HJB_KC_SEARCH, DP ? 0 : nodes, DP ? 0 : nodes * bpn, DP ? 0 : nodes * fpn,                          \
          k_search<DD, PP, DP><<<dims(g, LL, (const void*)k_search<DD, PP, DP>, kSBX, tsm), dim3(kSBX, kSBY), \
-                                tsm, g->st>>>(g->L0, g->C0, dt, U, Uprev, pol, F, g->partial + 2 * nblk, rect))
+                                tsm, g->st>>>(g->L0, g->C0, dt, U, Uprev, pol, F, g->partial + 2 * nblk, rect, tiles))
 #define SRCH(DD, PP)                       \
   do {                                     \
     SRCH1(DD, PP, false, g->L0);           \
@@ -857,6 +939,16 @@ static hjb_status policy_update_dev(hjb_grid* g, double dt, const double* U, con
 #undef SRCH
 #undef SRCH1
   CKL();
+  if (use_tma) {  // deep tiles: windows staged in shared memory by TMA (partials after the others')
+    if (g->P == 1)
+      LAUNCH(HJB_KC_SEARCH, 0, 0, 0, k_search_tma<1><<<g->tma_grid, kWT, g->tma_smem, g->st>>>(
+                                         g->L0, g->C0, dt, U, Uprev, pol, F, g->partial + 2 * nblk, g->tma, g->d_rng, umap));
+    else
+      LAUNCH(HJB_KC_SEARCH, 0, 0, 0, k_search_tma<2><<<g->tma_grid, kWT, g->tma_smem, g->st>>>(
+                                         g->L0, g->C0, dt, U, Uprev, pol, F, g->partial + 2 * nblk, g->tma, g->d_rng, umap));
+    CKL();
+    nblk += g->tma_grid;
+  }
   hjb_status err;
   double changed = 0.0;
   const double R = host_finalize(g, nblk, 0x1u, SC_NONE, &err, &changed);

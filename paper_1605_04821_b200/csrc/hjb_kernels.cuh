@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(kTX, HJB_SEARCH_MINB) k_search(LevelDev L, Coe
                                                 const double* __restrict__ U,
                                                 const double* __restrict__ Uprev,
                                                 uint8_t* __restrict__ pol, double* __restrict__ F,
-                                                double* partial, SkipRect skip) {
+                                                double* partial, SkipRect skip, SkipRect tiles) {
   constexpr int E = 2 * P + 1;
   extern __shared__ double tab[];
   stage_tables<D, P, true>(C, tab);
@@ -146,6 +146,7 @@ __global__ void __launch_bounds__(kTX, HJB_SEARCH_MINB) k_search(LevelDev L, Coe
   for (int row = r_beg + blockIdx.y * kSBY + threadIdx.y; row < r_end; row += gridDim.y * kSBY)
   for (int col = c_beg + blockIdx.x * kSBX + threadIdx.x; col < c_end; col += gridDim.x * kSBX) {
     if (!DEEP && col >= skip.c0 && col < skip.c1 && row >= skip.r0 && row < skip.r1) continue;
+    if (DEEP && col >= tiles.c0 && col < tiles.c1 && row >= tiles.r0 && row < tiles.r1) continue;  // TMA tiles
     Node<D> nd;
     node_at<D>(L, col, row, nd);
     load_fields<D>(C, nd);

@@ -257,8 +257,9 @@ def test_edge_cases():
 @pytest.mark.parametrize("name,mk", [("cfg1", lambda: bj_config(1)), ("cfg2_513", lambda: bj_config(2, n=513)),
                                      ("cfg0_K7", lambda: bj_config(0, n=65, K=7))])
 def test_deep_kernels_match_general(name, mk, monkeypatch):
-    """The lean deep-rectangle kernels (no truncation code) give bit-identical search results and
-    operator applications to the general kernels everywhere (HJB_NO_DEEP disables them)."""
+    """The lean deep-rectangle kernels (no truncation code) and the TMA-windowed search tiles give
+    bit-identical search results and operator applications to the general kernels everywhere
+    (HJB_NO_DEEP / HJB_NO_TMA disable them)."""
     torch = require_gpu()
     p = mk()
     rng = np.random.default_rng(11)
@@ -266,11 +267,13 @@ def test_deep_kernels_match_general(name, mk, monkeypatch):
     U = Uprev + 0.05 * rng.uniform(-1, 1, size=p.N)
     x = random_vector(p)
     out = {}
-    for mode in ("general", "deep"):
+    for mode in ("general", "deep", "deep_tma"):
+        monkeypatch.delenv("HJB_NO_DEEP", raising=False)
+        monkeypatch.delenv("HJB_NO_TMA", raising=False)
         if mode == "general":
             monkeypatch.setenv("HJB_NO_DEEP", "1")
-        else:
-            monkeypatch.delenv("HJB_NO_DEEP", raising=False)
+        elif mode == "deep":
+            monkeypatch.setenv("HJB_NO_TMA", "1")
         g, _ = setup(p)
         pol = torch.zeros(p.N, dtype=torch.uint8, device="cuda")
         F = torch.zeros(p.N, dtype=torch.float64, device="cuda")
@@ -280,7 +283,8 @@ def test_deep_kernels_match_general(name, mk, monkeypatch):
         torch.cuda.synchronize()
         out[mode] = (pol.cpu().numpy(), F.cpu().numpy(), st, y.cpu().numpy())
         g.close()
-    assert np.array_equal(out["general"][0], out["deep"][0])
-    assert np.array_equal(out["general"][1], out["deep"][1])
-    assert out["general"][2] == out["deep"][2]
-    assert np.array_equal(out["general"][3], out["deep"][3])
+    for m in ("deep", "deep_tma"):
+        assert np.array_equal(out["general"][0], out[m][0]), m
+        assert np.array_equal(out["general"][1], out[m][1]), m
+        assert out["general"][2] == out[m][2], m
+        assert np.array_equal(out["general"][3], out[m][3]), m
