@@ -353,6 +353,29 @@ static SkipRect deep_rect(hjb_grid* g, const LevelDev& L) {
   return r;
 }
 
+// `outer` minus `inner` as up to 4 rectangles (top/bottom full width, left/right beside inner), so
+// each piece gets its own launch shape (a thin strip launched over the whole grid would leave the
+// work to a handful of CTAs)
+static int ring_strips(const SkipRect& outer, const SkipRect& inner, SkipRect* out) {
+  int k = 0;
+  const bool empty = inner.c1 <= inner.c0 || inner.r1 <= inner.r0;
+  if (empty) {
+    out[k++] = outer;
+    return k;
+  }
+  if (inner.r0 > outer.r0) out[k++] = SkipRect{outer.c0, outer.c1, outer.r0, inner.r0};
+  if (outer.r1 > inner.r1) out[k++] = SkipRect{outer.c0, outer.c1, inner.r1, outer.r1};
+  if (inner.c0 > outer.c0) out[k++] = SkipRect{outer.c0, inner.c0, inner.r0, inner.r1};
+  if (outer.c1 > inner.c1) out[k++] = SkipRect{inner.c1, outer.c1, inner.r0, inner.r1};
+  return k;
+}
+static LevelDev shape_of(const LevelDev& L, const SkipRect& r) {
+  LevelDev S = L;
+  S.nI = r.c1 - r.c0;
+  S.nrows = r.r1 - r.r0;
+  return S;
+}
+
 // ---------------------------------------------------------------------------- dimension dispatch
 template <int D>
 static void launch_operator(hjb_grid* g, const LevelDev& L, const CoefDev& C, int mode, int ndot, double dt,
@@ -366,27 +389,30 @@ static void launch_operator(hjb_grid* g, const LevelDev& L, const CoefDev& C, in
                      (ndot >= 1 ? 8.0 : 0.0) + 8.0 * g->nplanes0;
   const double fpn = (2.0 * g->P + 1.0) * (1 << D) * 2.0 + 4.0 + 2.0 * ndot;
   const size_t tsm = (size_t)g->K * (g->P * D + D + 1) * sizeof(double);  // control tables in smem
-  // the deep rectangle of this level (2D): lean fast-path kernel there, general kernel elsewhere
-  const SkipRect rect = deep_rect(g, L);
+  // the deep rectangle of this level (2D): lean fast-path kernel there, general kernel on the
+  // boundary-layer strips around it (small levels: one general launch)
+  const SkipRect full{0, L.nI, 0, L.nrows};
+  SkipRect rect = deep_rect(g, L);
+  if ((int64_t)L.nI * L.nrows < (1 << 16)) rect = SkipRect{0, 0, 0, 0};
   const bool has_deep = rect.c1 > rect.c0 && rect.r1 > rect.r0;
-  LevelDev Ld = L;  // launch shape of the rectangle
-  Ld.nI = rect.c1 - rect.c0;
-  Ld.nrows = rect.r1 - rect.r0;
-  double* part2 = g->partial;
-#define OPL1(PP, M, ND, DP, LL, PART)                                                                        \
-  LAUNCH(cls, nodes, nodes * bpn, nodes * fpn,                                                              \
-         k_operator<D, PP, M, ND, DP><<<dims(g, LL, (const void*)k_operator<D, PP, M, ND, DP>, kBX, tsm),   \
-                                       dim3(kBX, kBY), tsm, st>>>(L, C, dt, omega, pol, x, b, y, u, PART, rect))
-#define OPLP(PP, M, ND)                                                                                     \
+  SkipRect strips[4];
+  const int ns = ring_strips(full, rect, strips);
+#define OPL1(PP, M, ND, DP, RR)                                                                             \
   do {                                                                                                      \
-    OPL1(PP, M, ND, false, L, g->partial);                                                                  \
-    int nb = g->nblk_last;                                                                                  \
-    if (has_deep) {                                                                                         \
-      part2 = g->partial + 2 * nb;                                                                          \
-      OPL1(PP, M, ND, true, Ld, part2);                                                                     \
-      nb += g->nblk_last;                                                                                   \
-    }                                                                                                       \
-    g->nblk_last = nb;                                                                                      \
+    const LevelDev LL = shape_of(L, RR);                                                                    \
+    const double nn = (double)LL.nI * LL.nrows;                                                             \
+    LAUNCH(cls, nn, nn * bpn, nn * fpn,                                                                     \
+           k_operator<D, PP, M, ND, DP><<<dims(g, LL, (const void*)k_operator<D, PP, M, ND, DP>, kBX, tsm), \
+                                         dim3(kBX, kBY), tsm, st>>>(L, C, dt, omega, pol, x, b, y, u,       \
+                                                                    g->partial + 2 * nb, RR));              \
+    nb += g->nblk_last;                                                                                     \
+  } while (0)
+#define OPLP(PP, M, ND)                                           \
+  do {                                                            \
+    int nb = 0;                                                   \
+    for (int k = 0; k < ns; ++k) OPL1(PP, M, ND, false, strips[k]); \
+    if (has_deep) OPL1(PP, M, ND, true, rect);                    \
+    g->nblk_last = nb;                                            \
   } while (0)
 #define OPL(M, ND)                                                                                          \
   do {                                                                                                      \
@@ -409,7 +435,7 @@ static void launch_operator(hjb_grid* g, const LevelDev& L, const CoefDev& C, in
 #undef OPL
 #undef OPLP
 #undef OPL1
-  (void)part2;
+  (void)nodes;
 }
 
 // ---------------------------------------------------------------------------- API: misc
@@ -795,7 +821,7 @@ static hjb_status setup_deep(hjb_grid* g) {
     T.tiles = SkipRect{dr.c0, dr.c0 + T.ntx * kWX, dr.r0, dr.r0 + T.nty * kWY};
     const int E = 2 * P + 1;
     const size_t ntab = (size_t)K * (P * D + D + 2 + g->Q);
-    const size_t smem = (((ntab + 15) & ~(size_t)15) + (size_t)2 * E * 2 * T.slot) * sizeof(double);
+    const size_t smem = (ntab + (size_t)2 * E * 2 * T.slot) * sizeof(double) + 128;
     if (T.ntx > 0 && T.nty > 0 && T.bw <= 256 && T.bh <= 256 && smem <= 200 * 1024 && tma_encoder()) {
       const void* fn = P == 1 ? (const void*)k_search_tma<1> : (const void*)k_search_tma<2>;
       CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -905,28 +931,33 @@ static hjb_status policy_update_dev(hjb_grid* g, double dt, const double* U, con
   const double bpn = 8.0 + 8.0 + 1.0 + 1.0 + 8.0 + 8.0 * g->Q + 8.0 * g->nplanes0;
   const double fpn = g->K * ((2.0 * g->P + 1.0) * (1 << g->D) * 2.0 + 2.0 * g->Q + 4.0);
   const size_t tsm = (size_t)g->K * (g->P * g->D + g->D + 2 + g->Q) * sizeof(double);
-  // deep rectangle (2D): lean fast-path kernel there, general kernel on the boundary layer
+  // deep rectangle (2D): lean fast-path kernel there (TMA-windowed tiles inside it), general
+  // kernel on the boundary-layer strips
+  const SkipRect full{0, g->L0.nI, 0, g->L0.nrows};
   const SkipRect rect = deep_rect(g, g->L0);
   const bool has_deep = rect.c1 > rect.c0 && rect.r1 > rect.r0;
-  LevelDev Ld = g->L0;
-  Ld.nI = rect.c1 - rect.c0;
-  Ld.nrows = rect.r1 - rect.r0;
   int nblk = 0;
   CUtensorMap umap;
   const bool use_tma = has_deep && g->tma_ok && ((uintptr_t)U & 15) == 0 && encode_pair_view(g, U, &umap);
   const SkipRect tiles = use_tma ? g->tma.tiles : SkipRect{0, 0, 0, 0};
-#define SRCH1(DD, PP, DP, LL)                                                                                 \
-  LAUNCH(HJB_KC_SEARCH, DP ? 0 : nodes, DP ? 0 : nodes * bpn, DP ? 0 : nodes * fpn,                          \
-         k_search<DD, PP, DP><<<dims(g, LL, (const void*)k_search<DD, PP, DP>, kSBX, tsm), dim3(kSBX, kSBY), \
-                                tsm, g->st>>>(g->L0, g->C0, dt, U, Uprev, pol, F, g->partial + 2 * nblk, rect, tiles))
-#define SRCH(DD, PP)                       \
-  do {                                     \
-    SRCH1(DD, PP, false, g->L0);           \
-    nblk += g->nblk_last;                  \
-    if (has_deep) {                        \
-      SRCH1(DD, PP, true, Ld);             \
-      nblk += g->nblk_last;                \
-    }                                      \
+  SkipRect gstrips[4], dstrips[4];
+  const int ngs = ring_strips(full, rect, gstrips);
+  const int nds = has_deep ? ring_strips(rect, tiles, dstrips) : 0;
+#define SRCH1(DD, PP, DP, RR)                                                                                 \
+  do {                                                                                                        \
+    const LevelDev LL = shape_of(g->L0, RR);                                                                  \
+    if (LL.nI > 0 && LL.nrows > 0) {                                                                          \
+      LAUNCH(HJB_KC_SEARCH, 0, 0, 0,                                                                          \
+             k_search<DD, PP, DP><<<dims(g, LL, (const void*)k_search<DD, PP, DP>, kSBX, tsm),                \
+                                    dim3(kSBX, kSBY), tsm, g->st>>>(g->L0, g->C0, dt, U, Uprev, pol, F,       \
+                                                                    g->partial + 2 * nblk, RR));             \
+      nblk += g->nblk_last;                                                                                   \
+    }                                                                                                         \
+  } while (0)
+#define SRCH(DD, PP)                                          \
+  do {                                                        \
+    for (int k = 0; k < ngs; ++k) SRCH1(DD, PP, false, gstrips[k]); \
+    for (int k = 0; k < nds; ++k) SRCH1(DD, PP, true, dstrips[k]);  \
   } while (0)
   if (g->D == 2) {
     if (g->P == 1) SRCH(2, 1);
@@ -939,6 +970,9 @@ static hjb_status policy_update_dev(hjb_grid* g, double dt, const double* U, con
 #undef SRCH
 #undef SRCH1
   CKL();
+  g->prof.nodes[HJB_KC_SEARCH] += nodes;  // algorithmic totals of the whole search (all launches)
+  g->prof.bytes[HJB_KC_SEARCH] += nodes * bpn;
+  g->prof.flops[HJB_KC_SEARCH] += nodes * fpn;
   if (use_tma) {  // deep tiles: windows staged in shared memory by TMA (partials after the others')
     if (g->P == 1)
       LAUNCH(HJB_KC_SEARCH, 0, 0, 0, k_search_tma<1><<<g->tma_grid, kWT, g->tma_smem, g->st>>>(

@@ -227,6 +227,24 @@ __device__ __forceinline__ void split_p(double o, int i, int nm2, Split& p) {
   if (p.c > nm2) { p.c = nm2; p.s = 1.0; }
 }
 
+// untruncated +-o pair in one dimension from one floor: +o -> (i + fl, o - fl); -o -> (i - fl - [s != 0],
+// 1 - s or 0).  Used by the general path's untruncated case and by the fast path alike, so the two
+// give bit-identical cells and fractions.
+__device__ __forceinline__ void pair_split(double o, int i, int& cp, double& sp, int& cm, double& sm) {
+  const double fl = floor(o);
+  const int fi = (int)fl;
+  sp = o - fl;
+  const bool frac = sp != 0.0;
+  cp = i + fi;
+  cm = i - fi - (frac ? 1 : 0);
+  sm = frac ? 1.0 - sp : 0.0;
+}
+__device__ __forceinline__ void single_split(double o, int i, int& c, double& s) {
+  const double fl = floor(o);
+  c = i + (int)fl;
+  s = o - fl;
+}
+
 // general (possibly truncated) endpoint t = i + mu o, binding coordinate snapped onto the face
 template <int D>
 __device__ __forceinline__ void cell_general(const LevelDev& L, const Node<D>& nd, const double* o, double mu,
@@ -470,10 +488,10 @@ __device__ __forceinline__ double row_geometry(const LevelDev& L, const double* 
     if (inside) {  // untruncated pair (A = B = 1); a zero step gets weight 0 (its terms cancel)
 #pragma unroll
       for (int d = 0; d < D; ++d) {
-        Split P_, M_;
-        split_pm(o[d], nd.i[d], nm2, P_, M_);
-        tp.c[d] = P_.c; tp.s[d] = P_.s;
-        tm.c[d] = M_.c; tm.s[d] = M_.s;
+        pair_split(o[d], nd.i[d], tp.c[d], tp.s[d], tm.c[d], tm.s[d]);
+        // |o| == dist: the endpoint sits on the upper face -> last cell with fraction 1
+        if (tp.c[d] > nm2) { tp.c[d] = nm2; tp.s[d] = 1.0; }
+        if (tm.c[d] > nm2) { tm.c[d] = nm2; tm.s[d] = 1.0; }
       }
       const double w = nz ? L.inv_2k2 : 0.0;
       tp.w = w;
@@ -512,9 +530,8 @@ __device__ __forceinline__ double row_geometry(const LevelDev& L, const double* 
     if (inside) {
 #pragma unroll
       for (int d = 0; d < D; ++d) {
-        Split P_;
-        split_p(o[d], nd.i[d], nm2, P_);
-        t.c[d] = P_.c; t.s[d] = P_.s;
+        single_split(o[d], nd.i[d], t.c[d], t.s[d]);
+        if (t.c[d] > nm2) { t.c[d] = nm2; t.s[d] = 1.0; }
       }
       t.w = nz ? L.inv_k2 : 0.0;
     } else {
@@ -564,14 +581,7 @@ __device__ __forceinline__ double row_geometry_fast(const LevelDev& L, const Nod
     bool nz = false;
 #pragma unroll
     for (int d = 0; d < D; ++d) {
-      const double fl = floor(o[p][d]);
-      const int fi = (int)fl;
-      const double sp = o[p][d] - fl;
-      const bool frac = sp != 0.0;
-      taps[2 * p].c[d] = nd.i[d] + fi;
-      taps[2 * p].s[d] = sp;
-      taps[2 * p + 1].c[d] = nd.i[d] - fi - (frac ? 1 : 0);
-      taps[2 * p + 1].s[d] = frac ? 1.0 - sp : 0.0;
+      pair_split(o[p][d], nd.i[d], taps[2 * p].c[d], taps[2 * p].s[d], taps[2 * p + 1].c[d], taps[2 * p + 1].s[d]);
       nz |= (o[p][d] != 0.0);
     }
     const double w = nz ? L.inv_2k2 : 0.0;
@@ -582,9 +592,7 @@ __device__ __forceinline__ double row_geometry_fast(const LevelDev& L, const Nod
   bool nz = false;
 #pragma unroll
   for (int d = 0; d < D; ++d) {
-    const double fl = floor(o[P][d]);
-    taps[2 * P].c[d] = nd.i[d] + (int)fl;
-    taps[2 * P].s[d] = o[P][d] - fl;
+    single_split(o[P][d], nd.i[d], taps[2 * P].c[d], taps[2 * P].s[d]);
     nz |= (o[P][d] != 0.0);
   }
   taps[2 * P].w = nz ? L.inv_k2 : 0.0;

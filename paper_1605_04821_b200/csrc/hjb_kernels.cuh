@@ -29,15 +29,15 @@ enum OpMode : int {
 #ifndef HJB_SEARCH_MINB
 #define HJB_SEARCH_MINB 1
 #endif
-// DEEP: only the nodes of `rect`, all of whose endpoints (every control) are strictly inside the
-// box -> the lean fast path with no truncation code; otherwise every node outside `rect`.
+// Every node of the rectangle `it` (loop coordinates).  DEEP: `it` lies in the deep rectangle (all
+// endpoints of every control strictly inside the box) -> the lean fast path, no truncation code.
 template <int D, int P, int MODE, int NDOT, bool DEEP>
 __global__ void __launch_bounds__(kTX, HJB_OP_MINB) k_operator(LevelDev L, CoefDev C, double dt, double omega,
                                                   const uint8_t* __restrict__ pol,
                                                   const double* __restrict__ x,
                                                   const double* __restrict__ b, double* __restrict__ y,
                                                   const double* __restrict__ u, double* partial,
-                                                  SkipRect rect) {
+                                                  SkipRect it) {
   constexpr bool GATHER = (MODE != OP_JACOBI0);
   constexpr bool SELF = (MODE == OP_JACOBI || MODE == OP_JACOBI0);
   constexpr int E = 2 * P + 1;
@@ -49,24 +49,22 @@ __global__ void __launch_bounds__(kTX, HJB_OP_MINB) k_operator(LevelDev L, CoefD
   const double* tbd = tab + C.K * P * D;
   const double* tcc = tbd + C.K * D;
   double dots[2] = {0.0, 0.0};
-  const int col = (DEEP ? rect.c0 : 0) + blockIdx.x * kBX + threadIdx.x;
-  const int col_end = DEEP ? rect.c1 : L.nI;
-  const int row_end = DEEP ? rect.r1 : L.nrows;
-  const bool active = col < col_end;
-  const bool col_in_rect = col >= rect.c0 && col < rect.c1;
+  const int col = it.c0 + blockIdx.x * kBX + threadIdx.x;
+  const int row_end = it.r1;
+  const bool active = col < it.c1;
 #ifdef HJB_OP_PIPE
   constexpr bool PIPE = true;   // software pipelining of the streamed per-node inputs (costs
 #else                           // registers; measured slower, profiles/r01_v3)
   constexpr bool PIPE = false;
 #endif
   NodeIn<D, P> in;
-  int row = (DEEP ? rect.r0 : 0) + blockIdx.y * kBY + threadIdx.y;
+  int row = it.r0 + blockIdx.y * kBY + threadIdx.y;
   const int rstride = gridDim.y * kBY;
   if (PIPE && active && row < row_end) fetch_node<D, P, XJ, BJ>(L, C, pol, x, b, col, row, in);
   for (; row < row_end; row += rstride) {
     NodeIn<D, P> nx;
     const int rn = row + rstride;
-    const bool go = active && (DEEP || !(col_in_rect && row >= rect.r0 && row < rect.r1));
+    const bool go = active;
     if (PIPE && active && rn < row_end) fetch_node<D, P, XJ, BJ>(L, C, pol, x, b, col, rn, nx);
     if (!PIPE && go) fetch_node<D, P, XJ, BJ>(L, C, pol, x, b, col, row, in);
     if (go) {
@@ -124,14 +122,14 @@ __global__ void __launch_bounds__(kTX, HJB_OP_MINB) k_operator(LevelDev L, CoefD
 // ================================================================== control search
 // For every owned interior node: H^a = acc_a - wsum_a U_j + c^a U_j + f^a for all a (lowest-index
 // argmin), policy/F outputs, partials: [max R, changed count].
-// DEEP: only the nodes of `skip` (every endpoint of every control strictly inside the box: the lean
-// fast path); otherwise every node outside `skip`.
+// Every node of the rectangle `it` (loop coordinates).  DEEP: `it` lies in the deep rectangle -> the
+// lean fast path.
 template <int D, int P, bool DEEP>
 __global__ void __launch_bounds__(kTX, HJB_SEARCH_MINB) k_search(LevelDev L, CoefDev C, double dt,
                                                 const double* __restrict__ U,
                                                 const double* __restrict__ Uprev,
                                                 uint8_t* __restrict__ pol, double* __restrict__ F,
-                                                double* partial, SkipRect skip, SkipRect tiles) {
+                                                double* partial, SkipRect it) {
   constexpr int E = 2 * P + 1;
   extern __shared__ double tab[];
   stage_tables<D, P, true>(C, tab);
@@ -141,12 +139,10 @@ __global__ void __launch_bounds__(kTX, HJB_SEARCH_MINB) k_search(LevelDev L, Coe
   const double* tfc = tcc + C.K;
   const double* tfb = tfc + C.K;
   double red[2] = {0.0, 0.0};
-  const int c_beg = DEEP ? skip.c0 : 0, c_end = DEEP ? skip.c1 : L.nI;
-  const int r_beg = DEEP ? skip.r0 : 0, r_end = DEEP ? skip.r1 : L.nrows;
+  const int c_beg = it.c0, c_end = it.c1;
+  const int r_beg = it.r0, r_end = it.r1;
   for (int row = r_beg + blockIdx.y * kSBY + threadIdx.y; row < r_end; row += gridDim.y * kSBY)
   for (int col = c_beg + blockIdx.x * kSBX + threadIdx.x; col < c_end; col += gridDim.x * kSBX) {
-    if (!DEEP && col >= skip.c0 && col < skip.c1 && row >= skip.r0 && row < skip.r1) continue;
-    if (DEEP && col >= tiles.c0 && col < tiles.c1 && row >= tiles.r0 && row < tiles.r1) continue;  // TMA tiles
     Node<D> nd;
     node_at<D>(L, col, row, nd);
     load_fields<D>(C, nd);

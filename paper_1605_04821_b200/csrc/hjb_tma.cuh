@@ -108,7 +108,9 @@ __global__ void __launch_bounds__(kWT, 1) k_search_tma(LevelDev L, CoefDev C, do
   const double* tcc = tbd + C.K * D;
   const double* tfc = tcc + C.K;
   const double* tfb = tfc + C.K;
-  double* boxes = sm + ((ntab + 15) & ~15);  // [2 stages][E][2 parities][slot]
+  // [2 stages][E][2 parities][slot]; TMA destinations must be 128-byte aligned and the dynamic
+  // shared window starts after the static variables, so align explicitly (+128 B in the launch)
+  double* boxes = (double*)(((uintptr_t)(sm + ntab) + 127) & ~(uintptr_t)127);
   if (tid == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&umap) : "memory");
     mbar_init(&bars[0], 1);
