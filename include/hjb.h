@@ -295,7 +295,9 @@ typedef enum {
 } hjb_kernel_class;
 
 typedef struct {
-  int64_t launches[HJB_KC_COUNT];
+  int64_t launches[HJB_KC_COUNT];   /* kernel launches (one operator application may be several:
+                                       the deep-rectangle kernel + boundary-layer strips)        */
+  int64_t calls[HJB_KC_COUNT];      /* logical applications (operator sweeps, searches, ...)      */
   double ms[HJB_KC_COUNT];
   double bytes[HJB_KC_COUNT];
   double flops[HJB_KC_COUNT];

@@ -91,13 +91,14 @@ class StepStats(C.Structure):
 
 
 class Profile(C.Structure):
-    _fields_ = [("launches", C.c_int64 * HJB_KC_COUNT), ("ms", C.c_double * HJB_KC_COUNT),
+    _fields_ = [("launches", C.c_int64 * HJB_KC_COUNT), ("calls", C.c_int64 * HJB_KC_COUNT),
+                ("ms", C.c_double * HJB_KC_COUNT),
                 ("bytes", C.c_double * HJB_KC_COUNT), ("flops", C.c_double * HJB_KC_COUNT),
                 ("nodes", C.c_double * HJB_KC_COUNT), ("total_launches", C.c_int64),
                 ("timed", C.c_int32)]
 
     def as_dict(self):
-        per = {k: dict(launches=self.launches[i], ms=self.ms[i], bytes=self.bytes[i],
+        per = {k: dict(launches=self.launches[i], calls=self.calls[i], ms=self.ms[i], bytes=self.bytes[i],
                        flops=self.flops[i], nodes=self.nodes[i])
                for i, k in enumerate(KERNEL_CLASSES)}
         return dict(classes=per, total_launches=self.total_launches, timed=bool(self.timed))

@@ -420,6 +420,7 @@ static void launch_operator(hjb_grid* g, const LevelDev& L, const CoefDev& C, in
     else if (g->P == 2) OPLP(2, M, ND);                                                                     \
     else OPLP((D > 2 ? 3 : 2), M, ND);                                                                      \
   } while (0)
+  g->prof.calls[cls] += 1;
   if (mode == OP_APPLY) {
     if (ndot == 0) OPL(OP_APPLY, 0);
     else if (ndot == 1) OPL(OP_APPLY, 1);
@@ -970,6 +971,7 @@ static hjb_status policy_update_dev(hjb_grid* g, double dt, const double* U, con
 #undef SRCH
 #undef SRCH1
   CKL();
+  g->prof.calls[HJB_KC_SEARCH] += 1;
   g->prof.nodes[HJB_KC_SEARCH] += nodes;  // algorithmic totals of the whole search (all launches)
   g->prof.bytes[HJB_KC_SEARCH] += nodes * bpn;
   g->prof.flops[HJB_KC_SEARCH] += nodes * fpn;

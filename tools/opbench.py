@@ -47,7 +47,8 @@ def report(tag, reps):
     for k, v in pr["classes"].items():
         if v["launches"] and v["ms"] > 0:
             gbs = v["bytes"] / (v["ms"] / 1e3) / 1e9
-            print(f"  [{tag}] {k:9s} launches={v['launches']:5d} ms/launch={v['ms'] / v['launches']:9.4f} "
+            calls = v.get("calls") or v["launches"]
+            print(f"  [{tag}] {k:9s} calls={calls:5d} launches={v['launches']:5d} ms/call={v['ms'] / calls:9.4f} "
                   f"GB/s={gbs:8.1f} ({gbs / peaks['hbm_gbs']:.3f} of HBM) TF/s={v['flops'] / (v['ms'] / 1e3) / 1e12:7.3f}",
                   flush=True)
 
