@@ -111,8 +111,12 @@ __global__ void __launch_bounds__(kWT, 1) k_search_tma(LevelDev L, CoefDev C, do
   // [2 stages][E][2 parities][slot]; TMA destinations must be 128-byte aligned and the dynamic
   // shared window starts after the static variables, so align explicitly (+128 B in the launch)
   double* boxes = (double*)(((uintptr_t)(sm + ntab) + 127) & ~(uintptr_t)127);
+  // the descriptor must stay in the parameter space: take its address here, at kernel scope (a
+  // by-reference lambda capture of the parameter may materialise a local-memory copy, which TMA
+  // cannot use)
+  const CUtensorMap* const mp = &umap;
   if (tid == 0) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&umap) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)mp) : "memory");
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -125,7 +129,7 @@ __global__ void __launch_bounds__(kWT, 1) k_search_tma(LevelDev L, CoefDev C, do
   double red[2] = {0.0, 0.0};
 
   // thread 0: load the 2(2P+1) boxes of control a for the tile at (ix0, iy0) into stage st
-  auto issue = [&](int a, int st, int ix0, int iy0) {
+  auto issue = [&, mp](int a, int st, int ix0, int iy0) {
     if (tid != 0) return;
     const double* sd = tsd + a * P * D;
     const double* bd = tbd + a * D;
@@ -141,8 +145,8 @@ __global__ void __launch_bounds__(kWT, 1) k_search_tma(LevelDev L, CoefDev C, do
       org[st][e][1] = ye;
       org[st][e][2] = yo;
       double* b0 = boxes + (size_t)((st * E + e) * 2) * W.slot;
-      tma_load_2d(b0, &umap, wx0, ye, &bars[st]);
-      tma_load_2d(b0 + W.slot, &umap, n + wx0, yo, &bars[st]);
+      tma_load_2d(b0, mp, wx0, ye, &bars[st]);
+      tma_load_2d(b0 + W.slot, mp, n + wx0, yo, &bars[st]);
     }
   };
 
