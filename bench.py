@@ -242,7 +242,7 @@ def run_b200(args):
     stream = torch.cuda.current_stream(dev)
     total = args.warmup + args.steps
     # per-step inputs (problem data, generated before the timed region)
-    n_all = total + (0 if args.no_e2e else args.steps)   # the e2e steps continue the same march
+    n_all = total
     psis = [packed_psi(p, s * p.dt, device=dev) for s in range(1, n_all + 1)]
     srcs = [p.f_tables(s * p.dt) for s in range(1, n_all + 1)]
 
@@ -262,6 +262,8 @@ def run_b200(args):
         do_step(s, U, U2, pol, psis[s - 1])
         U, U2 = U2, U
     torch.cuda.synchronize()
+    # state at the start of the timed region: the e2e pass replays exactly these steps
+    snap = None if args.no_e2e else (U.cpu().pin_memory(), U2.cpu().pin_memory(), pol.cpu().pin_memory())
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
     g.profile_reset(time_kernels=not args.no_time_kernels)
@@ -332,7 +334,7 @@ def run_b200(args):
     # --------------------------------------------------------------- e2e through host buffers
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(g, p, args, U, U2, stream, srcs, psis, nI, dev, lay, bar, allmax, skw, mgkw)
+        e2e = run_e2e(g, p, args, snap, stream, srcs, psis, nI, dev, lay, bar, allmax, skw, mgkw)
 
     pis = [st["pi_iters"] for st in stats]
     kr = [st["krylov_iters_total"] for st in stats]
@@ -381,22 +383,17 @@ def traffic_for(cls, config, c):
     return e["dram_bytes_per_node"] * c["nodes"] / max(1, c["calls"] or c["launches"])
 
 
-def run_e2e(g, p, args, U_dev, U2_dev, stream, srcs, psis, nI, dev, lay, bar, allmax, skw, mgkw):
-    """The same steps through hjb_step with pinned HOST buffers: each step copies U_prev, the policy
-    and psi host->device and U + policy device->host inside the timed region (inside the call)."""
+def run_e2e(g, p, args, snap, stream, srcs, psis, nI, dev, lay, bar, allmax, skw, mgkw):
+    """The SAME K steps as the timed region (replayed from its starting state) through hjb_step with
+    pinned HOST buffers: each step copies U_prev, the policy and psi host->device and U + policy
+    device->host inside the timed region (inside the call)."""
     import torch
     N = lay["local_elems"]
-    Uh_prev = torch.empty(N, dtype=torch.float64, pin_memory=True)
-    Uh = torch.empty(N, dtype=torch.float64, pin_memory=True)
-    polh = torch.zeros(N, dtype=torch.uint8, pin_memory=True)
-    Uh_prev.copy_(U_dev.cpu())       # U^{n-1}
-    Uh.copy_(U2_dev.cpu())           # U^{n-2}: the march continues with the extrapolated guess
+    Uh_prev, Uh, polh = snap          # U^{W}, U^{W-1}, policy at the start of the timed region
     psih = [x.cpu().pin_memory() for x in psis]
     Uh_np, Uhp_np, pol_np = Uh.numpy(), Uh_prev.numpy(), polh.numpy()
     psi_np = [x.numpy() for x in psih]
-    base = args.warmup + args.steps
-    if args.steps + args.warmup < 2:
-        raise SystemExit("e2e needs two previous steps (use --no-e2e)")
+    base = args.warmup
     n_e2e = args.steps
     bar()
     torch.cuda.synchronize()
@@ -408,7 +405,8 @@ def run_e2e(g, p, args, U_dev, U2_dev, stream, srcs, psis, nI, dev, lay, bar, al
         s = base + i + 1
         fb, fc = srcs[s - 1]
         g.set_source(fb, fc)
-        g.step(p.dt, Uhp_np, Uh_np, pol_np, psi_np[s - 1], guess=_lib.HJB_GUESS_EXTRAPOLATE, mg=mgkw, **skw)
+        g.step(p.dt, Uhp_np, Uh_np, pol_np, psi_np[s - 1], mg=mgkw, **skw,
+               guess=_lib.HJB_GUESS_EXTRAPOLATE if s >= 2 else _lib.HJB_GUESS_PREV)
         Uhp_np, Uh_np = Uh_np, Uhp_np
     ev1.record(stream)
     torch.cuda.synchronize()

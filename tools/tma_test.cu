@@ -16,8 +16,9 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 template <int MODE>
-__global__ void k_tma(const __grid_constant__ CUtensorMap map, int x, int y, int bw, int bh, double* out,
-                      int* status) {
+__global__ void k_tma(const __grid_constant__ CUtensorMap map, const CUtensorMap* gmap, int x, int y, int bw,
+                      int bh, double* out, int* status) {
+  const CUtensorMap* mp = (MODE == 2) ? gmap : &map;
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) uint64_t bar;
   double* box = (double*)(((uintptr_t)sm + 127) & ~(uintptr_t)127);
@@ -29,14 +30,17 @@ __global__ void k_tma(const __grid_constant__ CUtensorMap map, int x, int y, int
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar)),
                  "r"(bw * bh * 8) : "memory");
-    if (MODE == 0)
+    if (MODE == 3)
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(smem_u32(box)), "l"((const void*)gmap), "r"(bw * bh * 8), "r"(smem_u32(&bar)) : "memory");
+    else if (MODE == 0)
       asm volatile(
           "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
-          ::"r"(smem_u32(box)), "l"((uint64_t)&map), "r"(x), "r"(y), "r"(smem_u32(&bar)) : "memory");
+          ::"r"(smem_u32(box)), "l"((uint64_t)mp), "r"(x), "r"(y), "r"(smem_u32(&bar)) : "memory");
     else
       asm volatile(
           "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
-          ::"r"(smem_u32(box)), "l"((uint64_t)&map), "r"(x), "r"(y), "r"(smem_u32(&bar)) : "memory");
+          ::"r"(smem_u32(box)), "l"((uint64_t)mp), "r"(x), "r"(y), "r"(smem_u32(&bar)) : "memory");
   }
   uint32_t done = 0;
   long long spin = 0;
@@ -52,7 +56,8 @@ __global__ void k_tma(const __grid_constant__ CUtensorMap map, int x, int y, int
     for (int e = threadIdx.x; e < bw * bh; e += blockDim.x) out[e] = box[e];
 }
 
-int main() {
+int main(int argc, char** argv) {
+  const int only = argc > 1 ? atoi(argv[1]) : -1;
   const int n = 257, rows = 257, bw = 36, bh = 7;
   std::vector<double> h((size_t)n * rows);
   for (size_t i = 0; i < h.size(); ++i) h[i] = (double)i;
@@ -75,11 +80,24 @@ int main() {
                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   printf("encode: %d (entry point query %d)\n", (int)r, (int)q);
   const int x = n + 40, y = 60;  // odd rows of pair-row 60.. : local rows 121, 123, ...
-  for (int mode = 0; mode < 2; ++mode) {
+  CUtensorMap* gmap;
+  cudaMalloc(&gmap, sizeof(CUtensorMap));
+  cudaMemcpy(gmap, &map, sizeof(CUtensorMap), cudaMemcpyHostToDevice);
+  for (int mode = 0; mode < 6; ++mode) {
+    if (only >= 0 && mode != only) continue;
     cudaMemset(st, 0, 4);
     const size_t smem = bw * bh * 8 + 128;
-    if (mode == 0) k_tma<0><<<1, 128, smem>>>(map, x, y, bw, bh, out, st);
-    else k_tma<1><<<1, 128, smem>>>(map, x, y, bw, bh, out, st);
+    CUtensorMap m2 = map;
+    if (mode >= 4) {
+      CUresult r2 = enc(&m2, mode == 4 ? CU_TENSOR_MAP_DATA_TYPE_UINT64 : CU_TENSOR_MAP_DATA_TYPE_INT64, 2, d, dims,
+                        strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      printf("encode mode %d: %d\n", mode, (int)r2);
+    }
+    if (mode == 0 || mode >= 4) k_tma<0><<<1, 128, smem>>>(m2, gmap, x, y, bw, bh, out, st);
+    else if (mode == 1) k_tma<1><<<1, 128, smem>>>(map, gmap, x, y, bw, bh, out, st);
+    else if (mode == 2) k_tma<2><<<1, 128, smem>>>(map, gmap, x, y, bw, bh, out, st);
+    else k_tma<3><<<1, 128, smem>>>(map, (const CUtensorMap*)(d + (size_t)y * 2 * n + (x & ~1)), x, y, bw, bh, out, st);
     cudaError_t e = cudaDeviceSynchronize();
     int hs = 0;
     cudaMemcpy(&hs, st, 4, cudaMemcpyDeviceToHost);
@@ -88,10 +106,13 @@ int main() {
     int bad = 0;
     for (int j = 0; j < bh && hs == 1; ++j)
       for (int i = 0; i < bw; ++i) {
-        const size_t el = (size_t)(y + j) * 2 * n + (x + i);  // element in the flat array
+        const size_t el = mode == 3 ? (size_t)y * 2 * n + (x & ~1) + j * bw + i   // 1D bulk copy
+                                    : (size_t)(y + j) * 2 * n + (x + i);          // element in the flat array
         if (o[j * bw + i] != h[el]) ++bad;
       }
-    printf("mode %d (%s): err=%s status=%d mismatches=%d\n", mode, mode == 0 ? ".tile" : "no .tile",
+    printf("mode %d (%s): err=%s status=%d mismatches=%d\n", mode,
+           mode == 0 ? ".tile, param map, F64" : mode == 1 ? "no .tile, param map" : mode == 2 ? ".tile, global map"
+           : mode == 3 ? "1D cp.async.bulk" : mode == 4 ? ".tile, UINT64 map" : ".tile, INT64 map",
            cudaGetErrorString(e), hs, bad);
   }
   return 0;
