@@ -26,6 +26,9 @@ enum OpMode : int {
 #ifndef HJB_OP_MINB
 #define HJB_OP_MINB 4   // <= 128 registers: 16 resident warps per SM (measured best, profiles/r01_v3)
 #endif
+#ifndef HJB_OP_ILP
+#define HJB_OP_ILP 1
+#endif
 #ifndef HJB_SEARCH_MINB
 #define HJB_SEARCH_MINB 1
 #endif
@@ -52,69 +55,75 @@ __global__ void __launch_bounds__(kTX, HJB_OP_MINB) k_operator(LevelDev L, CoefD
   const int col = it.c0 + blockIdx.x * kBX + threadIdx.x;
   const int row_end = it.r1;
   const bool active = col < it.c1;
-#ifdef HJB_OP_PIPE
-  constexpr bool PIPE = true;   // software pipelining of the streamed per-node inputs (costs
-#else                           // registers; measured slower, profiles/r01_v3)
-  constexpr bool PIPE = false;
-#endif
-  NodeIn<D, P> in;
-  int row = it.r0 + blockIdx.y * kBY + threadIdx.y;
+  // DEEP: ILP nodes per thread per pass (rows row, row + stride, ...): their loads and gathers are
+  // in flight together (HJB_OP_ILP, default 1)
+  constexpr int U = DEEP ? HJB_OP_ILP : 1;
   const int rstride = gridDim.y * kBY;
-  if (PIPE && active && row < row_end) fetch_node<D, P, XJ, BJ>(L, C, pol, x, b, col, row, in);
-  for (; row < row_end; row += rstride) {
-    NodeIn<D, P> nx;
-    const int rn = row + rstride;
-    const bool go = active;
-    if (PIPE && active && rn < row_end) fetch_node<D, P, XJ, BJ>(L, C, pol, x, b, col, rn, nx);
-    if (!PIPE && go) fetch_node<D, P, XJ, BJ>(L, C, pol, x, b, col, row, in);
-    if (go) {
-      Node<D> nd;
-      node_from<D, P>(L, col, row, in, nd);
-      if (GATHER) prefetch_ahead(L, x, nd.loc, col);
-      const int a = in.a;
-      Tap<D> taps[E];
-      double wsum;
+  for (int row0 = it.r0 + blockIdx.y * kBY + threadIdx.y; row0 < row_end; row0 += rstride * U) {
+    NodeIn<D, P> in[U];
+    bool ok[U];
+#pragma unroll
+    for (int v = 0; v < U; ++v) {
+      ok[v] = active && row0 + v * rstride < row_end;
+      if (ok[v]) fetch_node<D, P, XJ, BJ>(L, C, pol, x, b, col, row0 + v * rstride, in[v]);
+    }
+    Node<D> nd[U];
+    Tap<D> taps[U][E];
+    double wsum[U];
+#pragma unroll
+    for (int v = 0; v < U; ++v) {
+      if (!ok[v]) continue;
+      node_from<D, P>(L, col, row0 + v * rstride, in[v], nd[v]);
+      const int a = in[v].a;
       if (DEEP) {
         double o[P + 1][D];
-        row_offsets<D, P>(L, tsd + a * P * D, tbd + a * D, nd, o);
-        wsum = row_geometry_fast<D, P>(L, nd, o, taps);
+        row_offsets<D, P>(L, tsd + a * P * D, tbd + a * D, nd[v], o);
+        wsum[v] = row_geometry_fast<D, P>(L, nd[v], o, taps[v]);
       } else {
-        wsum = row_taps<D, P>(L, tsd + a * P * D, tbd + a * D, nd, taps);
+        wsum[v] = row_taps<D, P>(L, tsd + a * P * D, tbd + a * D, nd[v], taps[v]);
       }
+    }
+    double vals[U][E];
+    if (GATHER) {
+#pragma unroll
+      for (int v = 0; v < U; ++v)
+        if (ok[v])
+#pragma unroll
+          for (int e = 0; e < E; ++e) vals[v][e] = tap_value<D>(L, x, taps[v][e]);
+    }
+#pragma unroll
+    for (int v = 0; v < U; ++v) {
+      if (!ok[v]) continue;
       double acc = 0.0, self = 0.0;
       if (GATHER) {
-        double vals[E];
 #pragma unroll
-        for (int e = 0; e < E; ++e) vals[e] = tap_value<D>(L, x, taps[e]);
-#pragma unroll
-        for (int e = 0; e < E; ++e) acc = fma(taps[e].w, vals[e], acc);
+        for (int e = 0; e < E; ++e) acc = fma(taps[v][e].w, vals[v][e], acc);
       }
       if (SELF) {
 #pragma unroll
-        for (int e = 0; e < E; ++e) self += tap_self<D>(nd, taps[e]);
+        for (int e = 0; e < E; ++e) self += tap_self<D>(nd[v], taps[v][e]);
       }
-      const double c = nd.cn + tcc[a];
+      const double c = nd[v].cn + tcc[in[v].a];
       double out;
       if (MODE == OP_JACOBI0) {
-        const double diag = 1.0 + dt * (wsum - self - c);
-        out = omega * in.bj / diag;
+        const double diag = 1.0 + dt * (wsum[v] - self - c);
+        out = omega * in[v].bj / diag;
       } else {
-        const double xj = in.xj;
-        const double Ax = xj - dt * (acc - wsum * xj + c * xj);
+        const double xj = in[v].xj;
+        const double Ax = xj - dt * (acc - wsum[v] * xj + c * xj);
         if (MODE == OP_APPLY) {
           out = Ax;
         } else if (MODE == OP_RESID) {
-          out = in.bj - Ax;
+          out = in[v].bj - Ax;
         } else {
-          const double diag = 1.0 + dt * (wsum - self - c);
-          out = xj + omega * (in.bj - Ax) / diag;
+          const double diag = 1.0 + dt * (wsum[v] - self - c);
+          out = xj + omega * (in[v].bj - Ax) / diag;
         }
       }
-      y[nd.loc] = out;
-      if (NDOT >= 1) dots[0] = fma(out, __ldg(u + nd.loc), dots[0]);
+      y[nd[v].loc] = out;
+      if (NDOT >= 1) dots[0] = fma(out, __ldg(u + nd[v].loc), dots[0]);
       if (NDOT >= 2) dots[1] = fma(out, out, dots[1]);
     }
-    if (PIPE) in = nx;
   }
   if (NDOT > 0) block_reduce_store<2>(dots, partial);
 }

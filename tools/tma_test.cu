@@ -58,7 +58,15 @@ __global__ void k_tma(const __grid_constant__ CUtensorMap map, const CUtensorMap
 
 int main(int argc, char** argv) {
   const int only = argc > 1 ? atoi(argv[1]) : -1;
-  const int n = 257, rows = 257, bw = 36, bh = 7;
+  const int n = 257, rows = 257;
+  int bw = 36, bh = 7;
+  int dtype_f32 = 0, promo_none = 0;
+  if (only >= 6) {  // argv: mode bw bh f32 promo_none
+    bw = atoi(argv[2]);
+    bh = atoi(argv[3]);
+    dtype_f32 = atoi(argv[4]);
+    promo_none = atoi(argv[5]);
+  }
   std::vector<double> h((size_t)n * rows);
   for (size_t i = 0; i < h.size(); ++i) h[i] = (double)i;
   double *d, *out;
@@ -83,6 +91,25 @@ int main(int argc, char** argv) {
   CUtensorMap* gmap;
   cudaMalloc(&gmap, sizeof(CUtensorMap));
   cudaMemcpy(gmap, &map, sizeof(CUtensorMap), cudaMemcpyHostToDevice);
+  if (only >= 6) {
+    CUtensorMap m3;
+    const int es_b = dtype_f32 ? 4 : 8;
+    const cuuint64_t dims3[2] = {(cuuint64_t)(2 * n * 8 / es_b), (cuuint64_t)(rows / 2)};
+    const cuuint32_t box3[2] = {(cuuint32_t)bw, (cuuint32_t)bh};
+    CUresult r3 = enc(&m3, dtype_f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, d, dims3,
+                      strides, box3, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                      promo_none ? CU_TENSOR_MAP_L2_PROMOTION_NONE : CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    cudaMemset(st, 0, 4);
+    const int bytes_total = bw * bh * es_b;
+    k_tma<0><<<1, 128, bytes_total + 256>>>(m3, gmap, 8, 3, bytes_total / 8, 1, out, st);
+    cudaError_t e = cudaDeviceSynchronize();
+    int hs = 0;
+    cudaMemcpy(&hs, st, 4, cudaMemcpyDeviceToHost);
+    printf("mode %d: box {%d,%d} %s promo %s encode=%d -> err=%s status=%d\n", only, bw, bh,
+           dtype_f32 ? "F32" : "F64", promo_none ? "none" : "256B", (int)r3, cudaGetErrorString(e), hs);
+    return 0;
+  }
   for (int mode = 0; mode < 6; ++mode) {
     if (only >= 0 && mode != only) continue;
     cudaMemset(st, 0, 4);
