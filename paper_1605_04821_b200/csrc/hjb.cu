@@ -798,9 +798,7 @@ static hjb_status setup_deep(hjb_grid* g) {
   // TMA-windowed search tiles inside the deep rectangle of the fine level (single tensor map view)
   g->tma_ok = false;
 #ifndef HJB_NO_TMA
-  // opt-in (HJB_TMA=1): the TMA path still loses a transaction on the B200 (trap in mbar_wait,
-  // profiles/README.md); the deep-rectangle direct kernel is the default
-  if (getenv("HJB_TMA") && !getenv("HJB_NO_TMA")) {
+  if (!getenv("HJB_NO_TMA")) {
     double jit[2] = {0, 0};
     for (int a = 0; a < K; ++a)
       for (int e = 0; e <= P; ++e)
@@ -810,7 +808,7 @@ static hjb_status setup_deep(hjb_grid* g) {
         }
     const SkipRect dr = deep_rect(g, L);
     TmaGeom T{};
-    T.bw = (kWX - 1 + (int)std::ceil(jit[0] + 2e-6) + 3 + 1) & ~1;
+    T.bw = (kWX - 1 + (int)std::ceil(jit[0] + 2e-6) + 3 + 1 + 1) & ~1;  // +1: aligned box start
     const int bwy = kWY - 1 + (int)std::ceil(jit[1] + 2e-6) + 3;
     T.bh = (bwy + 1) / 2 + 1;
     T.slot = ((T.bw * T.bh + 15) / 16) * 16;

@@ -10,7 +10,9 @@
 // Row pitch: the grid has n (odd) doubles per row, which a TMA tensor map cannot describe (global
 // strides must be multiples of 16 bytes).  The map therefore views the array as PAIRS of rows
 // ({2n, rows/2}, stride 16 n bytes): local row 2y' is x in [0, n) of pair-row y', local row 2y'+1
-// is x in [n, 2n).  Each window is two boxes, its even and its odd rows.
+// is x in [n, 2n).  Each window is two boxes, its even and its odd rows.  The first element of a
+// box must be 16-byte aligned (an odd FLOAT64 start coordinate is an illegal instruction on the
+// B200, tools/tma_test.cu), so each box starts at the even element at or just before the window.
 #pragma once
 #include <cuda.h>  // CUtensorMap (type only; the encoder is fetched through cudaGetDriverEntryPoint)
 
@@ -90,7 +92,7 @@ __global__ void __launch_bounds__(kWT, 1) k_search_tma(LevelDev L, CoefDev C, do
   constexpr int D = 2, E = 2 * P + 1;
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) uint64_t bars[2];
-  __shared__ int org[2][E][3];  // wx0, first even pair-row, first odd pair-row
+  __shared__ int org[2][E][4];  // x origin (cells) of the even / odd box, first even / odd pair-row
   __shared__ double rng[2 * P + 2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // control tables (stage_tables<SRC> layout): sigma_dir | b_dir | c_ctrl | f_ctrl | f_basis
@@ -141,12 +143,14 @@ __global__ void __launch_bounds__(kWT, 1) k_search_tma(LevelDev L, CoefDev C, do
       win_origin<P>(L, sd, bd, e, rng, ix0, iy0, wx0, wy0);
       const int r0 = wy0 - lr0;
       const int ye = (r0 + 1) >> 1, yo = r0 >> 1;
-      org[st][e][0] = wx0;
-      org[st][e][1] = ye;
-      org[st][e][2] = yo;
+      const int xe = wx0 - (wx0 & 1), xo = wx0 - ((n + wx0) & 1);  // 16-byte aligned box starts
+      org[st][e][0] = xe;
+      org[st][e][1] = xo;
+      org[st][e][2] = ye;
+      org[st][e][3] = yo;
       double* b0 = boxes + (size_t)((st * E + e) * 2) * W.slot;
-      tma_load_2d(b0, mp, wx0, ye, &bars[st]);
-      tma_load_2d(b0 + W.slot, mp, n + wx0, yo, &bars[st]);
+      tma_load_2d(b0, mp, xe, ye, &bars[st]);
+      tma_load_2d(b0 + W.slot, mp, n + xo, yo, &bars[st]);
     }
   };
 
@@ -178,13 +182,12 @@ __global__ void __launch_bounds__(kWT, 1) k_search_tma(LevelDev L, CoefDev C, do
       double acc = 0.0;
 #pragma unroll
       for (int e = 0; e < E; ++e) {
-        const int wx0 = org[st][e][0];
         const int r = taps[e].c[1] - lr0;        // local row of the cell's lower edge
         const int q = r & 1, yq = r >> 1;        // its parity box and pair-row
         const int r1 = r + 1, q1 = r1 & 1, y1 = r1 >> 1;
         const double* bx = boxes + (size_t)((st * E + e) * 2) * W.slot;
-        const double* p0 = bx + q * W.slot + (yq - org[st][e][1 + q]) * W.bw + (taps[e].c[0] - wx0);
-        const double* p1 = bx + q1 * W.slot + (y1 - org[st][e][1 + q1]) * W.bw + (taps[e].c[0] - wx0);
+        const double* p0 = bx + q * W.slot + (yq - org[st][e][2 + q]) * W.bw + (taps[e].c[0] - org[st][e][q]);
+        const double* p1 = bx + q1 * W.slot + (y1 - org[st][e][2 + q1]) * W.bw + (taps[e].c[0] - org[st][e][q1]);
         const double v00 = p0[0], v10 = p0[1], v01 = p1[0], v11 = p1[1];
         const double aa = fma(taps[e].s[0], v10 - v00, v00);
         const double bb = fma(taps[e].s[0], v11 - v01, v01);

@@ -267,7 +267,7 @@ def test_deep_kernels_match_general(name, mk, monkeypatch):
     U = Uprev + 0.05 * rng.uniform(-1, 1, size=p.N)
     x = random_vector(p)
     out = {}
-    for mode in ("general", "deep"):
+    for mode in ("general", "deep", "deep_tma"):
         monkeypatch.delenv("HJB_NO_DEEP", raising=False)
         monkeypatch.delenv("HJB_NO_TMA", raising=False)
         if mode == "general":
@@ -283,7 +283,7 @@ def test_deep_kernels_match_general(name, mk, monkeypatch):
         torch.cuda.synchronize()
         out[mode] = (pol.cpu().numpy(), F.cpu().numpy(), st, y.cpu().numpy())
         g.close()
-    for m in ("deep",):
+    for m in ("deep", "deep_tma"):
         assert np.array_equal(out["general"][0], out[m][0]), m
         assert np.array_equal(out["general"][1], out[m][1]), m
         assert out["general"][2] == out[m][2], m

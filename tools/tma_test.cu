@@ -102,11 +102,12 @@ int main(int argc, char** argv) {
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     cudaMemset(st, 0, 4);
     const int bytes_total = bw * bh * es_b;
-    k_tma<0><<<1, 128, bytes_total + 256>>>(m3, gmap, 8, 3, bytes_total / 8, 1, out, st);
+    const int cx = argc > 6 ? atoi(argv[6]) : 8, cy = argc > 7 ? atoi(argv[7]) : 3;
+    k_tma<0><<<1, 128, bytes_total + 256>>>(m3, gmap, cx, cy, bytes_total / 8, 1, out, st);
     cudaError_t e = cudaDeviceSynchronize();
     int hs = 0;
     cudaMemcpy(&hs, st, 4, cudaMemcpyDeviceToHost);
-    printf("mode %d: box {%d,%d} %s promo %s encode=%d -> err=%s status=%d\n", only, bw, bh,
+    printf("mode %d: box {%d,%d} at (%d,%d) %s promo %s encode=%d -> err=%s status=%d\n", only, bw, bh, cx, cy,
            dtype_f32 ? "F32" : "F64", promo_none ? "none" : "256B", (int)r3, cudaGetErrorString(e), hs);
     return 0;
   }
