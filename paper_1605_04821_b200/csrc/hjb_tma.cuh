@@ -82,8 +82,11 @@ __device__ __forceinline__ void win_origin(const LevelDev& L, const double* sd, 
   wy0 = iy0 + (int)floor(lo[1]);
 }
 
+#ifndef HJB_TMA_MINB
+#define HJB_TMA_MINB 1
+#endif
 template <int P>
-__global__ void __launch_bounds__(kWT, 1) k_search_tma(LevelDev L, CoefDev C, double dt,
+__global__ void __launch_bounds__(kWT, HJB_TMA_MINB) k_search_tma(LevelDev L, CoefDev C, double dt,
                                                        const double* __restrict__ U,
                                                        const double* __restrict__ Uprev,
                                                        uint8_t* __restrict__ pol, double* __restrict__ F,

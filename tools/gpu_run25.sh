@@ -1,0 +1,9 @@
+#!/bin/bash
+cd "$GRAFT_REPO_ROOT" || cd /root/repo
+O=gpurun_out; mkdir -p $O
+for v in tma1 tma2; do
+  for c in 4 2; do
+    echo "=== $v cfg$c" >> $O/opbench25.log
+    HJB_LIB=build_variants/$v.so timeout 300 python tools/opbench.py --cfg $c --reps 10 --only search >> $O/opbench25.log 2>&1
+  done
+done
