@@ -798,7 +798,8 @@ static hjb_status setup_deep(hjb_grid* g) {
   // TMA-windowed search tiles inside the deep rectangle of the fine level (single tensor map view)
   g->tma_ok = false;
 #ifndef HJB_NO_TMA
-  if (!getenv("HJB_NO_TMA")) {
+  // opt-in (HJB_TMA=1): measured slower than the direct deep kernel at cfg2/cfg4
+  if (getenv("HJB_TMA") && !getenv("HJB_NO_TMA")) {
     double jit[2] = {0, 0};
     for (int a = 0; a < K; ++a)
       for (int e = 0; e <= P; ++e)

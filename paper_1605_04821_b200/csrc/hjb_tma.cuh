@@ -83,7 +83,7 @@ __device__ __forceinline__ void win_origin(const LevelDev& L, const double* sd, 
 }
 
 #ifndef HJB_TMA_MINB
-#define HJB_TMA_MINB 1
+#define HJB_TMA_MINB 2   // <= 128 registers: two CTAs per SM overlap each other's TMA waits
 #endif
 template <int P>
 __global__ void __launch_bounds__(kWT, HJB_TMA_MINB) k_search_tma(LevelDev L, CoefDev C, double dt,

@@ -270,10 +270,13 @@ def test_deep_kernels_match_general(name, mk, monkeypatch):
     for mode in ("general", "deep", "deep_tma"):
         monkeypatch.delenv("HJB_NO_DEEP", raising=False)
         monkeypatch.delenv("HJB_NO_TMA", raising=False)
+        monkeypatch.delenv("HJB_TMA", raising=False)
         if mode == "general":
             monkeypatch.setenv("HJB_NO_DEEP", "1")
         elif mode == "deep":
             monkeypatch.setenv("HJB_NO_TMA", "1")
+        else:
+            monkeypatch.setenv("HJB_TMA", "1")
         g, _ = setup(p)
         pol = torch.zeros(p.N, dtype=torch.uint8, device="cuda")
         F = torch.zeros(p.N, dtype=torch.float64, device="cuda")
