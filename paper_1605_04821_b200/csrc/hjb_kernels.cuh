@@ -34,8 +34,11 @@ enum OpMode : int {
 #endif
 // Every node of the rectangle `it` (loop coordinates).  DEEP: `it` lies in the deep rectangle (all
 // endpoints of every control strictly inside the box) -> the lean fast path, no truncation code.
+#ifndef HJB_OP_DEEP_MINB
+#define HJB_OP_DEEP_MINB HJB_OP_MINB
+#endif
 template <int D, int P, int MODE, int NDOT, bool DEEP>
-__global__ void __launch_bounds__(kTX, HJB_OP_MINB) k_operator(LevelDev L, CoefDev C, double dt, double omega,
+__global__ void __launch_bounds__(kTX, DEEP ? HJB_OP_DEEP_MINB : HJB_OP_MINB) k_operator(LevelDev L, CoefDev C, double dt, double omega,
                                                   const uint8_t* __restrict__ pol,
                                                   const double* __restrict__ x,
                                                   const double* __restrict__ b, double* __restrict__ y,

@@ -7,7 +7,7 @@ the library's own launch shapes), on SAMPLED outputs the oracle computes one by 
   * one full implicit step (hjb_step with bench.py's solver settings): the oracle's nonlinear
     residual R_j(U_gpu) at sampled rows is at the solver tolerance -- by D6 this bounds
     |U_gpu - U*| (a property that holds at any size).
-cfg2 (2049^2, K = 64) and cfg4 (16385^2, K = 32, 2.7e8 unknowns).
+cfg2 (2049^2, K = 64), cfg3 (129^3, K = 96, trilinear) and cfg4 (16385^2, K = 32, 2.7e8 unknowns).
 """
 import numpy as np
 import pytest
@@ -34,7 +34,7 @@ def _sample_interior(p, m, seed=5):
     return np.unique(idx.astype(np.int64))
 
 
-@pytest.mark.parametrize("cfg", [2, 4])
+@pytest.mark.parametrize("cfg", [2, 3, 4])
 def test_fullsize_apply_sampled(cfg):
     torch = require_gpu()
     from synth.device import grid_for
@@ -66,7 +66,7 @@ def test_fullsize_apply_sampled(cfg):
     assert err.max() <= tol, (err.max(), tol)
 
 
-@pytest.mark.parametrize("cfg", [2, 4])
+@pytest.mark.parametrize("cfg", [2, 3, 4])
 def test_fullsize_search_and_step_sampled(cfg):
     torch = require_gpu()
     from synth.device import grid_for, initial_values, packed_psi
