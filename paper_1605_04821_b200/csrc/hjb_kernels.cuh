@@ -35,7 +35,7 @@ enum OpMode : int {
 // Every node of the rectangle `it` (loop coordinates).  DEEP: `it` lies in the deep rectangle (all
 // endpoints of every control strictly inside the box) -> the lean fast path, no truncation code.
 #ifndef HJB_OP_DEEP_MINB
-#define HJB_OP_DEEP_MINB HJB_OP_MINB
+#define HJB_OP_DEEP_MINB 6  // lean deep kernels fit 80 registers: 24 resident warps (cfg4 sweep -17 %)
 #endif
 template <int D, int P, int MODE, int NDOT, bool DEEP>
 __global__ void __launch_bounds__(kTX, DEEP ? HJB_OP_DEEP_MINB : HJB_OP_MINB) k_operator(LevelDev L, CoefDev C, double dt, double omega,
@@ -136,8 +136,11 @@ __global__ void __launch_bounds__(kTX, DEEP ? HJB_OP_DEEP_MINB : HJB_OP_MINB) k_
 // argmin), policy/F outputs, partials: [max R, changed count].
 // Every node of the rectangle `it` (loop coordinates).  DEEP: `it` lies in the deep rectangle -> the
 // lean fast path.
+#ifndef HJB_SEARCH_DEEP_MINB
+#define HJB_SEARCH_DEEP_MINB HJB_SEARCH_MINB
+#endif
 template <int D, int P, bool DEEP>
-__global__ void __launch_bounds__(kTX, HJB_SEARCH_MINB) k_search(LevelDev L, CoefDev C, double dt,
+__global__ void __launch_bounds__(kTX, DEEP ? HJB_SEARCH_DEEP_MINB : HJB_SEARCH_MINB) k_search(LevelDev L, CoefDev C, double dt,
                                                 const double* __restrict__ U,
                                                 const double* __restrict__ Uprev,
                                                 uint8_t* __restrict__ pol, double* __restrict__ F,
