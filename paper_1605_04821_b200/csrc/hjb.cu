@@ -127,7 +127,7 @@ struct hjb_grid {
   TmaGeom tma{};
   size_t tma_smem = 0;
   int tma_grid = 0;
-  double rdiff_ax[2] = {0, 0}, rdrift_ax[2] = {0, 0};
+  double rdiff_ax[3] = {0, 0, 0}, rdrift_ax[3] = {0, 0, 0};
   double* rng_part = nullptr; // k_field_ranges block partials
 };
 
@@ -337,42 +337,59 @@ static int prefetch_rows(hjb_grid* g, const LevelDev& L) {
 #endif
 }
 
-// rectangle (loop coordinates) of level L whose nodes have every endpoint of every control strictly
-// inside the box (2D only; empty when unknown, e.g. with per-node sigma/b offset fields)
+// every owned interior node of level L as a box
+static SkipRect full_box(hjb_grid* g, const LevelDev& L) {
+  if (g->D == 2) return SkipRect{0, L.nI, 0, L.nrows, 0, 1};
+  return SkipRect{0, L.nI, 0, L.nrows / L.nI, 0, L.nI};
+}
+
+// box (loop coordinates) of level L whose nodes have every endpoint of every control strictly
+// inside the domain (empty when unknown, e.g. with per-node sigma/b offset fields)
 static SkipRect deep_rect(hjb_grid* g, const LevelDev& L) {
-  SkipRect r{0, 0, 0, 0};
-  if (g->D != 2 || !g->reach_ok) return r;
-  const double rx = std::max(g->rdiff_ax[0] * (L.kh / g->L0.kh), g->rdrift_ax[0] * (L.k2h / g->L0.k2h));
-  const double ry = std::max(g->rdiff_ax[1] * (L.kh / g->L0.kh), g->rdrift_ax[1] * (L.k2h / g->L0.k2h));
-  const int n = L.n;
-  const int mx = (int)std::floor(rx + 1e-6) + 1, my = (int)std::floor(ry + 1e-6) + 1;
-  const int c0 = mx - 1, c1 = n - 1 - mx;  // col = i0 - 1, i0 in [mx, n-1-mx]
-  const int i1lo = std::max<int>(my, (int)L.row_first), i1hi = std::min<int>(n - 1 - my, (int)L.row_first + L.nrows - 1);
-  if (c1 <= c0 || i1hi < i1lo) return r;
-  r = SkipRect{c0, c1, i1lo - (int)L.row_first, i1hi + 1 - (int)L.row_first};
+  SkipRect r{0, 0, 0, 0, 0, 0};
+  if (!g->reach_ok) return r;
+  const int D = g->D, n = L.n;
+  int m[3];
+  for (int d = 0; d < D; ++d) {
+    const double rr = std::max(g->rdiff_ax[d] * (L.kh / g->L0.kh), g->rdrift_ax[d] * (L.k2h / g->L0.k2h));
+    m[d] = (int)std::floor(rr + 1e-6) + 1;  // i in [m, n-1-m]
+  }
+  const int c0 = m[0] - 1, c1 = n - 1 - m[0];
+  const int slow = D - 1;
+  const int planes = (D == 2) ? L.nrows : L.nrows / L.nI;
+  const int zlo = std::max<int>(m[slow], (int)L.row_first), zhi = std::min<int>(n - 1 - m[slow], (int)L.row_first + planes - 1);
+  if (c1 <= c0 || zhi < zlo) return r;
+  r = SkipRect{c0, c1, zlo - (int)L.row_first, zhi + 1 - (int)L.row_first, 0, 1};
+  if (D == 3) {
+    r.y0 = m[1] - 1;
+    r.y1 = n - 1 - m[1];
+    if (r.y1 <= r.y0) return SkipRect{0, 0, 0, 0, 0, 0};
+  }
   return r;
 }
 
-// `outer` minus `inner` as up to 4 rectangles (top/bottom full width, left/right beside inner), so
-// each piece gets its own launch shape (a thin strip launched over the whole grid would leave the
-// work to a handful of CTAs)
-static int ring_strips(const SkipRect& outer, const SkipRect& inner, SkipRect* out) {
+// `outer` minus `inner` as up to 6 boxes (slowest axis slabs, then y slabs, then x slabs), so each
+// piece gets its own launch shape (a thin strip launched over the whole grid would leave the work
+// to a handful of CTAs)
+static int ring_strips(const SkipRect& o, const SkipRect& in, SkipRect* out) {
   int k = 0;
-  const bool empty = inner.c1 <= inner.c0 || inner.r1 <= inner.r0;
+  const bool empty = in.c1 <= in.c0 || in.r1 <= in.r0 || in.y1 <= in.y0;
   if (empty) {
-    out[k++] = outer;
+    out[k++] = o;
     return k;
   }
-  if (inner.r0 > outer.r0) out[k++] = SkipRect{outer.c0, outer.c1, outer.r0, inner.r0};
-  if (outer.r1 > inner.r1) out[k++] = SkipRect{outer.c0, outer.c1, inner.r1, outer.r1};
-  if (inner.c0 > outer.c0) out[k++] = SkipRect{outer.c0, inner.c0, inner.r0, inner.r1};
-  if (outer.c1 > inner.c1) out[k++] = SkipRect{inner.c1, outer.c1, inner.r0, inner.r1};
+  if (in.r0 > o.r0) out[k++] = SkipRect{o.c0, o.c1, o.r0, in.r0, o.y0, o.y1};
+  if (o.r1 > in.r1) out[k++] = SkipRect{o.c0, o.c1, in.r1, o.r1, o.y0, o.y1};
+  if (in.y0 > o.y0) out[k++] = SkipRect{o.c0, o.c1, in.r0, in.r1, o.y0, in.y0};
+  if (o.y1 > in.y1) out[k++] = SkipRect{o.c0, o.c1, in.r0, in.r1, in.y1, o.y1};
+  if (in.c0 > o.c0) out[k++] = SkipRect{o.c0, in.c0, in.r0, in.r1, in.y0, in.y1};
+  if (o.c1 > in.c1) out[k++] = SkipRect{in.c1, o.c1, in.r0, in.r1, in.y0, in.y1};
   return k;
 }
 static LevelDev shape_of(const LevelDev& L, const SkipRect& r) {
   LevelDev S = L;
   S.nI = r.c1 - r.c0;
-  S.nrows = r.r1 - r.r0;
+  S.nrows = (r.r1 - r.r0) * (r.y1 - r.y0);
   return S;
 }
 
@@ -391,11 +408,11 @@ static void launch_operator(hjb_grid* g, const LevelDev& L, const CoefDev& C, in
   const size_t tsm = (size_t)g->K * (g->P * D + D + 1) * sizeof(double);  // control tables in smem
   // the deep rectangle of this level (2D): lean fast-path kernel there, general kernel on the
   // boundary-layer strips around it (small levels: one general launch)
-  const SkipRect full{0, L.nI, 0, L.nrows};
+  const SkipRect full = full_box(g, L);
   SkipRect rect = deep_rect(g, L);
   if ((int64_t)L.nI * L.nrows < (1 << 16)) rect = SkipRect{0, 0, 0, 0};
   const bool has_deep = rect.c1 > rect.c0 && rect.r1 > rect.r0;
-  SkipRect strips[4];
+  SkipRect strips[6];
   const int ns = ring_strips(full, rect, strips);
 #define OPL1(PP, M, ND, DP, RR)                                                                             \
   do {                                                                                                      \
@@ -748,22 +765,25 @@ static hjb_status setup_deep(hjb_grid* g) {
 #ifdef HJB_NO_DEEP
   return HJB_OK;
 #endif
-  if (g->D != 2 || g->C0.sigma_node || g->C0.b_node || getenv("HJB_NO_DEEP")) return HJB_OK;
-  const int P = g->P, D = 2, K = g->K;
+  if (g->C0.sigma_node || g->C0.b_node || getenv("HJB_NO_DEEP")) return HJB_OK;
+  const int P = g->P, D = g->D, K = g->K;
   const LevelDev& L = g->L0;
   if (L.nrows <= 0) return HJB_OK;
   // per-rank ranges of the scale fields
   const int nv = 2 * P + 2;
   if (!g->rng_part) TRY(dalloc((void**)&g->rng_part, (size_t)kMaxBlocks * 8 * sizeof(double)));
   if (!g->d_rng) TRY(dalloc((void**)&g->d_rng, 8 * sizeof(double)));
-  dim3 gd;
-  if (P == 1) {
-    gd = dims(g, L, (const void*)k_field_ranges<2, 1>);
-    k_field_ranges<2, 1><<<gd, dim3(kBX, kBY), 0, g->st>>>(L, g->C0, g->rng_part);
+#define FRNG(DD, PP) \
+  k_field_ranges<DD, PP><<<dims(g, L, (const void*)k_field_ranges<DD, PP>), dim3(kBX, kBY), 0, g->st>>>(L, g->C0, g->rng_part)
+  if (D == 2) {
+    if (P == 1) FRNG(2, 1);
+    else FRNG(2, 2);
   } else {
-    gd = dims(g, L, (const void*)k_field_ranges<2, 2>);
-    k_field_ranges<2, 2><<<gd, dim3(kBX, kBY), 0, g->st>>>(L, g->C0, g->rng_part);
+    if (P == 1) FRNG(3, 1);
+    else if (P == 2) FRNG(3, 2);
+    else FRNG(3, 3);
   }
+#undef FRNG
   CKL();
   const int nb = g->nblk_last;
   std::vector<double> part((size_t)nb * nv);
@@ -783,7 +803,7 @@ static hjb_status setup_deep(hjb_grid* g) {
   CK(cudaStreamSynchronize(g->st));
   // reach per axis over all controls / endpoints (diffusion and drift separately: they scale
   // differently across multigrid levels)
-  g->rdiff_ax[0] = g->rdiff_ax[1] = g->rdrift_ax[0] = g->rdrift_ax[1] = 0.0;
+  for (int d = 0; d < 3; ++d) g->rdiff_ax[d] = g->rdrift_ax[d] = 0.0;
   for (int a = 0; a < K; ++a)
     for (int e = 0; e <= P; ++e)
       for (int d = 0; d < D; ++d) {
@@ -799,7 +819,7 @@ static hjb_status setup_deep(hjb_grid* g) {
   g->tma_ok = false;
 #ifndef HJB_NO_TMA
   // opt-in (HJB_TMA=1): measured slower than the direct deep kernel at cfg2/cfg4
-  if (getenv("HJB_TMA") && !getenv("HJB_NO_TMA")) {
+  if (D == 2 && getenv("HJB_TMA") && !getenv("HJB_NO_TMA")) {
     double jit[2] = {0, 0};
     for (int a = 0; a < K; ++a)
       for (int e = 0; e <= P; ++e)
@@ -935,14 +955,14 @@ static hjb_status policy_update_dev(hjb_grid* g, double dt, const double* U, con
   const size_t tsm = (size_t)g->K * (g->P * g->D + g->D + 2 + g->Q) * sizeof(double);
   // deep rectangle (2D): lean fast-path kernel there (TMA-windowed tiles inside it), general
   // kernel on the boundary-layer strips
-  const SkipRect full{0, g->L0.nI, 0, g->L0.nrows};
+  const SkipRect full = full_box(g, g->L0);
   const SkipRect rect = deep_rect(g, g->L0);
   const bool has_deep = rect.c1 > rect.c0 && rect.r1 > rect.r0;
   int nblk = 0;
   CUtensorMap umap;
   const bool use_tma = has_deep && g->tma_ok && ((uintptr_t)U & 15) == 0 && encode_pair_view(g, U, &umap);
   const SkipRect tiles = use_tma ? g->tma.tiles : SkipRect{0, 0, 0, 0};
-  SkipRect gstrips[4], dstrips[4];
+  SkipRect gstrips[6], dstrips[6];
   const int ngs = ring_strips(full, rect, gstrips);
   const int nds = has_deep ? ring_strips(rect, tiles, dstrips) : 0;
 #define SRCH1(DD, PP, DP, RR)                                                                                 \

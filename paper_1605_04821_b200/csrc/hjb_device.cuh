@@ -189,10 +189,22 @@ __device__ __forceinline__ void node_from(const LevelDev& L, int col, int row, c
 // ----------------------------------------------------------------------------- cells
 // floor split of t = i + o for an UNTRUNCATED offset: c = i + floor(o), s = o - floor(o), via
 // round-to-nearest by the 1.5*2^52 magic constant (no fp64<->int conversion instructions).
-// rectangle of (col, row) loop coordinates handled by another kernel
+// box of nodes in loop coordinates: col = i0 - 1 in [c0, c1); slab rows (2D: i1 - row_first, 3D:
+// planes i2 - row_first) in [r0, r1); 3D only: y = i1 - 1 in [y0, y1) (2D: y0 = 0, y1 = 1).  Its
+// k-th line is  row = (y0 + k % ny) + Y (r0 + k / ny),  ny = y1 - y0, Y = nI (3D) or 1 (2D).
 struct SkipRect {
   int c0, c1, r0, r1;
+  int y0 = 0, y1 = 1;
 };
+
+template <int D>
+__device__ __forceinline__ int box_row(const LevelDev& L, const SkipRect& b, int k) {
+  const int ny = b.y1 - b.y0;
+  if (D == 2 || ny == 1) return (D == 3 ? b.y0 : 0) + (D == 3 ? L.nI : 1) * (b.r0 + k);
+  const int z = k / ny;
+  return b.y0 + (k - z * ny) + L.nI * (b.r0 + z);
+}
+__device__ __forceinline__ int box_lines(const SkipRect& b) { return (b.r1 - b.r0) * (b.y1 - b.y0); }
 
 struct Split {
   int c;

@@ -56,19 +56,21 @@ __global__ void __launch_bounds__(kTX, DEEP ? HJB_OP_DEEP_MINB : HJB_OP_MINB) k_
   const double* tcc = tbd + C.K * D;
   double dots[2] = {0.0, 0.0};
   const int col = it.c0 + blockIdx.x * kBX + threadIdx.x;
-  const int row_end = it.r1;
+  const int nk = box_lines(it);
   const bool active = col < it.c1;
   // DEEP: ILP nodes per thread per pass (rows row, row + stride, ...): their loads and gathers are
   // in flight together (HJB_OP_ILP, default 1)
   constexpr int U = DEEP ? HJB_OP_ILP : 1;
   const int rstride = gridDim.y * kBY;
-  for (int row0 = it.r0 + blockIdx.y * kBY + threadIdx.y; row0 < row_end; row0 += rstride * U) {
+  for (int k0 = blockIdx.y * kBY + threadIdx.y; k0 < nk; k0 += rstride * U) {
     NodeIn<D, P> in[U];
     bool ok[U];
+    int rows[U];
 #pragma unroll
     for (int v = 0; v < U; ++v) {
-      ok[v] = active && row0 + v * rstride < row_end;
-      if (ok[v]) fetch_node<D, P, XJ, BJ>(L, C, pol, x, b, col, row0 + v * rstride, in[v]);
+      ok[v] = active && k0 + v * rstride < nk;
+      rows[v] = ok[v] ? box_row<D>(L, it, k0 + v * rstride) : 0;
+      if (ok[v]) fetch_node<D, P, XJ, BJ>(L, C, pol, x, b, col, rows[v], in[v]);
     }
     Node<D> nd[U];
     Tap<D> taps[U][E];
@@ -76,7 +78,7 @@ __global__ void __launch_bounds__(kTX, DEEP ? HJB_OP_DEEP_MINB : HJB_OP_MINB) k_
 #pragma unroll
     for (int v = 0; v < U; ++v) {
       if (!ok[v]) continue;
-      node_from<D, P>(L, col, row0 + v * rstride, in[v], nd[v]);
+      node_from<D, P>(L, col, rows[v], in[v], nd[v]);
       const int a = in[v].a;
       if (DEEP) {
         double o[P + 1][D];
@@ -154,10 +156,10 @@ __global__ void __launch_bounds__(kTX, DEEP ? HJB_SEARCH_DEEP_MINB : HJB_SEARCH_
   const double* tfc = tcc + C.K;
   const double* tfb = tfc + C.K;
   double red[2] = {0.0, 0.0};
-  const int c_beg = it.c0, c_end = it.c1;
-  const int r_beg = it.r0, r_end = it.r1;
-  for (int row = r_beg + blockIdx.y * kSBY + threadIdx.y; row < r_end; row += gridDim.y * kSBY)
-  for (int col = c_beg + blockIdx.x * kSBX + threadIdx.x; col < c_end; col += gridDim.x * kSBX) {
+  const int nk = box_lines(it);
+  for (int k = blockIdx.y * kSBY + threadIdx.y; k < nk; k += gridDim.y * kSBY)
+  for (int col = it.c0 + blockIdx.x * kSBX + threadIdx.x; col < it.c1; col += gridDim.x * kSBX) {
+    const int row = box_row<D>(L, it, k);
     Node<D> nd;
     node_at<D>(L, col, row, nd);
     load_fields<D>(C, nd);

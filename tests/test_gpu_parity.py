@@ -255,7 +255,8 @@ def test_edge_cases():
 
 
 @pytest.mark.parametrize("name,mk", [("cfg1", lambda: bj_config(1)), ("cfg2_513", lambda: bj_config(2, n=513)),
-                                     ("cfg0_K7", lambda: bj_config(0, n=65, K=7))])
+                                     ("cfg0_K7", lambda: bj_config(0, n=65, K=7)),
+                                     ("cfg3_33", lambda: bj_config(3, n=33))])
 def test_deep_kernels_match_general(name, mk, monkeypatch):
     """The lean deep-rectangle kernels (no truncation code) and the TMA-windowed search tiles give
     bit-identical search results and operator applications to the general kernels everywhere
