@@ -38,7 +38,7 @@ enum OpMode : int {
 #define HJB_OP_DEEP_MINB 6  // lean deep kernels fit 80 registers: 24 resident warps (cfg4 sweep -17 %)
 #endif
 template <int D, int P, int MODE, int NDOT, bool DEEP>
-__global__ void __launch_bounds__(kTX, DEEP ? HJB_OP_DEEP_MINB : HJB_OP_MINB) k_operator(LevelDev L, CoefDev C, double dt, double omega,
+__global__ void __launch_bounds__(kTX, (DEEP && D == 2) ? HJB_OP_DEEP_MINB : HJB_OP_MINB) k_operator(LevelDev L, CoefDev C, double dt, double omega,
                                                   const uint8_t* __restrict__ pol,
                                                   const double* __restrict__ x,
                                                   const double* __restrict__ b, double* __restrict__ y,
@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(kTX, DEEP ? HJB_OP_DEEP_MINB : HJB_OP_MINB) k_
 #define HJB_SEARCH_DEEP_MINB 4  // 128 registers, no spills: cfg4 search 178 -> 156 ms
 #endif
 template <int D, int P, bool DEEP>
-__global__ void __launch_bounds__(kTX, DEEP ? HJB_SEARCH_DEEP_MINB : HJB_SEARCH_MINB) k_search(LevelDev L, CoefDev C, double dt,
+__global__ void __launch_bounds__(kTX, DEEP ? (D == 2 ? HJB_SEARCH_DEEP_MINB : 3) : HJB_SEARCH_MINB) k_search(LevelDev L, CoefDev C, double dt,
                                                 const double* __restrict__ U,
                                                 const double* __restrict__ Uprev,
                                                 uint8_t* __restrict__ pol, double* __restrict__ F,
