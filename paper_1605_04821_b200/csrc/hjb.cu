@@ -410,7 +410,9 @@ static void launch_operator(hjb_grid* g, const LevelDev& L, const CoefDev& C, in
   // boundary-layer strips around it (small levels: one general launch)
   const SkipRect full = full_box(g, L);
   SkipRect rect = deep_rect(g, L);
-  if ((int64_t)L.nI * L.nrows < (1 << 16)) rect = SkipRect{0, 0, 0, 0};
+  // small levels: one launch; 3D: the box + 6 slabs measured slower than one general launch
+  // (cfg3 step 89 -> 114 ms), so the operator keeps the general kernel there
+  if ((int64_t)L.nI * L.nrows < (1 << 16) || g->D == 3) rect = SkipRect{0, 0, 0, 0, 0, 0};
   const bool has_deep = rect.c1 > rect.c0 && rect.r1 > rect.r0;
   SkipRect strips[6];
   const int ns = ring_strips(full, rect, strips);
@@ -479,7 +481,7 @@ extern "C" void hjb_solve_params_default(int32_t dim, hjb_solve_params* o) {
   o->tol_pi = 1e-10;
   o->max_pi = 50;
   hjb_mg_params_default(dim, &o->mg);
-  o->pi_forcing = 0.1;
+  o->pi_forcing = 0.03;
   o->guess = HJB_GUESS_PREV;
 }
 
