@@ -58,6 +58,19 @@ struct LevelDev {
 
 // L2 prefetch of the grid line `pf_rows` slowest-axis rows ahead of node j: the leading edge of
 // the gather band, which would otherwise miss L2 (one line per 16 lanes)
+// load used for the interpolation gathers (A/B knob for the cache operator: 0 = ld.global.nc,
+// 1 = ld.global.ca, 2 = ld.global.cg)
+#ifndef HJB_GLD_MODE
+#define HJB_GLD_MODE 0
+#endif
+#if HJB_GLD_MODE == 1
+#define HJB_GLD(p) __ldca(p)
+#elif HJB_GLD_MODE == 2
+#define HJB_GLD(p) __ldcg(p)
+#else
+#define HJB_GLD(p) __ldg(p)
+#endif
+
 __device__ __forceinline__ void prefetch_ahead(const LevelDev& L, const double* v, int j, int col) {
   if (L.pf_rows <= 0 || (col & 15) != 0) return;
   const long long a = (long long)j + (long long)L.pf_rows * L.row_elems;
@@ -300,18 +313,18 @@ __device__ __forceinline__ double gather_interp(const LevelDev& L, const double*
                                                 const double* s) {
   if (D == 2) {
     const double* p = v + ((c[1] - (int)L.local_row0) * L.n + c[0]);
-    const double v00 = __ldg(p), v10 = __ldg(p + 1);
-    const double v01 = __ldg(p + L.n), v11 = __ldg(p + L.n + 1);
+    const double v00 = HJB_GLD(p), v10 = HJB_GLD(p + 1);
+    const double v01 = HJB_GLD(p + L.n), v11 = HJB_GLD(p + L.n + 1);
     const double a = fma(s[0], v10 - v00, v00);
     const double b = fma(s[0], v11 - v01, v01);
     return fma(s[1], b - a, a);
   } else {
     const int n = L.n, nn = n * n;
     const double* p = v + (((c[2] - (int)L.local_row0) * n + c[1]) * n + c[0]);
-    const double v000 = __ldg(p), v100 = __ldg(p + 1);
-    const double v010 = __ldg(p + n), v110 = __ldg(p + n + 1);
-    const double v001 = __ldg(p + nn), v101 = __ldg(p + nn + 1);
-    const double v011 = __ldg(p + nn + n), v111 = __ldg(p + nn + n + 1);
+    const double v000 = HJB_GLD(p), v100 = HJB_GLD(p + 1);
+    const double v010 = HJB_GLD(p + n), v110 = HJB_GLD(p + n + 1);
+    const double v001 = HJB_GLD(p + nn), v101 = HJB_GLD(p + nn + 1);
+    const double v011 = HJB_GLD(p + nn + n), v111 = HJB_GLD(p + nn + n + 1);
     const double a0 = fma(s[0], v100 - v000, v000);
     const double b0 = fma(s[0], v110 - v010, v010);
     const double a1 = fma(s[0], v101 - v001, v001);
@@ -457,17 +470,17 @@ template <int D>
 __device__ __forceinline__ double tap_value(const LevelDev& L, const double* __restrict__ v, const Tap<D>& t) {
   const double* p = v + tap_base<D>(L, t);
   if (D == 2) {
-    const double v00 = __ldg(p), v10 = __ldg(p + 1);
-    const double v01 = __ldg(p + L.n), v11 = __ldg(p + L.n + 1);
+    const double v00 = HJB_GLD(p), v10 = HJB_GLD(p + 1);
+    const double v01 = HJB_GLD(p + L.n), v11 = HJB_GLD(p + L.n + 1);
     const double a = fma(t.s[0], v10 - v00, v00);
     const double b = fma(t.s[0], v11 - v01, v01);
     return fma(t.s[1], b - a, a);
   } else {
     const int n = L.n, nn = n * n;
-    const double v000 = __ldg(p), v100 = __ldg(p + 1);
-    const double v010 = __ldg(p + n), v110 = __ldg(p + n + 1);
-    const double v001 = __ldg(p + nn), v101 = __ldg(p + nn + 1);
-    const double v011 = __ldg(p + nn + n), v111 = __ldg(p + nn + n + 1);
+    const double v000 = HJB_GLD(p), v100 = HJB_GLD(p + 1);
+    const double v010 = HJB_GLD(p + n), v110 = HJB_GLD(p + n + 1);
+    const double v001 = HJB_GLD(p + nn), v101 = HJB_GLD(p + nn + 1);
+    const double v011 = HJB_GLD(p + nn + n), v111 = HJB_GLD(p + nn + n + 1);
     const double a0 = fma(t.s[0], v100 - v000, v000);
     const double b0 = fma(t.s[0], v110 - v010, v010);
     const double a1 = fma(t.s[0], v101 - v001, v001);
