@@ -18,6 +18,14 @@
 #include "hjb_comm.h"
 #include "hjb_kernels.cuh"
 #include "hjb_tma.cuh"
+#include "hjb_win.cuh"
+
+#ifndef HJB_KC_A
+#define HJB_KC_A 1.0
+#endif
+#ifndef HJB_KC_B
+#define HJB_KC_B 1.0
+#endif
 
 using namespace hjb;
 
@@ -127,6 +135,10 @@ struct hjb_grid {
   TmaGeom tma{};
   size_t tma_smem = 0;
   int tma_grid = 0;
+  bool win_ok = false;        // shared-memory window search over the deep box (k_search_win)
+  WinGeom win{};
+  size_t win_smem = 0;
+  int win_grid = 0;
   double rdiff_ax[3] = {0, 0, 0}, rdrift_ax[3] = {0, 0, 0};
   double* rng_part = nullptr; // k_field_ranges block partials
 };
@@ -762,8 +774,79 @@ static bool encode_pair_view(hjb_grid* g, const double* U, CUtensorMap* map) {
 // Per-rank ranges of the per-node scale fields -> per-axis reach of every control's endpoints ->
 // the rectangle of nodes none of whose endpoints can be truncated (2D, no sigma/b offset fields).
 // deep_rect() scales it to each multigrid level; the lean kernels run there.
+// shared-memory window search (hjb_win.cuh): choose the tile of the fine level's deep box whose
+// window [tile - m, tile + m] fits in shared memory at the least staging + idle-thread cost
+static hjb_status setup_win(hjb_grid* g) {
+  const int D = g->D, P = g->P, K = g->K;
+  const LevelDev& L = g->L0;
+  const SkipRect dr = deep_rect(g, L);
+  if (dr.c1 <= dr.c0 || dr.r1 <= dr.r0 || dr.y1 <= dr.y0) return HJB_OK;
+  int m[3] = {0, 0, 0}, ex[3] = {1, 1, 1};
+  for (int d = 0; d < D; ++d) m[d] = (int)std::floor(std::max(g->rdiff_ax[d], g->rdrift_ax[d]) + 1e-6) + 1;
+  ex[0] = dr.c1 - dr.c0;
+  ex[1] = D == 2 ? dr.r1 - dr.r0 : dr.y1 - dr.y0;
+  ex[2] = D == 3 ? dr.r1 - dr.r0 : 1;
+  const int ntab = ((K * (P * D + D + 2 + g->Q) + 15) / 16) * 16;
+  const size_t limit = 200 * 1024;
+  const double loads = (double)K * (2 * P + 1) * (1 << D);  // shared-memory gathers per node
+  static const int T0[] = {32, 64, 128}, T1[] = {1, 2, 4, 8, 16, 32, 64}, T2[] = {1, 2, 3, 4, 6, 8};
+  double best = INFINITY;
+  WinGeom W{};
+  for (int t0 : T0)
+    for (int t1 : T1)
+      for (int t2 : T2) {
+        if (D == 2 && t2 != 1) continue;
+        const int t[3] = {t0, t1, t2};
+        const int nodes = t0 * t1 * t2;
+        if (nodes < kWinNT) continue;
+        int w[3], nt[3];
+        double vol = 1.0, slots = 1.0, cov = 1.0;
+        for (int d = 0; d < 3; ++d) {
+          w[d] = t[d] + 2 * m[d];
+          nt[d] = (ex[d] + t[d] - 1) / t[d];
+          vol *= w[d];
+          slots *= (double)nt[d] * t[d];
+          cov *= ex[d];
+        }
+        if ((ntab + vol) * sizeof(double) > limit) continue;
+        const double ntiles = (double)nt[0] * nt[1] * nt[2];
+        // idle threads in partial tiles, window staging (~4 gathers per staged double), and fewer
+        // tiles than SMs
+        double cost = (slots / cov) * (1.0 + 4.0 * vol / nodes / loads);
+        if (ntiles < g->sms) cost *= (double)g->sms / ntiles;
+        if (cost < best) {
+          best = cost;
+          for (int d = 0; d < 3; ++d) {
+            W.t[d] = t[d];
+            W.m[d] = m[d];
+            W.w[d] = w[d];
+            W.nt[d] = nt[d];
+          }
+          W.ntiles = nt[0] * nt[1] * nt[2];
+          W.tab = ntab;
+        }
+      }
+  if (!std::isfinite(best)) return HJB_OK;
+  const size_t smem = ((size_t)W.tab + (size_t)W.w[0] * W.w[1] * W.w[2]) * sizeof(double);
+  const void* fn = nullptr;
+  if (D == 2) fn = P == 1 ? (const void*)k_search_win<2, 1> : (const void*)k_search_win<2, 2>;
+  else fn = P == 1 ? (const void*)k_search_win<3, 1> : P == 2 ? (const void*)k_search_win<3, 2> : (const void*)k_search_win<3, 3>;
+  CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kWinNT, smem) != cudaSuccess || occ < 1) {
+    cudaGetLastError();
+    return HJB_OK;
+  }
+  g->win = W;
+  g->win_smem = smem;
+  g->win_grid = std::min(W.ntiles, std::min(occ * g->sms, kMaxBlocks));
+  g->win_ok = true;
+  return HJB_OK;
+}
+
 static hjb_status setup_deep(hjb_grid* g) {
   g->reach_ok = false;
+  g->win_ok = false;
 #ifdef HJB_NO_DEEP
   return HJB_OK;
 #endif
@@ -859,6 +942,9 @@ static hjb_status setup_deep(hjb_grid* g) {
     }
   }
 #endif
+  g->win_ok = false;
+  const char* wenv = getenv("HJB_WIN");
+  if (!(wenv && wenv[0] == '0') && !g->tma_ok) TRY(setup_win(g));
   return HJB_OK;
 }
 
@@ -966,7 +1052,8 @@ static hjb_status policy_update_dev(hjb_grid* g, double dt, const double* U, con
   const SkipRect tiles = use_tma ? g->tma.tiles : SkipRect{0, 0, 0, 0};
   SkipRect gstrips[6], dstrips[6];
   const int ngs = ring_strips(full, rect, gstrips);
-  const int nds = has_deep ? ring_strips(rect, tiles, dstrips) : 0;
+  const bool use_win = has_deep && !use_tma && g->win_ok;  // the window kernel covers the whole box
+  const int nds = (has_deep && !use_win) ? ring_strips(rect, tiles, dstrips) : 0;
 #define SRCH1(DD, PP, DP, RR)                                                                                 \
   do {                                                                                                        \
     const LevelDev LL = shape_of(g->L0, RR);                                                                  \
@@ -998,6 +1085,23 @@ static hjb_status policy_update_dev(hjb_grid* g, double dt, const double* U, con
   g->prof.nodes[HJB_KC_SEARCH] += nodes;  // algorithmic totals of the whole search (all launches)
   g->prof.bytes[HJB_KC_SEARCH] += nodes * bpn;
   g->prof.flops[HJB_KC_SEARCH] += nodes * fpn;
+  if (use_win) {  // deep box: the tile's neighbourhood of U staged in shared memory
+#define WIN(DD, PP)                                                                                        \
+  LAUNCH(HJB_KC_SEARCH, 0, 0, 0,                                                                           \
+         k_search_win<DD, PP><<<g->win_grid, kWinNT, g->win_smem, g->st>>>(g->L0, g->C0, dt, U, Uprev, pol, F, \
+                                                                         g->partial + 2 * nblk, rect, g->win))
+    if (g->D == 2) {
+      if (g->P == 1) WIN(2, 1);
+      else WIN(2, 2);
+    } else {
+      if (g->P == 1) WIN(3, 1);
+      else if (g->P == 2) WIN(3, 2);
+      else WIN(3, 3);
+    }
+#undef WIN
+    CKL();
+    nblk += g->win_grid;
+  }
   if (use_tma) {  // deep tiles: windows staged in shared memory by TMA (partials after the others')
     if (g->P == 1)
       LAUNCH(HJB_KC_SEARCH, 0, 0, 0, k_search_tma<1><<<g->tma_grid, kWT, g->tma_smem, g->st>>>(
@@ -1087,8 +1191,17 @@ static hjb_status build_levels(hjb_grid* g, const hjb_mg_params* mp) {
     const int64_t nc = (n - 1) / 2 + 1;
     Level l;
     const double hc = (g->hi - g->lo) / (double)(nc - 1);
-    const double kc = (mp->coarse_k_mode == 1) ? std::sqrt(hc) : g->k;
-    const double k2c = (mp->coarse_k_mode == 1) ? hc : g->h;
+    // SL steps on the coarse level: 0 = the fine k (and drift step h); 1 = the scheme's own rule
+    // k_l = sqrt(h_l); 2 = the fine steps, but at least HJB_KC_A / HJB_KC_B coarse cells (keeps
+    // the interpolation diffusion ~ h_l^2 / k^2 of the rediscretised operator bounded)
+    double kc = g->k, k2c = g->h;
+    if (mp->coarse_k_mode == 1) {
+      kc = std::sqrt(hc);
+      k2c = hc;
+    } else if (mp->coarse_k_mode == 2) {
+      kc = std::max(g->k, HJB_KC_A * hc);
+      k2c = std::max(g->h, HJB_KC_B * hc);
+    }
     l.L = full_level(D, nc, g->lo, g->hi, kc, k2c);
     l.replicated = (g->R > 1) && lf.replicated;
     if (g->R > 1 && !lf.replicated) {

@@ -308,23 +308,23 @@ __device__ __forceinline__ double ray_mu(const LevelDev& L, const Node<D>& nd, c
 }
 
 // ----------------------------------------------------------------------------- interpolation
-template <int D>
-__device__ __forceinline__ double gather_interp(const LevelDev& L, const double* __restrict__ v, const int* c,
-                                                const double* s) {
+// multilinear interpolation from the corner p of the tap's cell, strides sy (next x2 line) and sz
+// (next x3 plane); LDG = the load (global: the read-only path, shared memory: plain loads).  One
+// arithmetic order for every caller, so global and shared-memory gathers agree bit for bit.
+template <int D, bool SMEM>
+__device__ __forceinline__ double interp_at(const double* __restrict__ p, int sy, int sz, const double* s) {
+#define HJB_LD(q) (SMEM ? *(q) : HJB_GLD(q))
   if (D == 2) {
-    const double* p = v + ((c[1] - (int)L.local_row0) * L.n + c[0]);
-    const double v00 = HJB_GLD(p), v10 = HJB_GLD(p + 1);
-    const double v01 = HJB_GLD(p + L.n), v11 = HJB_GLD(p + L.n + 1);
+    const double v00 = HJB_LD(p), v10 = HJB_LD(p + 1);
+    const double v01 = HJB_LD(p + sy), v11 = HJB_LD(p + sy + 1);
     const double a = fma(s[0], v10 - v00, v00);
     const double b = fma(s[0], v11 - v01, v01);
     return fma(s[1], b - a, a);
   } else {
-    const int n = L.n, nn = n * n;
-    const double* p = v + (((c[2] - (int)L.local_row0) * n + c[1]) * n + c[0]);
-    const double v000 = HJB_GLD(p), v100 = HJB_GLD(p + 1);
-    const double v010 = HJB_GLD(p + n), v110 = HJB_GLD(p + n + 1);
-    const double v001 = HJB_GLD(p + nn), v101 = HJB_GLD(p + nn + 1);
-    const double v011 = HJB_GLD(p + nn + n), v111 = HJB_GLD(p + nn + n + 1);
+    const double v000 = HJB_LD(p), v100 = HJB_LD(p + 1);
+    const double v010 = HJB_LD(p + sy), v110 = HJB_LD(p + sy + 1);
+    const double v001 = HJB_LD(p + sz), v101 = HJB_LD(p + sz + 1);
+    const double v011 = HJB_LD(p + sz + sy), v111 = HJB_LD(p + sz + sy + 1);
     const double a0 = fma(s[0], v100 - v000, v000);
     const double b0 = fma(s[0], v110 - v010, v010);
     const double a1 = fma(s[0], v101 - v001, v001);
@@ -333,6 +333,15 @@ __device__ __forceinline__ double gather_interp(const LevelDev& L, const double*
     const double p1 = fma(s[1], b1 - a1, a1);
     return fma(s[2], p1 - p0, p0);
   }
+#undef HJB_LD
+}
+
+template <int D>
+__device__ __forceinline__ double gather_interp(const LevelDev& L, const double* __restrict__ v, const int* c,
+                                                const double* s) {
+  const int base = D == 2 ? (c[1] - (int)L.local_row0) * L.n + c[0]
+                          : ((c[2] - (int)L.local_row0) * L.n + c[1]) * L.n + c[0];
+  return interp_at<D, false>(v + base, L.n, L.n * L.n, s);
 }
 
 // multilinear weight of node i (multi-index) in the cell (c, s); 0 if not a vertex
@@ -468,27 +477,7 @@ __device__ __forceinline__ int tap_base(const LevelDev& L, const Tap<D>& t) {
 
 template <int D>
 __device__ __forceinline__ double tap_value(const LevelDev& L, const double* __restrict__ v, const Tap<D>& t) {
-  const double* p = v + tap_base<D>(L, t);
-  if (D == 2) {
-    const double v00 = HJB_GLD(p), v10 = HJB_GLD(p + 1);
-    const double v01 = HJB_GLD(p + L.n), v11 = HJB_GLD(p + L.n + 1);
-    const double a = fma(t.s[0], v10 - v00, v00);
-    const double b = fma(t.s[0], v11 - v01, v01);
-    return fma(t.s[1], b - a, a);
-  } else {
-    const int n = L.n, nn = n * n;
-    const double v000 = HJB_GLD(p), v100 = HJB_GLD(p + 1);
-    const double v010 = HJB_GLD(p + n), v110 = HJB_GLD(p + n + 1);
-    const double v001 = HJB_GLD(p + nn), v101 = HJB_GLD(p + nn + 1);
-    const double v011 = HJB_GLD(p + nn + n), v111 = HJB_GLD(p + nn + n + 1);
-    const double a0 = fma(t.s[0], v100 - v000, v000);
-    const double b0 = fma(t.s[0], v110 - v010, v010);
-    const double a1 = fma(t.s[0], v101 - v001, v001);
-    const double b1 = fma(t.s[0], v111 - v011, v011);
-    const double p0 = fma(t.s[1], b0 - a0, a0);
-    const double p1 = fma(t.s[1], b1 - a1, a1);
-    return fma(t.s[2], p1 - p0, p0);
-  }
+  return interp_at<D, false>(v + tap_base<D>(L, t), L.n, L.n * L.n, t.s);
 }
 
 // endpoints of control a at node nd: taps[2p] = +sigma_p, taps[2p+1] = -sigma_p, taps[2P] = drift.
@@ -670,9 +659,9 @@ __device__ __forceinline__ double warp_max(double v) {
 __device__ __forceinline__ int block_linear() { return blockIdx.y * gridDim.x + blockIdx.x; }
 
 // block-reduce NV values (sum, or max if MAXMASK bit set) and write partial[block*NV + k]
-template <int NV>
+template <int NV, int NT = kTX>
 __device__ __forceinline__ void block_reduce_store(double (&val)[NV], double* partial, unsigned maxmask = 0u) {
-  constexpr int NW = kTX / 32;
+  constexpr int NW = NT / 32;
   __shared__ double sm[NV][NW];
   const int tid = threadIdx.y * blockDim.x + threadIdx.x;
   const int lane = tid & 31, wid = tid >> 5;

@@ -25,6 +25,8 @@ ap.add_argument("--eta", type=float, default=0.03)
 ap.add_argument("--nu", type=int, default=2)
 ap.add_argument("--omega", type=float, default=None)
 ap.add_argument("--kmode", type=int, default=None)
+ap.add_argument("--no-gmres", action="store_true")
+ap.add_argument("--exact-only", action="store_true")
 args = ap.parse_args()
 
 p = bj_config(args.cfg, n=args.n)
@@ -73,7 +75,8 @@ for k in range(8):
 rates = [res[i + 1] / res[i] for i in range(len(res) - 1)]
 print("stationary V-cycle residual ratios:", " ".join(f"{q:.3f}" for q in rates), flush=True)
 
-for tol_name, tol in (("eta", max(1e-12 * fn, args.eta * r0n)), ("exact", 1e-12 * fn)):
+cases = (("eta", max(1e-12 * fn, args.eta * r0n)), ("exact", 1e-12 * fn))
+for tol_name, tol in cases[1:] if args.exact_only else cases:
     # library BiCGSTAB
     xb = U0.clone()
     torch.cuda.synchronize()
@@ -84,6 +87,8 @@ for tol_name, tol in (("eta", max(1e-12 * fn, args.eta * r0n)), ("exact", 1e-12 
     tb = time.time() - t0
     print(f"[{tol_name}] BiCGSTAB: iters={st['iters']} precond={2 * st['iters']} rres={st['rres']:.2e} "
           f"{tb * 1e3:.1f} ms", flush=True)
+    if args.no_gmres:
+        continue
     # GMRES(m), right preconditioned, classical Gram-Schmidt with one re-orthogonalisation
     torch.cuda.synchronize()
     t0 = time.time()
