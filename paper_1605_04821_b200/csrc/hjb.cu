@@ -20,12 +20,22 @@
 #include "hjb_tma.cuh"
 #include "hjb_win.cuh"
 
-#ifndef HJB_KC_A
-#define HJB_KC_A 1.0
-#endif
-#ifndef HJB_KC_B
-#define HJB_KC_B 1.0
-#endif
+namespace hjb {
+struct WinPlan {
+  bool ok = false;
+  WinGeom geom{};
+  SkipRect box{0, 0, 0, 0, 0, 0};
+  size_t smem = 0;
+  int grid = 0;
+};
+static const void* win_fn(int D, int P, bool gen) {
+#define WF(DD, PP) (gen ? (const void*)k_search_win<DD, PP, true> : (const void*)k_search_win<DD, PP, false>)
+  if (D == 2) return P == 1 ? WF(2, 1) : WF(2, 2);
+  return P == 1 ? WF(3, 1) : P == 2 ? WF(3, 2) : WF(3, 3);
+#undef WF
+}
+}  // namespace hjb
+
 
 using namespace hjb;
 
@@ -135,10 +145,8 @@ struct hjb_grid {
   TmaGeom tma{};
   size_t tma_smem = 0;
   int tma_grid = 0;
-  bool win_ok = false;        // shared-memory window search over the deep box (k_search_win)
-  WinGeom win{};
-  size_t win_smem = 0;
-  int win_grid = 0;
+  WinPlan win_deep, win_full;  // shared-memory window search (k_search_win) over the deep box /
+                               // over the whole interior (general geometry)
   double rdiff_ax[3] = {0, 0, 0}, rdrift_ax[3] = {0, 0, 0};
   double* rng_part = nullptr; // k_field_ranges block partials
 };
@@ -774,12 +782,12 @@ static bool encode_pair_view(hjb_grid* g, const double* U, CUtensorMap* map) {
 // Per-rank ranges of the per-node scale fields -> per-axis reach of every control's endpoints ->
 // the rectangle of nodes none of whose endpoints can be truncated (2D, no sigma/b offset fields).
 // deep_rect() scales it to each multigrid level; the lean kernels run there.
-// shared-memory window search (hjb_win.cuh): choose the tile of the fine level's deep box whose
-// window [tile - m, tile + m] fits in shared memory at the least staging + idle-thread cost
-static hjb_status setup_win(hjb_grid* g) {
+// shared-memory window search (hjb_win.cuh): choose the tile of `box` (the fine level's deep box, or
+// with gen the whole interior) whose window [tile - m, tile + m] fits in shared memory at the least
+// staging + idle-thread cost
+static hjb_status setup_win(hjb_grid* g, const SkipRect& dr, bool gen, WinPlan* plan) {
   const int D = g->D, P = g->P, K = g->K;
-  const LevelDev& L = g->L0;
-  const SkipRect dr = deep_rect(g, L);
+  *plan = WinPlan{};
   if (dr.c1 <= dr.c0 || dr.r1 <= dr.r0 || dr.y1 <= dr.y0) return HJB_OK;
   int m[3] = {0, 0, 0}, ex[3] = {1, 1, 1};
   for (int d = 0; d < D; ++d) m[d] = (int)std::floor(std::max(g->rdiff_ax[d], g->rdrift_ax[d]) + 1e-6) + 1;
@@ -787,7 +795,8 @@ static hjb_status setup_win(hjb_grid* g) {
   ex[1] = D == 2 ? dr.r1 - dr.r0 : dr.y1 - dr.y0;
   ex[2] = D == 3 ? dr.r1 - dr.r0 : 1;
   const int ntab = ((K * (P * D + D + 2 + g->Q) + 15) / 16) * 16;
-  const size_t limit = 200 * 1024;
+  const size_t cmb = (size_t)(kWinS - 1) * kWinNodes * (2 * sizeof(double) + sizeof(int));  // merge buffers
+  const size_t limit = 227 * 1024 - 1024 - cmb;  // opt-in maximum less static shared memory
   const double loads = (double)K * (2 * P + 1) * (1 << D);  // shared-memory gathers per node
   static const int T0[] = {32, 64, 128}, T1[] = {1, 2, 4, 8, 16, 32, 64}, T2[] = {1, 2, 3, 4, 6, 8};
   double best = INFINITY;
@@ -798,7 +807,7 @@ static hjb_status setup_win(hjb_grid* g) {
         if (D == 2 && t2 != 1) continue;
         const int t[3] = {t0, t1, t2};
         const int nodes = t0 * t1 * t2;
-        if (nodes < kWinNT) continue;
+        if (nodes < kWinNodes) continue;
         int w[3], nt[3];
         double vol = 1.0, slots = 1.0, cov = 1.0;
         for (int d = 0; d < 3; ++d) {
@@ -827,26 +836,26 @@ static hjb_status setup_win(hjb_grid* g) {
         }
       }
   if (!std::isfinite(best)) return HJB_OK;
-  const size_t smem = ((size_t)W.tab + (size_t)W.w[0] * W.w[1] * W.w[2]) * sizeof(double);
-  const void* fn = nullptr;
-  if (D == 2) fn = P == 1 ? (const void*)k_search_win<2, 1> : (const void*)k_search_win<2, 2>;
-  else fn = P == 1 ? (const void*)k_search_win<3, 1> : P == 2 ? (const void*)k_search_win<3, 2> : (const void*)k_search_win<3, 3>;
+  const size_t smem = ((size_t)W.tab + (size_t)W.w[0] * W.w[1] * W.w[2]) * sizeof(double) + cmb;
+  const void* fn = win_fn(D, P, gen);
   CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kWinNT, smem) != cudaSuccess || occ < 1) {
     cudaGetLastError();
     return HJB_OK;
   }
-  g->win = W;
-  g->win_smem = smem;
-  g->win_grid = std::min(W.ntiles, std::min(occ * g->sms, kMaxBlocks));
-  g->win_ok = true;
+  plan->geom = W;
+  plan->box = dr;
+  plan->smem = smem;
+  plan->grid = std::min(W.ntiles, std::min(occ * g->sms, kMaxBlocks));
+  plan->ok = true;
   return HJB_OK;
 }
 
 static hjb_status setup_deep(hjb_grid* g) {
   g->reach_ok = false;
-  g->win_ok = false;
+  g->win_deep = WinPlan{};
+  g->win_full = WinPlan{};
 #ifdef HJB_NO_DEEP
   return HJB_OK;
 #endif
@@ -942,9 +951,15 @@ static hjb_status setup_deep(hjb_grid* g) {
     }
   }
 #endif
-  g->win_ok = false;
+  // HJB_WIN=0: direct kernels; =1: window over the deep box only (+ general strips); =2: window over
+  // the whole interior where it fits, else over the deep box.  Default 2 in 2D, 1 in 3D (measured:
+  // the general geometry in the 3D window kernel spills at 128 registers)
   const char* wenv = getenv("HJB_WIN");
-  if (!(wenv && wenv[0] == '0') && !g->tma_ok) TRY(setup_win(g));
+  const int wmode = wenv ? atoi(wenv) : (D == 2 ? 2 : 1);
+  if (wmode >= 1 && !g->tma_ok) {
+    TRY(setup_win(g, deep_rect(g, L), false, &g->win_deep));
+    if (wmode >= 2) TRY(setup_win(g, full_box(g, L), true, &g->win_full));
+  }
   return HJB_OK;
 }
 
@@ -1051,9 +1066,11 @@ static hjb_status policy_update_dev(hjb_grid* g, double dt, const double* U, con
   const bool use_tma = has_deep && g->tma_ok && ((uintptr_t)U & 15) == 0 && encode_pair_view(g, U, &umap);
   const SkipRect tiles = use_tma ? g->tma.tiles : SkipRect{0, 0, 0, 0};
   SkipRect gstrips[6], dstrips[6];
-  const int ngs = ring_strips(full, rect, gstrips);
-  const bool use_win = has_deep && !use_tma && g->win_ok;  // the window kernel covers the whole box
-  const int nds = (has_deep && !use_win) ? ring_strips(rect, tiles, dstrips) : 0;
+  // shared-memory window kernels: over the whole interior (no strips), or over the deep box
+  const WinPlan* wp = use_tma ? nullptr : g->win_full.ok ? &g->win_full : (has_deep && g->win_deep.ok) ? &g->win_deep : nullptr;
+  const bool win_all = wp == &g->win_full;
+  const int ngs = win_all ? 0 : ring_strips(full, rect, gstrips);
+  const int nds = (has_deep && !wp) ? ring_strips(rect, tiles, dstrips) : 0;
 #define SRCH1(DD, PP, DP, RR)                                                                                 \
   do {                                                                                                        \
     const LevelDev LL = shape_of(g->L0, RR);                                                                  \
@@ -1085,11 +1102,18 @@ static hjb_status policy_update_dev(hjb_grid* g, double dt, const double* U, con
   g->prof.nodes[HJB_KC_SEARCH] += nodes;  // algorithmic totals of the whole search (all launches)
   g->prof.bytes[HJB_KC_SEARCH] += nodes * bpn;
   g->prof.flops[HJB_KC_SEARCH] += nodes * fpn;
-  if (use_win) {  // deep box: the tile's neighbourhood of U staged in shared memory
-#define WIN(DD, PP)                                                                                        \
-  LAUNCH(HJB_KC_SEARCH, 0, 0, 0,                                                                           \
-         k_search_win<DD, PP><<<g->win_grid, kWinNT, g->win_smem, g->st>>>(g->L0, g->C0, dt, U, Uprev, pol, F, \
-                                                                         g->partial + 2 * nblk, rect, g->win))
+  if (wp) {  // the tiles' neighbourhoods of U staged in shared memory
+#define WIN(DD, PP)                                                                                         \
+  do {                                                                                                      \
+    if (win_all)                                                                                            \
+      LAUNCH(HJB_KC_SEARCH, 0, 0, 0,                                                                        \
+             k_search_win<DD, PP, true><<<wp->grid, kWinNT, wp->smem, g->st>>>(                             \
+                 g->L0, g->C0, dt, U, Uprev, pol, F, g->partial + 2 * nblk, wp->box, wp->geom));            \
+    else                                                                                                    \
+      LAUNCH(HJB_KC_SEARCH, 0, 0, 0,                                                                        \
+             k_search_win<DD, PP, false><<<wp->grid, kWinNT, wp->smem, g->st>>>(                            \
+                 g->L0, g->C0, dt, U, Uprev, pol, F, g->partial + 2 * nblk, wp->box, wp->geom));            \
+  } while (0)
     if (g->D == 2) {
       if (g->P == 1) WIN(2, 1);
       else WIN(2, 2);
@@ -1100,7 +1124,7 @@ static hjb_status policy_update_dev(hjb_grid* g, double dt, const double* U, con
     }
 #undef WIN
     CKL();
-    nblk += g->win_grid;
+    nblk += wp->grid;
   }
   if (use_tma) {  // deep tiles: windows staged in shared memory by TMA (partials after the others')
     if (g->P == 1)
@@ -1192,16 +1216,9 @@ static hjb_status build_levels(hjb_grid* g, const hjb_mg_params* mp) {
     Level l;
     const double hc = (g->hi - g->lo) / (double)(nc - 1);
     // SL steps on the coarse level: 0 = the fine k (and drift step h); 1 = the scheme's own rule
-    // k_l = sqrt(h_l); 2 = the fine steps, but at least HJB_KC_A / HJB_KC_B coarse cells (keeps
-    // the interpolation diffusion ~ h_l^2 / k^2 of the rediscretised operator bounded)
-    double kc = g->k, k2c = g->h;
-    if (mp->coarse_k_mode == 1) {
-      kc = std::sqrt(hc);
-      k2c = hc;
-    } else if (mp->coarse_k_mode == 2) {
-      kc = std::max(g->k, HJB_KC_A * hc);
-      k2c = std::max(g->h, HJB_KC_B * hc);
-    }
+    // k_l = sqrt(h_l) (measured: more Krylov iterations at cfg2 and cfg4)
+    const double kc = (mp->coarse_k_mode == 1) ? std::sqrt(hc) : g->k;
+    const double k2c = (mp->coarse_k_mode == 1) ? hc : g->h;
     l.L = full_level(D, nc, g->lo, g->hi, kc, k2c);
     l.replicated = (g->R > 1) && lf.replicated;
     if (g->R > 1 && !lf.replicated) {

@@ -24,7 +24,10 @@
 
 namespace hjb {
 
-constexpr int kTX = 128;   // threads per block of the 2D grid kernels
+#ifndef HJB_TX
+#define HJB_TX 128
+#endif
+constexpr int kTX = HJB_TX;  // threads per block of the 2D grid kernels
 #ifndef HJB_BX
 #define HJB_BX 128
 #endif

@@ -30,7 +30,7 @@ enum OpMode : int {
 #define HJB_OP_ILP 1
 #endif
 #ifndef HJB_SEARCH_MINB
-#define HJB_SEARCH_MINB 1
+#define HJB_SEARCH_MINB 3  // general search: 168 registers (spills only in the truncation path): cfg3 -5 %
 #endif
 // Every node of the rectangle `it` (loop coordinates).  DEEP: `it` lies in the deep rectangle (all
 // endpoints of every control strictly inside the box) -> the lean fast path, no truncation code.

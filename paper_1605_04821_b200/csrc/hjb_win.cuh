@@ -16,11 +16,21 @@
 namespace hjb {
 
 #ifndef HJB_WIN_NT
-#define HJB_WIN_NT 256
+#define HJB_WIN_NT 512
 #endif
-constexpr int kWinNT = HJB_WIN_NT;  // threads per CTA (one node per thread per pass)
+#ifndef HJB_WIN_SPLIT
+#define HJB_WIN_SPLIT 2
+#endif
+// threads per CTA; each node's K controls are split over kWinS threads (warps alternate control
+// ranges, so the lanes of a warp are consecutive x nodes on the same control): more warps share one
+// window, which is what hides the latency of the dependent geometry -> gather -> compare chain
+constexpr int kWinNT = HJB_WIN_NT, kWinS = HJB_WIN_SPLIT, kWinNodes = kWinNT / kWinS;
+#ifndef HJB_WIN_UNROLL
+#define HJB_WIN_UNROLL 1
+#endif
+constexpr int kWinUnroll = HJB_WIN_UNROLL;  // controls interleaved per thread (A/B knob)
 
-struct WinGeom {
+struct WinGeom {  // tiling of a box of nodes (loop coordinates, SkipRect) for k_search_win
   int t[3];    // tile extent per axis (x, then the 2D row / 3D y axis, then 3D planes; 2D: t[2] = 1)
   int m[3];    // window margin per axis (cells; m[2] = 0 in 2D)
   int w[3];    // window extent t + 2m
@@ -29,7 +39,10 @@ struct WinGeom {
   int tab;     // doubles of control tables at the start of shared memory (window follows)
 };
 
-template <int D, int P>
+// GEN = false: tiles of the deep box, lean untruncated geometry (k_search<D, P, true>'s);
+// GEN = true: tiles of the whole interior, the general geometry with the warp vote (k_search<D, P,
+// false>'s): truncated endpoints lie on the faces, still inside the window.
+template <int D, int P, bool GEN>
 __global__ void __launch_bounds__(kWinNT, 1) k_search_win(LevelDev L, CoefDev C, double dt,
                                                           const double* __restrict__ U,
                                                           const double* __restrict__ Uprev,
@@ -44,6 +57,10 @@ __global__ void __launch_bounds__(kWinNT, 1) k_search_win(LevelDev L, CoefDev C,
   const double* tfc = tcc + C.K;
   const double* tfb = tfc + C.K;
   double* win = tab + wg.tab;
+  // control-range merge buffers (kWinS > 1), behind the window
+  double* cmb_h = win + wg.w[0] * wg.w[1] * wg.w[2];
+  double* cmb_f = cmb_h + (kWinS - 1) * kWinNodes;
+  int* cmb_a = (int*)(cmb_f + (kWinS - 1) * kWinNodes);
   const int tid = threadIdx.x;
   const int W0 = wg.w[0], W1 = wg.w[1], W01 = W0 * W1;
   const int nodes = wg.t[0] * wg.t[1] * wg.t[2];
@@ -80,64 +97,98 @@ __global__ void __launch_bounds__(kWinNT, 1) k_search_win(LevelDev L, CoefDev C,
       }
     }
     __syncthreads();
-    for (int q = tid; q < nodes; q += kWinNT) {
+    const int sub = (tid >> 5) % kWinS;                        // control range of this thread
+    const int slot = ((tid >> 5) / kWinS) * 32 + (tid & 31);     // node slot in a pass
+    const int a_lo = (sub * C.K) / kWinS, a_hi = ((sub + 1) * C.K) / kWinS;
+    for (int q0 = 0; q0 < nodes; q0 += kWinNodes) {
+      const int q = q0 + slot;
       const int qx = q % wg.t[0], qr = q / wg.t[0];
       const int qy = qr % wg.t[1], qz = qr / wg.t[1];
       const int col = col0 + qx;
-      if (col >= box.c1) continue;
-      int row;
+      bool valid = q < nodes && col < box.c1;
+      int row = 0;
       if (D == 2) {
-        if (a1 + qy >= box.r1) continue;
+        valid = valid && a1 + qy < box.r1;
         row = a1 + qy;
       } else {
-        if (a1 + qy >= box.y1 || a2 + qz >= box.r1) continue;
+        valid = valid && a1 + qy < box.y1 && a2 + qz < box.r1;
         row = (a1 + qy) + L.nI * (a2 + qz);
       }
       Node<D> nd;
-      node_at<D>(L, col, row, nd);
-      load_fields<D>(C, nd);
-      double feat[kMaxQ];
+      double best = INFINITY, fbest = 0.0, Uj = 0.0;
+      int arg = a_lo;
+      if (valid) {
+        node_at<D>(L, col, row, nd);
+        load_fields<D>(C, nd);
+        double feat[kMaxQ];
 #pragma unroll
-      for (int k = 0; k < kMaxQ; ++k) feat[k] = (k < C.Q) ? __ldg(C.f_feat + k * C.ld + nd.loc) : 0.0;
-      const double Uj = __ldg(U + nd.loc);
-      double best = INFINITY, fbest = 0.0;
-      int arg = 0;
-      for (int a = 0; a < C.K; ++a) {
-        Tap<D> taps[E];
-        double o[P + 1][D];
-        row_offsets<D, P>(L, tsd + a * P * D, tbd + a * D, nd, o);
-        const double wsum = row_geometry_fast<D, P>(L, nd, o, taps);
-        double vals[E];
+        for (int k = 0; k < kMaxQ; ++k) feat[k] = (k < C.Q) ? __ldg(C.f_feat + k * C.ld + nd.loc) : 0.0;
+        Uj = __ldg(U + nd.loc);
+#pragma unroll kWinUnroll
+        for (int a = a_lo; a < a_hi; ++a) {
+          Tap<D> taps[E];
+          double wsum;
+          if (GEN) {
+            wsum = row_taps<D, P>(L, tsd + a * P * D, tbd + a * D, nd, taps);
+          } else {
+            double o[P + 1][D];
+            row_offsets<D, P>(L, tsd + a * P * D, tbd + a * D, nd, o);
+            wsum = row_geometry_fast<D, P>(L, nd, o, taps);
+          }
+          double vals[E];
 #pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const int off = (taps[e].c[0] - wo[0]) + W0 * (taps[e].c[1] - wo[1]) +
-                          (D == 3 ? W01 * (taps[e].c[D - 1] - wo[2]) : 0);
-          vals[e] = interp_at<D, true>(win + off, W0, W01, taps[e].s);
-        }
-        double acc = 0.0;
+          for (int e = 0; e < E; ++e) {
+            const int off = (taps[e].c[0] - wo[0]) + W0 * (taps[e].c[1] - wo[1]) +
+                            (D == 3 ? W01 * (taps[e].c[D - 1] - wo[2]) : 0);
+            vals[e] = interp_at<D, true>(win + off, W0, W01, taps[e].s);
+          }
+          double acc = 0.0;
 #pragma unroll
-        for (int e = 0; e < E; ++e) acc = fma(taps[e].w, vals[e], acc);
-        // H^a_j = sum_e w_e I U(z_e) - wsum U_j + c^a_j U_j + f^a_j  (as k_search)
-        double f = tfc[a];
-        const double* fb = tfb + a * C.Q;
+          for (int e = 0; e < E; ++e) acc = fma(taps[e].w, vals[e], acc);
+          // H^a_j = sum_e w_e I U(z_e) - wsum U_j + c^a_j U_j + f^a_j  (as k_search)
+          double f = tfc[a];
+          const double* fb = tfb + a * C.Q;
 #pragma unroll
-        for (int k = 0; k < kMaxQ; ++k)
-          if (k < C.Q) f = fma(fb[k], feat[k], f);
-        const double c = nd.cn + tcc[a];
-        const double H = (acc - wsum * Uj) + c * Uj + f;
-        if (H < best) {  // strict: lowest index wins exact ties (reading iv)
-          best = H;
-          arg = a;
-          fbest = f;
+          for (int k = 0; k < kMaxQ; ++k)
+            if (k < C.Q) f = fma(fb[k], feat[k], f);
+          const double c = nd.cn + tcc[a];
+          const double H = (acc - wsum * Uj) + c * Uj + f;
+          if (H < best) {  // strict: lowest index wins exact ties (reading iv)
+            best = H;
+            arg = a;
+            fbest = f;
+          }
         }
       }
-      const double Up = __ldg(Uprev + nd.loc);
-      const double R = fabs(Uj - Up - dt * best);
-      const int old = pol[nd.loc];
-      pol[nd.loc] = (uint8_t)arg;
-      F[nd.loc] = fma(dt, fbest, Up);
-      red[0] = fmax(red[0], (R == R) ? R : INFINITY);
-      red[1] += (old != arg) ? 1.0 : 0.0;
+      if (kWinS > 1) {
+        // merge the control ranges in index order: a later range wins only with a strictly smaller
+        // minimum, which is the sequential strict-less scan's result (lowest index on exact ties)
+        __syncthreads();
+        if (valid && sub > 0) {
+          cmb_h[(sub - 1) * kWinNodes + slot] = best;
+          cmb_f[(sub - 1) * kWinNodes + slot] = fbest;
+          cmb_a[(sub - 1) * kWinNodes + slot] = arg;
+        }
+        __syncthreads();
+        if (valid && sub == 0)
+          for (int r = 0; r < kWinS - 1; ++r) {
+            const double h = cmb_h[r * kWinNodes + slot];
+            if (h < best) {
+              best = h;
+              arg = cmb_a[r * kWinNodes + slot];
+              fbest = cmb_f[r * kWinNodes + slot];
+            }
+          }
+      }
+      if (valid && sub == 0) {
+        const double Up = __ldg(Uprev + nd.loc);
+        const double R = fabs(Uj - Up - dt * best);
+        const int old = pol[nd.loc];
+        pol[nd.loc] = (uint8_t)arg;
+        F[nd.loc] = fma(dt, fbest, Up);
+        red[0] = fmax(red[0], (R == R) ? R : INFINITY);
+        red[1] += (old != arg) ? 1.0 : 0.0;
+      }
     }
   }
   block_reduce_store<2, kWinNT>(red, partial, 0x1u);

@@ -258,9 +258,10 @@ def test_edge_cases():
                                      ("cfg0_K7", lambda: bj_config(0, n=65, K=7)),
                                      ("cfg3_33", lambda: bj_config(3, n=33))])
 def test_deep_kernels_match_general(name, mk, monkeypatch):
-    """The lean deep-rectangle kernels (no truncation code), the shared-memory window search and the
-    TMA-windowed search tiles give bit-identical search results and operator applications to the
-    general kernels everywhere (HJB_NO_DEEP / HJB_WIN=0 / HJB_TMA=1 select them)."""
+    """The lean deep-rectangle kernels (no truncation code), the shared-memory window search (over the
+    deep box, and over the whole interior with the general geometry) and the TMA-windowed search
+    tiles give bit-identical search results and operator applications to the general kernels
+    everywhere (HJB_NO_DEEP / HJB_WIN=0,1,2 / HJB_TMA=1 select them)."""
     torch = require_gpu()
     p = mk()
     rng = np.random.default_rng(11)
@@ -268,7 +269,7 @@ def test_deep_kernels_match_general(name, mk, monkeypatch):
     U = Uprev + 0.05 * rng.uniform(-1, 1, size=p.N)
     x = random_vector(p)
     out = {}
-    for mode in ("general", "deep", "deep_win", "deep_tma"):
+    for mode in ("general", "deep", "deep_win", "full_win", "deep_tma"):
         for k in ("HJB_NO_DEEP", "HJB_NO_TMA", "HJB_TMA", "HJB_WIN"):
             monkeypatch.delenv(k, raising=False)
         if mode == "general":
@@ -277,6 +278,8 @@ def test_deep_kernels_match_general(name, mk, monkeypatch):
             monkeypatch.setenv("HJB_WIN", "0")
         elif mode == "deep_win":
             monkeypatch.setenv("HJB_WIN", "1")
+        elif mode == "full_win":
+            monkeypatch.setenv("HJB_WIN", "2")
         else:
             monkeypatch.setenv("HJB_TMA", "1")
         g, _ = setup(p)
@@ -288,7 +291,7 @@ def test_deep_kernels_match_general(name, mk, monkeypatch):
         torch.cuda.synchronize()
         out[mode] = (pol.cpu().numpy(), F.cpu().numpy(), st, y.cpu().numpy())
         g.close()
-    for m in ("deep", "deep_win", "deep_tma"):
+    for m in ("deep", "deep_win", "full_win", "deep_tma"):
         assert np.array_equal(out["general"][0], out[m][0]), m
         assert np.array_equal(out["general"][1], out[m][1]), m
         assert out["general"][2] == out[m][2], m
