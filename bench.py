@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--json-out", default=None)
     ap.add_argument("--pi-forcing", type=float, default=None, help="solver setting (default: library's)")
     ap.add_argument("--nu", type=int, default=None, help="V(nu,nu) smoothing sweeps (default: library's 2)")
+    ap.add_argument("--nu-pre", type=int, default=None, help="pre-smoothing sweeps (overrides --nu)")
+    ap.add_argument("--nu-post", type=int, default=None, help="post-smoothing sweeps (overrides --nu)")
     return ap.parse_args()
 
 
@@ -248,6 +250,10 @@ def run_b200(args):
 
     skw = {} if args.pi_forcing is None else {"pi_forcing": args.pi_forcing}
     mgkw = {} if args.nu is None else {"nu_pre": args.nu, "nu_post": args.nu}
+    if args.nu_pre is not None:
+        mgkw["nu_pre"] = args.nu_pre
+    if args.nu_post is not None:
+        mgkw["nu_post"] = args.nu_post
 
     def do_step(s, Uin, Uout, polbuf, psi):
         # initial iterate: linear extrapolation 2 U^{n-1} - U^{n-2} once two steps exist (Uout holds

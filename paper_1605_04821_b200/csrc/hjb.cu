@@ -83,6 +83,7 @@ struct Level {
   double* fields = nullptr;       // coarse levels: injected field planes
   CoefDev C{};
   double* Ainv = nullptr;         // coarsest level dense inverse
+  double* dg = nullptr;           // smoothed levels: the diagonal of A (per policy, hjb_mg_setup)
 };
 
 struct hjb_grid {
@@ -145,6 +146,7 @@ struct hjb_grid {
   TmaGeom tma{};
   size_t tma_smem = 0;
   int tma_grid = 0;
+  bool use_dg = true;          // smoother reads the stored diagonal (Level::dg)
   WinPlan win_deep, win_full;  // shared-memory window search (k_search_win) over the deep box /
                                // over the whole interior (general geometry)
   double rdiff_ax[3] = {0, 0, 0}, rdrift_ax[3] = {0, 0, 0};
@@ -419,11 +421,13 @@ static void launch_operator(hjb_grid* g, const LevelDev& L, const CoefDev& C, in
                             double omega, const uint8_t* pol, const double* x, const double* b, double* y,
                             const double* u, bool fine = true) {
   cudaStream_t st = g->st;
-  const int cls = !fine ? HJB_KC_MG_COARSE
-                        : (mode == OP_APPLY ? HJB_KC_APPLY : (mode == OP_RESID ? HJB_KC_RESID : HJB_KC_SMOOTH));
+  const int cls = mode == OP_DIAG ? HJB_KC_COARSE  // multigrid setup
+                  : !fine ? HJB_KC_MG_COARSE
+                          : (mode == OP_APPLY ? HJB_KC_APPLY : (mode == OP_RESID ? HJB_KC_RESID : HJB_KC_SMOOTH));
   const double nodes = (double)L.n_own;
-  const double bpn = 1.0 + 8.0 + (mode != OP_JACOBI0 ? 8.0 : 0.0) + (mode != OP_APPLY ? 8.0 : 0.0) +
-                     (ndot >= 1 ? 8.0 : 0.0) + 8.0 * g->nplanes0;
+  const bool gathers = mode != OP_JACOBI0 && mode != OP_DIAG;
+  const double bpn = 1.0 + 8.0 + (gathers ? 8.0 : 0.0) + (mode != OP_APPLY && mode != OP_DIAG ? 8.0 : 0.0) +
+                     (ndot >= 1 || mode == OP_JACOBI_D ? 8.0 : 0.0) + 8.0 * g->nplanes0;
   const double fpn = (2.0 * g->P + 1.0) * (1 << D) * 2.0 + 4.0 + 2.0 * ndot;
   const size_t tsm = (size_t)g->K * (g->P * D + D + 1) * sizeof(double);  // control tables in smem
   // the deep rectangle of this level (2D): lean fast-path kernel there, general kernel on the
@@ -469,6 +473,10 @@ static void launch_operator(hjb_grid* g, const LevelDev& L, const CoefDev& C, in
     else OPL(OP_RESID, 2);
   } else if (mode == OP_JACOBI) {
     OPL(OP_JACOBI, 0);
+  } else if (mode == OP_JACOBI_D) {
+    OPL(OP_JACOBI_D, 0);
+  } else if (mode == OP_DIAG) {
+    OPL(OP_DIAG, 0);
   } else {
     OPL(OP_JACOBI0, 0);
   }
@@ -580,6 +588,7 @@ static void free_levels(hjb_grid* g) {
       cudaFree(l.fields);
     }
     cudaFree(l.Ainv);
+    cudaFree(l.dg);
   }
   g->levels.clear();
   g->mg_ready = false;
@@ -1268,6 +1277,10 @@ static hjb_status build_levels(hjb_grid* g, const hjb_mg_params* mp) {
     TRY(dalloc((void**)&l.res, vb));
     CK(cudaMemsetAsync(l.tmp, 0, vb, g->st));
     CK(cudaMemsetAsync(l.res, 0, vb, g->st));
+    if (i + 1 < g->levels.size()) {
+      TRY(dalloc((void**)&l.dg, vb));
+      CK(cudaMemsetAsync(l.dg, 0, vb, g->st));
+    }
     if (i > 0) {
       TRY(dalloc((void**)&l.x, vb));
       TRY(dalloc((void**)&l.b, vb));
@@ -1374,6 +1387,17 @@ extern "C" hjb_status hjb_mg_setup(hjb_grid_t g, double dt, const uint8_t* polic
   g->mg_dt = dt;
   if (g->D == 2) TRY(inject_all<2>(g));
   else TRY(inject_all<3>(g));
+  // the diagonal of every smoothed level's operator (the smoother reads it instead of recomputing
+  // the self weights; HJB_NO_DIAG=1 recomputes them in every sweep -- bit-identical either way)
+  g->use_dg = !getenv("HJB_NO_DIAG");
+  if (g->use_dg)
+    for (size_t l = 0; l + 1 < g->levels.size(); ++l) {
+      Level& lv = g->levels[l];
+      const uint8_t* pol = (l == 0) ? g->mg_pol0 : lv.pol;
+      if (g->D == 2) launch_operator<2>(g, lv.L, lv.C, OP_DIAG, 0, dt, 0.0, pol, nullptr, nullptr, lv.dg, nullptr, l == 0);
+      else launch_operator<3>(g, lv.L, lv.C, OP_DIAG, 0, dt, 0.0, pol, nullptr, nullptr, lv.dg, nullptr, l == 0);
+    }
+  CKL();
   g->mg_ready = true;
   return HJB_OK;
 }
@@ -1397,10 +1421,20 @@ static hjb_status vcycle(hjb_grid* g, size_t l, const double* b, double* out) {
   const int npre = g->mgp.nu_pre, npost = g->mgp.nu_post;
   double* bufs[2] = {out, lv.tmp};
   int cur = ((npre - 1 + npost) % 2 == 0) ? 0 : 1;  // so the last sweep lands in `out`
-  launch_operator<D>(g, L, lv.C, OP_JACOBI0, 0, dt, om, pol, nullptr, b, bufs[cur], nullptr, fine);
+  const int jmode = g->use_dg ? OP_JACOBI_D : OP_JACOBI;
+  if (g->use_dg) {
+    const double nn = (double)L.n_own;
+    g->prof.calls[fine ? HJB_KC_SMOOTH : HJB_KC_MG_COARSE] += 1;
+    LAUNCH(fine ? HJB_KC_SMOOTH : HJB_KC_MG_COARSE, nn, 24.0 * nn, 2.0 * nn,
+           k_jacobi0_diag<D><<<dims(g, L, (const void*)k_jacobi0_diag<D>), dim3(kBX, kBY), 0, st>>>(L, om, b, lv.dg,
+                                                                                                  bufs[cur]));
+    CKL();
+  } else {
+    launch_operator<D>(g, L, lv.C, OP_JACOBI0, 0, dt, om, pol, nullptr, b, bufs[cur], nullptr, fine);
+  }
   for (int k = 1; k < npre; ++k) {
     TRY(halo_exchange(g, lv, bufs[cur], lv.H));
-    launch_operator<D>(g, L, lv.C, OP_JACOBI, 0, dt, om, pol, bufs[cur], b, bufs[1 - cur], nullptr, fine);
+    launch_operator<D>(g, L, lv.C, jmode, 0, dt, om, pol, bufs[cur], b, bufs[1 - cur], lv.dg, fine);
     cur = 1 - cur;
   }
   TRY(halo_exchange(g, lv, bufs[cur], lv.H));
@@ -1431,7 +1465,7 @@ static hjb_status vcycle(hjb_grid* g, size_t l, const double* b, double* out) {
          k_prolong_add<D><<<dims(g, L, (const void*)k_prolong_add<D>), dim3(kBX, kBY), 0, st>>>(L, lc.L, lc.x, bufs[cur]));
   for (int k = 0; k < npost; ++k) {
     TRY(halo_exchange(g, lv, bufs[cur], lv.H));
-    launch_operator<D>(g, L, lv.C, OP_JACOBI, 0, dt, om, pol, bufs[cur], b, bufs[1 - cur], nullptr, fine);
+    launch_operator<D>(g, L, lv.C, jmode, 0, dt, om, pol, bufs[cur], b, bufs[1 - cur], lv.dg, fine);
     cur = 1 - cur;
   }
   CKL();

@@ -20,6 +20,8 @@ enum OpMode : int {
   OP_RESID = 1,    // y = b - A x                (+ optional dots)
   OP_JACOBI = 2,   // y = x + omega (b - A x) / D
   OP_JACOBI0 = 3,  // y = omega b / D            (x = 0; geometry only, no gathers)
+  OP_DIAG = 4,     // y = D = 1 + dt (sum_e w_e - self - c)   (MG setup: stored per level)
+  OP_JACOBI_D = 5, // OP_JACOBI with D read from the stored diagonal (passed as u): no self weights
 };
 
 // NDOT: 0, 1 -> partial[0] = sum y*u ; 2 -> partial[0] = sum y*u, partial[1] = sum y*y
@@ -44,11 +46,11 @@ __global__ void __launch_bounds__(kTX, (DEEP && D == 2) ? HJB_OP_DEEP_MINB : HJB
                                                   const double* __restrict__ b, double* __restrict__ y,
                                                   const double* __restrict__ u, double* partial,
                                                   SkipRect it) {
-  constexpr bool GATHER = (MODE != OP_JACOBI0);
-  constexpr bool SELF = (MODE == OP_JACOBI || MODE == OP_JACOBI0);
+  constexpr bool GATHER = (MODE != OP_JACOBI0 && MODE != OP_DIAG);
+  constexpr bool SELF = (MODE == OP_JACOBI || MODE == OP_JACOBI0 || MODE == OP_DIAG);
   constexpr int E = 2 * P + 1;
-  constexpr bool XJ = (MODE != OP_JACOBI0);
-  constexpr bool BJ = (MODE != OP_APPLY);
+  constexpr bool XJ = GATHER;
+  constexpr bool BJ = (MODE != OP_APPLY && MODE != OP_DIAG);
   extern __shared__ double tab[];
   stage_tables<D, P, false>(C, tab);
   const double* tsd = tab;
@@ -113,6 +115,8 @@ __global__ void __launch_bounds__(kTX, (DEEP && D == 2) ? HJB_OP_DEEP_MINB : HJB
       if (MODE == OP_JACOBI0) {
         const double diag = 1.0 + dt * (wsum[v] - self - c);
         out = omega * in[v].bj / diag;
+      } else if (MODE == OP_DIAG) {
+        out = 1.0 + dt * (wsum[v] - self - c);
       } else {
         const double xj = in[v].xj;
         const double Ax = xj - dt * (acc - wsum[v] * xj + c * xj);
@@ -121,12 +125,12 @@ __global__ void __launch_bounds__(kTX, (DEEP && D == 2) ? HJB_OP_DEEP_MINB : HJB
         } else if (MODE == OP_RESID) {
           out = in[v].bj - Ax;
         } else {
-          const double diag = 1.0 + dt * (wsum[v] - self - c);
+          const double diag = (MODE == OP_JACOBI_D) ? __ldg(u + nd[v].loc) : 1.0 + dt * (wsum[v] - self - c);
           out = xj + omega * (in[v].bj - Ax) / diag;
         }
       }
       y[nd[v].loc] = out;
-      if (NDOT >= 1) dots[0] = fma(out, __ldg(u + nd[v].loc), dots[0]);
+      if (NDOT >= 1 && MODE != OP_JACOBI_D) dots[0] = fma(out, __ldg(u + nd[v].loc), dots[0]);
       if (NDOT >= 2) dots[1] = fma(out, out, dots[1]);
     }
   }
@@ -438,6 +442,17 @@ __global__ void __launch_bounds__(kTX) k_extrapolate(LevelDev L, const double* _
   FOR_INTERIOR(L) {
     const int j = interior_offset<D>(L, col, row);
     u[j] = fma(2.0, up[j], -u[j]);
+  }
+}
+
+// first smoothing sweep from x = 0 with the stored diagonal: y = omega b / D (the arithmetic of
+// k_operator<..., OP_JACOBI0>, without its per-node geometry)
+template <int D>
+__global__ void __launch_bounds__(kTX) k_jacobi0_diag(LevelDev L, double omega, const double* __restrict__ b,
+                                                      const double* __restrict__ dg, double* __restrict__ y) {
+  FOR_INTERIOR(L) {
+    const int j = interior_offset<D>(L, col, row);
+    y[j] = omega * __ldg(b + j) / __ldg(dg + j);
   }
 }
 

@@ -296,3 +296,31 @@ def test_deep_kernels_match_general(name, mk, monkeypatch):
         assert np.array_equal(out["general"][1], out[m][1]), m
         assert out["general"][2] == out[m][2], m
         assert np.array_equal(out["general"][3], out[m][3]), m
+
+
+@pytest.mark.parametrize("name,mk", [("cfg1", lambda: bj_config(1)), ("cfg2_513", lambda: bj_config(2, n=513)),
+                                     ("cfg3_33", lambda: bj_config(3, n=33))])
+def test_stored_diagonal_smoother_is_bit_identical(name, mk, monkeypatch):
+    """The smoother reading the diagonal stored at hjb_mg_setup (default) gives the same V-cycle,
+    bit for bit, as recomputing the self weights in every sweep (HJB_NO_DIAG=1)."""
+    torch = require_gpu()
+    p = mk()
+    x = to_dev(random_vector(p), torch)
+    out = {}
+    for mode in ("stored", "recomputed"):
+        monkeypatch.delenv("HJB_NO_DIAG", raising=False)
+        if mode == "recomputed":
+            monkeypatch.setenv("HJB_NO_DIAG", "1")
+        g, _ = setup(p)
+        U0 = to_dev(p.g(p.all_idx()), torch)
+        pol = torch.zeros(p.N, dtype=torch.uint8, device="cuda")
+        F = torch.zeros(p.N, dtype=torch.float64, device="cuda")
+        g.policy_update(p.dt, U0, U0, pol, F)
+        g.mg_setup(p.dt, pol)
+        y = torch.zeros(p.N, dtype=torch.float64, device="cuda")
+        g.mg_apply(x, y)
+        torch.cuda.synchronize()
+        out[mode] = y.cpu().numpy()
+        g.close()
+    assert np.array_equal(out["stored"], out["recomputed"])
+    assert np.abs(out["stored"]).max() > 0
