@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--nu", type=int, default=None, help="V(nu,nu) smoothing sweeps (default: library's 2)")
     ap.add_argument("--nu-pre", type=int, default=None, help="pre-smoothing sweeps (overrides --nu)")
     ap.add_argument("--nu-post", type=int, default=None, help="post-smoothing sweeps (overrides --nu)")
+    ap.add_argument("--gamma", type=int, default=None, help="multigrid cycle index (default: library's 2)")
+    ap.add_argument("--gamma-min", type=int, default=None, help="min coarse-level nodes for a revisit")
     return ap.parse_args()
 
 
@@ -254,6 +256,10 @@ def run_b200(args):
         mgkw["nu_pre"] = args.nu_pre
     if args.nu_post is not None:
         mgkw["nu_post"] = args.nu_post
+    if args.gamma is not None:
+        mgkw["gamma"] = args.gamma
+    if args.gamma_min is not None:
+        mgkw["gamma_min_nodes"] = args.gamma_min
 
     def do_step(s, Uin, Uout, polbuf, psi):
         # initial iterate: linear extrapolation 2 U^{n-1} - U^{n-2} once two steps exist (Uout holds

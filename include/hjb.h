@@ -195,18 +195,25 @@ hjb_status hjb_apply(hjb_grid_t g, double dt, const uint8_t* policy, const doubl
 typedef struct {
   int32_t nu_pre, nu_post;   /* smoothing sweeps (default 2, 2)                               */
   double omega;              /* Jacobi damping in (0,1] (default 1.0; Gershgorin-safe)        */
-  int32_t coarse_max_n;      /* coarsen while n > coarse_max_n (default 17 in 2D, 9 in 3D)   */
+  int32_t coarse_max_n;      /* coarsen while n > coarse_max_n (default 9 in 2D, 5 in 3D)    */
   int32_t coarse_k_mode;     /* 0: coarse levels keep the fine SL step k (default);
                                 1: k_l = sqrt(h_l) (the scheme's own rule on each level)      */
   int32_t max_levels;        /* cap on levels (default 32)                                     */
   int32_t gather_n;          /* nranks > 1: levels with n <= gather_n (or slabs thinner than
                                 their halo) are replicated on every rank after an all-gather
                                 (default 129 in 2D, 33 in 3D; BASELINE cfg4 "129^2 on one GPU") */
+  int32_t gamma;             /* cycle index on the large levels: 1 = V-cycle, 2 = W-cycle (the
+                                coarse correction of level l is refined by gamma - 1 further
+                                cycles on the residual of level l+1); default 2               */
+  int32_t gamma_min_nodes;   /* revisit level l+1 only if it owns >= gamma_min_nodes interior
+                                nodes (smaller levels are launch-latency bound: plain V there);
+                                default 131072                                                */
 } hjb_mg_params;
 
 void hjb_mg_params_default(int32_t dim, hjb_mg_params* out);
 hjb_status hjb_mg_setup(hjb_grid_t g, double dt, const uint8_t* policy, const hjb_mg_params* p);
-/* x = M^{-1} b: one V(nu_pre, nu_post) cycle from x = 0 (interior entries; boundary of x = 0). */
+/* x = M^{-1} b: one (nu_pre, nu_post) cycle of index gamma from x = 0 (interior entries; boundary
+   of x = 0). */
 hjb_status hjb_mg_apply(hjb_grid_t g, const double* b, double* x);
 
 /* --------------------------------------------------------------------------- solve

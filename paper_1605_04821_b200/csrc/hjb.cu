@@ -84,6 +84,8 @@ struct Level {
   CoefDev C{};
   double* Ainv = nullptr;         // coarsest level dense inverse
   double* dg = nullptr;           // smoothed levels: the diagonal of A (per policy, hjb_mg_setup)
+  double* r2 = nullptr;           // W-cycle (gamma > 1): coarse residual / correction of a revisit
+  double* e2 = nullptr;
 };
 
 struct hjb_grid {
@@ -147,6 +149,9 @@ struct hjb_grid {
   size_t tma_smem = 0;
   int tma_grid = 0;
   bool use_dg = true;          // smoother reads the stored diagonal (Level::dg)
+  int mg_gamma = 1;            // cycle index on levels owning >= gamma_min nodes (hjb_mg_params)
+  int nu_coarse = 0;           // > 0: smoothing sweeps on levels >= 1 (experiment knob HJB_NU_COARSE)
+  int64_t gamma_min = 0;       // revisit a coarse level only if it has >= gamma_min owned nodes
   WinPlan win_deep, win_full;  // shared-memory window search (k_search_win) over the deep box /
                                // over the whole interior (general geometry)
   double rdiff_ax[3] = {0, 0, 0}, rdrift_ax[3] = {0, 0, 0};
@@ -499,6 +504,8 @@ extern "C" void hjb_mg_params_default(int32_t dim, hjb_mg_params* o) {
   o->coarse_k_mode = 0;
   o->max_levels = 32;
   o->gather_n = (dim == 3) ? 33 : 129;
+  o->gamma = 2;
+  o->gamma_min_nodes = 131072;
 }
 
 extern "C" void hjb_solve_params_default(int32_t dim, hjb_solve_params* o) {
@@ -589,6 +596,8 @@ static void free_levels(hjb_grid* g) {
     }
     cudaFree(l.Ainv);
     cudaFree(l.dg);
+    cudaFree(l.r2);
+    cudaFree(l.e2);
   }
   g->levels.clear();
   g->mg_ready = false;
@@ -1375,7 +1384,8 @@ extern "C" hjb_status hjb_mg_setup(hjb_grid_t g, double dt, const uint8_t* polic
   hjb_mg_params def;
   hjb_mg_params_default(g->D, &def);
   const hjb_mg_params* p = mp ? mp : &def;
-  if (p->nu_pre < 1 || p->nu_post < 0 || !(p->omega > 0.0) || p->omega > 1.0 || p->max_levels < 1)
+  if (p->nu_pre < 1 || p->nu_post < 0 || !(p->omega > 0.0) || p->omega > 1.0 || p->max_levels < 1 ||
+      p->gamma < 1 || p->gamma > 3 || p->gamma_min_nodes < 0)
     return fail(HJB_ERR_INVALID_ARG, "bad multigrid parameters");
   const bool rebuild = g->levels.empty() || std::memcmp(&g->mgp, p, sizeof(hjb_mg_params)) != 0 ||
                        g->levels[0].C.ld != g->C0.ld;
@@ -1390,6 +1400,21 @@ extern "C" hjb_status hjb_mg_setup(hjb_grid_t g, double dt, const uint8_t* polic
   // the diagonal of every smoothed level's operator (the smoother reads it instead of recomputing
   // the self weights; HJB_NO_DIAG=1 recomputes them in every sweep -- bit-identical either way)
   g->use_dg = !getenv("HJB_NO_DIAG");
+  g->mg_gamma = p->gamma;
+  g->gamma_min = p->gamma_min_nodes;
+  g->nu_coarse = getenv("HJB_NU_COARSE") ? std::max(0, atoi(getenv("HJB_NU_COARSE"))) : 0;
+  if (g->mg_gamma > 1)
+    for (size_t l = 1; l + 1 < g->levels.size(); ++l) {
+      Level& lv = g->levels[l];
+      if (lv.L.n_own < g->gamma_min) continue;
+      const size_t vb = (size_t)lv.elems * sizeof(double);
+      if (!lv.r2) {
+        TRY(dalloc((void**)&lv.r2, vb));
+        TRY(dalloc((void**)&lv.e2, vb));
+        CK(cudaMemsetAsync(lv.r2, 0, vb, g->st));
+        CK(cudaMemsetAsync(lv.e2, 0, vb, g->st));
+      }
+    }
   if (g->use_dg)
     for (size_t l = 0; l + 1 < g->levels.size(); ++l) {
       Level& lv = g->levels[l];
@@ -1418,7 +1443,8 @@ static hjb_status vcycle(hjb_grid* g, size_t l, const double* b, double* out) {
     return HJB_OK;
   }
   const double dt = g->mg_dt, om = g->mgp.omega;
-  const int npre = g->mgp.nu_pre, npost = g->mgp.nu_post;
+  const int npre = (l > 0 && g->nu_coarse > 0) ? g->nu_coarse : g->mgp.nu_pre;
+  const int npost = (l > 0 && g->nu_coarse > 0) ? g->nu_coarse : g->mgp.nu_post;
   double* bufs[2] = {out, lv.tmp};
   int cur = ((npre - 1 + npost) % 2 == 0) ? 0 : 1;  // so the last sweep lands in `out`
   const int jmode = g->use_dg ? OP_JACOBI_D : OP_JACOBI;
@@ -1460,6 +1486,17 @@ static hjb_status vcycle(hjb_grid* g, size_t l, const double* b, double* out) {
     CKL();
   }
   TRY(vcycle<D>(g, l + 1, lc.b, lc.x));
+  const int gamma = (lc.L.n_own >= g->gamma_min) ? g->mg_gamma : 1;
+  for (int k = 1; k < gamma && l + 2 < g->levels.size(); ++k) {  // W-cycle: revisit the coarse level
+    const uint8_t* pc = lc.pol;
+    TRY(halo_exchange(g, lc, lc.x, lc.H));
+    launch_operator<D>(g, lc.L, lc.C, OP_RESID, 0, dt, 0.0, pc, lc.x, lc.b, lc.r2, nullptr, false);
+    TRY(vcycle<D>(g, l + 1, lc.r2, lc.e2));
+    const double nc = (double)lc.L.n_own;
+    LAUNCH(HJB_KC_VECTOR, nc, 24.0 * nc, nc,
+           k_add_interior<D><<<dims(g, lc.L, (const void*)k_add_interior<D>), dim3(kBX, kBY), 0, st>>>(lc.L, lc.e2, lc.x));
+    CKL();
+  }
   TRY(halo_exchange(g, lc, lc.x, 1));
   LAUNCH(HJB_KC_TRANSFER, L.n_own, 16.0 * L.n_own + 8.0 * lc.L.n_own, 4.0 * L.n_own,
          k_prolong_add<D><<<dims(g, L, (const void*)k_prolong_add<D>), dim3(kBX, kBY), 0, st>>>(L, lc.L, lc.x, bufs[cur]));

@@ -457,6 +457,15 @@ __global__ void __launch_bounds__(kTX) k_jacobi0_diag(LevelDev L, double omega, 
 }
 
 template <int D>
+__global__ void __launch_bounds__(kTX) k_add_interior(LevelDev L, const double* __restrict__ a,
+                                                      double* __restrict__ y) {
+  FOR_INTERIOR(L) {
+    const int j = interior_offset<D>(L, col, row);
+    y[j] += a[j];
+  }
+}
+
+template <int D>
 __global__ void __launch_bounds__(kTX) k_copy_interior(LevelDev L, const double* __restrict__ a,
                                                            double* __restrict__ b) {
   FOR_INTERIOR(L) {

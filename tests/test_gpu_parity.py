@@ -324,3 +324,16 @@ def test_stored_diagonal_smoother_is_bit_identical(name, mk, monkeypatch):
         g.close()
     assert np.array_equal(out["stored"], out["recomputed"])
     assert np.abs(out["stored"]).max() > 0
+
+
+@pytest.mark.parametrize("gamma,gmin", [(1, 0), (2, 0), (3, 0)])
+def test_step_parity_cycle_index(gamma, gmin):
+    """V-, W- and gamma = 3 cycles on every level (the default revisits only large levels, which the
+    small parity grids do not have): same fixed point as the oracle, exact policy evaluations."""
+    p = bj_config(2, n=129)
+    Ug, _, stats = _gpu_march(p, 2, pi_forcing=0.0, mg={"gamma": gamma, "gamma_min_nodes": gmin})
+    Uo = p.g(p.all_idx())
+    for s in range(1, 3):
+        Uo, _, _ = howard_step(p, Uo, s * p.dt, p.dt)
+    assert np.abs(Ug - Uo).max() <= 1e-8 * max(1.0, np.abs(Uo).max())
+    assert all(st["final_rres"] <= 1e-12 for st in stats)

@@ -148,6 +148,7 @@ def _slab_march(p, R, steps, **kw):
 @pytest.mark.parametrize("name,cfg,n,K,R,steps,mg", [
     ("cfg0_R2", 0, 33, 16, 2, 2, {}),
     ("cfg2_257_R3_slab_coarse_levels", 2, 257, 8, 3, 1, {"gather_n": 33}),
+    ("cfg2_257_R2_wcycle_on_slab_levels", 2, 257, 8, 2, 1, {"gather_n": 33, "gamma": 2, "gamma_min_nodes": 0}),
     ("cfg3_17_R2", 3, 17, None, 2, 1, {}),
 ])
 def test_slab_step_matches_oracle(name, cfg, n, K, R, steps, mg):
@@ -163,5 +164,5 @@ def test_slab_step_matches_oracle(name, cfg, n, K, R, steps, mg):
     for q in parts[1:]:
         assert [st["pi_iters"] for st in q[2]] == [st["pi_iters"] for st in parts[0][2]]
         assert [st["krylov_iters_total"] for st in q[2]] == [st["krylov_iters_total"] for st in parts[0][2]]
-    if mg.get("gather_n") == 33:
+    if mg.get("gather_n") == 33 and "gamma" not in mg:
         assert parts[0][2][-1]["n_levels"] >= 4
