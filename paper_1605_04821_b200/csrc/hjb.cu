@@ -131,11 +131,13 @@ struct hjb_grid {
   double mg_dt = 0.0;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   // instrumentation (hjb_profile_*)
-  static constexpr int kSlots = 256;
+  // ring of per-launch event pairs; when it is full the OLDER half is drained (long finished: the
+  // host runs at most a queue depth ahead), so timing never stalls the launch pipeline
+  static constexpr int kSlots = 4096;
   bool prof_timing = false;
   cudaEvent_t pev[2 * kSlots] = {};
   int pcls[kSlots] = {};
-  int npend = 0;
+  int phead = 0, npend = 0;
   hjb_profile prof{};
   int nplanes0 = 0;  // per-node coefficient planes read by the operator (sigma/b/c fields)
   int sms = 148;
@@ -159,19 +161,24 @@ struct hjb_grid {
 };
 
 // ---------------------------------------------------------------------------- instrumentation
-static void prof_drain(hjb_grid* g) {
-  if (g->npend == 0) return;
-  cudaEventSynchronize(g->pev[2 * g->npend - 1]);
-  for (int i = 0; i < g->npend; ++i) {
+// accumulate the `m` oldest pending launches
+static void prof_drain_oldest(hjb_grid* g, int m) {
+  if (m <= 0) return;
+  const int K = hjb_grid::kSlots;
+  cudaEventSynchronize(g->pev[2 * ((g->phead + m - 1) % K) + 1]);
+  for (int i = 0; i < m; ++i) {
+    const int k = (g->phead + i) % K;
     float ms = 0.f;
-    if (cudaEventElapsedTime(&ms, g->pev[2 * i], g->pev[2 * i + 1]) == cudaSuccess) g->prof.ms[g->pcls[i]] += ms;
+    if (cudaEventElapsedTime(&ms, g->pev[2 * k], g->pev[2 * k + 1]) == cudaSuccess) g->prof.ms[g->pcls[k]] += ms;
   }
-  g->npend = 0;
+  g->phead = (g->phead + m) % K;
+  g->npend -= m;
 }
+static void prof_drain(hjb_grid* g) { prof_drain_oldest(g, g->npend); }
 static void prof_pre(hjb_grid* g, int) {
   if (!g->prof_timing) return;
-  if (g->npend == hjb_grid::kSlots) prof_drain(g);
-  cudaEventRecord(g->pev[2 * g->npend], g->st);
+  if (g->npend == hjb_grid::kSlots) prof_drain_oldest(g, hjb_grid::kSlots / 2);
+  cudaEventRecord(g->pev[2 * ((g->phead + g->npend) % hjb_grid::kSlots)], g->st);
 }
 static void prof_post(hjb_grid* g, int cls, double nodes, double bytes, double flops) {
   g->prof.launches[cls] += 1;
@@ -180,8 +187,9 @@ static void prof_post(hjb_grid* g, int cls, double nodes, double bytes, double f
   g->prof.bytes[cls] += bytes;
   g->prof.flops[cls] += flops;
   if (!g->prof_timing) return;
-  cudaEventRecord(g->pev[2 * g->npend + 1], g->st);
-  g->pcls[g->npend] = cls;
+  const int k = (g->phead + g->npend) % hjb_grid::kSlots;
+  cudaEventRecord(g->pev[2 * k + 1], g->st);
+  g->pcls[k] = cls;
   g->npend += 1;
 }
 // LAUNCH(class, nodes, algorithmic bytes, algorithmic flops, kernel<<<...>>>(...))
