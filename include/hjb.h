@@ -204,7 +204,7 @@ typedef struct {
                                 (default 129 in 2D, 33 in 3D; BASELINE cfg4 "129^2 on one GPU") */
   int32_t gamma;             /* cycle index on the large levels: 1 = V-cycle, 2 = W-cycle (the
                                 coarse correction of level l is refined by gamma - 1 further
-                                cycles on the residual of level l+1); default 2               */
+                                cycles on the residual of level l+1); default 2 in 2D, 1 in 3D */
   int32_t gamma_min_nodes;   /* revisit level l+1 only if it owns >= gamma_min_nodes interior
                                 nodes (smaller levels are launch-latency bound: plain V there);
                                 default 131072                                                */
