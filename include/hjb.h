@@ -233,7 +233,8 @@ typedef struct {
                                 inexact evaluation is re-evaluated exactly before the step ends, so
                                 the fixed point is unchanged (DESIGN.md §3 reading xxii).
                                 0 = exact evaluation every iteration (the paper's Howard loop);
-                                default 0.03 (measured best at cfg4 among 0.03 / 0.1 / 0.3).     */
+                                default 0.01 (with the W-cycle measured best at cfg4 among
+                                0 / 0.003 / 0.01 / 0.03 / 0.1: 2071 / 1466 / 1441 / 1696 / 1700 ms). */
   int32_t guess;             /* hjb_step's initial iterate (the fixed point does not depend on it):
                                 HJB_GUESS_PREV (default): U_prev, as the paper's time march;
                                 HJB_GUESS_GIVEN: U as passed by the caller;

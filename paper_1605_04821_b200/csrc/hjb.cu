@@ -533,7 +533,7 @@ extern "C" void hjb_solve_params_default(int32_t dim, hjb_solve_params* o) {
   o->tol_pi = 1e-10;
   o->max_pi = 50;
   hjb_mg_params_default(dim, &o->mg);
-  o->pi_forcing = 0.03;
+  o->pi_forcing = 0.01;  // with the W-cycle (solves are cheap): 3 PI per step at cfg4 (DESIGN.md §3 xxii)
   o->guess = HJB_GUESS_PREV;
 }
 
