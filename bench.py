@@ -340,7 +340,7 @@ def run_b200(args):
                            "frac": ach / pk, "peak_source": src,
                            "launch_ms": c["ms"] / max(1, c["calls"] or c["launches"])}
     shares = {k: round(v["ms"] / ms_total, 4) for k, v in cls.items() if v["ms"] > 0}
-    if shares:   # launches over < 4096 nodes are not event-timed (library: kTimeMinNodes) + host gaps
+    if shares:   # launches over < 16384 nodes are not event-timed (library: kTimeMinNodes) + host gaps
         shares["untimed_small_launches_and_gaps"] = round(max(0.0, 1.0 - sum(shares.values())), 4)
     hbm_frac = {k: (v["bytes"] / (v["ms"] / 1e3) / 1e9) / float(peaks["hbm_gbs"])
                 for k, v in cls.items() if v["ms"] > 0 and k != "search"}

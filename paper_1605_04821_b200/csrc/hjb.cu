@@ -179,7 +179,7 @@ static void prof_drain(hjb_grid* g) { prof_drain_oldest(g, g->npend); }
 // levels, launch-latency bound) are not timed -- two event records each would add ~10 % to a W-cycle
 // step -- and their bytes / flops / nodes are left out so every class total stays the timed subset;
 // their device time is the unattributed remainder.  nodes <= 0: accounted by the caller, always timed.
-constexpr double kTimeMinNodes = 4096.0;
+constexpr double kTimeMinNodes = 16384.0;
 static bool prof_timed(const hjb_grid* g, double nodes) {
   return g->prof_timing && (nodes <= 0.0 || nodes >= kTimeMinNodes);
 }
