@@ -283,8 +283,11 @@ hjb_status hjb_step(hjb_grid_t g, double dt, const double* U_prev, double* U, ui
 
 /* ------------------------------------------------------------------- instrumentation
  * Every kernel launch of the library is counted per class.  With time_kernels != 0 each launch
- * is also bracketed by CUDA events on the grid's stream and its device time summed per class
- * (the events add ~2 us of host work per launch; off by default).  `bytes` is the ALGORITHMIC
+ * over >= 16384 nodes (and every control search) is also bracketed by CUDA events on the grid's
+ * stream and its device time summed per class (the events add ~2 us of host work per launch; off
+ * by default); smaller launches -- the launch-latency-bound small multigrid levels -- are then
+ * counted in `launches` only, not in calls / bytes / flops / nodes, so every class total is the
+ * timed subset and their device time is the unattributed remainder.  `bytes` is the ALGORITHMIC
  * HBM traffic of the launches (the per-node formulas of DESIGN.md §6 times the nodes each launch
  * processed), `flops` the algorithmic fp64 operations, so that bytes/ms and
  * flops/ms are roofline numerators.  Counters are per handle; reset clears them.              */
