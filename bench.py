@@ -4,6 +4,9 @@
 One "step" = one implicit Euler step t_{n-1} -> t_n solved by policy iteration through the C-ABI
 (`hjb_step`: control search + GMG-preconditioned BiCGSTAB per policy iteration), i.e. every row
 of SURVEY.md §8(a) once.  Metric (BASELINE.json): unknowns*steps/s = N_I * K / time.
+Steps follow the config's own schedule (cfg4: T = 1 in 8 implicit steps): step s of the run is step
+((s-1) mod n_steps) + 1 of a march, which restarts from g = u*(0) after n_steps, so every timed
+step lies in t in (0, T] (warm-up + timed steps may span several marches).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg4] [--impl b200|reference]
 
@@ -245,10 +248,11 @@ def run_b200(args):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # 256 MiB > 126 MB L2
     stream = torch.cuda.current_stream(dev)
     total = args.warmup + args.steps
-    # per-step inputs (problem data, generated before the timed region)
-    n_all = total
-    psis = [packed_psi(p, s * p.dt, device=dev) for s in range(1, n_all + 1)]
-    srcs = [p.f_tables(s * p.dt) for s in range(1, n_all + 1)]
+    # per-step inputs of one march (problem data, generated before the timed region)
+    ns = p.n_steps
+    psis = [packed_psi(p, s * p.dt, device=dev) for s in range(1, ns + 1)]
+    srcs = [p.f_tables(s * p.dt) for s in range(1, ns + 1)]
+    U0 = U.clone()                             # g = u*(0): every march starts here
 
     skw = {} if args.pi_forcing is None else {"pi_forcing": args.pi_forcing}
     mgkw = {} if args.nu is None else {"nu_pre": args.nu, "nu_post": args.nu}
@@ -261,17 +265,24 @@ def run_b200(args):
     if args.gamma_min is not None:
         mgkw["gamma_min_nodes"] = args.gamma_min
 
-    def do_step(s, Uin, Uout, polbuf, psi):
-        # initial iterate: linear extrapolation 2 U^{n-1} - U^{n-2} once two steps exist (Uout holds
-        # U^{n-2}: ping-pong buffers); the fixed point does not depend on it (DESIGN.md xxiv)
-        fb, fc = srcs[s - 1]
+    def step_of(s):          # step index within its march (1..n_steps)
+        return (s - 1) % ns + 1
+
+    def do_step(s, Uin, Uout, polbuf):
+        # march restart: U^0 = g (a device copy, part of the step's setup a1).  Initial iterate:
+        # linear extrapolation 2 U^{n-1} - U^{n-2} once two steps exist (Uout holds U^{n-2}:
+        # ping-pong buffers); the fixed point does not depend on it (DESIGN.md xxiv)
+        si = step_of(s)
+        if si == 1:
+            Uin.copy_(U0)
+        fb, fc = srcs[si - 1]
         g.set_source(fb, fc)
-        return g.step(p.dt, Uin, Uout, polbuf, psi, mg=mgkw, guess=(_lib.HJB_GUESS_EXTRAPOLATE if s >= 2
-                                                                    else _lib.HJB_GUESS_PREV), **skw)
+        return g.step(p.dt, Uin, Uout, polbuf, psis[si - 1], mg=mgkw,
+                      guess=(_lib.HJB_GUESS_EXTRAPOLATE if si >= 2 else _lib.HJB_GUESS_PREV), **skw)
 
     stats = []
     for s in range(1, args.warmup + 1):
-        do_step(s, U, U2, pol, psis[s - 1])
+        do_step(s, U, U2, pol)
         U, U2 = U2, U
     torch.cuda.synchronize()
     # state at the start of the timed region: the e2e pass replays exactly these steps
@@ -286,7 +297,7 @@ def run_b200(args):
     for i, s in enumerate(range(args.warmup + 1, total + 1)):
         flush.zero_()
         ev[i][0].record(stream)
-        stats.append(do_step(s, U, U2, pol, psis[s - 1]))
+        stats.append(do_step(s, U, U2, pol))
         ev[i][1].record(stream)
         U, U2 = U2, U
     torch.cuda.synchronize()
@@ -298,7 +309,7 @@ def run_b200(args):
     ms_total = allmax(sum(ms_steps))          # device time, max over ranks
     value = nI * args.steps / (ms_total / 1e3)
     # solution sanity vs the manufactured solution (not a parity claim; parity is in tests/)
-    t_end = total * p.dt
+    t_end = step_of(total) * p.dt
     from synth.device import local_index
     li = local_index(p, lay, device=dev)
     own = ~p.is_boundary(li)
@@ -318,10 +329,13 @@ def run_b200(args):
         per_launch_ms = c["ms"] / max(1, c["calls"] or c["launches"])   # per application
         if dom == "search":
             pk, src = fp64_peak()
-            ach = c["flops"] / (c["ms"] / 1e3) / 1e12
+            ach = c["nodes"] * search_flops_per_node(p) / (c["ms"] / 1e3) / 1e12
             roof = {"bound": "alu", "kernel": dom, "achieved": ach, "peak": pk, "unit": "TFLOP/s",
                     "frac": ach / pk, "traffic": traffic_for(dom, args.config, c),
-                    "peak_source": src, "launch_ms": per_launch_ms}
+                    "peak_source": src, "launch_ms": per_launch_ms,
+                    "flops_per_node": search_flops_per_node(p),
+                    "flop_count": "SURVEY §8(d): K[(2P+1) 2^d 2 + 2Q + 4], Q = 6 (2D) / 13 (3D) basis "
+                                  "terms of D8 (the library's own count uses the config's Q)"}
         else:
             ach = c["bytes"] / (c["ms"] / 1e3) / 1e9
             pk = float(peaks["hbm_gbs"])
@@ -335,9 +349,10 @@ def run_b200(args):
         if "search" in timed and dom != "search":
             c = timed["search"]
             pk, src = fp64_peak()
-            ach = c["flops"] / (c["ms"] / 1e3) / 1e12
+            ach = c["nodes"] * search_flops_per_node(p) / (c["ms"] / 1e3) / 1e12
             roof_search = {"bound": "alu", "achieved": ach, "peak": pk, "unit": "TFLOP/s",
                            "frac": ach / pk, "peak_source": src,
+                           "flops_per_node": search_flops_per_node(p),
                            "launch_ms": c["ms"] / max(1, c["calls"] or c["launches"])}
     shares = {k: round(v["ms"] / ms_total, 4) for k, v in cls.items() if v["ms"] > 0}
     if shares:   # launches over < 16384 nodes are not event-timed (library: kTimeMinNodes) + host gaps
@@ -348,7 +363,7 @@ def run_b200(args):
     # --------------------------------------------------------------- e2e through host buffers
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(g, p, args, snap, stream, srcs, psis, nI, dev, lay, bar, allmax, skw, mgkw)
+        e2e = run_e2e(g, p, args, snap, stream, srcs, psis, nI, dev, lay, bar, allmax, skw, mgkw, U0, step_of)
 
     pis = [st["pi_iters"] for st in stats]
     kr = [st["krylov_iters_total"] for st in stats]
@@ -357,24 +372,68 @@ def run_b200(args):
         "warmup": args.warmup, "ms_per_step": ms_total / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": workload_name(args.config, p), "n": p.n, "d": p.d, "K": p.K,
-                   "unknowns": nI, "dt": p.dt, "steps_from_t": args.warmup * p.dt,
+                   "unknowns": nI, "dt": p.dt, "n_steps_per_march": p.n_steps,
                    "parallelism": f"slab{world}", "l2": "256 MiB L2 flush before every timed step; "
                    "working set > L2"},
         "roofline": roof, "roofline_search": roof_search,
         "hbm_frac_by_class": hbm_frac, "time_share_by_class": shares,
+        "ms_per_step_spread": {"min": min(ms_steps), "median": statistics.median(ms_steps),
+                               "max": max(ms_steps), "all": [round(x, 2) for x in ms_steps]},
+        "t_range": [round((step_of(args.warmup + 1) - 1) * p.dt, 6), round(p.T, 6)]
+        if args.steps >= ns else [round((step_of(s) - 1) * p.dt, 6) for s in (args.warmup + 1, total)],
+        "march": f"T = {p.T:g} in {ns} implicit steps; restart from u*(0) after step {ns}",
         "mg_cycles_per_pi": (2 * sum(kr) / max(1, sum(pis))),
         "krylov_iters_per_pi": sum(kr) / max(1, sum(pis)), "pi_iters_per_step": sum(pis) / len(pis),
         "levels": stats[-1]["n_levels"], "final_rres": max(st["final_rres"] for st in stats),
+        "final_rres_inf": max(st["final_rres_inf"] for st in stats),
+        "final_R": max(st["final_R"] for st in stats),
         "max_err_vs_ustar": err, "wall_s_timed": wall,
         "gpu_launches": int(prof["total_launches"]), "clocks": clocks, "e2e": e2e,
     }
     if not args.no_cpu_baseline and rank == 0 and world == 1:
         v, s, desc = oracle_sample(cfg)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc,
-                                "seconds": s, "host_cpus": os.cpu_count()}
+                                "seconds": s, "host_cpus": os.cpu_count(),
+                                "fullsize_sample": oracle_fullsize_sample(p, U, pol)}
     if rank == 0:
         emit(line, args)
     g.close()
+
+
+def search_flops_per_node(p):
+    """K [(2P+1) 2^d 2 + 2Q + 4] algorithmic fp64 flops per node of the control search,
+    with Q = 6 (2D) / 13 (3D) source basis terms (derivation D8)."""
+    q = 6 if p.d == 2 else 13
+    return p.K * ((2 * p.P + 1) * (1 << p.d) * 2 + 2 * q + 4)
+
+
+def oracle_fullsize_sample(p, U, pol, m=1 << 15):
+    """SURVEY §8(d) oracle baseline at the FULL config size: the oracle's brute-force control search
+    and matrix-free apply on m sampled interior rows of the real grid (1 thread), as rows/s."""
+    import numpy as np
+    from threadpoolctl import threadpool_limits
+
+    from oracle.howard import control_search
+    from oracle.scheme import apply_operator
+    rng = np.random.default_rng(11)
+    mi = [rng.integers(1, p.n - 1, size=m) for _ in range(p.d)]
+    idx = np.zeros(m, dtype=np.int64)
+    for k in reversed(range(p.d)):
+        idx = idx * p.n + mi[k]
+    Uh = U.cpu().numpy()
+    polh = pol.cpu().numpy().astype(np.int64)
+    fields = p.fields(idx)
+    with threadpool_limits(limits=1):
+        t0 = time.perf_counter()
+        control_search(p, Uh, Uh, p.dt, p.dt, fields=fields, idx=idx)
+        ts = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        apply_operator(p, polh, Uh, p.dt, idx=idx, fields=fields)
+        ta = time.perf_counter() - t0
+    return {"search_rows_per_s": m / ts, "apply_rows_per_s": m / ta, "rows": m, "cores": 1,
+            "search_s": ts, "apply_s": ta,
+            "sample": f"oracle control search (K={p.K}) and apply on {m} random interior rows of the "
+                      f"full {p.n}^{p.d} grid, 1 thread"}
 
 
 def workload_name(cfg, p):
@@ -397,10 +456,11 @@ def traffic_for(cls, config, c):
     return e["dram_bytes_per_node"] * c["nodes"] / max(1, c["calls"] or c["launches"])
 
 
-def run_e2e(g, p, args, snap, stream, srcs, psis, nI, dev, lay, bar, allmax, skw, mgkw):
+def run_e2e(g, p, args, snap, stream, srcs, psis, nI, dev, lay, bar, allmax, skw, mgkw, U0, step_of):
     """The SAME K steps as the timed region (replayed from its starting state) through hjb_step with
     pinned HOST buffers: each step copies U_prev, the policy and psi host->device and U + policy
-    device->host inside the timed region (inside the call)."""
+    device->host inside the timed region (inside the call).  A march restart passes a pinned host
+    copy of g = u*(0) (prepared before the timed region, one per restart) as U_prev."""
     import torch
     N = lay["local_elems"]
     Uh_prev, Uh, polh = snap          # U^{W}, U^{W-1}, policy at the start of the timed region
@@ -409,6 +469,8 @@ def run_e2e(g, p, args, snap, stream, srcs, psis, nI, dev, lay, bar, allmax, skw
     psi_np = [x.numpy() for x in psih]
     base = args.warmup
     n_e2e = args.steps
+    restarts = [s for s in range(base + 1, base + n_e2e + 1) if step_of(s) == 1]
+    u0h = {s: U0.cpu().pin_memory().numpy() for s in restarts}
     bar()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -417,10 +479,13 @@ def run_e2e(g, p, args, snap, stream, srcs, psis, nI, dev, lay, bar, allmax, skw
     from paper_1605_04821_b200 import _lib
     for i in range(n_e2e):
         s = base + i + 1
-        fb, fc = srcs[s - 1]
+        si = step_of(s)
+        if si == 1:
+            Uhp_np = u0h[s]
+        fb, fc = srcs[si - 1]
         g.set_source(fb, fc)
-        g.step(p.dt, Uhp_np, Uh_np, pol_np, psi_np[s - 1], mg=mgkw, **skw,
-               guess=_lib.HJB_GUESS_EXTRAPOLATE if s >= 2 else _lib.HJB_GUESS_PREV)
+        g.step(p.dt, Uhp_np, Uh_np, pol_np, psi_np[si - 1], mg=mgkw, **skw,
+               guess=_lib.HJB_GUESS_EXTRAPOLATE if si >= 2 else _lib.HJB_GUESS_PREV)
         Uhp_np, Uh_np = Uh_np, Uhp_np
     ev1.record(stream)
     torch.cuda.synchronize()

@@ -57,7 +57,8 @@ typedef enum {
   HJB_ERR_CUDA = 5,
   HJB_ERR_NCCL = 6,
   HJB_ERR_NOT_CONVERGED = 7, /* Krylov or policy iteration hit max iterations; U holds the best iterate */
-  HJB_ERR_BREAKDOWN = 8,     /* BiCGSTAB rho or (r_hat, v) == 0 */
+  HJB_ERR_BREAKDOWN = 8,     /* BiCGSTAB (r_hat, v) == 0, rho == 0 or omega == 0 in the last of
+                                its restarts (x is never updated with a non-finite coefficient) */
   HJB_ERR_NONFINITE = 9      /* NaN/Inf in a residual */
 } hjb_status;
 
@@ -241,6 +242,11 @@ typedef struct {
                                 HJB_GUESS_EXTRAPOLATE: U holds U^{n-2} on entry and the iterate is
                                 2 U_prev - U^{n-2} (linear extrapolation in time, DESIGN.md xxiv).
                                 Boundary entries are always set to psi(t_n) (if given).         */
+  double krylov_rtol_inf;    /* secondary stop of an EXACT evaluation: also ||F - A X||_inf <=
+                                krylov_rtol_inf ||F||_inf (default 1e-9; 0 = off).  The 2-norm rule
+                                alone bounds ||r||_inf only by sqrt(N) krylov_rtol ||F||_2 (SURVEY
+                                §8c-xvii; reading xvii).  Inexact evaluations (pi_forcing)
+                                use the 2-norm rule only.                                       */
 } hjb_solve_params;
 
 #define HJB_GUESS_PREV 0
@@ -276,8 +282,10 @@ typedef struct {
   double final_rres;                         /* true relative residual of the last solve */
   double ms_search, ms_setup, ms_solve;      /* device time per phase (CUDA events) */
   int32_t n_levels;
+  double final_rres_inf;                     /* ||F - A X||_inf / ||F||_inf of the last solve */
 } hjb_step_stats;
 
+/* U may alias U_prev (in-place step): U_prev is then copied to an internal buffer first.    */
 hjb_status hjb_step(hjb_grid_t g, double dt, const double* U_prev, double* U, uint8_t* policy,
                     const double* psi_packed, const hjb_solve_params* p, hjb_step_stats* out);
 

@@ -11,6 +11,7 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -214,7 +215,10 @@ static void prof_post(hjb_grid* g, int cls, double nodes, double bytes, double f
 // CTAs are made co-resident (occupancy x SMs) so the lines in flight form one band that moves
 // through the grid and the +-reach rows it gathers from stay in L2.
 static int occupancy_of(const void* fn, size_t smem = 0) {
+  // shared by every handle; thread-rank grids (HJB_COMM_THREADS) call it concurrently
+  static std::mutex mu;
   static std::map<std::pair<const void*, size_t>, int> cache;
+  std::lock_guard<std::mutex> lock(mu);
   const auto key = std::make_pair(fn, smem);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
@@ -535,6 +539,7 @@ extern "C" void hjb_solve_params_default(int32_t dim, hjb_solve_params* o) {
   hjb_mg_params_default(dim, &o->mg);
   o->pi_forcing = 0.01;  // with the W-cycle (solves are cheap): 3 PI per step at cfg4 (DESIGN.md §3 xxii)
   o->guess = HJB_GUESS_PREV;
+  o->krylov_rtol_inf = 1e-9;  // SURVEY §8c-xvii secondary stop (reading xvii)
 }
 
 // ---------------------------------------------------------------------------- API: partition
@@ -1423,7 +1428,7 @@ extern "C" hjb_status hjb_mg_setup(hjb_grid_t g, double dt, const uint8_t* polic
   if (g->mg_gamma > 1)
     for (size_t l = 1; l + 1 < g->levels.size(); ++l) {
       Level& lv = g->levels[l];
-      if (lv.L.n_own < g->gamma_min) continue;
+      if (ipow(lv.L.n - 2, g->D) < g->gamma_min) continue;  // global count: same on every rank
       const size_t vb = (size_t)lv.elems * sizeof(double);
       if (!lv.r2) {
         TRY(dalloc((void**)&lv.r2, vb));
@@ -1503,7 +1508,8 @@ static hjb_status vcycle(hjb_grid* g, size_t l, const double* b, double* out) {
     CKL();
   }
   TRY(vcycle<D>(g, l + 1, lc.b, lc.x));
-  const int gamma = (lc.L.n_own >= g->gamma_min) ? g->mg_gamma : 1;
+  // revisit decided on the level's GLOBAL interior count, so every rank takes the same branch
+  const int gamma = (ipow(lc.L.n - 2, D) >= g->gamma_min) ? g->mg_gamma : 1;
   for (int k = 1; k < gamma && l + 2 < g->levels.size(); ++k) {  // W-cycle: revisit the coarse level
     const uint8_t* pc = lc.pol;
     TRY(halo_exchange(g, lc, lc.x, lc.H));
@@ -1578,11 +1584,14 @@ static hjb_status bicgstab(hjb_grid* g, double dt, const uint8_t* pol, const dou
   double bn2, bninf;
   TRY(norms_dev<D>(g, F, &bn2, &bninf));
   double tol = sp->krylov_rtol * bn2;
+  // secondary max-norm stop of an exact evaluation (reading xvii): ||r||_inf <= rtol_inf ||F||_inf
+  const double tol_inf = (eta > 0.0 || !(sp->krylov_rtol_inf > 0.0)) ? INFINITY : sp->krylov_rtol_inf * bninf;
   int it = 0;
   hjb_status err = HJB_OK;
   double rr = 0.0;
-  bool converged = false;
-  for (int restart = 0; restart < 4 && !converged; ++restart) {
+  bool converged = false, broke = false, early = false;
+  double tol_iter = tol;  // target of the recursive residual (tightened if the max-norm stop fails)
+  for (int restart = 0; restart < 6 && !converged; ++restart) {
     // r = F - A x ; rhat = r ; p = r
     TRY(halo_exchange(g, lv0, x, H));
     launch_operator<D>(g, L, C, OP_RESID, 0, dt, 0.0, pol, x, F, g->r, nullptr);
@@ -1592,10 +1601,11 @@ static hjb_status bicgstab(hjb_grid* g, double dt, const uint8_t* pol, const dou
     rr = host_finalize(g, g->nblk_last, 0u, SC_INIT, &err);
     if (err != HJB_OK) return err;
     if (!std::isfinite(rr)) return fail(HJB_ERR_NONFINITE, "non-finite residual");
-    if (restart == 0 && eta > 0.0) tol = std::max(tol, eta * std::sqrt(rr));
-    if (std::sqrt(rr) <= tol) { converged = true; break; }
+    if (restart == 0 && eta > 0.0) tol = tol_iter = std::max(tol, eta * std::sqrt(rr));
+    if (std::sqrt(rr) <= tol && tol_inf == INFINITY) { converged = early = true; break; }
     int inner = 0;
-    while (it < sp->krylov_maxit) {
+    broke = false;
+    while (it < sp->krylov_maxit && std::sqrt(rr) > tol_iter) {
       if (inner > 0)
         LAUNCH(HJB_KC_VECTOR, L.n_own, 32.0 * L.n_own, 4.0 * L.n_own,
                k_bicg_p<D><<<dims(g, L, (const void*)k_bicg_p<D>), dim3(kBX, kBY), 0, st>>>(L, g->S, g->r, g->p, g->v));
@@ -1618,28 +1628,34 @@ static hjb_status bicgstab(hjb_grid* g, double dt, const uint8_t* pol, const dou
       ++it;
       ++inner;
       rr = g->hS->rr;
+      // a breakdown keeps every coefficient finite (alpha = 0 / omega = 0 steps, scal_update), so x
+      // is valid here: restart from it
+      if (g->hS->breakdown) { broke = true; break; }
       if (!std::isfinite(rr)) return fail(HJB_ERR_NONFINITE, "non-finite residual in BiCGSTAB");
-      if (std::sqrt(rr) <= tol) break;
-      if (g->hS->breakdown) break;  // restart from the current iterate
     }
-    // true residual check (recursive residual drifts, SURVEY hard part 5)
+    // true residual check (recursive residual drifts, SURVEY hard part 5) in both norms
     TRY(halo_exchange(g, lv0, x, H));
     launch_operator<D>(g, L, C, OP_RESID, 0, dt, 0.0, pol, x, F, g->r, nullptr);
     double tr2, trinf;
     TRY(norms_dev<D>(g, g->r, &tr2, &trinf));
+    if (!std::isfinite(tr2)) return fail(HJB_ERR_NONFINITE, "non-finite true residual");
     if (out) {
       out->iters = it;
       out->rres = bn2 > 0 ? tr2 / bn2 : tr2;
       out->rres_inf = bninf > 0 ? trinf / bninf : trinf;
     }
-    if (tr2 <= tol) { converged = true; break; }
+    if (tr2 <= tol && trinf <= tol_inf) { converged = true; break; }
+    // tighten the 2-norm target in proportion to the max-norm excess (or the drift of the recursion)
+    if (trinf > tol_inf) tol_iter = std::min(tol_iter, 0.5 * tr2 * (tol_inf / trinf));
+    else tol_iter = std::min(tol_iter, 0.5 * tol * (tol / std::max(tr2, tol)));
     if (it >= sp->krylov_maxit) break;
   }
-  if (out && converged && it == 0) {
+  if (out && early) {
     out->iters = 0;
     out->rres = bn2 > 0 ? std::sqrt(rr) / bn2 : 0.0;
     out->rres_inf = 0.0;
   }
+  if (!converged && broke) return fail(HJB_ERR_BREAKDOWN, "BiCGSTAB breakdown in its last restart");
   if (!converged) return fail(HJB_ERR_NOT_CONVERGED, "BiCGSTAB did not reach the tolerance");
   return HJB_OK;
 }
@@ -1671,11 +1687,14 @@ extern "C" hjb_status hjb_step(hjb_grid_t g, double dt, const double* U_prev, do
   const bool h_pol = policy && !is_device_ptr(policy), h_psi = psi && !is_device_ptr(psi);
   const double* dprev = U_prev;
   double* dU = U;
+  const bool alias = (U == U_prev) && !h_prev;  // in-place step on device memory
   uint8_t* dpol = policy ? policy : g->pol_int;
   const double* dpsi = psi;
-  if (h_prev) {
+  if (h_prev || alias) {
+    // host U_prev is staged; a device U_prev that is also the output U is copied first, else the
+    // first solve would overwrite U^{n-1} and every later F = U^{n-1} + dt f would be wrong
     if (!g->stage_prev) TRY(dalloc((void**)&g->stage_prev, vb));
-    CK(cudaMemcpyAsync(g->stage_prev, U_prev, vb, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(g->stage_prev, U_prev, vb, h_prev ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st));
     dprev = g->stage_prev;
   }
   if (sp->guess < HJB_GUESS_PREV || sp->guess > HJB_GUESS_EXTRAPOLATE)
@@ -1751,7 +1770,7 @@ extern "C" hjb_status hjb_step(hjb_grid_t g, double dt, const double* U_prev, do
     const double eta = (settled || g->K == 1) ? 0.0 : sp->pi_forcing;  // K = 1: the policy is final
     hjb_status s = g->D == 2 ? bicgstab<2>(g, dt, dpol, g->F, dU, sp, &ss, eta)
                              : bicgstab<3>(g, dt, dpol, g->F, dU, sp, &ss, eta);
-    last_exact = (ss.rres <= sp->krylov_rtol);
+    last_exact = (ss.rres <= sp->krylov_rtol) && (!(sp->krylov_rtol_inf > 0.0) || ss.rres_inf <= sp->krylov_rtol_inf);
     cudaEventRecord(g->ev[2], st);
     cudaEventSynchronize(g->ev[2]);
     cudaEventElapsedTime(&ms, g->ev[0], g->ev[1]);
@@ -1762,6 +1781,7 @@ extern "C" hjb_status hjb_step(hjb_grid_t g, double dt, const double* U_prev, do
     S.krylov_iters[slot] = ss.iters;
     S.krylov_iters_total += ss.iters;
     S.final_rres = ss.rres;
+    S.final_rres_inf = ss.rres_inf;
     if (s != HJB_OK) { result = s; break; }
   }
   S.n_levels = (int32_t)g->levels.size();

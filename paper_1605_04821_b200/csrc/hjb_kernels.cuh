@@ -273,7 +273,9 @@ __device__ __forceinline__ void scal_update(KScal* S, const double* red, int whi
   } else if (which == SC_AFTER_V) {  // red[0] = (rhat, v)
     S->rhat_v = red[0];
     if (red[0] == 0.0 || !(red[0] == red[0])) S->breakdown = 1;
-    S->alpha = S->rho / red[0];
+    // on breakdown alpha = 0 keeps x finite: the half step is skipped and the omega step that
+    // follows is a plain minimal-residual step; the host then restarts from x
+    S->alpha = S->breakdown == 1 ? 0.0 : S->rho / red[0];
   } else if (which == SC_AFTER_T) {  // red = [(t,s), (t,t)]
     S->ts = red[0]; S->tt = red[1];
     S->omega = (red[1] > 0.0) ? red[0] / red[1] : 0.0;

@@ -63,6 +63,8 @@ def test_fullsize_apply_sampled(cfg):
     # of ~(n-1) eps cells in the fraction s at large n (the grid-unit GPU path has ~|o| eps)
     tol = 1e-12 + 4.0 * (p.n - 1) * np.finfo(float).eps
     err = np.abs(yg - yo) / scale
+    print(f"cfg{cfg}: row-wise apply error / rounding scale: max {err.max():.3e} (tolerance {tol:.3e}); "
+          f"max-norm relative {np.abs(yg - yo).max() / np.abs(yo).max():.3e}")
     assert err.max() <= tol, (err.max(), tol)
 
 

@@ -229,6 +229,36 @@ def test_host_pointer_step_matches_device():
     assert np.array_equal(Uh, Ud.cpu().numpy())
 
 
+def test_in_place_device_step_matches_out_of_place():
+    """U == U_prev on device memory: U_prev is copied before the first solve overwrites
+    it, so the in-place step equals the out-of-place step bitwise (and the oracle)."""
+    torch = require_gpu()
+    p = bj_config(0)
+    g, fields = setup(p)
+    U0 = p.g(p.all_idx())
+    psi = to_dev(p.psi(p.dt, p.boundary_idx()), torch)
+    Ud = torch.empty(p.N, dtype=torch.float64, device="cuda")
+    st1 = g.step(p.dt, to_dev(U0, torch), Ud, None, psi)
+    Uin = to_dev(U0, torch)
+    st2 = g.step(p.dt, Uin, Uin, None, psi)
+    assert np.array_equal(Uin.cpu().numpy(), Ud.cpu().numpy()), (st1, st2)
+    Uo, _, _ = howard_step(p, U0, p.dt, p.dt)
+    assert np.abs(Uin.cpu().numpy() - Uo).max() <= 1e-8 * max(1.0, np.abs(Uo).max())
+
+
+def test_exact_evaluation_meets_max_norm_stop():
+    """Reading xvii: an exact policy evaluation also satisfies ||F - A X||_inf <= 1e-9 ||F||_inf
+    (secondary stop), reported in the step statistics."""
+    torch = require_gpu()
+    p = bj_config(2, n=257, K=8)
+    g, fields = setup(p)
+    U0 = p.g(p.all_idx())
+    psi = to_dev(p.psi(p.dt, p.boundary_idx()), torch)
+    Ud = torch.empty(p.N, dtype=torch.float64, device="cuda")
+    st = g.step(p.dt, to_dev(U0, torch), Ud, None, psi, pi_forcing=0.0)
+    assert st["final_rres"] <= 1e-12 and st["final_rres_inf"] <= 1e-9, st
+
+
 def test_edge_cases():
     torch = require_gpu()
     # single control -> exactly one policy evaluation (S:379)

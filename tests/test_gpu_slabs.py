@@ -166,3 +166,19 @@ def test_slab_step_matches_oracle(name, cfg, n, K, R, steps, mg):
         assert [st["krylov_iters_total"] for st in q[2]] == [st["krylov_iters_total"] for st in parts[0][2]]
     if mg.get("gather_n") == 33 and "gamma" not in mg:
         assert parts[0][2][-1]["n_levels"] >= 4
+
+
+def test_wcycle_revisit_is_rank_independent():
+    """the W-cycle revisit is decided on a coarse level's GLOBAL interior count, so every
+    rank count takes the same branch.  gamma_min_nodes = 127^2 (the 129^2 level of n = 257) sits
+    exactly at the global count: a per-rank count (~127^2 / R) would skip the revisit for R > 1
+    (and desynchronise the collectives across ranks).  Identical Krylov counts for R = 1, 2, 3."""
+    p = bj_config(2, n=257, K=8)
+    mg = {"gather_n": 33, "gamma": 2, "gamma_min_nodes": 127 * 127}
+    counts = []
+    for R in (1, 2, 3):
+        parts = _slab_march(p, R, 1, mg=mg, pi_forcing=1e-2)
+        counts.append([st["krylov_iters"] for st in parts[0][2]])
+        for q in parts[1:]:
+            assert [st["krylov_iters"] for st in q[2]] == counts[-1]
+    assert counts[0] == counts[1] == counts[2], counts

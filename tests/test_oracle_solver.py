@@ -8,7 +8,7 @@ import os
 import numpy as np
 import pytest
 
-from oracle.howard import control_search, howard_step, march
+from oracle.howard import control_search, hamiltonian, howard_step, march
 from oracle.scheme import Geometry, apply_operator
 from oracle.system import assemble, dense_solve, solve
 from synth import bj_config, problem_A, problem_B
@@ -172,3 +172,52 @@ def test_manufactured_convergence_rate():
     rate = 0.5 * math.log2(errs[0] / errs[2])     # averaged over two refinements
     assert 0.5 <= rate <= 1.3 and errs[1] < errs[0] and errs[2] < errs[1], errs
     assert errs[-1] < 0.02
+
+
+
+def test_manufactured_convergence_noisy_scales():
+    """The cfg2 coefficient model with its per-node noise (reading xv) and K = (n-1)/2 (theta*(x_j)
+    on the control grid, so u* is exact for the discrete control set): the marched oracle solution
+    converges to u* (P:138-141).  The sharp pin of the scale branch is the consistency test below."""
+    errs = []
+    for n in (17, 33, 65):
+        p = bj_config(2, n=n, K=(n - 1) // 2, n_steps=2)
+        assert p.meta["noisy"]
+        U, _, _ = march(p)
+        errs.append(np.abs(U - p.u_exact(p.T, p.all_idx())).max())
+    rate = 0.5 * math.log2(errs[0] / errs[2])
+    assert 0.5 <= rate <= 1.5 and errs[1] < errs[0] and errs[2] < errs[1], errs
+
+
+def test_noisy_scale_branch_consistency():
+    """Pins the per-node scale branch of oracle.scheme.node_coefficients (sigma_scale / b_scale: the
+    whole cfg2/cfg4 noise model, reading xv) against the PDE, not against itself.  The manufactured
+    source is f^a = u*_t - L^a u* - c u* + (theta_a - theta*(x))^2 with the PERTURBED coefficients
+    (synth/problems.py), so at U = u*(t) on the grid, for EVERY control a and deep node j,
+        E^a_j = H^a_j(u*) - u*_t(x_j) - (theta_a - theta*(x_j))^2 = (L_hat^a - L^a) u*(x_j),
+    the LISL consistency error, O(k^2) + O(h^2/k^2) = O(h).  Measured when written
+    (K = 64, 2000 sampled deep nodes, n = 257 / 1025 / 4097): correct 2.9e-2 / 7.0e-3 / 1.8e-3
+    (rate 1.01 per halving of h); sigma_scale rows swapped 0.47 / 0.44 / 0.43; sigma_scale dropped
+    0.33 / 0.32 / 0.34; b_scale dropped 3.0e-2 / 1.7e-2 / 1.6e-2 (rate 0.22)."""
+    es = []
+    for n in (257, 1025, 4097):
+        p = bj_config(2, n=n, K=64)
+        geo = Geometry.of(p)
+        rng = np.random.default_rng(1)
+        i1 = rng.integers(n // 5, n - n // 5, 2000)
+        i2 = rng.integers(n // 5, n - n // 5, 2000)
+        idx = np.unique(i2 * n + i1)
+        t = 0.5
+        U = p.u_exact(t, p.all_idx())
+        f = p.fields(idx)
+        assert np.ptp(f["sigma_scale"][0]) > 0.01 and np.ptp(f["b_scale"]) > 0.01   # the branch is live
+        x = geo.node_x(idx)
+        ut = np.sin(np.pi * x[:, 0] / 2) * np.cos(np.pi * x[:, 1] / 2)         # d/dt of (1+t) sin cos
+        thstar = np.pi * np.abs(x[:, 0]) % np.pi
+        E = 0.0
+        for a in range(p.K):
+            H, _, _ = hamiltonian(p, idx, np.full(idx.size, a), U, t, f)
+            E = max(E, float(np.abs(H - ut - (a * math.pi / p.K - thstar) ** 2).max()))
+        es.append(E)
+    rate = math.log2(es[0] / es[2]) / 4                                          # h shrinks 16x
+    assert rate >= 0.85 and es[2] <= 4e-3, es
