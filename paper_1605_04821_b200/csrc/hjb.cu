@@ -20,6 +20,7 @@
 #include "hjb_kernels.cuh"
 #include "hjb_tma.cuh"
 #include "hjb_win.cuh"
+#include "hjb_search2.cuh"
 
 namespace hjb {
 struct WinPlan {
@@ -145,6 +146,7 @@ struct hjb_grid {
   int nblk_last = 1;  // CTAs of the last dims() launch (partials to reduce)
   // deep rectangles (2D): per-rank scale-field ranges and per-axis endpoint reach
   std::vector<double> h_sd, h_bd;  // host copies of sigma_dir / b_dir
+  std::vector<double> h_cc, h_fc, h_fb;  // host copies of c_ctrl / f_ctrl / f_basis (k_search_deep2 tables)
   double* d_rng = nullptr;    // [scmin_p, scmax_p]_p, [bsmin, bsmax]
   bool reach_ok = false;      // per-axis reach known (scale fields only): deep rectangles enabled
   bool tma_ok = false;        // TMA-windowed search tiles (k_search_tma)
@@ -159,6 +161,9 @@ struct hjb_grid {
                                // over the whole interior (general geometry)
   double rdiff_ax[3] = {0, 0, 0}, rdrift_ax[3] = {0, 0, 0};
   double* rng_part = nullptr; // k_field_ranges block partials
+  double2* upair = nullptr;   // (U_i, U_{i+1}) pair copy of the searched U (k_search_deep2)
+  bool drift_reg = false;     // deep drift endpoints stay within one cell of the node (|offset| < 1)
+  double h_rng[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // host copy of d_rng (scale-field ranges)
 };
 
 // ---------------------------------------------------------------------------- instrumentation
@@ -637,6 +642,7 @@ extern "C" hjb_status hjb_grid_destroy(hjb_grid_t g) {
   cudaFree(g->grecv);
   cudaFree(g->d_rng);
   cudaFree(g->rng_part);
+  cudaFree(g->upair);
   cudaFree(g->S);
   cudaFree(g->pol_int);
   cudaFree(g->stage_pol);
@@ -782,6 +788,9 @@ static hjb_status upload_tables(hjb_grid* g, const double* sigma_dir, const doub
   g->C0.f_ctrl = g->d_tab + nsd + nbd + nc + nfb;
   g->h_sd.assign(h.begin(), h.begin() + nsd);
   g->h_bd.assign(h.begin() + nsd, h.begin() + nsd + nbd);
+  g->h_cc.assign(h.begin() + nsd + nbd, h.begin() + nsd + nbd + nc);
+  g->h_fb.assign(h.begin() + nsd + nbd + nc, h.begin() + nsd + nbd + nc + nfb);
+  g->h_fc.assign(h.begin() + nsd + nbd + nc + nfb, h.begin() + tot);
   return HJB_OK;
 }
 
@@ -933,6 +942,7 @@ static hjb_status setup_deep(hjb_grid* g) {
   }
   for (int k = 0; k < nv; ++k)
     if (!std::isfinite(rng[k])) return HJB_OK;
+  std::memcpy(g->h_rng, rng, sizeof(rng));
   CK(cudaMemcpyAsync(g->d_rng, rng, nv * sizeof(double), cudaMemcpyHostToDevice, g->st));
   CK(cudaStreamSynchronize(g->st));
   // reach per axis over all controls / endpoints (diffusion and drift separately: they scale
@@ -949,6 +959,7 @@ static hjb_status setup_deep(hjb_grid* g) {
         rr = std::max(rr, r);
       }
   g->reach_ok = true;
+  g->drift_reg = g->rdrift_ax[0] < 1.0 - 1e-9 && g->rdrift_ax[1] < 1.0 - 1e-9;
   // TMA-windowed search tiles inside the deep rectangle of the fine level (single tensor map view)
   g->tma_ok = false;
 #ifndef HJB_NO_TMA
@@ -1062,6 +1073,8 @@ extern "C" hjb_status hjb_set_source(hjb_grid_t g, const double* f_basis, const 
   if (f_ctrl) std::memcpy(h.data() + (size_t)K * Q, f_ctrl, (size_t)K * sizeof(double));
   CK(cudaMemcpyAsync((void*)g->C0.f_basis, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice, g->st));
   CK(cudaStreamSynchronize(g->st));
+  g->h_fb.assign(h.begin(), h.begin() + (size_t)K * Q);
+  g->h_fc.assign(h.begin() + (size_t)K * Q, h.end());
   return HJB_OK;
 }
 
@@ -1089,6 +1102,83 @@ static hjb_status halo_input(hjb_grid* g, const double* x, const double** out) {
 }
 
 // ---------------------------------------------------------------------------- policy improvement
+// k_search_deep2 (hjb_search2.cuh): 2D, no offset fields, the control tables fit the parameter
+// structs, Q in {1,2,8}, scale fields of one sign over the rank (zero steps and the drift quadrant are
+// per-control facts), drift endpoints within one cell, table entries either 0 or far from underflow
+static bool search2_ok(hjb_grid* g) {
+  const int P = g->P, Q = g->Q, K = g->K;
+  const int S = 2 * P + 4 + Q + P + 2;
+  if (g->D != 2 || !(Q == 1 || Q == 2 || Q == 8) || K * S > kSTabN || K > 256) return false;
+  if (g->C0.sigma_node || g->C0.b_node || !g->reach_ok || !g->drift_reg) return false;
+  for (int p = 0; p < P; ++p)
+    if (!(g->h_rng[2 * p] > 0.0)) return false;     // min sigma scale > 0
+  if (!(g->h_rng[2 * P] > 0.0)) return false;       // min b scale > 0
+  for (double v : g->h_sd)
+    if (v != 0.0 && std::fabs(v) < 1e-200) return false;
+  for (double v : g->h_bd)
+    if (v != 0.0 && std::fabs(v) < 1e-200) return false;
+  return true;
+}
+
+template <int P, int Q>
+static void search2_launch(hjb_grid* g, const LevelDev& LL, double dt, const double* U, const double* Uprev,
+                           uint8_t* pol, double* F, const SkipRect& rect, const STab& tab, const STabQuad& quad,
+                           int* nblk) {
+  const void* fn = (const void*)k_search_deep2<P, Q>;
+  LAUNCH(HJB_KC_SEARCH, 0, 0, 0,
+         k_search_deep2<P, Q><<<dims(g, LL, fn, kSBX), dim3(kSBX, kSBY), 0, g->st>>>(
+             g->L0, g->C0, dt, U, g->upair, Uprev, pol, F, g->partial + 2 * *nblk, rect, tab, quad));
+  *nblk += g->nblk_last;
+}
+
+template <int P, int Q>
+static void search2_tables(hjb_grid* g, STab& tab, STabQuad& quad) {
+  using T = STabLayout<P, Q>;
+  const double* sd = g->h_sd.data();
+  const double* bd = g->h_bd.data();
+  const double inv_2k2 = g->L0.inv_2k2, inv_k2 = g->L0.inv_k2;
+  for (int a = 0; a < g->K; ++a) {
+    double* t = tab.v + a * T::S;
+    double wsum = 0.0;
+    for (int p = 0; p < P; ++p) {
+      t[T::SD + 2 * p] = sd[(a * P + p) * 2];
+      t[T::SD + 2 * p + 1] = sd[(a * P + p) * 2 + 1];
+      const bool nz = sd[(a * P + p) * 2] != 0.0 || sd[(a * P + p) * 2 + 1] != 0.0;
+      t[T::W + p] = nz ? inv_2k2 : 0.0;
+      wsum += 2.0 * t[T::W + p];
+    }
+    t[T::BD] = bd[a * 2];
+    t[T::BD + 1] = bd[a * 2 + 1];
+    t[T::WD] = (bd[a * 2] != 0.0 || bd[a * 2 + 1] != 0.0) ? inv_k2 : 0.0;
+    t[T::WSUM] = wsum + t[T::WD];
+    t[T::C] = g->h_cc[a];
+    t[T::FC] = g->h_fc[a];
+    for (int q = 0; q < Q; ++q) t[T::FB + q] = g->h_fb[(size_t)a * Q + q];
+    quad.v[a] = (bd[a * 2] < 0.0 ? 1 : 0) | (bd[a * 2 + 1] < 0.0 ? 2 : 0);
+  }
+}
+
+static hjb_status launch_search2(hjb_grid* g, double dt, const double* U, const double* Uprev, uint8_t* pol,
+                                 double* F, const SkipRect& rect, int* nblk) {
+  static thread_local STab tab;       // 24 KB + 1 KB: kernel parameters, not on the stack
+  static thread_local STabQuad quad;
+  const LevelDev LL = shape_of(g->L0, rect);
+#define S2(PP, QQ)                                                              \
+  do {                                                                          \
+    search2_tables<PP, QQ>(g, tab, quad);                                       \
+    search2_launch<PP, QQ>(g, LL, dt, U, Uprev, pol, F, rect, tab, quad, nblk); \
+  } while (0)
+  const int P = g->P, Q = g->Q;
+  if (P == 1) {
+    if (Q == 1) S2(1, 1); else if (Q == 2) S2(1, 2); else S2(1, 8);
+  } else {
+    if (Q == 1) S2(2, 1); else if (Q == 2) S2(2, 2); else S2(2, 8);
+  }
+#undef S2
+  CKL();
+  return HJB_OK;
+}
+
 // U's halo rows must already be exchanged
 static hjb_status policy_update_dev(hjb_grid* g, double dt, const double* U, const double* Uprev, uint8_t* pol,
                                     double* F, hjb_pi_stats* out) {
@@ -1110,7 +1200,9 @@ static hjb_status policy_update_dev(hjb_grid* g, double dt, const double* U, con
   const WinPlan* wp = use_tma ? nullptr : g->win_full.ok ? &g->win_full : (has_deep && g->win_deep.ok) ? &g->win_deep : nullptr;
   const bool win_all = wp == &g->win_full;
   const int ngs = win_all ? 0 : ring_strips(full, rect, gstrips);
-  const int nds = (has_deep && !wp) ? ring_strips(rect, tiles, dstrips) : 0;
+  // 2D deep rectangle without a window / TMA plan: the L1-lean k_search_deep2 (hjb_search2.cuh)
+  const bool deep2 = g->D == 2 && has_deep && !wp && !use_tma && search2_ok(g) && !getenv("HJB_NO_SEARCH2");
+  const int nds = (has_deep && !wp && !deep2) ? ring_strips(rect, tiles, dstrips) : 0;
 #define SRCH1(DD, PP, DP, RR)                                                                                 \
   do {                                                                                                        \
     const LevelDev LL = shape_of(g->L0, RR);                                                                  \
@@ -1165,6 +1257,14 @@ static hjb_status policy_update_dev(hjb_grid* g, double dt, const double* U, con
 #undef WIN
     CKL();
     nblk += wp->grid;
+  }
+  if (deep2) {
+    if (!g->upair) TRY(dalloc((void**)&g->upair, (size_t)g->N * sizeof(double2)));
+    const int64_t ne = g->N;
+    LAUNCH(HJB_KC_SEARCH, 0, 0, 0,
+           k_make_pairs<<<(int)std::min<int64_t>((ne + 255) / 256, (int64_t)g->sms * 8), 256, 0, g->st>>>(U, g->upair, ne));
+    CKL();
+    TRY(launch_search2(g, dt, U, Uprev, pol, F, rect, &nblk));
   }
   if (use_tma) {  // deep tiles: windows staged in shared memory by TMA (partials after the others')
     if (g->P == 1)

@@ -1,0 +1,180 @@
+// hjb_search2.cuh -- the 2D deep-rectangle control search, restructured for the L1 data pipe
+// (sm_100a).  Policy improvement of PAPER.md:147-156 (exhaustive linear search over the discrete
+// control set, footnote P:156): for every deep node j and every control a, in index order,
+//     H^a_j(U) = sum_e w_e I U(z_e) - (sum_e w_e) U_j + c^a_j U_j + f^a_j
+// with the lowest-index argmin (reading iv).  Same geometry, same operands, same arithmetic order as
+// k_search<2, P, true> (hjb_kernels.cuh) up to the rounding of equivalent formulations (the offset
+// k sigma formed as (k sc) sd, the minus endpoint interpolated from the far corner, per-control
+// weight sums): identical policies except at near-ties, F and R within rounding
+// (tests/test_gpu_parity.py::test_deep_kernels_match_general).
+//
+// What bounds k_search<2, P, true> at BASELINE cfg4 (ncu, profiles/r01_v9_ncu_full_search_cfg4.md and
+// DESIGN.md §6): the L1 data pipe (l1tex__data_pipe_lsu_wavefronts 71-83 % of peak): 20 scattered
+// 8-byte gathers per (node, control) at ~4.2 wavefronts each, plus ~24 shared-memory wavefronts
+// for the control tables.  This kernel removes both costs:
+//   * the control tables live in the kernel PARAMETER space (a __grid_constant__ struct, constant
+//     bank 0): a warp-uniform index a is served by the constant cache, not the L1 data pipe;
+//   * each bilinear tap reads two 16-byte pairs (U_i, U_{i+1}) of rows c1 and c1+1 from a pair copy
+//     UP[i] = (U[i], U[i+1]) built once per search (k_make_pairs): 2 LDG.128 instead of 4 LDG.64;
+//   * the drift endpoint of the deep rectangle stays within one cell of the node (|h b^a / h| < 1,
+//     checked on the host from the scale-field ranges), so its four taps come from the node's 3x3
+//     neighbourhood of U held in registers (the quadrant is per control): no gathers at all;
+//   * per (node, control) one floor per offset component serves both endpoints of a pair (the minus
+//     endpoint is interpolated from the far corner of its cell), addresses are 32-bit offsets from the
+//     node, and the weights / weight sum of the untruncated stencil are per-control table entries.
+#pragma once
+#include "hjb_device.cuh"
+
+namespace hjb {
+
+constexpr int kSTabN = 3072;  // doubles of control tables passed as a kernel parameter (24 KB)
+struct STab {
+  double v[kSTabN];  // per control a, stride P*2 + 2 + 2 + Q: sigma_dir [P][2] | b_dir [2] | c | f_ctrl | f_basis [Q]
+};
+
+// UP[i] = (U[i], U[i+1]) for every local element (the last one pairs with 0)
+__global__ void __launch_bounds__(256) k_make_pairs(const double* __restrict__ U, double2* __restrict__ UP, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double a = __ldg(U + i);
+    const double b = (i + 1 < n) ? __ldg(U + i + 1) : 0.0;
+    UP[i] = make_double2(a, b);
+  }
+}
+
+// bilinear value from the pairs (v00, v10) of row c1 and (v01, v11) of row c1+1 at fractions s
+__device__ __forceinline__ double interp_pairs(const double2 lo, const double2 hi, double s0, double s1) {
+  const double a = fma(s0, lo.y - lo.x, lo.x);
+  const double b = fma(s0, hi.y - hi.x, hi.x);
+  return fma(s1, b - a, a);
+}
+// the same bilinear value measured from the far corner: the cell's fractions are 1 - s0, 1 - s1
+// (the minus endpoint x - o of an untruncated pair sits at (i - fl - 1) + (1 - s) per axis when
+// x + o sits at (i + fl) + s, so it reuses the plus endpoint's s -- no separate split, and no
+// special case at s = 0, where it reads the corner v11 exactly)
+__device__ __forceinline__ double interp_pairs_mirror(const double2 lo, const double2 hi, double s0, double s1) {
+  const double a = fma(-s0, lo.y - lo.x, lo.y);
+  const double b = fma(-s0, hi.y - hi.x, hi.y);
+  return fma(-s1, b - a, b);
+}
+
+// base + 16 off as one wide multiply-add (IMAD.WIDE) instead of a sign-extend + shift-add pair
+__device__ __forceinline__ const double2* pair_at(const double2* base, int off) {
+  const double2* r;
+  asm("mad.wide.s32 %0, %1, 16, %2;" : "=l"(r) : "r"(off), "l"(base));
+  return r;
+}
+
+// floor split of an offset o (|o| < 2^31): fl as an integer and the fraction s = o - fl (exact)
+__device__ __forceinline__ void split_floor(double o, int& fl, double& s) {
+  const double f = floor(o);
+  s = o - f;
+  fl = __double2loint(f + 6755399441055744.0);  // 1.5 * 2^52: the integer in the low word (no F2I)
+}
+
+// per-control uniform data of the parameter-space table, after the P*2 + 2 + 2 + Q scheme doubles:
+//   w_p (P) | w_drift | wsum   -- the weights of the untruncated stencil (zero steps -> 0)
+template <int P, int Q>
+struct STabLayout {
+  static constexpr int SD = 0, BD = 2 * P, C = 2 * P + 2, FC = 2 * P + 3, FB = 2 * P + 4, W = 2 * P + 4 + Q,
+                       WD = W + P, WSUM = W + P + 1, S = W + P + 2;
+};
+struct STabQuad {
+  int v[256];  // drift endpoint quadrant per control: bit 0 = cell left of the node (x), bit 1 = below (y)
+};
+
+#ifndef HJB_SEARCH2_MINB
+#define HJB_SEARCH2_MINB 4
+#endif
+// Deep nodes only (every endpoint of every control strictly inside the box), no sigma/b offset
+// fields, scale fields of one sign (so a control's zero steps and drift quadrant are per-control
+// facts: host-checked), drift endpoints within one cell of the node.
+template <int P, int Q>
+__global__ void __launch_bounds__(kTX, HJB_SEARCH2_MINB) k_search_deep2(LevelDev L, CoefDev C, double dt,
+                                                                        const double* __restrict__ U,
+                                                                        const double2* __restrict__ UP,
+                                                                        const double* __restrict__ Uprev,
+                                                                        uint8_t* __restrict__ pol,
+                                                                        double* __restrict__ F, double* partial,
+                                                                        SkipRect it, const __grid_constant__ STab tab,
+                                                                        const __grid_constant__ STabQuad quad) {
+  using T = STabLayout<P, Q>;
+  double red[2] = {0.0, 0.0};
+  const int nk = box_lines(it);
+  const int n = L.n;
+  for (int k = blockIdx.y * kSBY + threadIdx.y; k < nk; k += gridDim.y * kSBY)
+    for (int col = it.c0 + blockIdx.x * kSBX + threadIdx.x; col < it.c1; col += gridDim.x * kSBX) {
+      const int row = box_row<2>(L, it, k);
+      Node<2> nd;
+      node_at<2>(L, col, row, nd);
+      load_fields<2>(C, nd);
+      prefetch_ahead(L, U, nd.loc, col);
+      double feat[Q > 0 ? Q : 1];
+#pragma unroll
+      for (int q = 0; q < Q; ++q) feat[q] = __ldg(C.f_feat + q * C.ld + nd.loc);
+      const double Uj = __ldg(U + nd.loc);
+      double nb[3][3];  // U at (i0 + c - 1, i1 + r - 1): nb[r][c]  (the drift endpoint's cells)
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) nb[r][c] = (r == 1 && c == 1) ? Uj : __ldg(U + nd.loc + (r - 1) * n + (c - 1));
+      double ksc[P];
+#pragma unroll
+      for (int p = 0; p < P; ++p) ksc[p] = L.kh * nd.sc[p];
+      const double kbs = L.k2h * nd.bs;
+      const double2* up = UP + nd.loc;       // pairs of the node's row ...
+      const double2* upn = up + n;           // ... and of the next row (one base per row: one
+                                             // wide multiply-add per load address)
+      double best = INFINITY, fbest = 0.0;
+      int arg = 0;
+      for (int a = 0; a < C.K; ++a) {
+        const double* t = tab.v + a * T::S;
+        double acc = 0.0;
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+          int fl0, fl1;
+          double s0, s1;
+          split_floor(ksc[p] * t[T::SD + 2 * p], fl0, s0);
+          split_floor(ksc[p] * t[T::SD + 2 * p + 1], fl1, s1);
+          const int off = fl1 * n + fl0;          // plus endpoint's cell corner, relative to the node
+          const int offm = -off - n - 1;          // minus endpoint's cell corner (i - fl - 1)
+          const double2 p0 = __ldg(pair_at(up, off)), p1 = __ldg(pair_at(upn, off));
+          const double2 m0 = __ldg(pair_at(up, offm)), m1 = __ldg(pair_at(upn, offm));
+          const double w = t[T::W + p];
+          acc = fma(w, interp_pairs(p0, p1, s0, s1), acc);
+          acc = fma(w, interp_pairs_mirror(m0, m1, s0, s1), acc);
+        }
+        {  // drift endpoint: within one cell of the node, its quadrant is a per-control fact
+          const double o0 = kbs * t[T::BD], o1 = kbs * t[T::BD + 1];
+          const double s0 = o0 - floor(o0), s1 = o1 - floor(o1);
+          double dv;
+          switch (quad.v[a]) {
+            case 0: dv = interp_pairs(make_double2(nb[1][1], nb[1][2]), make_double2(nb[2][1], nb[2][2]), s0, s1); break;
+            case 1: dv = interp_pairs(make_double2(nb[1][0], nb[1][1]), make_double2(nb[2][0], nb[2][1]), s0, s1); break;
+            case 2: dv = interp_pairs(make_double2(nb[0][1], nb[0][2]), make_double2(nb[1][1], nb[1][2]), s0, s1); break;
+            default: dv = interp_pairs(make_double2(nb[0][0], nb[0][1]), make_double2(nb[1][0], nb[1][1]), s0, s1); break;
+          }
+          acc = fma(t[T::WD], dv, acc);
+        }
+        double f = t[T::FC];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) f = fma(t[T::FB + q], feat[q], f);
+        const double cc = nd.cn + t[T::C];
+        const double H = (acc - t[T::WSUM] * Uj) + cc * Uj + f;
+        if (H < best) {  // strict: lowest index wins exact ties (reading iv)
+          best = H;
+          arg = a;
+          fbest = f;
+        }
+      }
+      const double Up = __ldg(Uprev + nd.loc);
+      const double R = fabs(Uj - Up - dt * best);
+      const int old = pol[nd.loc];
+      pol[nd.loc] = (uint8_t)arg;
+      F[nd.loc] = fma(dt, fbest, Up);
+      red[0] = fmax(red[0], (R == R) ? R : INFINITY);  // NaN -> inf (reported NONFINITE)
+      red[1] += (old != arg) ? 1.0 : 0.0;
+    }
+  block_reduce_store<2>(red, partial, 0x1u);
+}
+
+}  // namespace hjb

@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 
 from gpu_util import require_gpu, row_scale, setup, to_dev
-from oracle.howard import control_search, howard_step
+from oracle.howard import control_search, hamiltonian, howard_step
 from oracle.scheme import Geometry, apply_operator
 from oracle.system import assemble, solve
 from synth import bj_config, problem_A, problem_B, random_vector
@@ -291,7 +291,10 @@ def test_deep_kernels_match_general(name, mk, monkeypatch):
     """The lean deep-rectangle kernels (no truncation code), the shared-memory window search (over the
     deep box, and over the whole interior with the general geometry) and the TMA-windowed search
     tiles give bit-identical search results and operator applications to the general kernels
-    everywhere (HJB_NO_DEEP / HJB_WIN=0,1,2 / HJB_TMA=1 select them)."""
+    everywhere (HJB_NO_DEEP / HJB_WIN=0,1,2 / HJB_TMA=1 / HJB_NO_SEARCH2=1 select them).  The 2D
+    L1-lean deep search k_search_deep2 (hjb_search2.cuh, the default where it applies) uses
+    equivalent formulations with their own rounding: identical policies except at near-ties (both
+    controls within the oracle's 1e-12 rounding window, reading iv), F and R within rounding."""
     torch = require_gpu()
     p = mk()
     rng = np.random.default_rng(11)
@@ -299,12 +302,15 @@ def test_deep_kernels_match_general(name, mk, monkeypatch):
     U = Uprev + 0.05 * rng.uniform(-1, 1, size=p.N)
     x = random_vector(p)
     out = {}
-    for mode in ("general", "deep", "deep_win", "full_win", "deep_tma"):
-        for k in ("HJB_NO_DEEP", "HJB_NO_TMA", "HJB_TMA", "HJB_WIN"):
+    for mode in ("general", "deep_legacy", "deep_win", "full_win", "deep_tma", "deep2"):
+        for k in ("HJB_NO_DEEP", "HJB_NO_TMA", "HJB_TMA", "HJB_WIN", "HJB_NO_SEARCH2"):
             monkeypatch.delenv(k, raising=False)
         if mode == "general":
             monkeypatch.setenv("HJB_NO_DEEP", "1")
-        elif mode == "deep":
+        elif mode == "deep_legacy":
+            monkeypatch.setenv("HJB_WIN", "0")
+            monkeypatch.setenv("HJB_NO_SEARCH2", "1")
+        elif mode == "deep2":
             monkeypatch.setenv("HJB_WIN", "0")
         elif mode == "deep_win":
             monkeypatch.setenv("HJB_WIN", "1")
@@ -321,11 +327,27 @@ def test_deep_kernels_match_general(name, mk, monkeypatch):
         torch.cuda.synchronize()
         out[mode] = (pol.cpu().numpy(), F.cpu().numpy(), st, y.cpu().numpy())
         g.close()
-    for m in ("deep", "deep_win", "full_win", "deep_tma"):
+    for m in ("deep_legacy", "deep_win", "full_win", "deep_tma"):
         assert np.array_equal(out["general"][0], out[m][0]), m
         assert np.array_equal(out["general"][1], out[m][1]), m
         assert out["general"][2] == out[m][2], m
         assert np.array_equal(out["general"][3], out[m][3]), m
+    # k_search_deep2: near-tie aware comparison against the oracle's rounding window
+    pg, pd = out["general"][0].astype(np.int64), out["deep2"][0].astype(np.int64)
+    inter = Geometry.of(p).interior_idx()
+    diff = inter[pg[inter] != pd[inter]]
+    assert diff.size <= max(10, inter.size // 1000), diff.size
+    if diff.size:
+        f = p.fields(diff)
+        Ha, Sa, _ = hamiltonian(p, diff, pg[diff], U, p.dt, f)
+        Hb, Sb, _ = hamiltonian(p, diff, pd[diff], U, p.dt, f)
+        assert np.all(np.abs(Ha - Hb) <= 1e-12 * np.maximum(Sa, Sb)), np.abs(Ha - Hb).max()
+    same = inter[pg[inter] == pd[inter]]
+    Fg, Fd = out["general"][1][same], out["deep2"][1][same]
+    assert np.abs(Fg - Fd).max(initial=0.0) <= 1e-13 * max(1.0, np.abs(Fg).max())
+    Rg, Rd = out["general"][2]["R_max"], out["deep2"][2]["R_max"]
+    assert abs(Rg - Rd) <= 1e-12 * max(1.0, abs(Rg)), (Rg, Rd)
+    assert np.array_equal(out["general"][3], out["deep2"][3])      # the apply does not use it
 
 
 @pytest.mark.parametrize("name,mk", [("cfg1", lambda: bj_config(1)), ("cfg2_513", lambda: bj_config(2, n=513)),
