@@ -382,13 +382,15 @@ def run_b200(args):
         "t_range": [round((step_of(args.warmup + 1) - 1) * p.dt, 6), round(p.T, 6)]
         if args.steps >= ns else [round((step_of(s) - 1) * p.dt, 6) for s in (args.warmup + 1, total)],
         "march": f"T = {p.T:g} in {ns} implicit steps; restart from u*(0) after step {ns}",
+        "pi_per_step": pis, "krylov_per_step": kr,
         "mg_cycles_per_pi": (2 * sum(kr) / max(1, sum(pis))),
         "krylov_iters_per_pi": sum(kr) / max(1, sum(pis)), "pi_iters_per_step": sum(pis) / len(pis),
         "levels": stats[-1]["n_levels"], "final_rres": max(st["final_rres"] for st in stats),
         "final_rres_inf": max(st["final_rres_inf"] for st in stats),
         "final_R": max(st["final_R"] for st in stats),
         "max_err_vs_ustar": err, "wall_s_timed": wall,
-        "gpu_launches": int(prof["total_launches"]), "clocks": clocks, "e2e": e2e,
+        "gpu_launches": int(prof["total_launches"]), "graph_launches": int(prof["graph_launches"]),
+        "clocks": clocks, "e2e": e2e,
     }
     if not args.no_cpu_baseline and rank == 0 and world == 1:
         v, s, desc = oracle_sample(cfg)

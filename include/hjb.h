@@ -247,6 +247,15 @@ typedef struct {
                                 alone bounds ||r||_inf only by sqrt(N) krylov_rtol ||F||_2 (SURVEY
                                 §8c-xvii; reading xvii).  Inexact evaluations (pi_forcing)
                                 use the 2-norm rule only.                                       */
+  double theta;              /* hjb_step's time scheme (eq. FullScheme):
+                                1 = implicit Euler (default, the paper's experiments); 0 = explicit
+                                Euler: U^n = U^{n-1} + dt min_a H^a(U^{n-1}), one control search and
+                                one apply, no solve; 0 < theta < 1: policy iteration on
+                                (I - theta dt (L^pi + c)) U = U^{n-1} + (1-theta) dt (L^pi + c) U^{n-1}
+                                + dt f^pi, each policy from the search at theta U + (1-theta) U^{n-1}
+                                (reading xxvi).  f must be set at t_{n-1} + theta dt
+                                (P:124).  theta < 1 needs the CFL condition of Proposition CFL
+                                (P:437-441), see hjb_cfl_rate; it is not enforced.               */
 } hjb_solve_params;
 
 #define HJB_GUESS_PREV 0
@@ -289,6 +298,15 @@ typedef struct {
 hjb_status hjb_step(hjb_grid_t g, double dt, const double* U_prev, double* U, uint8_t* policy,
                     const double* psi_packed, const hjb_solve_params* p, hjb_step_stats* out);
 
+/* Positivity (CFL) rate of Proposition CFL (eq. CFL_trunc): the largest
+ *   sum_{p=1}^{P+1} (A^a_p + B^a_p) / (2 dx) - c^a_j
+ * over owned interior nodes j (truncated weights included, so it grows like dx^{-3/2} / dx^{-2}
+ * where one / both sides of a stencil overstep, Corollary CFL P:444-452) and over the control of
+ * each node (policy != NULL, device array) or over every control (policy == NULL).  A theta-step
+ * is of positive type if (1 - theta) dt * rate <= 1 and theta dt max c <= 1.  Collective (max over
+ * ranks).                                                                                       */
+hjb_status hjb_cfl_rate(hjb_grid_t g, const uint8_t* policy, double* rate);
+
 /* ------------------------------------------------------------------- instrumentation
  * Every kernel launch of the library is counted per class.  With time_kernels != 0 each launch
  * over >= 16384 nodes (and every control search) is also bracketed by CUDA events on the grid's
@@ -321,8 +339,11 @@ typedef struct {
   double bytes[HJB_KC_COUNT];
   double flops[HJB_KC_COUNT];
   double nodes[HJB_KC_COUNT];
-  int64_t total_launches;
+  int64_t total_launches;   /* kernels executed (a replayed graph counts every kernel it holds) */
   int32_t timed;            /* 1 if ms[] was collected */
+  int64_t graph_launches;   /* cudaGraphLaunch calls of the captured multigrid tail:
+                               the cycle from the first level owning <= 70000 nodes down is captured
+                               once per hierarchy and replayed; its kernels are untimed             */
 } hjb_profile;
 
 hjb_status hjb_profile_reset(hjb_grid_t g, int32_t time_kernels);

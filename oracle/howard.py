@@ -99,8 +99,13 @@ class StepStats:
 
 
 def howard_step(prob, U_prev_full, t, dt, fields=None, tol_pi=None, max_pi=50, k_scale=1.0,
-                policy0=None, solve_kw=None):
-    """One implicit Euler step (theta = 1) by policy iteration.
+                policy0=None, solve_kw=None, theta=1.0):
+    """One step t_{n-1} -> t_n = t of the theta-scheme (eq. FullScheme) by policy
+    iteration.  The row residual of control a is (derivation D1 with theta)
+        (A^a U - F^a)_j = U_j - U^{n-1}_j - dt H^a_j(V),   V = theta U + (1 - theta) U^{n-1},
+    (L_hat and c are linear in their argument), so the policy improvement is the control search at V
+    with f at t_{n-1} + theta dt.  theta = 0 (explicit Euler) needs no solve: U^n = U^{n-1} + dt
+    min_a H^a(U^{n-1}) at every interior node, boundary psi(t_n).
     Returns (U^n on the full grid, policy on the full grid, StepStats)."""
     geo = Geometry.of(prob, k_scale)
     interior = geo.interior_idx()
@@ -110,23 +115,36 @@ def howard_step(prob, U_prev_full, t, dt, fields=None, tol_pi=None, max_pi=50, k
     bidx = prob.boundary_idx()
     psi_full = np.zeros(prob.N)
     psi_full[bidx] = prob.psi(t, bidx)
+    t_theta = t - dt + theta * dt
+    pol_full = np.zeros(prob.N, dtype=np.int64)
+    stats = StepStats()
+    if theta == 0.0:                              # explicit Euler: one control search at U^{n-1}
+        sr = control_search(prob, U_prev_full, U_prev_full, t_theta, dt, fields=fields, idx=interior,
+                            k_scale=k_scale)
+        U = U_prev_full.copy()
+        U[interior] = U_prev_full[interior] + dt * sr.H
+        U[bidx] = psi_full[bidx]
+        pol_full[interior] = sr.policy
+        stats.pi_iters = 1
+        return U, pol_full, stats
     U = U_prev_full.copy()
     U[bidx] = psi_full[bidx]                      # a1: Dirichlet rows are identities
-    pol_full = np.zeros(prob.N, dtype=np.int64)
     if policy0 is not None:
         pol_full[interior] = policy0
-    stats = StepStats()
     have_policy = False
     for it in range(1, max_pi + 1):
-        sr = control_search(prob, U, U_prev_full, t, dt, fields=fields, idx=interior, k_scale=k_scale)
+        V = theta * U + (1.0 - theta) * U_prev_full
+        sr = control_search(prob, V, U_prev_full, t_theta, dt, fields=fields, idx=interior, k_scale=k_scale)
+        R = np.abs(U[interior] - U_prev_full[interior] - dt * sr.H)      # = sr.R when theta = 1
         changed = int(np.sum(sr.policy != pol_full[interior]))
         stats.changed.append(changed)
-        stats.residuals.append(float(sr.R.max(initial=0.0)))
-        if have_policy and (changed == 0 or sr.R.max(initial=0.0) <= tol_pi):
+        stats.residuals.append(float(R.max(initial=0.0)))
+        if have_policy and (changed == 0 or R.max(initial=0.0) <= tol_pi):
             break
         pol_full[interior] = sr.policy
         have_policy = True
-        sysm = assemble(prob, pol_full, dt, t, U_prev_full, psi_full, fields=fields, k_scale=k_scale)
+        sysm = assemble(prob, pol_full, dt, t, U_prev_full, psi_full, fields=fields, k_scale=k_scale,
+                        theta=theta)
         X, rres = solve(sysm, x0=U[interior], **(solve_kw or {}))
         stats.solve_rres.append(rres)
         U[interior] = X
@@ -134,8 +152,8 @@ def howard_step(prob, U_prev_full, t, dt, fields=None, tol_pi=None, max_pi=50, k
     return U, pol_full, stats
 
 
-def march(prob, n_steps=None, fields=None, k_scale=1.0, **kw):
-    """Implicit Euler march U^0 = g, U^n = step(U^{n-1}) to T (theta = 1)."""
+def march(prob, n_steps=None, fields=None, k_scale=1.0, theta=1.0, **kw):
+    """theta-scheme march U^0 = g, U^n = step(U^{n-1}) to T in n_steps uniform steps."""
     n_steps = n_steps or prob.n_steps
     dt = prob.T / n_steps
     idx = prob.all_idx()
@@ -146,6 +164,34 @@ def march(prob, n_steps=None, fields=None, k_scale=1.0, **kw):
     hist = []
     pol = None
     for s in range(1, n_steps + 1):
-        U, pol, st = howard_step(prob, U, s * dt, dt, fields=fields, k_scale=k_scale, **kw)
+        U, pol, st = howard_step(prob, U, s * dt, dt, fields=fields, k_scale=k_scale, theta=theta, **kw)
         hist.append(st)
+        if not np.all(np.isfinite(U)):
+            break                                  # an unstable explicit march (CFL violated)
     return U, pol, hist
+
+
+def cfl_rate(prob, fields=None, k_scale=1.0, policy=None):
+    """max over interior nodes i (and controls a) of  sum_p (A^a_p + B^a_p)/(2 dx) - c^a_i, the rate in
+    the positivity (CFL) condition of Proposition CFL (eq. CFL_trunc):
+        (1 - theta) dt [ sum_p (A_p + B_p)/(2 dx) - c ] <= 1   for all a, i
+    (the sum runs over the M = P + 1 pairs incl. the drift pair).  policy (full-grid control index):
+    the rate of those controls only (the condition is sufficient; a march only applies the controls
+    it selects).  Returns (rate, (node, control) of the max).  Truncated rows make it grow like
+    dx^{-3/2} (one side oversteps) or dx^{-2} (both sides), Corollary CFL."""
+    geo = Geometry.of(prob, k_scale)
+    interior = geo.interior_idx()
+    if fields is None:
+        fields = prob.fields(interior)
+    x = geo.node_x(interior)
+    best, arg = -np.inf, (None, None)
+    ctrls = [None] if policy is not None else range(prob.K)
+    for a in ctrls:
+        al = np.asarray(policy)[interior] if a is None else np.full(interior.size, a)
+        sig, b, c = node_coefficients(prob, interior, al, fields)
+        _, _, rowsum = lhat_rows(geo, x, sig, b)
+        r = rowsum - c
+        j = int(np.argmax(r))
+        if r[j] > best:
+            best, arg = float(r[j]), (int(interior[j]), int(al[j]))
+    return best, arg

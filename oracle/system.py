@@ -29,10 +29,15 @@ class System:
         self.A, self.F, self.interior, self.geo = A, F, interior, geo
 
 
-def assemble(prob, policy_full, dt, t, U_prev_full, psi_full, fields=None, k_scale=1.0):
-    """Assemble A^pi, F^pi at time t_n = t for the policy pi (theta = 1).
-    policy_full: control index per full-grid node (only interior entries used).
-    U_prev_full: U^{n-1} on the full grid.  psi_full: Dirichlet data (boundary entries used)."""
+def assemble(prob, policy_full, dt, t, U_prev_full, psi_full, fields=None, k_scale=1.0, theta=1.0):
+    """Assemble A^pi, F^pi of the theta-scheme, eq. (FullScheme), for the policy pi:
+        A^pi = I - theta dt (L_hat^pi + c^pi)                               (interior rows)
+        F^pi = U^{n-1} + (1 - theta) dt (L_hat^pi + c^pi)[U^{n-1}] + dt f^pi
+               + theta dt sum_{i in dOmega} l_hat_ji psi_i(t_n)
+    (B^{n,n} and B^{n,n-1} of P:419-424 with time-independent sigma, b).  c and f are evaluated at
+    t_{n-1} + theta dt; t is t_n.  U_prev_full holds psi(t_{n-1}) on the boundary.
+    policy_full: control index per full-grid node (only interior entries used).  theta = 1 is the
+    implicit Euler system of the paper's experiments (reading x)."""
     geo = Geometry.of(prob, k_scale)
     interior = geo.interior_idx()
     m = interior.size
@@ -52,18 +57,22 @@ def assemble(prob, policy_full, dt, t, U_prev_full, psi_full, fields=None, k_sca
 
     is_self = cflat == np.repeat(interior, cols.shape[1])
     l_jj = np.bincount(rows[is_self], weights=vflat[is_self], minlength=m)
-    diag = 1.0 + dt * (rowsum - l_jj - c)                       # B^{n,n}_jj
+    diag = 1.0 + theta * dt * (rowsum - l_jj - c)               # B^{n,n}_jj
 
     off = (~is_self) & (cpos >= 0)                              # interior off-diagonals
-    A = sp.coo_matrix((np.concatenate([-dt * vflat[off], diag]),
+    A = sp.coo_matrix((np.concatenate([-theta * dt * vflat[off], diag]),
                        (np.concatenate([rows[off], np.arange(m)]),
                         np.concatenate([cpos[off], np.arange(m)]))), shape=(m, m)).tocsr()
     A.sum_duplicates()
 
-    f = source_term(prob, t, alpha, fields)
+    t_theta = t - dt + theta * dt
+    f = source_term(prob, t_theta, alpha, fields)
     bnd = cpos < 0                                              # couplings to boundary nodes
     F = U_prev_full[interior] + dt * f
-    F = F + np.bincount(rows[bnd], weights=dt * vflat[bnd] * psi_full[cflat[bnd]], minlength=m)
+    F = F + np.bincount(rows[bnd], weights=theta * dt * vflat[bnd] * psi_full[cflat[bnd]], minlength=m)
+    if theta < 1.0:                                             # B^{n,n-1} U^{n-1}: explicit part
+        Lprev = np.sum(vals * (U_prev_full[cols] - U_prev_full[interior][:, None]), axis=1)
+        F = F + (1.0 - theta) * dt * (Lprev + c * U_prev_full[interior])
     return System(A, F, interior, geo)
 
 

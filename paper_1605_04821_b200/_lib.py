@@ -18,7 +18,7 @@ EXPORTS = ["hjb_last_error", "hjb_version", "hjb_grid_create", "hjb_grid_query",
            "hjb_set_coeffs", "hjb_set_source", "hjb_policy_update", "hjb_apply",
            "hjb_mg_params_default", "hjb_mg_setup", "hjb_mg_apply", "hjb_solve_params_default",
            "hjb_solve", "hjb_step", "hjb_profile_reset", "hjb_profile_read",
-           "hjb_partition", "hjb_halo_plan", "hjb_comm_unique_id"]
+           "hjb_partition", "hjb_halo_plan", "hjb_comm_unique_id", "hjb_cfl_rate"]
 
 HJB_COMM_NCCL, HJB_COMM_THREADS = 0, 1
 
@@ -64,7 +64,8 @@ class MgParams(C.Structure):
 class SolveParams(C.Structure):
     _fields_ = [("krylov_rtol", C.c_double), ("krylov_maxit", C.c_int32), ("use_mg", C.c_int32),
                 ("tol_pi", C.c_double), ("max_pi", C.c_int32), ("mg", MgParams),
-                ("pi_forcing", C.c_double), ("guess", C.c_int32), ("krylov_rtol_inf", C.c_double)]
+                ("pi_forcing", C.c_double), ("guess", C.c_int32), ("krylov_rtol_inf", C.c_double),
+                ("theta", C.c_double)]
 
 HJB_GUESS_PREV, HJB_GUESS_GIVEN, HJB_GUESS_EXTRAPOLATE = 0, 1, 2
 
@@ -95,13 +96,14 @@ class Profile(C.Structure):
                 ("ms", C.c_double * HJB_KC_COUNT),
                 ("bytes", C.c_double * HJB_KC_COUNT), ("flops", C.c_double * HJB_KC_COUNT),
                 ("nodes", C.c_double * HJB_KC_COUNT), ("total_launches", C.c_int64),
-                ("timed", C.c_int32)]
+                ("timed", C.c_int32), ("graph_launches", C.c_int64)]
 
     def as_dict(self):
         per = {k: dict(launches=self.launches[i], calls=self.calls[i], ms=self.ms[i], bytes=self.bytes[i],
                        flops=self.flops[i], nodes=self.nodes[i])
                for i, k in enumerate(KERNEL_CLASSES)}
-        return dict(classes=per, total_launches=self.total_launches, timed=bool(self.timed))
+        return dict(classes=per, total_launches=self.total_launches, timed=bool(self.timed),
+                    graph_launches=self.graph_launches)
 
 
 _lib = None
@@ -139,6 +141,7 @@ def load(path: str = None):
         "hjb_profile_read": (i32, [vp, C.POINTER(Profile)]),
         "hjb_partition": (i32, [i32, i64, i32, i32, i64, C.POINTER(Layout)]),
         "hjb_comm_unique_id": (i32, [vp]),
+        "hjb_cfl_rate": (i32, [vp, vp, C.POINTER(d)]),
         "hjb_halo_plan": (i32, [i32, i64, i32, i32, i64, HaloMsg * 2, C.POINTER(i32)]),
     }
     for name, (res, args) in sig.items():

@@ -162,6 +162,12 @@ class HJBGrid:
             check(code)
         return out
 
+    def cfl_rate(self, policy=None) -> float:
+        """Positivity rate max (sum_p (A_p+B_p)/(2dx) - c) of Proposition CFL (hjb_cfl_rate)."""
+        r = C.c_double()
+        check(self.lib.hjb_cfl_rate(self.h, _ptr(policy), C.byref(r)))
+        return r.value
+
     # ------------------------------------------------------------------ instrumentation
     def profile_reset(self, time_kernels: bool = False):
         check(self.lib.hjb_profile_reset(self.h, 1 if time_kernels else 0))

@@ -162,8 +162,24 @@ struct hjb_grid {
   double rdiff_ax[3] = {0, 0, 0}, rdrift_ax[3] = {0, 0, 0};
   double* rng_part = nullptr; // k_field_ranges block partials
   double2* upair = nullptr;   // (U_i, U_{i+1}) pair copy of the searched U (k_search_deep2)
+  double* vtheta = nullptr;   // theta U + (1-theta) U_prev (theta-scheme search argument)
   bool drift_reg = false;     // deep drift endpoints stay within one cell of the node (|offset| < 1)
   double h_rng[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // host copy of d_rng (scale-field ranges)
+  // CUDA graphs of the multigrid tail: the cycle from level graph_level down (levels owning <=
+  // kGraphMaxNodes nodes, launch-latency bound) is captured once per hierarchy and replayed
+  struct SubGraph {
+    size_t level;
+    const double* b;
+    double* out;
+    cudaGraphExec_t exec;
+    int64_t launches;
+  };
+  std::vector<SubGraph> graphs;
+  size_t graph_level = (size_t)-1;
+  double graph_dt = 0.0;          // dt / omega baked into the captured kernels' parameters
+  bool capturing = false;
+  int64_t cap_launches = 0;
+  cudaStream_t cap_st = nullptr;  // private capture stream (the legacy default stream cannot capture)
 };
 
 // ---------------------------------------------------------------------------- instrumentation
@@ -187,7 +203,7 @@ static void prof_drain(hjb_grid* g) { prof_drain_oldest(g, g->npend); }
 // their device time is the unattributed remainder.  nodes <= 0: accounted by the caller, always timed.
 constexpr double kTimeMinNodes = 16384.0;
 static bool prof_timed(const hjb_grid* g, double nodes) {
-  return g->prof_timing && (nodes <= 0.0 || nodes >= kTimeMinNodes);
+  return g->prof_timing && !g->capturing && (nodes <= 0.0 || nodes >= kTimeMinNodes);
 }
 static void prof_pre(hjb_grid* g, int, double nodes) {
   if (!prof_timed(g, nodes)) return;
@@ -195,6 +211,10 @@ static void prof_pre(hjb_grid* g, int, double nodes) {
   cudaEventRecord(g->pev[2 * ((g->phead + g->npend) % hjb_grid::kSlots)], g->st);
 }
 static void prof_post(hjb_grid* g, int cls, double nodes, double bytes, double flops) {
+  if (g->capturing) {  // recorded into a graph: counted at every replay instead
+    g->cap_launches += 1;
+    return;
+  }
   g->prof.launches[cls] += 1;
   g->prof.total_launches += 1;
   if (g->prof_timing && !prof_timed(g, nodes)) return;
@@ -494,7 +514,7 @@ static void launch_operator(hjb_grid* g, const LevelDev& L, const CoefDev& C, in
     else if (g->P == 2) OPLP(2, M, ND);                                                                     \
     else OPLP((D > 2 ? 3 : 2), M, ND);                                                                      \
   } while (0)
-  if (!g->prof_timing || nodes >= kTimeMinNodes) g->prof.calls[cls] += 1;  // applications in the timed subset
+  if (!g->capturing && (!g->prof_timing || nodes >= kTimeMinNodes)) g->prof.calls[cls] += 1;  // timed subset
   if (mode == OP_APPLY) {
     if (ndot == 0) OPL(OP_APPLY, 0);
     else if (ndot == 1) OPL(OP_APPLY, 1);
@@ -545,6 +565,7 @@ extern "C" void hjb_solve_params_default(int32_t dim, hjb_solve_params* o) {
   o->pi_forcing = 0.01;  // with the W-cycle (solves are cheap): 3 PI per step at cfg4 (DESIGN.md §3 xxii)
   o->guess = HJB_GUESS_PREV;
   o->krylov_rtol_inf = 1e-9;  // SURVEY §8c-xvii secondary stop (reading xvii)
+  o->theta = 1.0;             // implicit Euler (the paper's experiments)
 }
 
 // ---------------------------------------------------------------------------- API: partition
@@ -628,6 +649,9 @@ static void free_levels(hjb_grid* g) {
   }
   g->levels.clear();
   g->mg_ready = false;
+  for (auto& sg : g->graphs) cudaGraphExecDestroy(sg.exec);
+  g->graphs.clear();
+  g->graph_level = (size_t)-1;
 }
 
 extern "C" hjb_status hjb_grid_destroy(hjb_grid_t g) {
@@ -643,6 +667,8 @@ extern "C" hjb_status hjb_grid_destroy(hjb_grid_t g) {
   cudaFree(g->d_rng);
   cudaFree(g->rng_part);
   cudaFree(g->upair);
+  cudaFree(g->vtheta);
+  if (g->cap_st) cudaStreamDestroy(g->cap_st);
   cudaFree(g->S);
   cudaFree(g->pol_int);
   cudaFree(g->stage_pol);
@@ -1125,10 +1151,12 @@ static void search2_launch(hjb_grid* g, const LevelDev& LL, double dt, const dou
                            uint8_t* pol, double* F, const SkipRect& rect, const STab& tab, const STabQuad& quad,
                            int* nblk) {
   const void* fn = (const void*)k_search_deep2<P, Q>;
+  const int64_t tiles = (int64_t)((LL.nI + kSBX - 1) / kSBX) * ((LL.nrows + kSBY - 1) / kSBY);
+  const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, std::min<int64_t>((int64_t)occupancy_of(fn) * g->sms, kMaxBlocks)));
   LAUNCH(HJB_KC_SEARCH, 0, 0, 0,
-         k_search_deep2<P, Q><<<dims(g, LL, fn, kSBX), dim3(kSBX, kSBY), 0, g->st>>>(
+         k_search_deep2<P, Q><<<nb, dim3(kSBX, kSBY), 0, g->st>>>(
              g->L0, g->C0, dt, U, g->upair, Uprev, pol, F, g->partial + 2 * *nblk, rect, tab, quad));
-  *nblk += g->nblk_last;
+  *nblk += nb;
 }
 
 template <int P, int Q>
@@ -1326,6 +1354,8 @@ static int64_t level_halo(hjb_grid* g, const LevelDev& L) {
   return (int64_t)std::floor(std::max(rd, rb) * (1.0 + 1e-12)) + 1;
 }
 
+constexpr int64_t kGraphMaxNodes = 70000;  // 257^2 and below (measured: ~4 us of launch per kernel)
+
 static hjb_status build_levels(hjb_grid* g, const hjb_mg_params* mp) {
   free_levels(g);
   const int D = g->D;
@@ -1438,6 +1468,16 @@ static hjb_status build_levels(hjb_grid* g, const hjb_mg_params* mp) {
   Level& lc = g->levels.back();
   TRY(dalloc((void**)&lc.Ainv, (size_t)lc.L.n_own * lc.L.n_own * sizeof(double)));
   g->mgp = *mp;
+  // graph tail: the first level (>= 1) owning <= kGraphMaxNodes interior nodes whose whole sub-cycle
+  // runs without communication (one rank, or replicated levels) and is not revisited by a W-cycle
+  g->graph_level = (size_t)-1;
+  if (!getenv("HJB_NO_GRAPHS"))
+    for (size_t l = 1; l < g->levels.size(); ++l) {
+      const Level& lv = g->levels[l];
+      const bool no_comm = g->R == 1 || lv.replicated;
+      const bool revisited = mp->gamma > 1 && ipow(lv.L.n - 2, g->D) >= mp->gamma_min_nodes;
+      if (no_comm && !revisited && lv.L.n_own <= kGraphMaxNodes) { g->graph_level = l; break; }
+    }
   return HJB_OK;
 }
 
@@ -1517,6 +1557,11 @@ extern "C" hjb_status hjb_mg_setup(hjb_grid_t g, double dt, const uint8_t* polic
   for (size_t i = 1; i < g->levels.size(); ++i) g->levels[i].L.pf_rows = prefetch_rows(g, g->levels[i].L);
   g->mg_pol0 = policy;
   g->mg_dt = dt;
+  if (dt != g->graph_dt || getenv("HJB_NU_COARSE")) {  // captured graphs hold dt as a kernel parameter
+    for (auto& sg : g->graphs) cudaGraphExecDestroy(sg.exec);
+    g->graphs.clear();
+    g->graph_dt = dt;
+  }
   if (g->D == 2) TRY(inject_all<2>(g));
   else TRY(inject_all<3>(g));
   // the diagonal of every smoothed level's operator (the smoother reads it instead of recomputing
@@ -1552,6 +1597,40 @@ extern "C" hjb_status hjb_mg_setup(hjb_grid_t g, double dt, const uint8_t* polic
 // V(nu_pre, nu_post) from x = 0 on level l: out = M_l^{-1} b
 template <int D>
 static hjb_status vcycle(hjb_grid* g, size_t l, const double* b, double* out) {
+  if (l == g->graph_level && !g->capturing) {
+    hjb_grid::SubGraph* sg = nullptr;
+    for (auto& x : g->graphs)
+      if (x.level == l && x.b == b && x.out == out) sg = &x;
+    if (!sg) {  // capture the sub-cycle once on the private stream (kernels recorded, not run)
+      if (!g->cap_st) CK(cudaStreamCreateWithFlags(&g->cap_st, cudaStreamNonBlocking));
+      cudaStream_t keep = g->st;
+      g->cap_launches = 0;
+      g->st = g->cap_st;
+      g->capturing = true;
+      cudaGraph_t graph = nullptr;
+      cudaError_t e = cudaStreamBeginCapture(g->st, cudaStreamCaptureModeThreadLocal);
+      hjb_status st = (e == cudaSuccess) ? vcycle<D>(g, l, b, out) : HJB_ERR_CUDA;
+      cudaError_t e2 = cudaStreamEndCapture(g->st, &graph);
+      g->capturing = false;
+      g->st = keep;
+      if (e != cudaSuccess || e2 != cudaSuccess || st != HJB_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return st != HJB_OK ? st : fail(HJB_ERR_CUDA, "multigrid graph capture failed");
+      }
+      cudaGraphExec_t exec = nullptr;
+      e = cudaGraphInstantiate(&exec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (e != cudaSuccess) return fail(HJB_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+      const int64_t nl = g->cap_launches;
+      g->graphs.push_back(hjb_grid::SubGraph{l, b, out, exec, nl});
+      sg = &g->graphs.back();
+    }
+    CK(cudaGraphLaunch(sg->exec, g->st));
+    g->prof.total_launches += sg->launches;
+    g->prof.launches[HJB_KC_MG_COARSE] += sg->launches;
+    g->prof.graph_launches += 1;
+    return HJB_OK;
+  }
   Level& lv = g->levels[l];
   const uint8_t* pol = (l == 0) ? g->mg_pol0 : lv.pol;
   const LevelDev& L = lv.L;
@@ -1572,7 +1651,7 @@ static hjb_status vcycle(hjb_grid* g, size_t l, const double* b, double* out) {
   const int jmode = g->use_dg ? OP_JACOBI_D : OP_JACOBI;
   if (g->use_dg) {
     const double nn = (double)L.n_own;
-    if (!g->prof_timing || nn >= kTimeMinNodes) g->prof.calls[fine ? HJB_KC_SMOOTH : HJB_KC_MG_COARSE] += 1;
+    if (!g->capturing && (!g->prof_timing || nn >= kTimeMinNodes)) g->prof.calls[fine ? HJB_KC_SMOOTH : HJB_KC_MG_COARSE] += 1;
     LAUNCH(fine ? HJB_KC_SMOOTH : HJB_KC_MG_COARSE, nn, 24.0 * nn, 2.0 * nn,
            k_jacobi0_diag<D><<<dims(g, L, (const void*)k_jacobi0_diag<D>), dim3(kBX, kBY), 0, st>>>(L, om, b, lv.dg,
                                                                                                   bufs[cur]));
@@ -1771,6 +1850,143 @@ extern "C" hjb_status hjb_solve(hjb_grid_t g, double dt, const uint8_t* policy, 
   return g->D == 2 ? bicgstab<2>(g, dt, policy, F, x, sp, out) : bicgstab<3>(g, dt, policy, F, x, sp, out);
 }
 
+// ---------------------------------------------------------------------------- theta-scheme
+// y = A'_{dt'} x for the fine level (x's halos exchanged on a scratch copy when several ranks)
+static hjb_status apply_fine(hjb_grid* g, double dtp, const uint8_t* pol, const double* x, double* y) {
+  const double* xx;
+  TRY(halo_input(g, x, &xx));
+  if (g->D == 2) launch_operator<2>(g, g->L0, g->C0, OP_APPLY, 0, dtp, 0.0, pol, xx, nullptr, y, nullptr);
+  else launch_operator<3>(g, g->L0, g->C0, OP_APPLY, 0, dtp, 0.0, pol, xx, nullptr, y, nullptr);
+  CKL();
+  return HJB_OK;
+}
+
+static hjb_status theta_rhs(hjb_grid* g, const double* up, const double* y, double* out) {
+  const double nn = (double)g->L0.n_own;
+  if (g->D == 2)
+    LAUNCH(HJB_KC_VECTOR, nn, 32.0 * nn, 2.0 * nn,
+           k_theta_rhs<2><<<dims(g, g->L0, (const void*)k_theta_rhs<2>), dim3(kBX, kBY), 0, g->st>>>(g->L0, g->F, up, y, out));
+  else
+    LAUNCH(HJB_KC_VECTOR, nn, 32.0 * nn, 2.0 * nn,
+           k_theta_rhs<3><<<dims(g, g->L0, (const void*)k_theta_rhs<3>), dim3(kBX, kBY), 0, g->st>>>(g->L0, g->F, up, y, out));
+  CKL();
+  return HJB_OK;
+}
+
+// One theta-step (theta < 1) after hjb_step's staging (dU holds the initial iterate with psi(t_n)
+// on its boundary; dprev holds U^{n-1} with psi(t_{n-1})).  theta = 0: explicit Euler.
+static hjb_status theta_step(hjb_grid* g, double dt, const double* dprev, double* dU, uint8_t* dpol,
+                             const hjb_solve_params* sp, hjb_step_stats* S) {
+  const double th = sp->theta;
+  Level tmpl;
+  const Level& lv0 = fine_level(g, tmpl);
+  const int64_t ne = g->N;
+  cudaStream_t st = g->st;
+  float ms;
+  if (th == 0.0) {
+    // search at U^{n-1}: policy argmin_a H^a(U^{n-1}), F = U^{n-1} + dt f^pi; then
+    // U^n = F + U^{n-1} - A'_dt U^{n-1} = U^{n-1} + dt (L^pi + c) U^{n-1} + dt f^pi (interior)
+    const double* up;
+    TRY(halo_input(g, dprev, &up));
+    hjb_pi_stats pis{};
+    cudaEventRecord(g->ev[0], st);
+    TRY(policy_update_dev(g, dt, up, dprev, dpol, g->F, &pis));
+    cudaEventRecord(g->ev[1], st);
+    TRY(apply_fine(g, dt, dpol, dprev, g->v));
+    TRY(theta_rhs(g, dprev, g->v, dU));
+    cudaEventRecord(g->ev[2], st);
+    CK(cudaEventSynchronize(g->ev[2]));
+    cudaEventElapsedTime(&ms, g->ev[0], g->ev[1]);
+    S->ms_search += ms;
+    cudaEventElapsedTime(&ms, g->ev[1], g->ev[2]);
+    S->ms_solve += ms;
+    S->pi_iters = 1;
+    S->changed[0] = pis.changed;
+    S->R[0] = S->final_R = 0.0;  // explicit: the step is its own solution
+    return HJB_OK;
+  }
+  if (!g->vtheta) TRY(dalloc((void**)&g->vtheta, (size_t)ne * sizeof(double)));
+  hjb_status result = HJB_OK;
+  bool last_exact = true;
+  const int nb1 = (int)std::min<int64_t>((ne + 255) / 256, (int64_t)g->sms * 8);
+  for (int it = 1; it <= sp->max_pi; ++it) {
+    hjb_pi_stats pis{};
+    cudaEventRecord(g->ev[0], st);
+    // search at V = theta U + (1 - theta) U^{n-1} (row residual U - U^{n-1} - dt H(V), D1 with theta)
+    LAUNCH(HJB_KC_VECTOR, (double)ne, 24.0 * ne, 3.0 * ne, k_theta_mix<<<nb1, 256, 0, st>>>(th, dU, dprev, g->vtheta, ne));
+    CKL();
+    TRY(halo_exchange(g, lv0, g->vtheta, g->lay.halo));
+    TRY(policy_update_dev(g, dt, g->vtheta, dprev, dpol, g->F, &pis));
+    // F_theta = U^{n-1} + (1-theta) dt (L^pi + c) U^{n-1} + dt f^pi ; R = ||F_theta - A_{theta dt} U||_inf
+    TRY(apply_fine(g, (1.0 - th) * dt, dpol, dprev, g->v));
+    TRY(theta_rhs(g, dprev, g->v, g->F));
+    TRY(halo_exchange(g, lv0, dU, g->lay.halo));
+    if (g->D == 2) launch_operator<2>(g, g->L0, g->C0, OP_RESID, 0, th * dt, 0.0, dpol, dU, g->F, g->r, nullptr);
+    else launch_operator<3>(g, g->L0, g->C0, OP_RESID, 0, th * dt, 0.0, dpol, dU, g->F, g->r, nullptr);
+    double r2, Rinf;
+    TRY(g->D == 2 ? norms_dev<2>(g, g->r, &r2, &Rinf) : norms_dev<3>(g, g->r, &r2, &Rinf));
+    cudaEventRecord(g->ev[1], st);
+    CK(cudaEventSynchronize(g->ev[1]));
+    cudaEventElapsedTime(&ms, g->ev[0], g->ev[1]);
+    S->ms_search += ms;
+    const int slot = std::min(it - 1, HJB_MAX_PI_LOG - 1);
+    S->changed[slot] = pis.changed;
+    S->R[slot] = Rinf;
+    S->final_R = Rinf;
+    if (!std::isfinite(Rinf)) return fail(HJB_ERR_NONFINITE, "non-finite theta-scheme residual");
+    if (it > 1 && (Rinf <= sp->tol_pi || (pis.changed == 0 && last_exact))) break;
+    if (it == sp->max_pi) { result = fail(HJB_ERR_NOT_CONVERGED, "policy iteration hit max_pi"); break; }
+    const bool settled = (it > 1 && pis.changed == 0);
+    cudaEventRecord(g->ev[0], st);
+    if (sp->use_mg && !(settled && g->mg_ready && g->mg_pol0 == dpol && g->mg_dt == th * dt))
+      TRY(hjb_mg_setup(g, th * dt, dpol, &sp->mg));
+    cudaEventRecord(g->ev[1], st);
+    hjb_solve_stats ss{};
+    const double eta = (settled || g->K == 1) ? 0.0 : sp->pi_forcing;
+    hjb_status s2 = g->D == 2 ? bicgstab<2>(g, th * dt, dpol, g->F, dU, sp, &ss, eta)
+                              : bicgstab<3>(g, th * dt, dpol, g->F, dU, sp, &ss, eta);
+    last_exact = (ss.rres <= sp->krylov_rtol) && (!(sp->krylov_rtol_inf > 0.0) || ss.rres_inf <= sp->krylov_rtol_inf);
+    cudaEventRecord(g->ev[2], st);
+    CK(cudaEventSynchronize(g->ev[2]));
+    cudaEventElapsedTime(&ms, g->ev[0], g->ev[1]);
+    S->ms_setup += ms;
+    cudaEventElapsedTime(&ms, g->ev[1], g->ev[2]);
+    S->ms_solve += ms;
+    S->pi_iters = it;
+    S->krylov_iters[slot] = ss.iters;
+    S->krylov_iters_total += ss.iters;
+    S->final_rres = ss.rres;
+    S->final_rres_inf = ss.rres_inf;
+    if (s2 != HJB_OK) { result = s2; break; }
+  }
+  return result;
+}
+
+extern "C" hjb_status hjb_cfl_rate(hjb_grid_t g, const uint8_t* policy, double* rate) {
+  if (!g || !rate) return fail(HJB_ERR_INVALID_ARG, "null argument");
+  if (!g->have_coeffs) return fail(HJB_ERR_STATE, "call hjb_set_coeffs first");
+  if (policy && !is_device_ptr(policy)) return fail(HJB_ERR_INVALID_ARG, "policy must be a device array");
+  CK(cudaSetDevice(g->desc.device));
+  const LevelDev& L = g->L0;
+#define CFL(DD, PP)                                                                                       \
+  LAUNCH(HJB_KC_BOUNDARY, 0, 0, 0,                                                                        \
+         k_cfl<DD, PP><<<dims(g, L, (const void*)k_cfl<DD, PP>), dim3(kBX, kBY), 0, g->st>>>(L, g->C0, policy, \
+                                                                                            g->partial))
+  if (g->D == 2) {
+    if (g->P == 1) CFL(2, 1);
+    else CFL(2, 2);
+  } else {
+    if (g->P == 1) CFL(3, 1);
+    else if (g->P == 2) CFL(3, 2);
+    else CFL(3, 3);
+  }
+#undef CFL
+  CKL();
+  hjb_status err;
+  *rate = host_finalize(g, g->nblk_last, 0x1u, SC_NONE, &err);
+  return err;
+}
+
 // ---------------------------------------------------------------------------- step
 extern "C" hjb_status hjb_step(hjb_grid_t g, double dt, const double* U_prev, double* U, uint8_t* policy,
                                const double* psi, const hjb_solve_params* p, hjb_step_stats* out) {
@@ -1843,6 +2059,16 @@ extern "C" hjb_status hjb_step(hjb_grid_t g, double dt, const double* U_prev, do
   hjb_step_stats S{};
   float ms;
   hjb_status result = HJB_OK;
+  if (!(sp->theta >= 0.0 && sp->theta <= 1.0)) return fail(HJB_ERR_INVALID_ARG, "theta must be in [0, 1]");
+  if (sp->theta < 1.0) {
+    result = theta_step(g, dt, dprev, dU, dpol, sp, &S);
+    S.n_levels = (int32_t)g->levels.size();
+    if (h_U) CK(cudaMemcpyAsync(U, dU, vb, cudaMemcpyDeviceToHost, st));
+    if (h_pol) CK(cudaMemcpyAsync(policy, dpol, (size_t)g->N, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (out) *out = S;
+    return result;
+  }
   bool last_exact = true;  // the last policy evaluation reached krylov_rtol
   for (int it = 1; it <= sp->max_pi; ++it) {
     hjb_pi_stats pis{};

@@ -447,6 +447,50 @@ __global__ void __launch_bounds__(kTX) k_extrapolate(LevelDev L, const double* _
   }
 }
 
+// ================================================================== theta-scheme
+// V = theta U + (1 - theta) U_prev over every local element (boundary and halo entries included):
+// the argument of the policy search of the theta-scheme (DESIGN.md §3 reading xxvi)
+__global__ void __launch_bounds__(256) k_theta_mix(double theta, const double* __restrict__ u,
+                                                   const double* __restrict__ up, double* __restrict__ v,
+                                                   int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    v[i] = fma(theta, u[i], (1.0 - theta) * up[i]);
+}
+
+// out = F + U_prev - y at interior nodes, with F = U_prev + dt f^pi (the search's output) and
+// y = A'_{(1-theta) dt} U_prev = U_prev - (1-theta) dt (L^pi + c) U_prev: the theta-scheme right-hand
+// side U_prev + (1-theta) dt (L^pi + c) U_prev + dt f^pi (B^{n,n-1} of P:419-424); theta = 0: U^n
+template <int D>
+__global__ void __launch_bounds__(kTX) k_theta_rhs(LevelDev L, const double* __restrict__ F,
+                                                   const double* __restrict__ up, const double* __restrict__ y,
+                                                   double* __restrict__ out) {
+  FOR_INTERIOR(L) {
+    const int j = interior_offset<D>(L, col, row);
+    out[j] = F[j] + (up[j] - y[j]);
+  }
+}
+
+// positivity (CFL) rate of Proposition CFL: max over owned interior nodes of
+// sum_e w_e - c^a_j (= sum_p (A_p+B_p)/(2dx) - c, the M = P+1 pairs incl. the drift pair) for the
+// node's control (pol != null) or over every control (pol == null); partial [max, 0]
+template <int D, int P>
+__global__ void __launch_bounds__(kTX, HJB_SEARCH_MINB) k_cfl(LevelDev L, CoefDev C, const uint8_t* __restrict__ pol,
+                                                             double* partial) {
+  double red[2] = {-INFINITY, 0.0};
+  FOR_INTERIOR(L) {
+    Node<D> nd;
+    node_at<D>(L, col, row, nd);
+    load_fields<D>(C, nd);
+    const int a0 = pol ? (int)pol[nd.loc] : 0, a1 = pol ? a0 + 1 : C.K;
+    for (int a = a0; a < a1; ++a) {
+      Tap<D> taps[2 * P + 1];
+      const double wsum = row_geometry<D, P>(L, C.sigma_dir + a * P * D, C.b_dir + a * D, nd, taps);
+      red[0] = fmax(red[0], wsum - (nd.cn + C.c_ctrl[a]));
+    }
+  }
+  block_reduce_store<2>(red, partial, 0x1u);
+}
+
 // first smoothing sweep from x = 0 with the stored diagonal: y = omega b / D (the arithmetic of
 // k_operator<..., OP_JACOBI0>, without its per-node geometry)
 template <int D>

@@ -383,10 +383,11 @@ def bj_config(i: int, n: Optional[int] = None, K: Optional[int] = None,
 
 
 # =================================================================== paper problems
-def problem_A(nx: int, n_alpha: int = 40, T: float = 0.5, n_steps: int = 1) -> Problem:
+def problem_A(nx: int, n_alpha: int = 40, T: float = 0.5, n_steps: int = 1, shift: float = 0.0) -> Problem:
     """PAPER.md:465-471 (Problem A): u = (3/2 - t) sin x1 sin x2 on [-pi,pi]^2, b = alpha,
     sigma = sqrt2 (sin(x1+x2), cos(x1+x2)), c = 0, unit-circle controls
-    alpha_i = (cos 2 pi i/N, sin 2 pi i/N)."""
+    alpha_i = (cos 2 pi i/N, sin 2 pi i/N).  shift = 7 pi/8: the shifted domain
+    [-pi/8, 15 pi/8]^2 of Remark two-over, psi = u on its boundary (not zero)."""
     K = n_alpha
     d, P = 2, 1
     sigma_dir = np.zeros((K, P, d))
@@ -410,7 +411,8 @@ def problem_A(nx: int, n_alpha: int = 40, T: float = 0.5, n_steps: int = 1) -> P
         x1, x2 = p.coords(idx)
         return (1.5 - t) * xp.sin(x1) * xp.sin(x2)
 
-    p = Problem(name=f"problemA_{nx}", d=d, P=P, K=K, Q=2, n=nx, lo=-math.pi, hi=math.pi, T=T,
+    p = Problem(name=f"problemA_{nx}" + (f"_shift{shift:g}" if shift else ""), d=d, P=P, K=K, Q=2, n=nx,
+                lo=-math.pi + shift, hi=math.pi + shift, T=T,
                 n_steps=n_steps, sigma_dir=sigma_dir, b_dir=b_dir, c_ctrl=np.zeros(K),
                 _fields=fields, _f_tables=f_tables, _u_exact=u_exact)
     return p

@@ -378,6 +378,45 @@ def test_stored_diagonal_smoother_is_bit_identical(name, mk, monkeypatch):
     assert np.abs(out["stored"]).max() > 0
 
 
+@pytest.mark.parametrize("name,mk", [("cfg1", lambda: bj_config(1)), ("cfg2_513", lambda: bj_config(2, n=513)),
+                                     ("cfg3_33", lambda: bj_config(3, n=33))])
+def test_graph_tail_is_bit_identical(name, mk, monkeypatch):
+    """The multigrid tail replayed from a captured CUDA graph (default: the cycle from the first level
+    owning <= 70000 nodes down) gives the same V-cycle, bit for bit, as direct launches
+    (HJB_NO_GRAPHS=1), on the first application (capture + replay) and on later ones (replay after a
+    new hjb_mg_setup with another policy and dt: the graph is re-captured when dt changes)."""
+    torch = require_gpu()
+    p = mk()
+    x = to_dev(random_vector(p), torch)
+    out = {}
+    for mode in ("graphs", "direct"):
+        monkeypatch.delenv("HJB_NO_GRAPHS", raising=False)
+        if mode == "direct":
+            monkeypatch.setenv("HJB_NO_GRAPHS", "1")
+        g, _ = setup(p)
+        U0 = to_dev(p.g(p.all_idx()), torch)
+        pol = torch.zeros(p.N, dtype=torch.uint8, device="cuda")
+        F = torch.zeros(p.N, dtype=torch.float64, device="cuda")
+        ys = []
+        for dt, U in ((p.dt, U0), (p.dt, U0 + 0.1 * x), (0.5 * p.dt, U0)):
+            g.policy_update(dt, U, U0, pol, F)
+            g.mg_setup(dt, pol)
+            for _ in range(2):
+                y = torch.zeros(p.N, dtype=torch.float64, device="cuda")
+                g.mg_apply(x, y)
+                ys.append(y)
+        g.profile_reset(False)
+        g.mg_apply(x, torch.zeros_like(x))
+        prof = g.profile_read()
+        torch.cuda.synchronize()
+        out[mode] = ([y.cpu().numpy() for y in ys], prof)
+        g.close()
+    for a, b in zip(out["graphs"][0], out["direct"][0]):
+        assert np.array_equal(a, b) and np.abs(a).max() > 0
+    assert out["graphs"][1]["graph_launches"] >= 1 and out["direct"][1]["graph_launches"] == 0
+    assert out["graphs"][1]["total_launches"] == out["direct"][1]["total_launches"]
+
+
 @pytest.mark.parametrize("gamma,gmin", [(1, 0), (2, 0), (3, 0)])
 def test_step_parity_cycle_index(gamma, gmin):
     """V-, W- and gamma = 3 cycles on every level (the default revisits only large levels, which the
