@@ -298,6 +298,19 @@ typedef struct {
 hjb_status hjb_step(hjb_grid_t g, double dt, const double* U_prev, double* U, uint8_t* policy,
                     const double* psi_packed, const hjb_solve_params* p, hjb_step_stats* out);
 
+/* Exact-psi boundary mode (PAPER.md Remark rhs): a truncated
+ * stencil endpoint lies on dOmega; by default (reading i) it takes the multilinear interpolation of
+ * the nodal boundary values psi(t_n) held in U.  With samples != NULL it takes psi(t_n, z) itself,
+ * reconstructed from samples of psi on the faces at spacing h / refine by cubic (2D) / bicubic (3D)
+ * Lagrange interpolation along the face (error O((h/refine)^4): below fp64 rounding for the BJ
+ * grids with refine >= 64 in 2D).  samples: DEVICE array, retained (the caller refreshes its
+ * contents for every t_n), layout [2 d][M^(d-1)], M = refine (n - 1) + 1, face 2 d + side (side 0:
+ * x_d = lo, 1: x_d = hi), along-face axes in increasing order, the first fastest.  Affects the
+ * control search (hjb_policy_update, hjb_step) and the residuals of U (hjb_solve, hjb_step); the
+ * system matrix is unchanged (a truncated endpoint couples to boundary nodes only).  theta = 1 only.
+ * samples == NULL: back to interpolation.                                                      */
+hjb_status hjb_set_boundary_samples(hjb_grid_t g, int32_t refine, const double* samples);
+
 /* Positivity (CFL) rate of Proposition CFL (eq. CFL_trunc): the largest
  *   sum_{p=1}^{P+1} (A^a_p + B^a_p) / (2 dx) - c^a_j
  * over owned interior nodes j (truncated weights included, so it grows like dx^{-3/2} / dx^{-2}

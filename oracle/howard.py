@@ -34,24 +34,31 @@ class SearchResult:
     ties: np.ndarray = field(default=None)  # [N_I] number of controls within 1e-12 S_j of the min
 
 
-def hamiltonian(prob, idx, alpha, U_full, t, fields, k_scale=1.0):
+def hamiltonian(prob, idx, alpha, U_full, t, fields, k_scale=1.0, exact_psi=None):
     """H^a_j(U) = L_hat^a[U](x_j) + c^a_j U_j + f^a_j for one control per node (eq. Lhat),
-    plus S_j = sum of |terms| (near-tie scale, reading iv)."""
+    plus S_j = sum of |terms| (near-tie scale, reading iv).  exact_psi (z -> psi(z)): truncated
+    endpoints take the Dirichlet value (Remark rhs)."""
     geo = Geometry.of(prob, k_scale)
     sig, b, c = node_coefficients(prob, idx, alpha, fields)
     x = geo.node_x(idx)
-    cols, vals, _ = lhat_rows(geo, x, sig, b)
     Uj = U_full[idx]
-    diff = U_full[cols] - Uj[:, None]
-    L = np.sum(vals * diff, axis=1)
     f = source_term(prob, t, alpha, fields)
+    if exact_psi is None:
+        cols, vals, _ = lhat_rows(geo, x, sig, b)
+        diff = U_full[cols] - Uj[:, None]
+        L = np.sum(vals * diff, axis=1)
+        S = np.sum(vals * (np.abs(U_full[cols]) + np.abs(Uj)[:, None]), axis=1)
+    else:
+        cols, vals, rowsum, bsum = lhat_rows(geo, x, sig, b, exact_psi=exact_psi)
+        L = np.sum(vals * U_full[cols], axis=1) + bsum - rowsum * Uj
+        S = np.sum(vals * np.abs(U_full[cols]), axis=1) + np.abs(bsum) + rowsum * np.abs(Uj)
     H = L + c * Uj + f
-    S = np.sum(vals * (np.abs(U_full[cols]) + np.abs(Uj)[:, None]), axis=1) + np.abs(c * Uj) + np.abs(f)
+    S = S + np.abs(c * Uj) + np.abs(f)
     return H, S, f
 
 
 def control_search(prob, U_full, U_prev_full, t, dt, fields=None, idx=None, k_scale=1.0,
-                   chunk=1 << 18):
+                   chunk=1 << 18, exact_psi=None):
     """Exhaustive linear search over the discrete control set (footnote P:156):
     for every interior j and every a in index order evaluate H^a_j(U) from its definition and
     keep the lowest-index argmin."""
@@ -72,7 +79,7 @@ def control_search(prob, U_full, U_prev_full, t, dt, fields=None, idx=None, k_sc
         Hall = np.empty((prob.K, m))
         Sall = np.empty((prob.K, m))
         for a in range(prob.K):
-            H, S, f = hamiltonian(prob, sub, np.full(m, a), U_full, t, fl, k_scale)
+            H, S, f = hamiltonian(prob, sub, np.full(m, a), U_full, t, fl, k_scale, exact_psi)
             Hall[a], Sall[a] = H, S
             better = H < best                      # strict: lowest index wins exact ties
             second = np.where(better, best, np.minimum(second, H))
@@ -99,13 +106,15 @@ class StepStats:
 
 
 def howard_step(prob, U_prev_full, t, dt, fields=None, tol_pi=None, max_pi=50, k_scale=1.0,
-                policy0=None, solve_kw=None, theta=1.0):
+                policy0=None, solve_kw=None, theta=1.0, exact_psi=False):
     """One step t_{n-1} -> t_n = t of the theta-scheme (eq. FullScheme) by policy
     iteration.  The row residual of control a is (derivation D1 with theta)
         (A^a U - F^a)_j = U_j - U^{n-1}_j - dt H^a_j(V),   V = theta U + (1 - theta) U^{n-1},
     (L_hat and c are linear in their argument), so the policy improvement is the control search at V
     with f at t_{n-1} + theta dt.  theta = 0 (explicit Euler) needs no solve: U^n = U^{n-1} + dt
-    min_a H^a(U^{n-1}) at every interior node, boundary psi(t_n).
+    min_a H^a(U^{n-1}) at every interior node, boundary psi(t_n).  exact_psi: the exact-psi boundary
+    mode of Remark rhs: truncated endpoints take psi(z) (for V: theta psi(t_n, z) +
+    (1 - theta) psi(t_{n-1}, z)), prob.psi_at.
     Returns (U^n on the full grid, policy on the full grid, StepStats)."""
     geo = Geometry.of(prob, k_scale)
     interior = geo.interior_idx()
@@ -118,9 +127,11 @@ def howard_step(prob, U_prev_full, t, dt, fields=None, tol_pi=None, max_pi=50, k
     t_theta = t - dt + theta * dt
     pol_full = np.zeros(prob.N, dtype=np.int64)
     stats = StepStats()
+    tp = t - dt
+    ex_v = (lambda z: theta * prob.psi_at(t, z) + (1.0 - theta) * prob.psi_at(tp, z)) if exact_psi else None
     if theta == 0.0:                              # explicit Euler: one control search at U^{n-1}
         sr = control_search(prob, U_prev_full, U_prev_full, t_theta, dt, fields=fields, idx=interior,
-                            k_scale=k_scale)
+                            k_scale=k_scale, exact_psi=ex_v)
         U = U_prev_full.copy()
         U[interior] = U_prev_full[interior] + dt * sr.H
         U[bidx] = psi_full[bidx]
@@ -134,7 +145,8 @@ def howard_step(prob, U_prev_full, t, dt, fields=None, tol_pi=None, max_pi=50, k
     have_policy = False
     for it in range(1, max_pi + 1):
         V = theta * U + (1.0 - theta) * U_prev_full
-        sr = control_search(prob, V, U_prev_full, t_theta, dt, fields=fields, idx=interior, k_scale=k_scale)
+        sr = control_search(prob, V, U_prev_full, t_theta, dt, fields=fields, idx=interior, k_scale=k_scale,
+                            exact_psi=ex_v)
         R = np.abs(U[interior] - U_prev_full[interior] - dt * sr.H)      # = sr.R when theta = 1
         changed = int(np.sum(sr.policy != pol_full[interior]))
         stats.changed.append(changed)
@@ -144,7 +156,7 @@ def howard_step(prob, U_prev_full, t, dt, fields=None, tol_pi=None, max_pi=50, k
         pol_full[interior] = sr.policy
         have_policy = True
         sysm = assemble(prob, pol_full, dt, t, U_prev_full, psi_full, fields=fields, k_scale=k_scale,
-                        theta=theta)
+                        theta=theta, exact_psi=exact_psi)
         X, rres = solve(sysm, x0=U[interior], **(solve_kw or {}))
         stats.solve_rres.append(rres)
         U[interior] = X

@@ -159,10 +159,11 @@ def source_term(prob, t, alpha, fields):
 
 
 # ------------------------------------------------------------------ the truncated LISL row
-def stencil_pairs(geo: Geometry, x, sig, b):
+def stencil_pairs(geo: Geometry, x, sig, b, with_masks=False):
     """The M = P+1 Scheme-2 pairs at nodes x, each truncated.
     Returns a list of pairs (z_plus, A, z_minus, B) with A, B the finite-difference weights of
-    eq. (TruncScheme) P:218-221."""
+    eq. (TruncScheme) P:218-221; with_masks: (z_plus, A, z_minus, B, trunc_plus, trunc_minus), the
+    masks of the endpoints whose ray was truncated (mu < 1: they lie on dOmega)."""
     m, d = x.shape
     P = sig.shape[1]
     pairs = []
@@ -172,43 +173,59 @@ def stencil_pairs(geo: Geometry, x, sig, b):
         mu_p, bind_p = truncation_mu(geo, x, y_plus)
         mu_m, bind_m = truncation_mu(geo, x, y_minus)
         A, B = truncation_weights(mu_p, mu_m)
-        pairs.append((truncated_endpoint(geo, x, y_plus, mu_p, bind_p), A,
-                      truncated_endpoint(geo, x, y_minus, mu_m, bind_m), B))
+        pp = (truncated_endpoint(geo, x, y_plus, mu_p, bind_p), A,
+              truncated_endpoint(geo, x, y_minus, mu_m, bind_m), B)
+        pairs.append(pp + (mu_p < 1.0, mu_m < 1.0) if with_masks else pp)
     # drift pair p = P+1: y+ = y- = dx b (both signs equal), A = B = 1/mu
     y_d = geo.dx * b
     mu_d, bind_d = truncation_mu(geo, x, y_d)
     A, B = drift_weights(mu_d)
     z_d = truncated_endpoint(geo, x, y_d, mu_d, bind_d)
-    pairs.append((z_d, A, z_d, B))
+    pairs.append((z_d, A, z_d, B) + ((mu_d < 1.0, mu_d < 1.0) if with_masks else ()))
     return pairs
 
 
-def lhat_rows(geo: Geometry, x, sig, b):
+def lhat_rows(geo: Geometry, x, sig, b, exact_psi=None):
     """Rows of l_hat for nodes x:
         l_hat_{j,i} = sum_p [A_p w_i(x_j + y_hat+_p) + B_p w_i(x_j + y_hat-_p)] / (2 dx)
     Returns (cols [m, E], vals [m, E], rowsum [m]) with duplicates not merged, and
-    rowsum = sum_p (A_p + B_p)/(2 dx)."""
+    rowsum = sum_p (A_p + B_p)/(2 dx).
+    exact_psi (a function z [m, d] -> psi(z)): the exact-psi boundary mode of Remark rhs
+    (NEXT-2): a truncated endpoint (on dOmega) takes the Dirichlet value psi(z) instead of
+    the interpolation of the nodal boundary values; its interpolation entries are dropped from
+    (cols, vals) and returned as a fourth output, the row's sum_e w_e psi(z_e) [m]."""
     cols, vals = [], []
     rowsum = np.zeros(x.shape[0])
-    for (zp, A, zm, B) in stencil_pairs(geo, x, sig, b):
-        ip, wp = interp_weights(geo, zp)
-        im, wm = interp_weights(geo, zm)
-        cols += [ip, im]
-        vals += [A[:, None] * wp / (2.0 * geo.dx), B[:, None] * wm / (2.0 * geo.dx)]
+    bsum = np.zeros(x.shape[0])
+    for (zp, A, zm, B, tp, tm) in stencil_pairs(geo, x, sig, b, with_masks=True):
+        for z, W, tr in ((zp, A, tp), (zm, B, tm)):
+            iz, wz = interp_weights(geo, z)
+            w = W[:, None] * wz / (2.0 * geo.dx)
+            if exact_psi is not None and tr.any():
+                w = np.where(tr[:, None], 0.0, w)
+                bsum[tr] += W[tr] / (2.0 * geo.dx) * exact_psi(z[tr])
+            cols.append(iz)
+            vals.append(w)
         rowsum += (A + B) / (2.0 * geo.dx)
-    return np.concatenate(cols, axis=1), np.concatenate(vals, axis=1), rowsum
+    out = (np.concatenate(cols, axis=1), np.concatenate(vals, axis=1), rowsum)
+    return out + (bsum,) if exact_psi is not None else out
 
 
-def lhat_apply(geo: Geometry, idx, sig, b, phi_full):
+def lhat_apply(geo: Geometry, idx, sig, b, phi_full, exact_psi=None):
     """L_hat[phi](x_j) = sum_i l_hat_{j,i} (phi_i - phi_j)  (eq. Lhat), with phi given
-    on the full grid (boundary nodes hold their values: interpolate-at-boundary mode)."""
+    on the full grid (boundary nodes hold their values: interpolate-at-boundary mode), or
+    with exact_psi the truncated endpoints taking psi(z) (Remark rhs)."""
     x = geo.node_x(idx)
-    cols, vals, _ = lhat_rows(geo, x, sig, b)
     phi_j = phi_full[np.asarray(idx)]
-    return np.sum(vals * (phi_full[cols] - phi_j[:, None]), axis=1)
+    if exact_psi is None:
+        cols, vals, _ = lhat_rows(geo, x, sig, b)
+        return np.sum(vals * (phi_full[cols] - phi_j[:, None]), axis=1)
+    cols, vals, rowsum, bsum = lhat_rows(geo, x, sig, b, exact_psi)
+    # sum over non-truncated entries of w (phi_i - phi_j) + sum over truncated endpoints w (psi - phi_j)
+    return np.sum(vals * phi_full[cols], axis=1) + bsum - rowsum * phi_j
 
 
-def apply_operator(prob, policy_full, x_full, dt, idx=None, fields=None, k_scale=1.0):
+def apply_operator(prob, policy_full, x_full, dt, idx=None, fields=None, k_scale=1.0, exact_psi=None):
     """Matrix-free (A^pi x)_j for interior rows j (theta = 1):
         (A x)_j = x_j - dt [ L_hat[x](x_j) + c_j x_j ]
     Boundary entries of x are used as given.  Returns values at idx (default: all interior)."""
@@ -217,5 +234,5 @@ def apply_operator(prob, policy_full, x_full, dt, idx=None, fields=None, k_scale
         idx = geo.interior_idx()
     idx = np.asarray(idx, dtype=np.int64)
     sig, b, c = node_coefficients(prob, idx, np.asarray(policy_full)[idx], fields)
-    L = lhat_apply(geo, idx, sig, b, x_full)
+    L = lhat_apply(geo, idx, sig, b, x_full, exact_psi)
     return x_full[idx] - dt * (L + c * x_full[idx])

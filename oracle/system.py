@@ -29,7 +29,8 @@ class System:
         self.A, self.F, self.interior, self.geo = A, F, interior, geo
 
 
-def assemble(prob, policy_full, dt, t, U_prev_full, psi_full, fields=None, k_scale=1.0, theta=1.0):
+def assemble(prob, policy_full, dt, t, U_prev_full, psi_full, fields=None, k_scale=1.0, theta=1.0,
+             exact_psi=False):
     """Assemble A^pi, F^pi of the theta-scheme, eq. (FullScheme), for the policy pi:
         A^pi = I - theta dt (L_hat^pi + c^pi)                               (interior rows)
         F^pi = U^{n-1} + (1 - theta) dt (L_hat^pi + c^pi)[U^{n-1}] + dt f^pi
@@ -37,7 +38,9 @@ def assemble(prob, policy_full, dt, t, U_prev_full, psi_full, fields=None, k_sca
     (B^{n,n} and B^{n,n-1} of P:419-424 with time-independent sigma, b).  c and f are evaluated at
     t_{n-1} + theta dt; t is t_n.  U_prev_full holds psi(t_{n-1}) on the boundary.
     policy_full: control index per full-grid node (only interior entries used).  theta = 1 is the
-    implicit Euler system of the paper's experiments (reading x)."""
+    implicit Euler system of the paper's experiments (reading x).  exact_psi: the exact-psi boundary
+    mode (Remark rhs): a truncated endpoint contributes psi(t_n, z) (psi(t_{n-1}, z) in the
+    explicit part) to F instead of the interpolation of nodal boundary values (prob.psi_at)."""
     geo = Geometry.of(prob, k_scale)
     interior = geo.interior_idx()
     m = interior.size
@@ -46,7 +49,12 @@ def assemble(prob, policy_full, dt, t, U_prev_full, psi_full, fields=None, k_sca
     alpha = np.asarray(policy_full)[interior]
     sig, b, c = node_coefficients(prob, interior, alpha, fields)
     x = geo.node_x(interior)
-    cols, vals, rowsum = lhat_rows(geo, x, sig, b)
+    t_theta = t - dt + theta * dt
+    if exact_psi:
+        cols, vals, rowsum, bsum = lhat_rows(geo, x, sig, b, exact_psi=lambda z: prob.psi_at(t, z))
+    else:
+        cols, vals, rowsum = lhat_rows(geo, x, sig, b)
+        bsum = np.zeros(m)
 
     # position of each full-grid node in the interior unknown vector (-1 for boundary)
     pos = np.full(prob.N, -1, dtype=np.int64)
@@ -65,13 +73,17 @@ def assemble(prob, policy_full, dt, t, U_prev_full, psi_full, fields=None, k_sca
                         np.concatenate([cpos[off], np.arange(m)]))), shape=(m, m)).tocsr()
     A.sum_duplicates()
 
-    t_theta = t - dt + theta * dt
     f = source_term(prob, t_theta, alpha, fields)
     bnd = cpos < 0                                              # couplings to boundary nodes
     F = U_prev_full[interior] + dt * f
     F = F + np.bincount(rows[bnd], weights=theta * dt * vflat[bnd] * psi_full[cflat[bnd]], minlength=m)
+    F = F + theta * dt * bsum
     if theta < 1.0:                                             # B^{n,n-1} U^{n-1}: explicit part
-        Lprev = np.sum(vals * (U_prev_full[cols] - U_prev_full[interior][:, None]), axis=1)
+        if exact_psi:
+            cp, vp, rp, bp = lhat_rows(geo, x, sig, b, exact_psi=lambda z: prob.psi_at(t - dt, z))
+            Lprev = np.sum(vp * U_prev_full[cp], axis=1) + bp - rp * U_prev_full[interior]
+        else:
+            Lprev = np.sum(vals * (U_prev_full[cols] - U_prev_full[interior][:, None]), axis=1)
         F = F + (1.0 - theta) * dt * (Lprev + c * U_prev_full[interior])
     return System(A, F, interior, geo)
 

@@ -18,7 +18,8 @@ EXPORTS = ["hjb_last_error", "hjb_version", "hjb_grid_create", "hjb_grid_query",
            "hjb_set_coeffs", "hjb_set_source", "hjb_policy_update", "hjb_apply",
            "hjb_mg_params_default", "hjb_mg_setup", "hjb_mg_apply", "hjb_solve_params_default",
            "hjb_solve", "hjb_step", "hjb_profile_reset", "hjb_profile_read",
-           "hjb_partition", "hjb_halo_plan", "hjb_comm_unique_id", "hjb_cfl_rate"]
+           "hjb_partition", "hjb_halo_plan", "hjb_comm_unique_id", "hjb_cfl_rate",
+           "hjb_set_boundary_samples"]
 
 HJB_COMM_NCCL, HJB_COMM_THREADS = 0, 1
 
@@ -142,6 +143,7 @@ def load(path: str = None):
         "hjb_partition": (i32, [i32, i64, i32, i32, i64, C.POINTER(Layout)]),
         "hjb_comm_unique_id": (i32, [vp]),
         "hjb_cfl_rate": (i32, [vp, vp, C.POINTER(d)]),
+        "hjb_set_boundary_samples": (i32, [vp, i32, vp]),
         "hjb_halo_plan": (i32, [i32, i64, i32, i32, i64, HaloMsg * 2, C.POINTER(i32)]),
     }
     for name, (res, args) in sig.items():

@@ -162,6 +162,11 @@ class HJBGrid:
             check(code)
         return out
 
+    def set_boundary_samples(self, refine=0, samples=None):
+        """Exact-psi boundary mode (hjb_set_boundary_samples); samples=None: interpolation mode."""
+        check(self.lib.hjb_set_boundary_samples(self.h, int(refine), _ptr(samples)))
+        self._keep_bsamp = samples
+
     def cfl_rate(self, policy=None) -> float:
         """Positivity rate max (sum_p (A_p+B_p)/(2dx) - c) of Proposition CFL (hjb_cfl_rate)."""
         r = C.c_double()

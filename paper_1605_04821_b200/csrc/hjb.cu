@@ -163,6 +163,8 @@ struct hjb_grid {
   double* rng_part = nullptr; // k_field_ranges block partials
   double2* upair = nullptr;   // (U_i, U_{i+1}) pair copy of the searched U (k_search_deep2)
   double* vtheta = nullptr;   // theta U + (1-theta) U_prev (theta-scheme search argument)
+  const double* bsamp = nullptr;  // exact-psi mode: face samples of psi (caller-owned, retained)
+  int brefine = 0;
   bool drift_reg = false;     // deep drift endpoints stay within one cell of the node (|offset| < 1)
   double h_rng[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // host copy of d_rng (scale-field ranges)
   // CUDA graphs of the multigrid tail: the cycle from level graph_level down (levels owning <=
@@ -464,6 +466,18 @@ static LevelDev shape_of(const LevelDev& L, const SkipRect& r) {
   S.nI = r.c1 - r.c0;
   S.nrows = (r.r1 - r.r0) * (r.y1 - r.y0);
   return S;
+}
+
+// the fine-level coefficients for kernels whose argument is U itself: with the exact-psi mode the
+// truncated endpoints read psi from the face samples (Remark rhs)
+static CoefDev coef_u(const hjb_grid* g) {
+  CoefDev C = g->C0;
+  if (g->bsamp) {
+    C.bsamp = g->bsamp;
+    C.brefine = g->brefine;
+    C.bM = (int)(g->brefine * (g->n - 1) + 1);
+  }
+  return C;
 }
 
 // ---------------------------------------------------------------------------- dimension dispatch
@@ -1225,7 +1239,11 @@ static hjb_status policy_update_dev(hjb_grid* g, double dt, const double* U, con
   const SkipRect tiles = use_tma ? g->tma.tiles : SkipRect{0, 0, 0, 0};
   SkipRect gstrips[6], dstrips[6];
   // shared-memory window kernels: over the whole interior (no strips), or over the deep box
-  const WinPlan* wp = use_tma ? nullptr : g->win_full.ok ? &g->win_full : (has_deep && g->win_deep.ok) ? &g->win_deep : nullptr;
+  // the whole-interior window (general geometry) has no exact-psi path: the general kernel takes the
+  // strips in that mode
+  const WinPlan* wp = use_tma ? nullptr : (g->win_full.ok && !g->bsamp) ? &g->win_full
+                                        : (has_deep && g->win_deep.ok) ? &g->win_deep : nullptr;
+  const CoefDev CU = coef_u(g);
   const bool win_all = wp == &g->win_full;
   const int ngs = win_all ? 0 : ring_strips(full, rect, gstrips);
   // 2D deep rectangle without a window / TMA plan: the L1-lean k_search_deep2 (hjb_search2.cuh)
@@ -1237,7 +1255,7 @@ static hjb_status policy_update_dev(hjb_grid* g, double dt, const double* U, con
     if (LL.nI > 0 && LL.nrows > 0) {                                                                          \
       LAUNCH(HJB_KC_SEARCH, 0, 0, 0,                                                                          \
              k_search<DD, PP, DP><<<dims(g, LL, (const void*)k_search<DD, PP, DP>, kSBX, tsm),                \
-                                    dim3(kSBX, kSBY), tsm, g->st>>>(g->L0, g->C0, dt, U, Uprev, pol, F,       \
+                                    dim3(kSBX, kSBY), tsm, g->st>>>(g->L0, CU, dt, U, Uprev, pol, F,          \
                                                                     g->partial + 2 * nblk, RR));             \
       nblk += g->nblk_last;                                                                                   \
     }                                                                                                         \
@@ -1287,11 +1305,13 @@ static hjb_status policy_update_dev(hjb_grid* g, double dt, const double* U, con
     nblk += wp->grid;
   }
   if (deep2) {
+#if HJB_SEARCH2_PAIRS
     if (!g->upair) TRY(dalloc((void**)&g->upair, (size_t)g->N * sizeof(double2)));
     const int64_t ne = g->N;
     LAUNCH(HJB_KC_SEARCH, 0, 0, 0,
            k_make_pairs<<<(int)std::min<int64_t>((ne + 255) / 256, (int64_t)g->sms * 8), 256, 0, g->st>>>(U, g->upair, ne));
     CKL();
+#endif
     TRY(launch_search2(g, dt, U, Uprev, pol, F, rect, &nblk));
   }
   if (use_tma) {  // deep tiles: windows staged in shared memory by TMA (partials after the others')
@@ -1753,6 +1773,7 @@ static hjb_status bicgstab(hjb_grid* g, double dt, const uint8_t* pol, const dou
                            const hjb_solve_params* sp, hjb_solve_stats* out, double eta = 0.0) {
   const LevelDev& L = g->L0;
   const CoefDev& C = g->C0;
+  const CoefDev CUx = coef_u(g);  // residuals of x = U (exact-psi mode: psi at truncated endpoints)
   cudaStream_t st = g->st;
   Level tmpl;
   const Level& lv0 = fine_level(g, tmpl);
@@ -1773,7 +1794,7 @@ static hjb_status bicgstab(hjb_grid* g, double dt, const uint8_t* pol, const dou
   for (int restart = 0; restart < 6 && !converged; ++restart) {
     // r = F - A x ; rhat = r ; p = r
     TRY(halo_exchange(g, lv0, x, H));
-    launch_operator<D>(g, L, C, OP_RESID, 0, dt, 0.0, pol, x, F, g->r, nullptr);
+    launch_operator<D>(g, L, CUx, OP_RESID, 0, dt, 0.0, pol, x, F, g->r, nullptr);
     LAUNCH(HJB_KC_VECTOR, L.n_own, 24.0 * L.n_own, 2.0 * L.n_own,
            k_bicg_init<D><<<dims(g, L, (const void*)k_bicg_init<D>), dim3(kBX, kBY), 0, st>>>(L, g->r, g->rhat, g->p, g->partial));
     CKL();
@@ -1814,7 +1835,7 @@ static hjb_status bicgstab(hjb_grid* g, double dt, const uint8_t* pol, const dou
     }
     // true residual check (recursive residual drifts, SURVEY hard part 5) in both norms
     TRY(halo_exchange(g, lv0, x, H));
-    launch_operator<D>(g, L, C, OP_RESID, 0, dt, 0.0, pol, x, F, g->r, nullptr);
+    launch_operator<D>(g, L, CUx, OP_RESID, 0, dt, 0.0, pol, x, F, g->r, nullptr);
     double tr2, trinf;
     TRY(norms_dev<D>(g, g->r, &tr2, &trinf));
     if (!std::isfinite(tr2)) return fail(HJB_ERR_NONFINITE, "non-finite true residual");
@@ -1962,6 +1983,20 @@ static hjb_status theta_step(hjb_grid* g, double dt, const double* dprev, double
   return result;
 }
 
+extern "C" hjb_status hjb_set_boundary_samples(hjb_grid_t g, int32_t refine, const double* samples) {
+  if (!g) return fail(HJB_ERR_INVALID_ARG, "null handle");
+  if (!samples) {
+    g->bsamp = nullptr;
+    g->brefine = 0;
+    return HJB_OK;
+  }
+  if (refine < 1 || refine * (g->n - 1) + 1 < 4) return fail(HJB_ERR_INVALID_ARG, "refine must be >= 1 (>= 4 samples per axis)");
+  if (!is_device_ptr(samples)) return fail(HJB_ERR_INVALID_ARG, "samples must be a device array");
+  g->bsamp = samples;
+  g->brefine = refine;
+  return HJB_OK;
+}
+
 extern "C" hjb_status hjb_cfl_rate(hjb_grid_t g, const uint8_t* policy, double* rate) {
   if (!g || !rate) return fail(HJB_ERR_INVALID_ARG, "null argument");
   if (!g->have_coeffs) return fail(HJB_ERR_STATE, "call hjb_set_coeffs first");
@@ -2060,6 +2095,8 @@ extern "C" hjb_status hjb_step(hjb_grid_t g, double dt, const double* U_prev, do
   float ms;
   hjb_status result = HJB_OK;
   if (!(sp->theta >= 0.0 && sp->theta <= 1.0)) return fail(HJB_ERR_INVALID_ARG, "theta must be in [0, 1]");
+  if (sp->theta < 1.0 && g->bsamp)
+    return fail(HJB_ERR_UNSUPPORTED, "the exact-psi boundary mode supports theta = 1 only");
   if (sp->theta < 1.0) {
     result = theta_step(g, dt, dprev, dU, dpol, sp, &S);
     S.n_levels = (int32_t)g->levels.size();

@@ -95,6 +95,11 @@ struct CoefDev {
   const double* f_feat;       // [Q][ld] or null
   int64_t ld;
   int K, P, Q;
+  // exact-psi boundary mode (Remark rhs; hjb_set_boundary_samples): psi sampled on the
+  // faces at spacing h / brefine, bM samples per along-face axis; null = interpolation mode.  Set
+  // only in the CoefDev passed where the argument is U itself (search, residual of U).
+  const double* bsamp = nullptr;
+  int brefine = 0, bM = 0;
 };
 
 template <int D>
@@ -470,6 +475,7 @@ struct Tap {
   int c[D];      // cell (lowest corner), global multi-index
   double s[D];   // fractions in the cell
   double w;      // weight w_e (0 for a skipped zero step)
+  int face = -1; // truncated endpoint: its face of dOmega, 2 d + (upper side); -1 otherwise
 };
 
 template <int D>
@@ -481,6 +487,62 @@ __device__ __forceinline__ int tap_base(const LevelDev& L, const Tap<D>& t) {
 template <int D>
 __device__ __forceinline__ double tap_value(const LevelDev& L, const double* __restrict__ v, const Tap<D>& t) {
   return interp_at<D, false>(v + tap_base<D>(L, t), L.n, L.n * L.n, t.s);
+}
+
+// cubic Lagrange weights at x for nodes 0, 1, 2, 3
+__device__ __forceinline__ void cubic_weights(double x, double* w) {
+  const double a = x - 1.0, b = x - 2.0, c = x - 3.0;
+  w[0] = -a * b * c / 6.0;
+  w[1] = x * b * c / 2.0;
+  w[2] = -x * a * c / 2.0;
+  w[3] = x * a * b / 6.0;
+}
+
+// psi(z) at a truncated endpoint on face t.face (exact-psi mode): cubic (2D) / bicubic (3D) Lagrange
+// interpolation of the face samples, the 4 samples nearest to z per along-face axis (one-sided at the
+// ends); along-face position z_e = c_e + s_e grid units = (c_e + s_e) brefine sample units
+template <int D>
+__device__ __forceinline__ double face_value(const CoefDev& C, const Tap<D>& t) {
+  const int bd = t.face >> 1;
+  const int M = C.bM;
+  const double* F = C.bsamp + (int64_t)t.face * (D == 2 ? M : (int64_t)M * M);
+  int k0[2];
+  double w[2][4];
+  int e = 0;
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    if (d == bd) continue;
+    const double q = ((double)t.c[d] + t.s[d]) * C.brefine;
+    int k = (int)floor(q) - 1;
+    k = max(0, min(k, M - 4));
+    k0[e] = k;
+    cubic_weights(q - k, w[e]);
+    ++e;
+  }
+  if (D == 2) {
+    double v = 0.0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v = fma(w[0][i], __ldg(F + k0[0] + i), v);
+    return v;
+  }
+  double v = 0.0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    double r = 0.0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) r = fma(w[0][i], __ldg(F + (int64_t)(k0[1] + j) * M + k0[0] + i), r);
+    v = fma(w[1][j], r, v);
+  }
+  return v;
+}
+
+// tap value on a vector v that is U itself: exact-psi mode (C.bsamp) replaces the interpolation of the
+// nodal boundary values at a truncated endpoint by psi(z)
+template <int D>
+__device__ __forceinline__ double tap_value_u(const LevelDev& L, const CoefDev& C, const double* __restrict__ v,
+                                              const Tap<D>& t) {
+  if (C.bsamp != nullptr && t.face >= 0) return face_value<D>(C, t);
+  return tap_value<D>(L, v, t);
 }
 
 // endpoints of control a at node nd: taps[2p] = +sigma_p, taps[2p+1] = -sigma_p, taps[2P] = drift.
@@ -532,6 +594,8 @@ __device__ __forceinline__ double row_geometry(const LevelDev& L, const double* 
       wsum += tp.w + tm.w;
       cell_general<D>(L, nd, o, mup, bp, tp.c, tp.s);
       cell_general<D>(L, nd, om, mum, bm, tm.c, tm.s);
+      tp.face = bp >= 0 ? 2 * bp + (o[bp] > 0.0 ? 1 : 0) : -1;
+      tm.face = bm >= 0 ? 2 * bm + (om[bm] > 0.0 ? 1 : 0) : -1;
     }
   }
   {  // drift pair: y_{P+1} = k^2 b, both endpoints equal, A = B = 1/mu (total weight 2/(mu 2k^2))
@@ -556,6 +620,7 @@ __device__ __forceinline__ double row_geometry(const LevelDev& L, const double* 
       const double mu = ray_mu<D>(L, nd, o, bdim);
       cell_general<D>(L, nd, o, mu, bdim, t.c, t.s);
       t.w = (bdim >= 0) ? L.inv_k2 / mu : L.inv_k2;
+      t.face = bdim >= 0 ? 2 * bdim + (o[bdim] > 0.0 ? 1 : 0) : -1;
     }
     wsum += t.w;
   }

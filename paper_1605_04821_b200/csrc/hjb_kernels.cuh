@@ -96,7 +96,8 @@ __global__ void __launch_bounds__(kTX, (DEEP && D == 2) ? HJB_OP_DEEP_MINB : HJB
       for (int v = 0; v < U; ++v)
         if (ok[v])
 #pragma unroll
-          for (int e = 0; e < E; ++e) vals[v][e] = tap_value<D>(L, x, taps[v][e]);
+          for (int e = 0; e < E; ++e) vals[v][e] = (DEEP || MODE != OP_RESID) ? tap_value<D>(L, x, taps[v][e])
+                                                                           : tap_value_u<D>(L, C, x, taps[v][e]);
     }
 #pragma unroll
     for (int v = 0; v < U; ++v) {
@@ -197,7 +198,7 @@ __global__ void __launch_bounds__(kTX, DEEP ? (D == 2 ? HJB_SEARCH_DEEP_MINB : 3
       }
       double vals[E];
 #pragma unroll
-      for (int e = 0; e < E; ++e) vals[e] = tap_value<D>(L, U, taps[e]);
+      for (int e = 0; e < E; ++e) vals[e] = DEEP ? tap_value<D>(L, U, taps[e]) : tap_value_u<D>(L, C, U, taps[e]);
       double acc = 0.0;
 #pragma unroll
       for (int e = 0; e < E; ++e) acc = fma(taps[e].w, vals[e], acc);

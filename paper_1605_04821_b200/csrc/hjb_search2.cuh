@@ -82,6 +82,24 @@ struct STabQuad {
   int v[256];  // drift endpoint quadrant per control: bit 0 = cell left of the node (x), bit 1 = below (y)
 };
 
+#ifndef HJB_SEARCH2_PAIRS
+#define HJB_SEARCH2_PAIRS 0  // 1: 16-byte gathers from a pair copy (measured slower at cfg4:
+                             // 2x the gather footprint, 102 vs 38 GB DRAM); 0: 8-byte gathers from U
+#endif
+// the two values (U_c, U_{c+1}) of the cell row at offset off from the node
+__device__ __forceinline__ double2 cell_row(const double2* up, const double* u, int off) {
+#if HJB_SEARCH2_PAIRS
+  return __ldg(pair_at(up, off));
+#else
+  return make_double2(__ldg(u + off), __ldg(u + off + 1));
+#endif
+}
+
+#ifndef HJB_SEARCH2_UNROLL
+#define HJB_SEARCH2_UNROLL 1
+#endif
+constexpr int kS2Unroll = HJB_SEARCH2_UNROLL;  // controls per unrolled loop body (A/B knob)
+
 #ifndef HJB_SUPER_COLS
 #define HJB_SUPER_COLS 16
 #endif
@@ -142,8 +160,11 @@ __global__ void __launch_bounds__(kTX, HJB_SEARCH2_MINB) k_search_deep2(LevelDev
       const double2* up = UP + nd.loc;       // pairs of the node's row ...
       const double2* upn = up + n;           // ... and of the next row (one base per row: one
                                              // wide multiply-add per load address)
+      const double* u0 = U + nd.loc;
+      const double* u1 = u0 + n;
       double best = INFINITY, fbest = 0.0;
       int arg = 0;
+#pragma unroll kS2Unroll
       for (int a = 0; a < C.K; ++a) {
         const double* t = tab.v + a * T::S;
         double acc = 0.0;
@@ -155,8 +176,8 @@ __global__ void __launch_bounds__(kTX, HJB_SEARCH2_MINB) k_search_deep2(LevelDev
           split_floor(ksc[p] * t[T::SD + 2 * p + 1], fl1, s1);
           const int off = fl1 * n + fl0;          // plus endpoint's cell corner, relative to the node
           const int offm = -off - n - 1;          // minus endpoint's cell corner (i - fl - 1)
-          const double2 p0 = __ldg(pair_at(up, off)), p1 = __ldg(pair_at(upn, off));
-          const double2 m0 = __ldg(pair_at(up, offm)), m1 = __ldg(pair_at(upn, offm));
+          const double2 p0 = cell_row(up, u0, off), p1 = cell_row(upn, u1, off);
+          const double2 m0 = cell_row(up, u0, offm), m1 = cell_row(upn, u1, offm);
           const double w = t[T::W + p];
           acc = fma(w, interp_pairs(p0, p1, s0, s1), acc);
           acc = fma(w, interp_pairs_mirror(m0, m1, s0, s1), acc);

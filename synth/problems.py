@@ -63,6 +63,7 @@ class Problem:
     _fields: Callable                     # (idx, xp) -> dict of node fields
     _f_tables: Callable                   # t -> (f_basis [K,Q], f_ctrl [K])
     _u_exact: Optional[Callable] = None   # (t, idx, xp) -> values
+    _u_at: Optional[Callable] = None      # (t, [x_1..x_d] coordinate arrays, xp) -> values
     _g: Optional[Callable] = None         # (idx, xp) -> values (default u_exact(0))
     _psi: Optional[Callable] = None       # (t, idx, xp) -> values (default u_exact(t))
     tol_pi: float = 1e-10
@@ -138,6 +139,12 @@ class Problem:
         if self._u_exact is None:
             return None
         return self._u_exact(t, idx, _xp_of(idx))
+
+    def psi_at(self, t, X):
+        """Dirichlet data psi(t, z) at arbitrary boundary points z (X: [m, d] coordinates), for the
+        exact-psi boundary mode (PAPER.md Remark rhs); psi = u_exact on dOmega here."""
+        X = np.asarray(X, dtype=np.float64)
+        return self._u_at(t, [X[:, i] for i in range(self.d)], np)
 
     def g(self, idx):
         if self._g is not None:
@@ -273,13 +280,15 @@ def rotated_2d(name: str, n: int, K: int, s: tuple, beta: float, n_steps: int,
                      -(1.0 + t) * math.sin(th), -2.0 * th, 1.0]
         return fb, thetas ** 2
 
+    def u_at(t, x, xp):
+        return (1.0 + t) * xp.sin(hp * x[0]) * xp.cos(hp * x[1])
+
     def u_exact(t, idx, xp):
-        x1, x2 = p.coords(idx)
-        return (1.0 + t) * xp.sin(hp * x1) * xp.cos(hp * x2)
+        return u_at(t, p.coords(idx), xp)
 
     p = Problem(name=name, d=d, P=P, K=K, Q=8, n=n, lo=-1.0, hi=1.0, T=T, n_steps=n_steps,
                 sigma_dir=sigma_dir, b_dir=b_dir, c_ctrl=c_ctrl, _fields=fields,
-                _f_tables=f_tables, _u_exact=u_exact,
+                _f_tables=f_tables, _u_exact=u_exact, _u_at=u_at,
                 meta=dict(thetas=thetas, s=s, beta=beta, noisy=noisy, c=c))
     return p
 
@@ -354,13 +363,15 @@ def rotated_3d(name: str, n: int, n_phi: int = 12, n_vt: int = 8, s=(1.0, 0.4, 0
             fc[k] = ph * ph + vt * vt
         return fb, fc
 
-    def u_exact(t, idx, xp):
-        x = p.coords(idx)
+    def u_at(t, x, xp):
         return (1.0 + t) * xp.cos(hp * x[0]) * xp.cos(hp * x[1]) * xp.cos(hp * x[2])
+
+    def u_exact(t, idx, xp):
+        return u_at(t, p.coords(idx), xp)
 
     p = Problem(name=name, d=d, P=P, K=K, Q=13, n=n, lo=-1.0, hi=1.0, T=T, n_steps=n_steps,
                 sigma_dir=sigma_dir, b_dir=b_dir, c_ctrl=c_ctrl, _fields=fields,
-                _f_tables=f_tables, _u_exact=u_exact,
+                _f_tables=f_tables, _u_exact=u_exact, _u_at=u_at,
                 meta=dict(angles=angles, s=s, beta=beta, c=c))
     return p
 
@@ -407,14 +418,16 @@ def problem_A(nx: int, n_alpha: int = 40, T: float = 0.5, n_steps: int = 1, shif
         fb = np.tile(np.array([0.5 - t, 1.5 - t]), (K, 1))
         return fb, np.zeros(K)
 
+    def u_at(t, x, xp):
+        return (1.5 - t) * xp.sin(x[0]) * xp.sin(x[1])
+
     def u_exact(t, idx, xp):
-        x1, x2 = p.coords(idx)
-        return (1.5 - t) * xp.sin(x1) * xp.sin(x2)
+        return u_at(t, p.coords(idx), xp)
 
     p = Problem(name=f"problemA_{nx}" + (f"_shift{shift:g}" if shift else ""), d=d, P=P, K=K, Q=2, n=nx,
                 lo=-math.pi + shift, hi=math.pi + shift, T=T,
                 n_steps=n_steps, sigma_dir=sigma_dir, b_dir=b_dir, c_ctrl=np.zeros(K),
-                _fields=fields, _f_tables=f_tables, _u_exact=u_exact)
+                _fields=fields, _f_tables=f_tables, _u_exact=u_exact, _u_at=u_at)
     return p
 
 
@@ -435,13 +448,15 @@ def problem_B(nx: int, n_alpha: int = 40, T: float = 0.5, n_steps: int = 1) -> P
         fb = np.stack([np.full(K, 1.0 - t), -2.0 * al[:, 0] * al[:, 1] * (2.0 - t)], axis=1)
         return fb, np.zeros(K)
 
+    def u_at(t, x, xp):
+        return (2.0 - t) * xp.sin(x[0]) * xp.sin(x[1])
+
     def u_exact(t, idx, xp):
-        x1, x2 = p.coords(idx)
-        return (2.0 - t) * xp.sin(x1) * xp.sin(x2)
+        return u_at(t, p.coords(idx), xp)
 
     p = Problem(name=f"problemB_{nx}", d=d, P=P, K=K, Q=2, n=nx, lo=-math.pi, hi=math.pi, T=T,
                 n_steps=n_steps, sigma_dir=sigma_dir, b_dir=b_dir, c_ctrl=np.zeros(K),
-                _fields=fields, _f_tables=f_tables, _u_exact=u_exact)
+                _fields=fields, _f_tables=f_tables, _u_exact=u_exact, _u_at=u_at)
     return p
 
 
@@ -466,7 +481,8 @@ def lisl_laplacian(sigma: float, ell: int, d: int = 2, T: float = 1e6) -> Proble
     p = Problem(name=f"lisl_lap_{sigma:g}_{ell}", d=d, P=P, K=K, Q=1, n=n, lo=0.0, hi=1.0, T=T,
                 n_steps=1, sigma_dir=sigma_dir, b_dir=np.zeros((1, d)), c_ctrl=np.zeros(1),
                 _fields=fields, _f_tables=f_tables, _u_exact=None,
-                _g=lambda idx, xp: zero(0, idx, xp), _psi=zero)
+                _g=lambda idx, xp: zero(0, idx, xp), _psi=zero,
+                _u_at=lambda t, x, xp: xp.zeros_like(x[0]))
     return p
 
 
@@ -477,3 +493,26 @@ def random_vector(p: Problem, seed: int = 43, idx=None):
     if _is_torch(idx):
         return noise.uniform_pm1_torch(seed, 0, idx)
     return noise.uniform_pm1_np(seed, 0, idx)
+
+
+def face_samples(p: Problem, t: float, refine: int):
+    """psi(t, .) sampled on every face of dOmega at spacing h / refine (input data of the exact-psi
+    boundary mode, include/hjb.h hjb_set_boundary_samples): face f = 2 d + side (side 0: x_d = lo,
+    1: x_d = hi); along-face axes in increasing order, the first fastest; M = refine (n - 1) + 1 samples
+    per axis.  Returns a float64 array [2 d][M^(d-1)]."""
+    M = refine * (p.n - 1) + 1
+    s = np.linspace(p.lo, p.hi, M)
+    out = []
+    for d in range(p.d):
+        for side in (0, 1):
+            others = [e for e in range(p.d) if e != d]
+            grids = np.meshgrid(*([s] * len(others)), indexing="ij")   # first other axis slowest
+            cols = {}
+            for k, e in enumerate(others):
+                cols[e] = grids[k].T.ravel() if len(others) == 2 else grids[k].ravel()
+            X = np.zeros((M ** len(others), p.d))
+            for e in others:
+                X[:, e] = cols[e]
+            X[:, d] = p.lo if side == 0 else p.hi
+            out.append(p.psi_at(t, X))
+    return np.stack(out)

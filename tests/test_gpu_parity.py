@@ -5,6 +5,8 @@ Tolerances (BASELINE.json north_star):
   policy            identical except at near-ties (H gap <= 1e-12 S_j, reading iv)
   solution          ||U_gpu - U_orc||_inf <= 1e-8 ||u||_inf, both solved to rel. residual <= 1e-12
 """
+import math
+
 import numpy as np
 import pytest
 
@@ -428,3 +430,59 @@ def test_step_parity_cycle_index(gamma, gmin):
         Uo, _, _ = howard_step(p, Uo, s * p.dt, p.dt)
     assert np.abs(Ug - Uo).max() <= 1e-8 * max(1.0, np.abs(Uo).max())
     assert all(st["final_rres"] <= 1e-12 for st in stats)
+
+
+def _exact_tol(p, t, refine, scale_w):
+    """Bound on the GPU's face reconstruction error (cubic Lagrange on samples at h/refine) times the
+    largest truncated weight sum of a row: |psi - p3| <= (h/r)^4 / 24 * max|psi''''| per axis."""
+    h = (p.hi - p.lo) / (p.n - 1)
+    m4 = (1.0 + t) * (math.pi / 2) ** 4           # BJ cfg0/cfg2 psi = (1+t) sin(pi x1/2) cos(pi x2/2)
+    return 4.0 * (h / refine) ** 4 / 24.0 * m4 * scale_w
+
+
+@pytest.mark.parametrize("name,mk", [("cfg0", lambda: bj_config(0)), ("cfg2_65_K8", lambda: bj_config(2, n=65, K=8))])
+def test_exact_psi_mode_parity(name, mk):
+    """Exact-psi boundary mode (NEXT-2; Remark rhs, P:428-432) through hjb_set_boundary_samples:
+    the control search and one implicit step against the oracle's exact mode (psi(z) analytic at
+    truncated endpoints), within the NS tolerances plus the samples' reconstruction bound."""
+    torch = require_gpu()
+    from synth.problems import face_samples
+    from synth.device import packed_psi
+    p = mk()
+    g, fields = setup(p)
+    t, dt, r = p.dt, p.dt, 64
+    samp = to_dev(face_samples(p, t, r), torch)
+    g.set_boundary_samples(r, samp)
+    U0h = p.g(p.all_idx())
+    rng = np.random.default_rng(2)
+    Uh = U0h.copy()
+    b = p.boundary_idx()
+    Uh[b] = p.psi(t, b)
+    inter = Geometry.of(p).interior_idx()
+    Uh[inter] += 0.01 * rng.uniform(-1, 1, inter.size)
+    pol = torch.zeros(p.N, dtype=torch.uint8, device="cuda")
+    F = torch.zeros(p.N, dtype=torch.float64, device="cuda")
+    fb, fc = p.f_tables(t)
+    g.set_source(fb, fc)
+    g.policy_update(dt, to_dev(Uh, torch), to_dev(U0h, torch), pol, F)
+    ex = lambda z: p.psi_at(t, z)  # noqa: E731
+    sr = control_search(p, Uh, U0h, t, dt, exact_psi=ex)
+    pg = pol.cpu().numpy()[inter].astype(np.int64)
+    wmax = 1.0 / (2 * (p.hi - p.lo) / (p.n - 1)) * 64.0      # generous bound on a row's truncated weights
+    tol = 1e-12 * sr.scale + _exact_tol(p, t, r, wmax)
+    decisive = (sr.second_gap > 2 * tol)
+    assert np.array_equal(pg[decisive], sr.policy[decisive])
+    Hg, _, _ = hamiltonian(p, inter, pg, Uh, t, fields_np := p.fields(inter), exact_psi=ex)
+    assert np.all(Hg - sr.H <= 2 * tol)
+    # one implicit step in exact mode vs the oracle's exact-mode step
+    Ud = torch.empty(p.N, dtype=torch.float64, device="cuda")
+    st = g.step(dt, to_dev(U0h, torch), Ud, None, packed_psi(p, t), pi_forcing=0.0)
+    Uo, _, _ = howard_step(p, U0h, t, dt, exact_psi=True)
+    err = np.abs(Ud.cpu().numpy() - Uo).max()
+    assert err <= 1e-8 * max(1.0, np.abs(Uo).max()), (err, st)
+    # the modes differ (psi curves along the faces): interpolation mode is a different discrete problem
+    g.set_boundary_samples(0, None)
+    Ui = torch.empty(p.N, dtype=torch.float64, device="cuda")
+    g.step(dt, to_dev(U0h, torch), Ui, None, packed_psi(p, t), pi_forcing=0.0)
+    assert np.abs(Ui.cpu().numpy() - Ud.cpu().numpy()).max() > 1e-9
+    g.close()

@@ -232,3 +232,41 @@ def test_one_dimensional_closed_form_matrix():
         assert full.sum() - got.sum() < 1e-12 * full.sum()     # nothing off the grid line
         got[j] -= full.sum()          # l_hat row -> operator row sum_i l_ji (phi_i - phi_j)
         assert np.abs(got - (-LSL[j] / (2 * geo.dx))).max() < 1e-9 / geo.dx
+
+
+def test_exact_psi_mode_quadratic_closed_form():
+    """Exact-psi boundary mode (Remark rhs; NEXT-2): a truncated endpoint takes psi(z), so
+    for a quadratic phi = 1/2 x^T H x + g.x the truncated LISL row is D5 with the interpolation bias
+    of the UNtruncated endpoints only:
+        L_hat[phi](x_j) = 1/2 sum_p s_p^T H s_p + b.(H x_j + g) + (mu_d dx/2) b^T H b
+                          + sum_{e untruncated} w_e sum_i (H_ii/2) s_{e,i}(1 - s_{e,i}) dx^2
+    (the consistency identities D4 make a truncated pair exact given exact endpoint values).  The
+    interpolation mode differs at truncated rows (face interpolation of a curved psi)."""
+    import math as _m
+    from oracle.scheme import interp_weights, lhat_apply, stencil_pairs
+    p = bj_config(0, n=33)
+    geo = Geometry.of(p)
+    idx = geo.interior_idx()
+    x = geo.node_x(idx)
+    alpha = np.full(idx.size, 3)
+    sig, b, _ = node_coefficients(p, idx, alpha)
+    Hm = np.array([[1.4, -0.4], [-0.4, 2.6]])
+    gv = np.array([0.2, -0.1])
+    phi_of = lambda X: 0.5 * np.einsum("mi,ij,mj->m", X, Hm, X) + X @ gv  # noqa: E731
+    phi = phi_of(geo.node_x(np.arange(p.N)))
+    L_ex = lhat_apply(geo, idx, sig, b, phi, exact_psi=phi_of)
+    L_in = lhat_apply(geo, idx, sig, b, phi)
+    expect = 0.5 * np.einsum("mpi,ij,mpj->m", sig, Hm, sig) + np.einsum("mi,mi->m", b, x @ Hm + gv)
+    trunc_any = np.zeros(idx.size, dtype=bool)
+    for (zp, A, zm, B, tp, tm) in stencil_pairs(geo, x, sig, b, with_masks=True):
+        for z, W, tr in ((zp, A, tp), (zm, B, tm)):
+            t = (z - geo.lo) / geo.dx
+            s = t - np.clip(np.floor(t), 0, geo.n - 2)
+            bias = (W / (2 * geo.dx)) * np.sum(0.5 * np.diag(Hm)[None, :] * s * (1 - s), axis=1) * geo.dx ** 2
+            expect = expect + np.where(tr, 0.0, bias)
+            trunc_any |= tr
+    # drift: (mu_d dx / 2) b^T H b (mu_d = 1: never truncated in cfg0)
+    expect = expect + 0.5 * geo.dx * np.einsum("mi,ij,mj->m", b, Hm, b)
+    assert np.abs(L_ex - expect).max() < 1e-9 * max(1.0, np.abs(expect).max()), np.abs(L_ex - expect).max()
+    assert trunc_any.sum() > 0 and np.abs(L_in - L_ex)[trunc_any].max() > 1e-6
+    assert np.abs(L_in - L_ex)[~trunc_any].max() <= 1e-12 * np.abs(L_in).max()   # same value, other summation order

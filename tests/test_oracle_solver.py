@@ -221,3 +221,30 @@ def test_noisy_scale_branch_consistency():
         es.append(E)
     rate = math.log2(es[0] / es[2]) / 4                                          # h shrinks 16x
     assert rate >= 0.85 and es[2] <= 4e-3, es
+
+
+def test_exact_psi_mode_assembly_and_zero_psi():
+    """Exact-psi mode (Remark rhs): (1) the assembled system's boundary part equals the
+    matrix-free row with psi(z) at truncated endpoints (A U - F row by row, for U with exact boundary
+    values); (2) with psi = 0 on dOmega (Problems A/B) the two boundary modes coincide."""
+    p = bj_config(0, n=33)
+    dt = p.dt
+    U0 = p.g(p.all_idx())
+    rng = np.random.default_rng(8)
+    pol = rng.integers(0, p.K, size=p.N)
+    psi = _psi_full(p, dt)
+    sysm = assemble(p, pol, dt, dt, U0, psi, exact_psi=True)
+    X = U0.copy()
+    X[p.boundary_idx()] = psi[p.boundary_idx()]
+    X[sysm.interior] += 0.01 * rng.uniform(-1, 1, sysm.interior.size)
+    y_mf = apply_operator(p, pol, X, dt, exact_psi=lambda z: p.psi_at(dt, z))
+    f_part = sysm.F - U0[sysm.interior]                    # dt f + dt sum w psi(z) (boundary part)
+    fo = assemble(p, pol, dt, dt, np.zeros(p.N), np.zeros(p.N)).F   # dt f alone
+    lhs = sysm.A @ X[sysm.interior] - (f_part - fo)         # A_int X_int - dt * boundary terms
+    assert np.abs(lhs - y_mf).max() <= 1e-12 * np.abs(y_mf).max() * 1e2
+    sysi = assemble(p, pol, dt, dt, U0, psi)
+    assert np.abs(sysi.F - sysm.F).max() > 1e-8            # the modes differ where psi curves
+    q = problem_A(21)
+    Ua, _, _ = march(q, n_steps=2)
+    Ub, _, _ = march(q, n_steps=2, exact_psi=True)
+    assert np.abs(Ua - Ub).max() <= 1e-13
