@@ -209,6 +209,11 @@ typedef struct {
   int32_t gamma_min_nodes;   /* revisit level l+1 only if it owns >= gamma_min_nodes interior
                                 nodes (smaller levels are launch-latency bound: plain V there);
                                 default 131072                                                */
+  int32_t coarse_op;         /* 0: coarse operators rediscretised on each level with the injected
+                                policy (NS, default); 1: Galerkin A_{l+1} = R A_l P (PAPER.md:935,
+                                "constructed using the Galerkin principle"),
+                                stored ELL (<= 96 entries per row), 2D on one rank only
+                                (HJB_ERR_UNSUPPORTED otherwise)                               */
 } hjb_mg_params;
 
 void hjb_mg_params_default(int32_t dim, hjb_mg_params* out);

@@ -21,6 +21,7 @@
 #include "hjb_tma.cuh"
 #include "hjb_win.cuh"
 #include "hjb_search2.cuh"
+#include "hjb_galerkin.cuh"
 
 namespace hjb {
 struct WinPlan {
@@ -88,6 +89,8 @@ struct Level {
   double* dg = nullptr;           // smoothed levels: the diagonal of A (per policy, hjb_mg_setup)
   double* r2 = nullptr;           // W-cycle (gamma > 1): coarse residual / correction of a revisit
   double* e2 = nullptr;
+  int* gcol = nullptr;            // Galerkin coarse operator (levels >= 1): ELL [kGalW][elems]
+  double* gval = nullptr;
 };
 
 struct hjb_grid {
@@ -163,6 +166,10 @@ struct hjb_grid {
   double* rng_part = nullptr; // k_field_ranges block partials
   double2* upair = nullptr;   // (U_i, U_{i+1}) pair copy of the searched U (k_search_deep2)
   double* vtheta = nullptr;   // theta U + (1-theta) U_prev (theta-scheme search argument)
+  bool galerkin = false;      // coarse operators by the Galerkin product (hjb_mg_params.coarse_op)
+  int* gb_col = nullptr;      // B = A P scratch of the Galerkin setup (ELL [kGalWB][elems_0])
+  double* gb_val = nullptr;
+  int* d_flag = nullptr;      // device overflow flag
   const double* bsamp = nullptr;  // exact-psi mode: face samples of psi (caller-owned, retained)
   int brefine = 0;
   bool drift_reg = false;     // deep drift endpoints stay within one cell of the node (|offset| < 1)
@@ -566,6 +573,7 @@ extern "C" void hjb_mg_params_default(int32_t dim, hjb_mg_params* o) {
   o->gather_n = (dim == 3) ? 33 : 129;
   o->gamma = (dim == 3) ? 1 : 2;  // 3D: the V-cycle already contracts by <= 0.45 (W measured slower)
   o->gamma_min_nodes = 131072;
+  o->coarse_op = 0;  // rediscretised coarse operators (NS); 1 = Galerkin R A P (NEXT-4)
 }
 
 extern "C" void hjb_solve_params_default(int32_t dim, hjb_solve_params* o) {
@@ -660,8 +668,14 @@ static void free_levels(hjb_grid* g) {
     cudaFree(l.dg);
     cudaFree(l.r2);
     cudaFree(l.e2);
+    cudaFree(l.gcol);
+    cudaFree(l.gval);
   }
   g->levels.clear();
+  cudaFree(g->gb_col);
+  cudaFree(g->gb_val);
+  g->gb_col = nullptr;
+  g->gb_val = nullptr;
   g->mg_ready = false;
   for (auto& sg : g->graphs) cudaGraphExecDestroy(sg.exec);
   g->graphs.clear();
@@ -682,6 +696,7 @@ extern "C" hjb_status hjb_grid_destroy(hjb_grid_t g) {
   cudaFree(g->rng_part);
   cudaFree(g->upair);
   cudaFree(g->vtheta);
+  cudaFree(g->d_flag);
   if (g->cap_st) cudaStreamDestroy(g->cap_st);
   cudaFree(g->S);
   cudaFree(g->pol_int);
@@ -1559,6 +1574,64 @@ static hjb_status inject_all(hjb_grid* g) {
   return HJB_OK;
 }
 
+// Galerkin coarse operators A_{l+1} = R A_l P for every coarse level (2D, one rank), their diagonals,
+// and the coarsest level's dense inverse from its Galerkin rows (hjb_galerkin.cuh; NEXT-4)
+static hjb_status galerkin_setup(hjb_grid* g, double dt, const uint8_t* policy) {
+  if (g->D != 2 || g->R != 1)
+    return fail(HJB_ERR_UNSUPPORTED, "Galerkin coarse operators: 2D on one rank only");
+  if (!g->d_flag) TRY(dalloc((void**)&g->d_flag, sizeof(int)));
+  CK(cudaMemsetAsync(g->d_flag, 0, sizeof(int), g->st));
+  const size_t eb0 = (size_t)g->levels[0].elems;
+  if (!g->gb_col) {
+    TRY(dalloc((void**)&g->gb_col, (size_t)kGalWB * eb0 * sizeof(int)));
+    TRY(dalloc((void**)&g->gb_val, (size_t)kGalWB * eb0 * sizeof(double)));
+  }
+  for (size_t l = 1; l < g->levels.size(); ++l) {
+    Level& lv = g->levels[l];
+    if (!lv.gcol) {
+      TRY(dalloc((void**)&lv.gcol, (size_t)kGalW * lv.elems * sizeof(int)));
+      TRY(dalloc((void**)&lv.gval, (size_t)kGalW * lv.elems * sizeof(double)));
+      CK(cudaMemsetAsync(lv.gcol, 0xff, (size_t)kGalW * lv.elems * sizeof(int), g->st));
+    }
+  }
+  for (size_t l = 0; l + 1 < g->levels.size(); ++l) {
+    Level& lf = g->levels[l];
+    Level& lc = g->levels[l + 1];
+    const int64_t nf = (int64_t)lf.L.nI * lf.L.nrows, ncr = (int64_t)lc.L.nI * lc.L.nrows;
+    const int bf = (int)std::min<int64_t>((nf + 127) / 128, (int64_t)g->sms * 16);
+    const int bc = (int)std::min<int64_t>((ncr + 127) / 128, (int64_t)g->sms * 16);
+    CK(cudaMemsetAsync(g->gb_col, 0xff, (size_t)kGalWB * lf.elems * sizeof(int), g->st));
+    if (l == 0) {
+      if (g->P == 1)
+        LAUNCH(HJB_KC_COARSE, nf, 0, 0, k_gal_b_fine<1><<<bf, 128, 0, g->st>>>(lf.L, g->C0, dt, policy, lc.L.n, g->gb_col, g->gb_val, g->d_flag));
+      else
+        LAUNCH(HJB_KC_COARSE, nf, 0, 0, k_gal_b_fine<2><<<bf, 128, 0, g->st>>>(lf.L, g->C0, dt, policy, lc.L.n, g->gb_col, g->gb_val, g->d_flag));
+    } else {
+      LAUNCH(HJB_KC_COARSE, nf, 0, 0, k_gal_b_ell<<<bf, 128, 0, g->st>>>(lf.L, lf.gcol, lf.gval, lc.L.n, g->gb_col, g->gb_val, g->d_flag));
+    }
+    LAUNCH(HJB_KC_COARSE, ncr, 0, 0, k_gal_rb<<<bc, 128, 0, g->st>>>(lf.L, lc.L, g->gb_col, g->gb_val, lc.gcol, lc.gval, g->d_flag));
+    CKL();
+    if (l + 2 < g->levels.size())
+      LAUNCH(HJB_KC_COARSE, ncr, 0, 0, k_gal_diag<<<bc, 128, 0, g->st>>>(lc.L, lc.gcol, lc.gval, lc.dg));
+    CKL();
+  }
+  Level& lc = g->levels.back();
+  const int64_t Nc = lc.L.n_own;
+  if (g->levels.size() > 1) {
+    CK(cudaMemsetAsync(lc.Ainv, 0, (size_t)Nc * Nc * sizeof(double), g->st));
+    LAUNCH(HJB_KC_COARSE, Nc, 0, 0, k_gal_dense<<<(int)((Nc + 127) / 128), 128, 0, g->st>>>(lc.L, lc.gcol, lc.gval, lc.Ainv));
+    const size_t smem = (size_t)Nc * Nc * sizeof(double);
+    if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_coarse_invert, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    LAUNCH(HJB_KC_COARSE, Nc, 16.0 * Nc * Nc, 2.0 * Nc * Nc * Nc, k_coarse_invert<<<1, 1024, smem, g->st>>>(lc.Ainv, (int)Nc));
+    CKL();
+  }
+  int flag = 0;
+  CK(cudaMemcpyAsync(&flag, g->d_flag, sizeof(int), cudaMemcpyDeviceToHost, g->st));
+  CK(cudaStreamSynchronize(g->st));
+  if (flag) return fail(HJB_ERR_UNSUPPORTED, "Galerkin coarse operator row wider than the ELL width (96)");
+  return HJB_OK;
+}
+
 extern "C" hjb_status hjb_mg_setup(hjb_grid_t g, double dt, const uint8_t* policy, const hjb_mg_params* mp) {
   if (!g || !policy) return fail(HJB_ERR_INVALID_ARG, "null argument");
   TRY(check_dt(g, dt));
@@ -1567,7 +1640,7 @@ extern "C" hjb_status hjb_mg_setup(hjb_grid_t g, double dt, const uint8_t* polic
   hjb_mg_params_default(g->D, &def);
   const hjb_mg_params* p = mp ? mp : &def;
   if (p->nu_pre < 1 || p->nu_post < 0 || !(p->omega > 0.0) || p->omega > 1.0 || p->max_levels < 1 ||
-      p->gamma < 1 || p->gamma > 3 || p->gamma_min_nodes < 0)
+      p->gamma < 1 || p->gamma > 3 || p->gamma_min_nodes < 0 || p->coarse_op < 0 || p->coarse_op > 1)
     return fail(HJB_ERR_INVALID_ARG, "bad multigrid parameters");
   const bool rebuild = g->levels.empty() || std::memcmp(&g->mgp, p, sizeof(hjb_mg_params)) != 0 ||
                        g->levels[0].C.ld != g->C0.ld;
@@ -1584,6 +1657,8 @@ extern "C" hjb_status hjb_mg_setup(hjb_grid_t g, double dt, const uint8_t* polic
   }
   if (g->D == 2) TRY(inject_all<2>(g));
   else TRY(inject_all<3>(g));
+  g->galerkin = p->coarse_op == 1;
+  if (g->galerkin) TRY(galerkin_setup(g, dt, policy));
   // the diagonal of every smoothed level's operator (the smoother reads it instead of recomputing
   // the self weights; HJB_NO_DIAG=1 recomputes them in every sweep -- bit-identical either way)
   g->use_dg = !getenv("HJB_NO_DIAG");
@@ -1602,8 +1677,10 @@ extern "C" hjb_status hjb_mg_setup(hjb_grid_t g, double dt, const uint8_t* polic
         CK(cudaMemsetAsync(lv.e2, 0, vb, g->st));
       }
     }
+  if (g->galerkin) g->use_dg = true;  // the Galerkin smoother reads the stored diagonal
   if (g->use_dg)
     for (size_t l = 0; l + 1 < g->levels.size(); ++l) {
+      if (g->galerkin && l >= 1) continue;  // from the Galerkin rows (galerkin_setup)
       Level& lv = g->levels[l];
       const uint8_t* pol = (l == 0) ? g->mg_pol0 : lv.pol;
       if (g->D == 2) launch_operator<2>(g, lv.L, lv.C, OP_DIAG, 0, dt, 0.0, pol, nullptr, nullptr, lv.dg, nullptr, l == 0);
@@ -1612,6 +1689,36 @@ extern "C" hjb_status hjb_mg_setup(hjb_grid_t g, double dt, const uint8_t* polic
   CKL();
   g->mg_ready = true;
   return HJB_OK;
+}
+
+// Jacobi damping of level l: Galerkin coarse operators are not M-matrices (positive off-diagonals,
+// rows not diagonally dominant: measured at cfg2 513^2), where omega = 1 diverges (stationary
+// rho 1.6) and 0.8 contracts (0.063): min(omega, 0.8) there (reading xxix)
+static double level_omega(const hjb_grid* g, size_t l) {
+  return (g->galerkin && l >= 1) ? std::min(g->mgp.omega, kGalOmega) : g->mgp.omega;
+}
+
+// one residual (OP_RESID: y = b - A x) or damped-Jacobi sweep (OP_JACOBI / OP_JACOBI_D) on level l:
+// the matrix-free rediscretised operator, or on Galerkin levels (l >= 1) the stored R A P rows
+template <int D>
+static void level_sweep(hjb_grid* g, size_t l, int mode, const double* x, const double* b, double* y) {
+  Level& lv = g->levels[l];
+  const uint8_t* pol = (l == 0) ? g->mg_pol0 : lv.pol;
+  const double dt = g->mg_dt, om = level_omega(g, l);
+  if (g->galerkin && l >= 1) {
+    const int64_t nn = (int64_t)lv.L.nI * lv.L.nrows;
+    const int nb = (int)std::max<int64_t>(1, std::min<int64_t>((nn + 127) / 128, (int64_t)g->sms * 16));
+    const double bytes = (8.0 * 3 + 12.0 * kGalW) * nn;
+    if (mode == OP_RESID)
+      LAUNCH(HJB_KC_MG_COARSE, nn, bytes, 2.0 * kGalW * nn,
+             k_gal_sweep<false><<<nb, 128, 0, g->st>>>(lv.L, lv.gcol, lv.gval, x, b, lv.dg, 0.0, y));
+    else
+      LAUNCH(HJB_KC_MG_COARSE, nn, bytes + 8.0 * nn, 2.0 * kGalW * nn,
+             k_gal_sweep<true><<<nb, 128, 0, g->st>>>(lv.L, lv.gcol, lv.gval, x, b, lv.dg, om, y));
+    return;
+  }
+  launch_operator<D>(g, lv.L, lv.C, mode, 0, dt, mode == OP_RESID ? 0.0 : om, pol, x, b, y,
+                     mode == OP_JACOBI_D ? lv.dg : nullptr, l == 0);
 }
 
 // V(nu_pre, nu_post) from x = 0 on level l: out = M_l^{-1} b
@@ -1663,7 +1770,7 @@ static hjb_status vcycle(hjb_grid* g, size_t l, const double* b, double* out) {
     CKL();
     return HJB_OK;
   }
-  const double dt = g->mg_dt, om = g->mgp.omega;
+  const double dt = g->mg_dt, om = level_omega(g, l);
   const int npre = (l > 0 && g->nu_coarse > 0) ? g->nu_coarse : g->mgp.nu_pre;
   const int npost = (l > 0 && g->nu_coarse > 0) ? g->nu_coarse : g->mgp.nu_post;
   double* bufs[2] = {out, lv.tmp};
@@ -1681,11 +1788,11 @@ static hjb_status vcycle(hjb_grid* g, size_t l, const double* b, double* out) {
   }
   for (int k = 1; k < npre; ++k) {
     TRY(halo_exchange(g, lv, bufs[cur], lv.H));
-    launch_operator<D>(g, L, lv.C, jmode, 0, dt, om, pol, bufs[cur], b, bufs[1 - cur], lv.dg, fine);
+    level_sweep<D>(g, l, jmode, bufs[cur], b, bufs[1 - cur]);
     cur = 1 - cur;
   }
   TRY(halo_exchange(g, lv, bufs[cur], lv.H));
-  launch_operator<D>(g, L, lv.C, OP_RESID, 0, dt, 0.0, pol, bufs[cur], b, lv.res, nullptr, fine);
+  level_sweep<D>(g, l, OP_RESID, bufs[cur], b, lv.res);
   Level& lc = g->levels[l + 1];
   TRY(halo_exchange(g, lv, lv.res, 1));
   if (lc.replicated && !lv.replicated) {
@@ -1712,7 +1819,8 @@ static hjb_status vcycle(hjb_grid* g, size_t l, const double* b, double* out) {
   for (int k = 1; k < gamma && l + 2 < g->levels.size(); ++k) {  // W-cycle: revisit the coarse level
     const uint8_t* pc = lc.pol;
     TRY(halo_exchange(g, lc, lc.x, lc.H));
-    launch_operator<D>(g, lc.L, lc.C, OP_RESID, 0, dt, 0.0, pc, lc.x, lc.b, lc.r2, nullptr, false);
+    (void)pc;
+    level_sweep<D>(g, l + 1, OP_RESID, lc.x, lc.b, lc.r2);
     TRY(vcycle<D>(g, l + 1, lc.r2, lc.e2));
     const double nc = (double)lc.L.n_own;
     LAUNCH(HJB_KC_VECTOR, nc, 24.0 * nc, nc,
@@ -1724,7 +1832,7 @@ static hjb_status vcycle(hjb_grid* g, size_t l, const double* b, double* out) {
          k_prolong_add<D><<<dims(g, L, (const void*)k_prolong_add<D>), dim3(kBX, kBY), 0, st>>>(L, lc.L, lc.x, bufs[cur]));
   for (int k = 0; k < npost; ++k) {
     TRY(halo_exchange(g, lv, bufs[cur], lv.H));
-    launch_operator<D>(g, L, lv.C, jmode, 0, dt, om, pol, bufs[cur], b, bufs[1 - cur], lv.dg, fine);
+    level_sweep<D>(g, l, jmode, bufs[cur], b, bufs[1 - cur]);
     cur = 1 - cur;
   }
   CKL();

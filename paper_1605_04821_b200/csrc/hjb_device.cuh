@@ -19,8 +19,17 @@
 // of a warp are consecutive nodes), blocks striding over interior rows so the +-reach rows in
 // flight form a band that stays L2-resident.
 #pragma once
+#include <cassert>
 #include <cstdint>
 #include <cuda_runtime.h>
+
+// HJB_CHECK=1 (tools/build_variant.sh check -DHJB_CHECK=1): device-side bounds assertions on every
+// gather (compute-sanitizer is closed on this GPU pool)
+#ifdef HJB_CHECK
+#define HJB_ASSERT(c) assert(c)
+#else
+#define HJB_ASSERT(c) ((void)0)
+#endif
 
 namespace hjb {
 
@@ -486,6 +495,8 @@ __device__ __forceinline__ int tap_base(const LevelDev& L, const Tap<D>& t) {
 
 template <int D>
 __device__ __forceinline__ double tap_value(const LevelDev& L, const double* __restrict__ v, const Tap<D>& t) {
+  HJB_ASSERT(tap_base<D>(L, t) >= 0 &&
+             tap_base<D>(L, t) + (D == 2 ? L.n + 1 : L.n * L.n + L.n + 1) < L.local_elems);
   return interp_at<D, false>(v + tap_base<D>(L, t), L.n, L.n * L.n, t.s);
 }
 

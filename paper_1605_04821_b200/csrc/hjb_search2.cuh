@@ -176,6 +176,8 @@ __global__ void __launch_bounds__(kTX, HJB_SEARCH2_MINB) k_search_deep2(LevelDev
           split_floor(ksc[p] * t[T::SD + 2 * p + 1], fl1, s1);
           const int off = fl1 * n + fl0;          // plus endpoint's cell corner, relative to the node
           const int offm = -off - n - 1;          // minus endpoint's cell corner (i - fl - 1)
+          HJB_ASSERT(nd.loc + off >= 0 && nd.loc + off + n + 1 < L.local_elems);
+          HJB_ASSERT(nd.loc + offm >= 0 && nd.loc + offm + n + 1 < L.local_elems);
           const double2 p0 = cell_row(up, u0, off), p1 = cell_row(upn, u1, off);
           const double2 m0 = cell_row(up, u0, offm), m1 = cell_row(upn, u1, offm);
           const double w = t[T::W + p];

@@ -486,3 +486,49 @@ def test_exact_psi_mode_parity(name, mk):
     g.step(dt, to_dev(U0h, torch), Ui, None, packed_psi(p, t), pi_forcing=0.0)
     assert np.abs(Ui.cpu().numpy() - Ud.cpu().numpy()).max() > 1e-9
     g.close()
+
+
+@pytest.mark.parametrize("name,mk", [("cfg2_65_K8", lambda: bj_config(2, n=65, K=8)), ("cfg1_129", lambda: bj_config(1, n=129))])
+def test_galerkin_vcycle_and_solve_parity(name, mk):
+    """Galerkin coarse operators (NEXT-4): one GPU V(2,2) cycle with R A P coarse
+    levels (hjb_mg_params.coarse_op = 1) equals the oracle's Galerkin V(2,2) damped-Jacobi cycle
+    (oracle.multigrid: bilinear P, R = P^T/4, exact coarsest solve) on the same assembled fine
+    operator; the preconditioned BiCGSTAB solve matches SuperLU."""
+    torch = require_gpu()
+    from oracle.multigrid import galerkin_hierarchy, vcycle
+    p = mk()
+    g, fields = setup(p)
+    dt = p.dt
+    rng = np.random.default_rng(5)
+    pol = rng.integers(0, p.K, size=p.N)
+    z = np.zeros(p.N)
+    A = assemble(p, pol, dt, dt, z, z).A
+    inter = Geometry.of(p).interior_idx()
+    bi = rng.uniform(-1, 1, inter.size)
+    levels = galerkin_hierarchy(A, p.n)
+    xo = vcycle(levels, bi, nu1=2, nu2=2, omega=1.0, omega_coarse=0.8)   # the library's Galerkin damping
+    pold = to_dev(pol.astype(np.uint8), torch)
+    g.mg_setup(dt, pold, coarse_op=1)
+    bfull = np.zeros(p.N)
+    bfull[inter] = bi
+    xg = torch.zeros(p.N, dtype=torch.float64, device="cuda")
+    g.mg_apply(to_dev(bfull, torch), xg)
+    xg = xg.cpu().numpy()[inter]
+    assert np.abs(xg - xo).max() <= 1e-10 * np.abs(xo).max(), np.abs(xg - xo).max()
+    # preconditioned solve (Galerkin MG) vs SuperLU on A X = F
+    U0 = p.g(p.all_idx())
+    psi = np.zeros(p.N)
+    bidx = p.boundary_idx()
+    psi[bidx] = U0[bidx]
+    sysm = assemble(p, pol, dt, dt, U0, psi)
+    X, _ = solve(sysm)
+    Fd = torch.zeros(p.N, dtype=torch.float64, device="cuda")
+    fb, fc = p.f_tables(dt)
+    Fv = np.zeros(p.N)
+    Fv[inter] = U0[inter] + dt * (fb[pol[inter]] * p.fields(inter)["f_feat"].T).sum(1) + dt * fc[pol[inter]]
+    Fd.copy_(to_dev(Fv, torch))
+    x = to_dev(U0, torch)
+    st = g.solve(dt, pold, Fd, x, mg={"coarse_op": 1})
+    assert st["rres"] <= 1e-12
+    assert np.abs(x.cpu().numpy()[inter] - X).max() <= 1e-8 * max(1.0, np.abs(X).max()), st
+    g.close()
