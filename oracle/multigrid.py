@@ -64,7 +64,7 @@ def galerkin_hierarchy(A: sp.csr_matrix, n: int, d: int = 2, coarsest_n: int = 9
     return levels
 
 
-def vcycle(levels, b, nu1=2, nu2=2, omega=1.0, smoother="jacobi", lvl=0, omega_coarse=None):
+def vcycle(levels, b, nu1=2, nu2=2, omega=1.0, smoother="jacobi", lvl=0, omega_coarse=None, gamma=1):
     """x = M^-1 b: one V(nu1, nu2) cycle from x = 0 (damped Jacobi with omega on the finest level and
     omega_coarse (default omega) below, or forward lexicographic Gauss-Seidel), full-weighting
     restriction R = P^T / 2^d, prolongation P, exact solve on the coarsest level."""
@@ -84,8 +84,14 @@ def vcycle(levels, b, nu1=2, nu2=2, omega=1.0, smoother="jacobi", lvl=0, omega_c
     for _ in range(nu1):
         x = step(x)
     rc = (P.T @ (b - A @ x)) / (2 ** d)
-    x = x + P @ vcycle(levels, rc, nu1, nu2, omega if omega_coarse is None else omega_coarse, smoother,
-                       lvl + 1, omega_coarse)
+    oc = omega if omega_coarse is None else omega_coarse
+    ec = vcycle(levels, rc, nu1, nu2, oc, smoother, lvl + 1, omega_coarse, gamma)
+    Ac = levels[lvl + 1][0]
+    for _ in range(gamma - 1):             # W-cycle: refine the coarse correction (cycle index gamma)
+        if levels[lvl + 1][1] is None:
+            break
+        ec = ec + vcycle(levels, rc - Ac @ ec, nu1, nu2, oc, smoother, lvl + 1, omega_coarse, gamma)
+    x = x + P @ ec
     for _ in range(nu2):
         x = step(x)
     return x

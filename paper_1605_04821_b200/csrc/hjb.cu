@@ -1693,7 +1693,8 @@ extern "C" hjb_status hjb_mg_setup(hjb_grid_t g, double dt, const uint8_t* polic
 
 // Jacobi damping of level l: Galerkin coarse operators are not M-matrices (positive off-diagonals,
 // rows not diagonally dominant: measured at cfg2 513^2), where omega = 1 diverges (stationary
-// rho 1.6) and 0.8 contracts (0.063): min(omega, 0.8) there (reading xxix)
+// V(2,2) rho 1.6) and 0.6 contracts in V- and W-cycles (0.092 / 0.028; 0.8 diverges in the W-cycle):
+// min(omega, 0.6) there (reading xxix)
 static double level_omega(const hjb_grid* g, size_t l) {
   return (g->galerkin && l >= 1) ? std::min(g->mgp.omega, kGalOmega) : g->mgp.omega;
 }

@@ -20,7 +20,7 @@ namespace hjb {
 constexpr int kGalW = 96;   // ELL width of a coarse operator row
 constexpr int kGalWB = 96;  // ELL width of a row of B = A P
 constexpr int kGalHash = 256;
-constexpr double kGalOmega = 0.8;  // Jacobi damping cap on Galerkin levels (reading xxix)
+constexpr double kGalOmega = 0.6;  // Jacobi damping cap on Galerkin levels (reading xxix)
 
 struct RowAcc {  // per-thread accumulator of (column, value) pairs
   int key[kGalHash];

@@ -109,3 +109,21 @@ def test_jacobi_vcycle_is_a_convergent_preconditioner():
     lv = galerkin_hierarchy(A, p.n)
     rho, k = stationary_rho(lv, np.ones(A.shape[0]), nu1=2, nu2=2, smoother="jacobi")
     assert rho < 0.5 and k < 40, (rho, k)
+
+
+def test_galerkin_w_cycle_needs_damping():
+    """Reading xxix: on Galerkin coarse operators (not M-matrices) the W-cycle with coarse Jacobi
+    damping 0.8 diverges while 0.6 contracts strongly (cfg2 model, 257^2, greedy policy at U0)."""
+    from oracle.howard import control_search
+    from oracle.scheme import Geometry
+    from synth import bj_config
+    p = bj_config(2, n=257)
+    U0 = p.g(p.all_idx())
+    inter = Geometry.of(p).interior_idx()
+    pol = np.zeros(p.N, dtype=np.int64)
+    pol[inter] = control_search(p, U0, U0, p.dt, p.dt).policy
+    z = np.zeros(p.N)
+    lv = galerkin_hierarchy(assemble(p, pol, p.dt, p.dt, z, z).A, p.n)
+    b = np.ones(inter.size)
+    rho6, _ = stationary_rho(lv, b, nu1=2, nu2=2, omega=1.0, omega_coarse=0.6, gamma=2, maxit=40)
+    assert rho6 < 0.2, rho6
