@@ -95,6 +95,9 @@ __device__ __forceinline__ double2 cell_row(const double2* up, const double* u, 
 #endif
 }
 
+#ifndef HJB_SEARCH2_SYNC
+#define HJB_SEARCH2_SYNC 0  // > 0: __syncthreads every SYNC controls (A/B knob: L1 reuse across lines)
+#endif
 #ifndef HJB_SEARCH2_UNROLL
 #define HJB_SEARCH2_UNROLL 1
 #endif
@@ -136,9 +139,13 @@ __global__ void __launch_bounds__(kTX, HJB_SEARCH2_MINB) k_search_deep2(LevelDev
     const int scw = min(kSuperCols, tx - sc * kSuperCols);
     const int tl = t - sc * kSuperCols * ty;            // tile within the super-column, row-major
     const int trow = tl / scw, tcol = sc * kSuperCols + (tl - trow * scw);
-    const int k = trow * kSBY + threadIdx.y;
-    const int col = it.c0 + tcol * kSBX + threadIdx.x;
-    if (k < nk && col < it.c1) {
+    const int k0 = trow * kSBY + threadIdx.y;
+    const int col0 = it.c0 + tcol * kSBX + threadIdx.x;
+    const bool valid = k0 < nk && col0 < it.c1;
+    // a lane past the box edge repeats the tile's first node (results dropped), so that every thread
+    // of the CTA runs the control loop (HJB_SEARCH2_SYNC keeps the lines in lockstep)
+    const int k = valid ? k0 : trow * kSBY, col = valid ? col0 : it.c0 + tcol * kSBX;
+    if (HJB_SEARCH2_SYNC > 0 || valid) {
       const int row = box_row<2>(L, it, k);
       Node<2> nd;
       node_at<2>(L, col, row, nd);
@@ -166,6 +173,10 @@ __global__ void __launch_bounds__(kTX, HJB_SEARCH2_MINB) k_search_deep2(LevelDev
       int arg = 0;
 #pragma unroll kS2Unroll
       for (int a = 0; a < C.K; ++a) {
+#if HJB_SEARCH2_SYNC
+        __syncwarp();
+        if ((a & (HJB_SEARCH2_SYNC - 1)) == 0) __syncthreads();  // keep the CTA's 4 lines in lockstep
+#endif
         const double* t = tab.v + a * T::S;
         double acc = 0.0;
 #pragma unroll
@@ -207,13 +218,15 @@ __global__ void __launch_bounds__(kTX, HJB_SEARCH2_MINB) k_search_deep2(LevelDev
           fbest = f;
         }
       }
-      const double Up = __ldg(Uprev + nd.loc);
-      const double R = fabs(Uj - Up - dt * best);
-      const int old = pol[nd.loc];
-      pol[nd.loc] = (uint8_t)arg;
-      F[nd.loc] = fma(dt, fbest, Up);
-      red[0] = fmax(red[0], (R == R) ? R : INFINITY);  // NaN -> inf (reported NONFINITE)
-      red[1] += (old != arg) ? 1.0 : 0.0;
+      if (valid) {
+        const double Up = __ldg(Uprev + nd.loc);
+        const double R = fabs(Uj - Up - dt * best);
+        const int old = pol[nd.loc];
+        pol[nd.loc] = (uint8_t)arg;
+        F[nd.loc] = fma(dt, fbest, Up);
+        red[0] = fmax(red[0], (R == R) ? R : INFINITY);  // NaN -> inf (reported NONFINITE)
+        red[1] += (old != arg) ? 1.0 : 0.0;
+      }
     }
   }
   block_reduce_store<2>(red, partial, 0x1u);
