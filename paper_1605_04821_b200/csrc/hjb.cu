@@ -248,7 +248,7 @@ static void prof_post(hjb_grid* g, int cls, double nodes, double bytes, double f
 // 2D launch over the owned interior of level L: x covers an x1 line, y strides over lines.  All
 // CTAs are made co-resident (occupancy x SMs) so the lines in flight form one band that moves
 // through the grid and the +-reach rows it gathers from stay in L2.
-static int occupancy_of(const void* fn, size_t smem = 0) {
+static int occupancy_of(const void* fn, size_t smem = 0, int block = kTX) {
   // shared by every handle; thread-rank grids (HJB_COMM_THREADS) call it concurrently
   static std::mutex mu;
   static std::map<std::pair<const void*, size_t>, int> cache;
@@ -261,7 +261,7 @@ static int occupancy_of(const void* fn, size_t smem = 0) {
   cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 0);  // maximal L1
 #endif
   if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kTX, smem) != cudaSuccess || occ < 1) occ = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, block, smem) != cudaSuccess || occ < 1) occ = 1;
   cache[key] = occ;
   return occ;
 }
@@ -1175,16 +1175,16 @@ static bool search2_ok(hjb_grid* g) {
   return true;
 }
 
-template <int P, int Q>
+template <int P, int Q, bool STRIP>
 static void search2_launch(hjb_grid* g, const LevelDev& LL, double dt, const double* U, const double* Uprev,
                            uint8_t* pol, double* F, const SkipRect& rect, const STab& tab, const STabQuad& quad,
                            int* nblk) {
-  const void* fn = (const void*)k_search_deep2<P, Q>;
-  const int64_t tiles = (int64_t)((LL.nI + kSBX - 1) / kSBX) * ((LL.nrows + kSBY - 1) / kSBY);
-  const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, std::min<int64_t>((int64_t)occupancy_of(fn) * g->sms, kMaxBlocks)));
+  const void* fn = (const void*)k_search_deep2<P, Q, STRIP>;
+  const int64_t tiles = (int64_t)((LL.nI + kSBX - 1) / kSBX) * ((LL.nrows + kS2Y - 1) / kS2Y);
+  const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, std::min<int64_t>((int64_t)occupancy_of(fn, 0, kS2T) * g->sms, kMaxBlocks)));
   LAUNCH(HJB_KC_SEARCH, 0, 0, 0,
-         k_search_deep2<P, Q><<<nb, dim3(kSBX, kSBY), 0, g->st>>>(
-             g->L0, g->C0, dt, U, g->upair, Uprev, pol, F, g->partial + 2 * *nblk, rect, tab, quad));
+         k_search_deep2<P, Q, STRIP><<<nb, dim3(kSBX, kS2Y), 0, g->st>>>(
+             g->L0, STRIP ? coef_u(g) : g->C0, dt, U, g->upair, Uprev, pol, F, g->partial + 2 * *nblk, rect, tab, quad));
   *nblk += nb;
 }
 
@@ -1215,15 +1215,22 @@ static void search2_tables(hjb_grid* g, STab& tab, STabQuad& quad) {
   }
 }
 
+// the deep rectangle (strips = nullptr) or the boundary-layer strips around it (ns boxes)
 static hjb_status launch_search2(hjb_grid* g, double dt, const double* U, const double* Uprev, uint8_t* pol,
-                                 double* F, const SkipRect& rect, int* nblk) {
+                                 double* F, const SkipRect& rect, int* nblk, const SkipRect* strips = nullptr,
+                                 int ns = 0) {
   static thread_local STab tab;       // 24 KB + 1 KB: kernel parameters, not on the stack
   static thread_local STabQuad quad;
   const LevelDev LL = shape_of(g->L0, rect);
-#define S2(PP, QQ)                                                              \
-  do {                                                                          \
-    search2_tables<PP, QQ>(g, tab, quad);                                       \
-    search2_launch<PP, QQ>(g, LL, dt, U, Uprev, pol, F, rect, tab, quad, nblk); \
+#define S2(PP, QQ)                                                                                 \
+  do {                                                                                             \
+    search2_tables<PP, QQ>(g, tab, quad);                                                          \
+    if (!strips) search2_launch<PP, QQ, false>(g, LL, dt, U, Uprev, pol, F, rect, tab, quad, nblk); \
+    for (int k = 0; k < ns; ++k) {                                                                 \
+      const LevelDev LS = shape_of(g->L0, strips[k]);                                              \
+      if (LS.nI > 0 && LS.nrows > 0)                                                               \
+        search2_launch<PP, QQ, true>(g, LS, dt, U, Uprev, pol, F, strips[k], tab, quad, nblk);     \
+    }                                                                                              \
   } while (0)
   const int P = g->P, Q = g->Q;
   if (P == 1) {
@@ -1260,10 +1267,18 @@ static hjb_status policy_update_dev(hjb_grid* g, double dt, const double* U, con
                                         : (has_deep && g->win_deep.ok) ? &g->win_deep : nullptr;
   const CoefDev CU = coef_u(g);
   const bool win_all = wp == &g->win_full;
-  const int ngs = win_all ? 0 : ring_strips(full, rect, gstrips);
+  int ngs = win_all ? 0 : ring_strips(full, rect, gstrips);
   // 2D deep rectangle without a window / TMA plan: the L1-lean k_search_deep2 (hjb_search2.cuh)
   const bool deep2 = g->D == 2 && has_deep && !wp && !use_tma && search2_ok(g) && !getenv("HJB_NO_SEARCH2");
   const int nds = (has_deep && !wp && !deep2) ? ring_strips(rect, tiles, dstrips) : 0;
+  // with k_search_deep2 the boundary strips take its STRIP variant (HJB_NO_STRIP2: the general kernel)
+  const bool strip2 = deep2 && !getenv("HJB_NO_STRIP2");
+  SkipRect s2strips[6];
+  int ns2 = 0;
+  if (strip2) {
+    for (int k = 0; k < ngs; ++k) s2strips[ns2++] = gstrips[k];
+    ngs = 0;
+  }
 #define SRCH1(DD, PP, DP, RR)                                                                                 \
   do {                                                                                                        \
     const LevelDev LL = shape_of(g->L0, RR);                                                                  \
@@ -1328,6 +1343,7 @@ static hjb_status policy_update_dev(hjb_grid* g, double dt, const double* U, con
     CKL();
 #endif
     TRY(launch_search2(g, dt, U, Uprev, pol, F, rect, &nblk));
+    if (ns2 > 0) TRY(launch_search2(g, dt, U, Uprev, pol, F, rect, &nblk, s2strips, ns2));
   }
   if (use_tma) {  // deep tiles: windows staged in shared memory by TMA (partials after the others')
     if (g->P == 1)

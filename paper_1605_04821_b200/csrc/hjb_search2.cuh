@@ -98,6 +98,11 @@ __device__ __forceinline__ double2 cell_row(const double2* up, const double* u, 
 #ifndef HJB_SEARCH2_SYNC
 #define HJB_SEARCH2_SYNC 0  // > 0: __syncthreads every SYNC controls (A/B knob: L1 reuse across lines)
 #endif
+#ifndef HJB_S2Y
+#define HJB_S2Y 4
+#endif
+constexpr int kS2Y = HJB_S2Y;         // lines per CTA (x: 32 consecutive nodes per warp)
+constexpr int kS2T = 32 * kS2Y;       // threads per CTA
 #ifndef HJB_SEARCH2_UNROLL
 #define HJB_SEARCH2_UNROLL 1
 #endif
@@ -114,8 +119,11 @@ constexpr int kSuperCols = HJB_SUPER_COLS;  // tile columns per super-column (16
 // Deep nodes only (every endpoint of every control strictly inside the box), no sigma/b offset
 // fields, scale fields of one sign (so a control's zero steps and drift quadrant are per-control
 // facts: host-checked), drift endpoints within one cell of the node.
-template <int P, int Q>
-__global__ void __launch_bounds__(kTX, HJB_SEARCH2_MINB) k_search_deep2(LevelDev L, CoefDev C, double dt,
+// STRIP: a boundary-layer strip of the deep rectangle's ring: per control, a warp whose endpoints are
+// all strictly inside runs the lean arithmetic above; otherwise the control takes the general
+// truncated geometry (row_geometry, exact-psi aware) for the whole warp
+template <int P, int Q, bool STRIP = false>
+__global__ void __launch_bounds__(kS2T, HJB_SEARCH2_MINB) k_search_deep2(LevelDev L, CoefDev C, double dt,
                                                                         const double* __restrict__ U,
                                                                         const double2* __restrict__ UP,
                                                                         const double* __restrict__ Uprev,
@@ -127,24 +135,24 @@ __global__ void __launch_bounds__(kTX, HJB_SEARCH2_MINB) k_search_deep2(LevelDev
   double red[2] = {0.0, 0.0};
   const int nk = box_lines(it);
   const int n = L.n;
-  // tiles of kSBX columns x kSBY lines, ordered so that the CTAs running at one time cover a compact
+  // tiles of kSBX columns x kS2Y lines, ordered so that the CTAs running at one time cover a compact
   // patch: super-columns of kSuperCols tile columns, walked top to bottom, left to right.  The
   // patch's gather window (+-reach rows and columns around it) then stays in L2; a full-width band
   // of lines (the operator kernels' order) with 16-byte pairs and a 143-row reach does not
   // (measured at cfg4: 229 GB of DRAM reads per search, L2 hit rate 47 %).
-  const int tx = (it.c1 - it.c0 + kSBX - 1) / kSBX, ty = (nk + kSBY - 1) / kSBY;
+  const int tx = (it.c1 - it.c0 + kSBX - 1) / kSBX, ty = (nk + kS2Y - 1) / kS2Y;
   const int ntiles = tx * ty;
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const int sc = t / (kSuperCols * ty);               // super-column
     const int scw = min(kSuperCols, tx - sc * kSuperCols);
     const int tl = t - sc * kSuperCols * ty;            // tile within the super-column, row-major
     const int trow = tl / scw, tcol = sc * kSuperCols + (tl - trow * scw);
-    const int k0 = trow * kSBY + threadIdx.y;
+    const int k0 = trow * kS2Y + threadIdx.y;
     const int col0 = it.c0 + tcol * kSBX + threadIdx.x;
     const bool valid = k0 < nk && col0 < it.c1;
     // a lane past the box edge repeats the tile's first node (results dropped), so that every thread
     // of the CTA runs the control loop (HJB_SEARCH2_SYNC keeps the lines in lockstep)
-    const int k = valid ? k0 : trow * kSBY, col = valid ? col0 : it.c0 + tcol * kSBX;
+    const int k = valid ? k0 : trow * kS2Y, col = valid ? col0 : it.c0 + tcol * kSBX;
     if (HJB_SEARCH2_SYNC > 0 || valid) {
       const int row = box_row<2>(L, it, k);
       Node<2> nd;
@@ -178,6 +186,30 @@ __global__ void __launch_bounds__(kTX, HJB_SEARCH2_MINB) k_search_deep2(LevelDev
         if ((a & (HJB_SEARCH2_SYNC - 1)) == 0) __syncthreads();  // keep the CTA's 4 lines in lockstep
 #endif
         const double* t = tab.v + a * T::S;
+        if (STRIP) {
+          bool inside = true;
+#pragma unroll
+          for (int p = 0; p < P; ++p)
+            inside &= fabs(ksc[p] * t[T::SD + 2 * p]) < nd.dist[0] && fabs(ksc[p] * t[T::SD + 2 * p + 1]) < nd.dist[1];
+          inside &= fabs(kbs * t[T::BD]) < nd.dist[0] && fabs(kbs * t[T::BD + 1]) < nd.dist[1];
+          if (!__all_sync(__activemask(), inside)) {
+            Tap<2> taps[2 * P + 1];
+            const double wsum = row_geometry<2, P>(L, t + T::SD, t + T::BD, nd, taps);
+            double acc = 0.0;
+#pragma unroll
+            for (int e = 0; e < 2 * P + 1; ++e) acc = fma(taps[e].w, tap_value_u<2>(L, C, U, taps[e]), acc);
+            double f = t[T::FC];
+#pragma unroll
+            for (int q = 0; q < Q; ++q) f = fma(t[T::FB + q], feat[q], f);
+            const double H = (acc - wsum * Uj) + (nd.cn + t[T::C]) * Uj + f;
+            if (H < best) {
+              best = H;
+              arg = a;
+              fbest = f;
+            }
+            continue;
+          }
+        }
         double acc = 0.0;
 #pragma unroll
         for (int p = 0; p < P; ++p) {
@@ -229,7 +261,7 @@ __global__ void __launch_bounds__(kTX, HJB_SEARCH2_MINB) k_search_deep2(LevelDev
       }
     }
   }
-  block_reduce_store<2>(red, partial, 0x1u);
+  block_reduce_store<2, kS2T>(red, partial, 0x1u);
 }
 
 }  // namespace hjb

@@ -506,7 +506,7 @@ def test_galerkin_vcycle_and_solve_parity(name, mk):
     inter = Geometry.of(p).interior_idx()
     bi = rng.uniform(-1, 1, inter.size)
     levels = galerkin_hierarchy(A, p.n)
-X
+    xo = vcycle(levels, bi, nu1=2, nu2=2, omega=1.0, omega_coarse=0.6)   # the library's Galerkin damping
     pold = to_dev(pol.astype(np.uint8), torch)
     g.mg_setup(dt, pold, coarse_op=1)
     bfull = np.zeros(p.N)

@@ -30,7 +30,7 @@ case $job in
   ncufull)
     tag=$1; re=$2; skip=$3; shift 3
     timeout 600 "$@" > $O/plain_$tag.log 2>&1 && \
-      timeout 1500 ncu --set full --clock-control none --import-source on -k regex:$re -s $skip -c ${COUNT:-2} \
+      timeout 1500 ncu --set full --clock-control none --import-source on -k "regex:$re" -s $skip -c ${COUNT:-2} \
         -o $O/prof_$tag "$@" > $O/ncu_$tag.log 2>&1
     echo "ncu rc=$?" >> $O/ncu_$tag.log ;;
   opbench)

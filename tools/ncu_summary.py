@@ -56,7 +56,10 @@ METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
            "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
            "l1tex__t_sector_hit_rate.pct", "lts__t_sector_hit_rate.pct",
            "sm__throughput.avg.pct_of_peak_sustained_elapsed",
-           "launch__occupancy_limit_registers", "smsp__inst_executed.sum"]
+           "launch__occupancy_limit_registers", "smsp__inst_executed.sum",
+           "l1tex__data_pipe_lsu_wavefronts.sum.pct_of_peak_sustained_elapsed",
+           "sm__issue_active.avg.pct_of_peak_sustained_elapsed",
+           "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio"]
 
 
 def full(path):
