@@ -180,6 +180,7 @@ struct hjb_grid {
     size_t level;
     const double* b;
     double* out;
+    const uint8_t* pol0;
     cudaGraphExec_t exec;
     int64_t launches;
   };
@@ -1092,6 +1093,8 @@ extern "C" hjb_status hjb_set_coeffs(hjb_grid_t g, const hjb_coeffs* c) {
                 (c->b_node ? g->D : 0) + (c->c_node ? 1 : 0);
   g->have_coeffs = true;
   g->mg_ready = false;
+  for (auto& sg : g->graphs) cudaGraphExecDestroy(sg.exec);  // captured kernels hold field pointers
+  g->graphs.clear();
   {  // widest stencil offset: halo check (several ranks) and the L2 prefetch distance
     const double nodes = (double)g->L0.n_own;
     if (g->D == 2)
@@ -1741,10 +1744,12 @@ static void level_sweep(hjb_grid* g, size_t l, int mode, const double* x, const 
 // V(nu_pre, nu_post) from x = 0 on level l: out = M_l^{-1} b
 template <int D>
 static hjb_status vcycle(hjb_grid* g, size_t l, const double* b, double* out) {
-  if (l == g->graph_level && !g->capturing) {
+  // the whole cycle as one graph (one rank, no per-kernel timing), else its launch-bound tail
+  const bool whole = l == 0 && g->R == 1 && !g->prof_timing && g->graph_level != (size_t)-1;
+  if ((whole || l == g->graph_level) && !g->capturing) {
     hjb_grid::SubGraph* sg = nullptr;
     for (auto& x : g->graphs)
-      if (x.level == l && x.b == b && x.out == out) sg = &x;
+      if (x.level == l && x.b == b && x.out == out && x.pol0 == g->mg_pol0) sg = &x;
     if (!sg) {  // capture the sub-cycle once on the private stream (kernels recorded, not run)
       if (!g->cap_st) CK(cudaStreamCreateWithFlags(&g->cap_st, cudaStreamNonBlocking));
       cudaStream_t keep = g->st;
@@ -1766,7 +1771,7 @@ static hjb_status vcycle(hjb_grid* g, size_t l, const double* b, double* out) {
       cudaGraphDestroy(graph);
       if (e != cudaSuccess) return fail(HJB_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
       const int64_t nl = g->cap_launches;
-      g->graphs.push_back(hjb_grid::SubGraph{l, b, out, exec, nl});
+      g->graphs.push_back(hjb_grid::SubGraph{l, b, out, g->mg_pol0, exec, nl});
       sg = &g->graphs.back();
     }
     CK(cudaGraphLaunch(sg->exec, g->st));
