@@ -248,3 +248,21 @@ def test_exact_psi_mode_assembly_and_zero_psi():
     Ua, _, _ = march(q, n_steps=2)
     Ub, _, _ = march(q, n_steps=2, exact_psi=True)
     assert np.abs(Ua - Ub).max() <= 1e-13
+
+
+@pytest.mark.parametrize("mk", [lambda: bj_config(0), lambda: bj_config(2, n=65, K=8), lambda: problem_A(41)])
+def test_column_sums_nonnegative_under_the_bound(mk):
+    """Proposition prop-columns (the AGMG theory gate of P:1063-1071): the LISL matrix
+    has non-negative column sums if dt <= dx / (sup c^+ + (M - 1)(P + 1)), M = 3^d.  Checked on
+    the assembled interior matrix (random policy) at the bound; far above it (100x) the column sums
+    do go negative, so the condition is not vacuous here (measured: min column sum 0.91 / 0.90 / 0.78
+    at the bound, -7.6 / -9.0 / -21.5 at 100x, for cfg0 / cfg2-65 / Problem A)."""
+    p = mk()
+    rng = np.random.default_rng(1)
+    pol = rng.integers(0, p.K, size=p.N)
+    bound = p.h / (max(0.0, p.c_ctrl.max()) + (3 ** p.d - 1) * (p.P + 1))
+    z = np.zeros(p.N)
+    A = assemble(p, pol, bound, bound, z, z).A
+    assert np.asarray(A.sum(0)).min() >= 0.0
+    A100 = assemble(p, pol, 100 * bound, 100 * bound, z, z).A
+    assert np.asarray(A100.sum(0)).min() < 0.0
