@@ -261,6 +261,12 @@ typedef struct {
                                 (reading xxvi).  f must be set at t_{n-1} + theta dt
                                 (P:124).  theta < 1 needs the CFL condition of Proposition CFL
                                 (P:437-441), see hjb_cfl_rate; it is not enforced.               */
+  int32_t solver;            /* policy evaluation: 0 = right-preconditioned BiCGSTAB with geometric
+                                multigrid (default); 1 = flexible GCR(10) preconditioned by
+                                aggregation AMG (SURVEY §8(f)
+                                NEXT-1): the assembled operator, double pairwise aggregation,
+                                K-cycle with 2 inner GCR iterations per coarse level.  One rank;
+                                the setup is redone per policy.  Same stopping rules.           */
 } hjb_solve_params;
 
 #define HJB_GUESS_PREV 0

@@ -67,7 +67,7 @@ class SolveParams(C.Structure):
     _fields_ = [("krylov_rtol", C.c_double), ("krylov_maxit", C.c_int32), ("use_mg", C.c_int32),
                 ("tol_pi", C.c_double), ("max_pi", C.c_int32), ("mg", MgParams),
                 ("pi_forcing", C.c_double), ("guess", C.c_int32), ("krylov_rtol_inf", C.c_double),
-                ("theta", C.c_double)]
+                ("theta", C.c_double), ("solver", C.c_int32)]
 
 HJB_GUESS_PREV, HJB_GUESS_GIVEN, HJB_GUESS_EXTRAPOLATE = 0, 1, 2
 

@@ -22,6 +22,8 @@
 #include "hjb_win.cuh"
 #include "hjb_search2.cuh"
 #include "hjb_galerkin.cuh"
+#include "hjb_agmg.cuh"
+#include <cub/device/device_scan.cuh>
 
 namespace hjb {
 struct WinPlan {
@@ -170,6 +172,27 @@ struct hjb_grid {
   int* gb_col = nullptr;      // B = A P scratch of the Galerkin setup (ELL [kGalWB][elems_0])
   double* gb_val = nullptr;
   int* d_flag = nullptr;      // device overflow flag
+  // aggregation AMG (hjb_solve_params.solver = 1; hjb_agmg.cuh)
+  struct AgLevel {
+    int64_t N = 0;
+    int* col = nullptr;
+    double* val = nullptr;
+    double* dg = nullptr;
+    int* agg = nullptr;   // this level -> next (not on the coarsest)
+    int* mem = nullptr;   // members (<= 4) of the next level's aggregates: [4][N_next]
+    double *x = nullptr, *b = nullptr, *r = nullptr, *t = nullptr, *z[2] = {nullptr, nullptr},
+           *az[2] = {nullptr, nullptr};
+    double* Ainv = nullptr;
+  };
+  std::vector<AgLevel> ag;
+  const uint8_t* ag_pol = nullptr;
+  double ag_dt = 0.0;
+  bool ag_ready = false;
+  int* ag_i[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};  // setup scratch
+  void* ag_cub = nullptr;
+  size_t ag_cub_bytes = 0;
+  double* ag_Z[16] = {};      // outer FGCR directions (compact)
+  double* ag_AZ[16] = {};
   const double* bsamp = nullptr;  // exact-psi mode: face samples of psi (caller-owned, retained)
   int brefine = 0;
   bool drift_reg = false;     // deep drift endpoints stay within one cell of the node (|offset| < 1)
@@ -191,6 +214,8 @@ struct hjb_grid {
   int64_t cap_launches = 0;
   cudaStream_t cap_st = nullptr;  // private capture stream (the legacy default stream cannot capture)
 };
+
+static void agmg_free(hjb_grid* g);
 
 // ---------------------------------------------------------------------------- instrumentation
 // accumulate the `m` oldest pending launches
@@ -589,6 +614,7 @@ extern "C" void hjb_solve_params_default(int32_t dim, hjb_solve_params* o) {
   o->guess = HJB_GUESS_PREV;
   o->krylov_rtol_inf = 1e-9;  // SURVEY §8c-xvii secondary stop (reading xvii)
   o->theta = 1.0;             // implicit Euler (the paper's experiments)
+  o->solver = 0;              // BiCGSTAB + geometric multigrid (1: GCR + aggregation AMG, NEXT-1)
 }
 
 // ---------------------------------------------------------------------------- API: partition
@@ -698,6 +724,7 @@ extern "C" hjb_status hjb_grid_destroy(hjb_grid_t g) {
   cudaFree(g->upair);
   cudaFree(g->vtheta);
   cudaFree(g->d_flag);
+  agmg_free(g);
   if (g->cap_st) cudaStreamDestroy(g->cap_st);
   cudaFree(g->S);
   cudaFree(g->pol_int);
@@ -1990,6 +2017,309 @@ static hjb_status bicgstab(hjb_grid* g, double dt, const uint8_t* pol, const dou
   return HJB_OK;
 }
 
+// ---------------------------------------------------------------------------- aggregation AMG
+// (PAPER.md:171-176, 1162-1164): setup per policy, K-cycle preconditioned
+// flexible GCR on the correction equation A e = F - A U (compact interior vectors)
+constexpr int kAgRestart = 10;
+constexpr double kAgOmega = 0.67;   // Jacobi damping of the K-cycle smoother (the paper uses GS)
+
+static void agmg_free_levels(hjb_grid* g) {
+  for (auto& l : g->ag) {
+    cudaFree(l.col); cudaFree(l.val); cudaFree(l.dg); cudaFree(l.agg); cudaFree(l.mem);
+    cudaFree(l.x); cudaFree(l.b); cudaFree(l.r); cudaFree(l.t); cudaFree(l.Ainv);
+    for (int k = 0; k < 2; ++k) { cudaFree(l.z[k]); cudaFree(l.az[k]); }
+  }
+  g->ag.clear();
+  g->ag_ready = false;
+}
+static void agmg_free(hjb_grid* g) {
+  agmg_free_levels(g);
+  for (auto& p : g->ag_i) { cudaFree(p); p = nullptr; }
+  cudaFree(g->ag_cub);
+  g->ag_cub = nullptr;
+  for (int k = 0; k < 16; ++k) { cudaFree(g->ag_Z[k]); cudaFree(g->ag_AZ[k]); g->ag_Z[k] = g->ag_AZ[k] = nullptr; }
+}
+
+static int ag_blocks(int64_t n, int bs = 256) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>((n + bs - 1) / bs, (int64_t)148 * 32));
+}
+
+static hjb_status ag_alloc_level(hjb_grid* g, hjb_grid::AgLevel& l, int64_t N) {
+  l.N = N;
+  TRY(dalloc((void**)&l.col, (size_t)kAgW * N * sizeof(int)));
+  TRY(dalloc((void**)&l.val, (size_t)kAgW * N * sizeof(double)));
+  TRY(dalloc((void**)&l.dg, (size_t)N * sizeof(double)));
+  double** vs[] = {&l.x, &l.b, &l.r, &l.t, &l.z[0], &l.z[1], &l.az[0], &l.az[1]};
+  for (double** v : vs) TRY(dalloc((void**)v, (size_t)N * sizeof(double)));
+  CK(cudaMemsetAsync(l.col, 0xff, (size_t)kAgW * N * sizeof(int), g->st));
+  return HJB_OK;
+}
+
+// one pairwise matching pass on A (N rows): agg [N], mem [2][Nc] (g->ag_i[4] / [5] are sized N)
+static hjb_status ag_pairwise(hjb_grid* g, int64_t N, const int* col, const double* val, int* agg, int* mem,
+                              int64_t* Nc) {
+  int *state = g->ag_i[0], *cand = g->ag_i[1], *flag = g->ag_i[2], *id = g->ag_i[3];
+  CK(cudaMemsetAsync(state, 0xff, (size_t)N * sizeof(int), g->st));
+  const int nb = ag_blocks(N, 128);
+  for (int round = 0; round < 4; ++round) {
+    LAUNCH(HJB_KC_COARSE, N, 0, 0, k_ag_candidates<<<nb, 128, 0, g->st>>>(N, col, val, state, cand, 0.25));
+    LAUNCH(HJB_KC_COARSE, N, 0, 0, k_ag_match<<<nb, 128, 0, g->st>>>(N, cand, state, round == 3 ? 1 : 0));
+  }
+  CKL();
+  LAUNCH(HJB_KC_COARSE, N, 0, 0, k_ag_leader_flags<<<ag_blocks(N), 256, 0, g->st>>>(N, state, flag));
+  size_t need = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, need, flag, id, (int)N, g->st);
+  if (need > g->ag_cub_bytes) {
+    cudaFree(g->ag_cub);
+    TRY(dalloc(&g->ag_cub, need));
+    g->ag_cub_bytes = need;
+  }
+  CK(cub::DeviceScan::ExclusiveSum(g->ag_cub, need, flag, id, (int)N, g->st));
+  int last[2];
+  CK(cudaMemcpyAsync(&last[0], id + N - 1, sizeof(int), cudaMemcpyDeviceToHost, g->st));
+  CK(cudaMemcpyAsync(&last[1], flag + N - 1, sizeof(int), cudaMemcpyDeviceToHost, g->st));
+  CK(cudaStreamSynchronize(g->st));
+  *Nc = (int64_t)last[0] + last[1];
+  CK(cudaMemsetAsync(mem, 0xff, (size_t)2 * *Nc * sizeof(int), g->st));
+  LAUNCH(HJB_KC_COARSE, N, 0, 0, k_ag_number<<<ag_blocks(N), 256, 0, g->st>>>(N, state, id, agg, mem, *Nc));
+  CKL();
+  return HJB_OK;
+}
+
+template <int D>
+static hjb_status agmg_setup(hjb_grid* g, double dt, const uint8_t* pol) {
+  if (g->R != 1) return fail(HJB_ERR_UNSUPPORTED, "aggregation AMG: one rank only");
+  agmg_free_levels(g);
+  const int64_t N0 = g->L0.n_own;
+  if (!g->d_flag) TRY(dalloc((void**)&g->d_flag, sizeof(int)));
+  CK(cudaMemsetAsync(g->d_flag, 0, sizeof(int), g->st));
+  if (!g->ag_i[0])
+    for (auto& p : g->ag_i) TRY(dalloc((void**)&p, (size_t)N0 * 2 * sizeof(int)));
+  g->ag.emplace_back();
+  TRY(ag_alloc_level(g, g->ag.back(), N0));
+  {
+    auto& l0 = g->ag.back();
+    const int nb = ag_blocks(N0, 128);
+#define AGF(PP) LAUNCH(HJB_KC_COARSE, N0, 0, 0, k_ag_fine<D, PP><<<nb, 128, 0, g->st>>>(g->L0, g->C0, dt, pol, l0.col, l0.val, l0.dg, g->d_flag))
+    if (g->P == 1) AGF(1);
+    else if (g->P == 2) AGF(2);
+    else AGF((D > 2 ? 3 : 2));
+#undef AGF
+    CKL();
+  }
+  const int64_t stop = std::max<int64_t>(64, (int64_t)std::cbrt((double)N0));
+  while (g->ag.back().N > stop && g->ag.size() < 20) {
+    auto& lf = g->ag.back();
+    const int64_t N = lf.N;
+    // pass 1 on A_l
+    int *agg1 = g->ag_i[4], *mem1 = g->ag_i[5];
+    int64_t N1 = 0;
+    TRY(ag_pairwise(g, N, lf.col, lf.val, agg1, mem1, &N1));
+    hjb_grid::AgLevel tmp;
+    TRY(ag_alloc_level(g, tmp, N1));
+    LAUNCH(HJB_KC_COARSE, N1, 0, 0, k_ag_coarse<<<ag_blocks(N1, 128), 128, 0, g->st>>>(N, lf.col, lf.val, agg1, N1, mem1, 2,
+                                                                                     tmp.col, tmp.val, tmp.dg, g->d_flag));
+    // pass 2 on A_1 (the scratch of pass 1 moves into fresh buffers first)
+    int *agg1c = nullptr, *mem1c = nullptr;
+    TRY(dalloc((void**)&agg1c, (size_t)N * sizeof(int)));
+    TRY(dalloc((void**)&mem1c, (size_t)2 * N1 * sizeof(int)));
+    CK(cudaMemcpyAsync(agg1c, agg1, (size_t)N * sizeof(int), cudaMemcpyDeviceToDevice, g->st));
+    CK(cudaMemcpyAsync(mem1c, mem1, (size_t)2 * N1 * sizeof(int), cudaMemcpyDeviceToDevice, g->st));
+    int64_t N2 = 0;
+    TRY(ag_pairwise(g, N1, tmp.col, tmp.val, g->ag_i[4], g->ag_i[5], &N2));
+    hjb_grid::AgLevel lc;
+    TRY(ag_alloc_level(g, lc, N2));
+    LAUNCH(HJB_KC_COARSE, N2, 0, 0, k_ag_coarse<<<ag_blocks(N2, 128), 128, 0, g->st>>>(N1, tmp.col, tmp.val, g->ag_i[4], N2,
+                                                                                     g->ag_i[5], 2, lc.col, lc.val, lc.dg, g->d_flag));
+    TRY(dalloc((void**)&lf.agg, (size_t)N * sizeof(int)));
+    TRY(dalloc((void**)&lf.mem, (size_t)4 * N2 * sizeof(int)));
+    CK(cudaMemsetAsync(lf.mem, 0xff, (size_t)4 * N2 * sizeof(int), g->st));
+    LAUNCH(HJB_KC_COARSE, N, 0, 0, k_ag_compose<<<ag_blocks(std::max(N, N2)), 256, 0, g->st>>>(N, agg1c, g->ag_i[4], lf.agg, N1,
+                                                                                             mem1c, g->ag_i[5], N2, lf.mem));
+    CKL();
+    CK(cudaStreamSynchronize(g->st));
+    cudaFree(agg1c);
+    cudaFree(mem1c);
+    hjb_grid::AgLevel* tl = &tmp;
+    cudaFree(tl->col); cudaFree(tl->val); cudaFree(tl->dg); cudaFree(tl->x); cudaFree(tl->b); cudaFree(tl->r);
+    cudaFree(tl->t);
+    for (int k = 0; k < 2; ++k) { cudaFree(tl->z[k]); cudaFree(tl->az[k]); }
+    if (N2 * 10 >= N * 9) {  // no coarsening: stop here (the level just built is dropped)
+      cudaFree(lf.agg); cudaFree(lf.mem);
+      lf.agg = nullptr; lf.mem = nullptr;
+      cudaFree(lc.col); cudaFree(lc.val); cudaFree(lc.dg); cudaFree(lc.x); cudaFree(lc.b); cudaFree(lc.r);
+      cudaFree(lc.t);
+      for (int k = 0; k < 2; ++k) { cudaFree(lc.z[k]); cudaFree(lc.az[k]); }
+      break;
+    }
+    g->ag.push_back(lc);
+  }
+  auto& lc = g->ag.back();
+  if (lc.N > 160) return fail(HJB_ERR_UNSUPPORTED, "aggregation stalled above the dense coarsest size (160)");
+  TRY(dalloc((void**)&lc.Ainv, (size_t)lc.N * lc.N * sizeof(double)));
+  CK(cudaMemsetAsync(lc.Ainv, 0, (size_t)lc.N * lc.N * sizeof(double), g->st));
+  LAUNCH(HJB_KC_COARSE, lc.N, 0, 0, k_ag_dense<<<1, 160, 0, g->st>>>(lc.N, lc.col, lc.val, lc.Ainv));
+  const size_t smem = (size_t)lc.N * lc.N * sizeof(double);
+  if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_coarse_invert, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  LAUNCH(HJB_KC_COARSE, lc.N, 0, 0, k_coarse_invert<<<1, 1024, smem, g->st>>>(lc.Ainv, (int)lc.N));
+  CKL();
+  int flag = 0;
+  CK(cudaMemcpyAsync(&flag, g->d_flag, sizeof(int), cudaMemcpyDeviceToHost, g->st));
+  CK(cudaStreamSynchronize(g->st));
+  if (flag) return fail(HJB_ERR_UNSUPPORTED, "aggregation AMG: a row wider than the ELL width (96)");
+  g->ag_pol = pol;
+  g->ag_dt = dt;
+  g->ag_ready = true;
+  return HJB_OK;
+}
+
+// dot products of compact vectors through the library's reduction path: returns (x.y, y.y)
+static hjb_status ag_dot(hjb_grid* g, int64_t N, const double* x, const double* y, double* xy, double* yy) {
+  const int nb = std::min(ag_blocks(N), kMaxBlocks);
+  LAUNCH(HJB_KC_VECTOR, N, 16.0 * N, 4.0 * N, k_ag_dot2<<<nb, 256, 0, g->st>>>(N, x, y, g->partial));
+  CKL();
+  hjb_status err;
+  *xy = host_finalize(g, nb, 0u, SC_NONE, &err, yy);
+  return err;
+}
+
+static hjb_status ag_kcycle(hjb_grid* g, size_t l, const double* b, double* x);
+
+// 2 flexible GCR iterations on level c (x0 = 0), preconditioned by its K-cycle: the K-cycle's
+// coarse-grid solve ("a number of Krylov subspace iterations")
+static hjb_status ag_inner(hjb_grid* g, size_t c, const double* b, double* x) {
+  auto& L = g->ag[c];
+  const int64_t N = L.N;
+  const int nb = ag_blocks(N);
+  CK(cudaMemsetAsync(x, 0, (size_t)N * sizeof(double), g->st));
+  CK(cudaMemcpyAsync(L.r, b, (size_t)N * sizeof(double), cudaMemcpyDeviceToDevice, g->st));
+  for (int it = 0; it < 2; ++it) {
+    TRY(ag_kcycle(g, c, L.r, L.z[it]));
+    LAUNCH(HJB_KC_MG_COARSE, N, 0, 0, k_ag_spmv<<<nb, 256, 0, g->st>>>(N, L.col, L.val, L.z[it], L.az[it]));
+    if (it == 1) {
+      double h, unused;
+      TRY(ag_dot(g, N, L.az[0], L.az[1], &h, &unused));
+      LAUNCH(HJB_KC_VECTOR, N, 0, 0, k_ag_axpby<<<nb, 256, 0, g->st>>>(N, -h, L.az[0], 1.0, L.az[1]));
+      LAUNCH(HJB_KC_VECTOR, N, 0, 0, k_ag_axpby<<<nb, 256, 0, g->st>>>(N, -h, L.z[0], 1.0, L.z[1]));
+    }
+    double unused, nn;
+    TRY(ag_dot(g, N, L.az[it], L.az[it], &unused, &nn));
+    const double nrm = std::sqrt(nn);
+    if (!(nrm > 0.0)) break;
+    LAUNCH(HJB_KC_VECTOR, N, 0, 0, k_ag_axpby<<<nb, 256, 0, g->st>>>(N, 0.0, L.az[it], 1.0 / nrm, L.az[it]));
+    LAUNCH(HJB_KC_VECTOR, N, 0, 0, k_ag_axpby<<<nb, 256, 0, g->st>>>(N, 0.0, L.z[it], 1.0 / nrm, L.z[it]));
+    double gam, unused2;
+    TRY(ag_dot(g, N, L.r, L.az[it], &gam, &unused2));
+    LAUNCH(HJB_KC_VECTOR, N, 0, 0, k_ag_axpby<<<nb, 256, 0, g->st>>>(N, gam, L.z[it], 1.0, x));
+    LAUNCH(HJB_KC_VECTOR, N, 0, 0, k_ag_axpby<<<nb, 256, 0, g->st>>>(N, -gam, L.az[it], 1.0, L.r));
+  }
+  CKL();
+  return HJB_OK;
+}
+
+// x = B_l^{-1} b: K-cycle of level l (one damped-Jacobi pre- and post-smoothing step)
+static hjb_status ag_kcycle(hjb_grid* g, size_t l, const double* b, double* x) {
+  auto& L = g->ag[l];
+  const int64_t N = L.N;
+  const int nb = ag_blocks(N);
+  if (l + 1 == g->ag.size()) {
+    LAUNCH(HJB_KC_COARSE, N, 0, 0, k_ag_dense_solve<<<1, 256, 0, g->st>>>((int)N, L.Ainv, b, x));
+    CKL();
+    return HJB_OK;
+  }
+  auto& C = g->ag[l + 1];
+  CK(cudaMemsetAsync(L.t, 0, (size_t)N * sizeof(double), g->st));
+  LAUNCH(HJB_KC_MG_COARSE, N, 0, 0, k_ag_sweep<true><<<nb, 256, 0, g->st>>>(N, L.col, L.val, L.dg, L.t, b, kAgOmega, x));
+  LAUNCH(HJB_KC_MG_COARSE, N, 0, 0, k_ag_sweep<false><<<nb, 256, 0, g->st>>>(N, L.col, L.val, L.dg, x, b, 0.0, L.t));
+  LAUNCH(HJB_KC_TRANSFER, C.N, 0, 0, k_ag_restrict<<<ag_blocks(C.N), 256, 0, g->st>>>(C.N, L.mem, 4, L.t, C.b));
+  if (l + 2 == g->ag.size()) TRY(ag_kcycle(g, l + 1, C.b, C.x));
+  else TRY(ag_inner(g, l + 1, C.b, C.x));
+  LAUNCH(HJB_KC_TRANSFER, N, 0, 0, k_ag_prolong<<<nb, 256, 0, g->st>>>(N, L.agg, C.x, x));
+  CK(cudaMemcpyAsync(L.t, x, (size_t)N * sizeof(double), cudaMemcpyDeviceToDevice, g->st));
+  LAUNCH(HJB_KC_MG_COARSE, N, 0, 0, k_ag_sweep<true><<<nb, 256, 0, g->st>>>(N, L.col, L.val, L.dg, L.t, b, kAgOmega, x));
+  CKL();
+  return HJB_OK;
+}
+
+// U += e with A e = F - A U solved by K-cycle-preconditioned flexible GCR(10) to
+// ||F - A U||_2 <= max(rtol ||F||_2, eta ||r_0||_2) (and the max-norm stop of an exact evaluation)
+template <int D>
+static hjb_status agmg_solve(hjb_grid* g, double dt, const uint8_t* pol, const double* F, double* U,
+                             const hjb_solve_params* sp, hjb_solve_stats* out, double eta) {
+  if (!g->ag_ready || g->ag_pol != pol || g->ag_dt != dt) TRY(agmg_setup<D>(g, dt, pol));
+  auto& L0 = g->ag[0];
+  const int64_t N = L0.N;
+  const int nb = ag_blocks(N);
+  for (int k = 0; k < kAgRestart; ++k)
+    if (!g->ag_Z[k]) {
+      TRY(dalloc((void**)&g->ag_Z[k], (size_t)N * sizeof(double)));
+      TRY(dalloc((void**)&g->ag_AZ[k], (size_t)N * sizeof(double)));
+    }
+  Level tmpl;
+  const Level& lv0 = fine_level(g, tmpl);
+  double bn2, bninf;
+  TRY(norms_dev<D>(g, F, &bn2, &bninf));
+  double tol = sp->krylov_rtol * bn2;
+  const double tol_inf = (eta > 0.0 || !(sp->krylov_rtol_inf > 0.0)) ? INFINITY : sp->krylov_rtol_inf * bninf;
+  int it = 0;
+  bool converged = false;
+  for (int restart = 0; restart < 6 && !converged; ++restart) {
+    // r = F - A U (matrix-free, the boundary data included); compact copy
+    TRY(halo_exchange(g, lv0, U, g->lay.halo));
+    launch_operator<D>(g, g->L0, coef_u(g), OP_RESID, 0, dt, 0.0, pol, U, F, g->r, nullptr);
+    double r2, rinf;
+    TRY(norms_dev<D>(g, g->r, &r2, &rinf));
+    if (!std::isfinite(r2)) return fail(HJB_ERR_NONFINITE, "non-finite residual");
+    if (restart == 0 && eta > 0.0) tol = std::max(tol, eta * r2);
+    if (out) {
+      out->iters = it;
+      out->rres = bn2 > 0 ? r2 / bn2 : r2;
+      out->rres_inf = bninf > 0 ? rinf / bninf : rinf;
+    }
+    if (r2 <= tol && rinf <= tol_inf) { converged = true; break; }
+    const double tol_it = (rinf > tol_inf) ? std::min(tol, 0.5 * r2 * (tol_inf / rinf)) : tol;
+    LAUNCH(HJB_KC_VECTOR, N, 16.0 * N, 0, k_ag_gather<D><<<dims(g, g->L0, (const void*)k_ag_gather<D>), dim3(kBX, kBY), 0, g->st>>>(g->L0, g->r, L0.r));
+    CK(cudaMemsetAsync(L0.x, 0, (size_t)N * sizeof(double), g->st));
+    double rn = r2;
+    int m = 0;
+    while (it < sp->krylov_maxit && rn > tol_it) {
+      TRY(ag_kcycle(g, 0, L0.r, g->ag_Z[m]));
+      LAUNCH(HJB_KC_APPLY, N, 0, 0, k_ag_spmv<<<nb, 256, 0, g->st>>>(N, L0.col, L0.val, g->ag_Z[m], g->ag_AZ[m]));
+      for (int k = 0; k < m; ++k) {
+        double h, unused;
+        TRY(ag_dot(g, N, g->ag_AZ[k], g->ag_AZ[m], &h, &unused));
+        LAUNCH(HJB_KC_VECTOR, N, 0, 0, k_ag_axpby<<<nb, 256, 0, g->st>>>(N, -h, g->ag_AZ[k], 1.0, g->ag_AZ[m]));
+        LAUNCH(HJB_KC_VECTOR, N, 0, 0, k_ag_axpby<<<nb, 256, 0, g->st>>>(N, -h, g->ag_Z[k], 1.0, g->ag_Z[m]));
+      }
+      double unused, nn;
+      TRY(ag_dot(g, N, g->ag_AZ[m], g->ag_AZ[m], &unused, &nn));
+      const double nrm = std::sqrt(nn);
+      if (!(nrm > 0.0) || !std::isfinite(nrm)) break;
+      LAUNCH(HJB_KC_VECTOR, N, 0, 0, k_ag_axpby<<<nb, 256, 0, g->st>>>(N, 0.0, g->ag_AZ[m], 1.0 / nrm, g->ag_AZ[m]));
+      LAUNCH(HJB_KC_VECTOR, N, 0, 0, k_ag_axpby<<<nb, 256, 0, g->st>>>(N, 0.0, g->ag_Z[m], 1.0 / nrm, g->ag_Z[m]));
+      double gam, rr;
+      TRY(ag_dot(g, N, g->ag_AZ[m], L0.r, &gam, &rr));
+      LAUNCH(HJB_KC_VECTOR, N, 0, 0, k_ag_axpby<<<nb, 256, 0, g->st>>>(N, gam, g->ag_Z[m], 1.0, L0.x));
+      LAUNCH(HJB_KC_VECTOR, N, 0, 0, k_ag_axpby<<<nb, 256, 0, g->st>>>(N, -gam, g->ag_AZ[m], 1.0, L0.r));
+      rn = std::sqrt(std::max(0.0, rr - gam * gam));
+      ++it;
+      if (++m == kAgRestart) m = 0;
+    }
+    LAUNCH(HJB_KC_VECTOR, N, 16.0 * N, 0, k_ag_scatter_add<D><<<dims(g, g->L0, (const void*)k_ag_scatter_add<D>), dim3(kBX, kBY), 0, g->st>>>(g->L0, L0.x, U));
+    CKL();
+    if (it >= sp->krylov_maxit) {
+      TRY(halo_exchange(g, lv0, U, g->lay.halo));
+      launch_operator<D>(g, g->L0, coef_u(g), OP_RESID, 0, dt, 0.0, pol, U, F, g->r, nullptr);
+      TRY(norms_dev<D>(g, g->r, &r2, &rinf));
+      if (out) { out->iters = it; out->rres = bn2 > 0 ? r2 / bn2 : r2; out->rres_inf = bninf > 0 ? rinf / bninf : rinf; }
+      converged = r2 <= tol && rinf <= tol_inf;
+      break;
+    }
+  }
+  if (!converged) return fail(HJB_ERR_NOT_CONVERGED, "AGMG-preconditioned GCR did not reach the tolerance");
+  return HJB_OK;
+}
+
 extern "C" hjb_status hjb_solve(hjb_grid_t g, double dt, const uint8_t* policy, const double* F, double* x,
                                 const hjb_solve_params* p, hjb_solve_stats* out) {
   if (!g || !policy || !F || !x) return fail(HJB_ERR_INVALID_ARG, "null argument");
@@ -1998,6 +2328,8 @@ extern "C" hjb_status hjb_solve(hjb_grid_t g, double dt, const uint8_t* policy, 
   hjb_solve_params def;
   hjb_solve_params_default(g->D, &def);
   const hjb_solve_params* sp = p ? p : &def;
+  if (sp->solver == 1)
+    return g->D == 2 ? agmg_solve<2>(g, dt, policy, F, x, sp, out, 0.0) : agmg_solve<3>(g, dt, policy, F, x, sp, out, 0.0);
   return g->D == 2 ? bicgstab<2>(g, dt, policy, F, x, sp, out) : bicgstab<3>(g, dt, policy, F, x, sp, out);
 }
 
@@ -2255,14 +2587,18 @@ extern "C" hjb_status hjb_step(hjb_grid_t g, double dt, const double* U_prev, do
     if (it == sp->max_pi) { result = fail(HJB_ERR_NOT_CONVERGED, "policy iteration hit max_pi"); break; }
     const bool settled = (it > 1 && pis.changed == 0);  // only reached after an inexact solve
     cudaEventRecord(g->ev[0], st);
-    if (sp->use_mg && !(settled && g->mg_ready && g->mg_pol0 == dpol && g->mg_dt == dt))
+    if (sp->solver == 0 && sp->use_mg && !(settled && g->mg_ready && g->mg_pol0 == dpol && g->mg_dt == dt))
       TRY(hjb_mg_setup(g, dt, dpol, &sp->mg));
+    if (sp->solver == 1 && !(settled && g->ag_ready && g->ag_pol == dpol && g->ag_dt == dt))
+      TRY(g->D == 2 ? agmg_setup<2>(g, dt, dpol) : agmg_setup<3>(g, dt, dpol));
     cudaEventRecord(g->ev[1], st);
     hjb_solve_stats ss{};
     // inexact Howard: while the policy still changes, evaluate it only to eta * ||r_0||
     const double eta = (settled || g->K == 1) ? 0.0 : sp->pi_forcing;  // K = 1: the policy is final
-    hjb_status s = g->D == 2 ? bicgstab<2>(g, dt, dpol, g->F, dU, sp, &ss, eta)
-                             : bicgstab<3>(g, dt, dpol, g->F, dU, sp, &ss, eta);
+    hjb_status s = sp->solver == 1 ? (g->D == 2 ? agmg_solve<2>(g, dt, dpol, g->F, dU, sp, &ss, eta)
+                                                : agmg_solve<3>(g, dt, dpol, g->F, dU, sp, &ss, eta))
+                   : g->D == 2 ? bicgstab<2>(g, dt, dpol, g->F, dU, sp, &ss, eta)
+                               : bicgstab<3>(g, dt, dpol, g->F, dU, sp, &ss, eta);
     last_exact = (ss.rres <= sp->krylov_rtol) && (!(sp->krylov_rtol_inf > 0.0) || ss.rres_inf <= sp->krylov_rtol_inf);
     cudaEventRecord(g->ev[2], st);
     cudaEventSynchronize(g->ev[2]);

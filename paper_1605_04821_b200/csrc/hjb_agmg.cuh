@@ -1,0 +1,274 @@
+// hjb_agmg.cuh -- aggregation-based algebraic multigrid (PAPER.md:171-176,
+// 1162-1164): the fine policy operator assembled on the interior unknowns (compact numbering), double
+// pairwise aggregation on the symmetric part's strongest negative couplings (parallel handshake
+// matching), 0/1 aggregate transfers, coarse operators P^T A P, and the kernels of the K-cycle.
+//
+// Matching (per pass): node i's candidate is the unaggregated j maximising s_ij = -(a_ij + a_ji)/2
+// with s_ij >= beta * max_k s_ik (beta = 0.25) and s_ij > 0 (lowest index on ties); i and j pair
+// when they choose each other; a few rounds, then the rest stay single.  (The oracle,
+// oracle/agmg.py, matches greedily in index order: the aggregates differ, the solve does not.)
+// Storage: ELL, column-major ([slot][row]), compact interior indices, -1 = empty.
+#pragma once
+#include "hjb_device.cuh"
+#include "hjb_galerkin.cuh"
+
+namespace hjb {
+
+constexpr int kAgW = 96;  // ELL width of every AGMG level (fine: <= 1 + 4 (2P+1) entries per row)
+
+template <int D>
+__device__ __forceinline__ int compact_of(const LevelDev& L, const int* i) {
+  return D == 2 ? (i[1] - 1) * L.nI + (i[0] - 1) : ((i[2] - 1) * L.nI + (i[1] - 1)) * L.nI + (i[0] - 1);
+}
+
+// fine operator A = I - dt (L_hat^pi + c^pi) on the interior unknowns (boundary couplings are data);
+// row t = compact index of the node
+template <int D, int P>
+__global__ void __launch_bounds__(128) k_ag_fine(LevelDev L, CoefDev C, double dt, const uint8_t* __restrict__ pol,
+                                                int* __restrict__ col, double* __restrict__ val,
+                                                double* __restrict__ diag, int* __restrict__ overflow) {
+  constexpr int E = 2 * P + 1;
+  const int64_t N = (int64_t)L.nI * L.nrows;
+  RowAcc A;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < N; q += (int64_t)gridDim.x * blockDim.x) {
+    const int row = (int)(q / L.nI), c0 = (int)(q - (int64_t)row * L.nI);
+    Node<D> nd;
+    node_at<D>(L, c0, row, nd);
+    load_fields<D>(C, nd);
+    const int a = pol[nd.loc];
+    Tap<D> taps[E];
+    const double wsum = row_geometry<D, P>(L, C.sigma_dir + a * P * D, C.b_dir + a * D, nd, taps);
+    const double cc = nd.cn + C.c_ctrl[a];
+    acc_init(A);
+    bool ok = acc_add(A, (int)q, 1.0 + dt * (wsum - cc));
+    for (int e = 0; e < E; ++e) {
+      if (taps[e].w == 0.0) continue;
+      for (int m = 0; m < (1 << D); ++m) {
+        int j[3];
+        double wc = 1.0;
+        bool interior = true;
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          const int h = (m >> d) & 1;
+          j[d] = taps[e].c[d] + h;
+          wc *= h ? taps[e].s[d] : 1.0 - taps[e].s[d];
+          interior &= (j[d] >= 1 && j[d] <= L.n - 2);
+        }
+        if (!interior || wc == 0.0) continue;
+        ok &= acc_add(A, compact_of<D>(L, j), -dt * taps[e].w * wc);
+      }
+    }
+    double dg = 0.0;
+    for (int k = 0; k < A.cnt; ++k)
+      if (A.key[A.order[k]] == (int)q) dg = A.val[A.order[k]];
+    diag[q] = dg;
+    if (!ok || !acc_store(A, kAgW, N, q, col, val)) atomicExch(overflow, 1);
+  }
+}
+
+// a_ji by scanning row j
+__device__ __forceinline__ double ell_entry(const int* __restrict__ col, const double* __restrict__ val, int64_t N,
+                                            int j, int i) {
+  for (int k = 0; k < kAgW; ++k) {
+    const int c = col[k * N + j];
+    if (c < 0) break;
+    if (c == i) return val[k * N + j];
+  }
+  return 0.0;
+}
+
+// one matching round: cand[i] for every unaggregated i (state[i] < 0)
+__global__ void __launch_bounds__(128) k_ag_candidates(int64_t N, const int* __restrict__ col,
+                                                      const double* __restrict__ val, const int* __restrict__ state,
+                                                      int* __restrict__ cand, double beta) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+    if (state[i] >= 0) { cand[i] = -1; continue; }
+    double strongest = 0.0, best = 0.0;
+    int bj = -1;
+    for (int k = 0; k < kAgW; ++k) {
+      const int j = col[k * N + i];
+      if (j < 0) break;
+      if (j == (int)i) continue;
+      const double s = -0.5 * (val[k * N + i] + ell_entry(col, val, N, j, (int)i));
+      strongest = fmax(strongest, s);
+      if (state[j] < 0 && (s > best || (s == best && s > 0.0 && j < bj))) {
+        best = s;
+        bj = j;
+      }
+    }
+    cand[i] = (bj >= 0 && best > 0.0 && best >= beta * strongest) ? bj : -1;
+  }
+}
+
+// handshake: i < j choosing each other pair (leader i); final = every still unaggregated node alone
+__global__ void __launch_bounds__(128) k_ag_match(int64_t N, const int* __restrict__ cand, int* __restrict__ state,
+                                                 int final_round) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+    if (state[i] >= 0) continue;
+    const int j = cand[i];
+    if (j >= 0 && j > (int)i && cand[j] == (int)i) {
+      state[i] = (int)i;
+      state[j] = (int)i;
+    } else if (final_round && (j < 0 || cand[j] != (int)i)) {
+      state[i] = (int)i;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_ag_leader_flags(int64_t N, const int* __restrict__ state, int* __restrict__ flag) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
+    flag[i] = (state[i] == (int)i) ? 1 : 0;
+}
+
+// agg[i] = id of i's leader (ids = exclusive scan of the leader flags); members of each aggregate
+__global__ void __launch_bounds__(256) k_ag_number(int64_t N, const int* __restrict__ state, const int* __restrict__ id,
+                                                  int* __restrict__ agg, int* __restrict__ mem, int64_t Nc) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+    const int a = id[state[i]];
+    agg[i] = a;
+    mem[(state[i] == (int)i ? 0 : 1) * Nc + a] = (int)i;
+  }
+}
+
+// compose two passes: agg = agg2[agg1], members (<= 4) of the final aggregates
+__global__ void __launch_bounds__(256) k_ag_compose(int64_t N, const int* __restrict__ agg1, const int* __restrict__ agg2,
+                                                   int* __restrict__ agg, int64_t N1, const int* __restrict__ mem1,
+                                                   const int* __restrict__ mem2, int64_t Nc, int* __restrict__ mem) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
+    agg[i] = agg2[agg1[i]];
+  for (int64_t I = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; I < Nc; I += (int64_t)gridDim.x * blockDim.x) {
+    int k = 0;
+    for (int a = 0; a < 2; ++a) {
+      const int m = mem2[a * Nc + I];
+      if (m < 0) continue;
+      for (int b = 0; b < 2; ++b) {
+        const int f = mem1[b * N1 + m];
+        if (f >= 0) mem[(k++) * Nc + I] = f;
+      }
+    }
+  }
+}
+
+// coarse row I = sum over the members i of row i with columns mapped through agg (P^T A P)
+__global__ void __launch_bounds__(128) k_ag_coarse(int64_t Nf, const int* __restrict__ fcol, const double* __restrict__ fval,
+                                                  const int* __restrict__ agg, int64_t Nc, const int* __restrict__ mem,
+                                                  int nmem, int* __restrict__ ccol, double* __restrict__ cval,
+                                                  double* __restrict__ cdiag, int* __restrict__ overflow) {
+  RowAcc A;
+  for (int64_t I = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; I < Nc; I += (int64_t)gridDim.x * blockDim.x) {
+    acc_init(A);
+    bool ok = true;
+    for (int mm = 0; mm < nmem; ++mm) {
+      const int i = mem[mm * Nc + I];
+      if (i < 0) continue;
+      for (int k = 0; k < kAgW; ++k) {
+        const int j = fcol[k * Nf + i];
+        if (j < 0) break;
+        ok &= acc_add(A, agg[j], fval[k * Nf + i]);
+      }
+    }
+    double dg = 0.0;
+    for (int k = 0; k < A.cnt; ++k)
+      if (A.key[A.order[k]] == (int)I) dg = A.val[A.order[k]];
+    cdiag[I] = dg;
+    if (!ok || !acc_store(A, kAgW, Nc, I, ccol, cval)) atomicExch(overflow, 1);
+  }
+}
+
+// y = b - A x (JAC = false) or y = x + omega (b - A x) / D
+template <bool JAC>
+__global__ void __launch_bounds__(256) k_ag_sweep(int64_t N, const int* __restrict__ col, const double* __restrict__ val,
+                                                 const double* __restrict__ dg, const double* __restrict__ x,
+                                                 const double* __restrict__ b, double omega, double* __restrict__ y) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+    double ax = 0.0;
+    for (int k = 0; k < kAgW; ++k) {
+      const int j = __ldg(col + k * N + i);
+      if (j < 0) break;
+      ax = fma(__ldg(val + k * N + i), __ldg(x + j), ax);
+    }
+    const double r = __ldg(b + i) - ax;
+    y[i] = JAC ? fma(omega, r / __ldg(dg + i), __ldg(x + i)) : r;
+  }
+}
+
+// y = A x
+__global__ void __launch_bounds__(256) k_ag_spmv(int64_t N, const int* __restrict__ col, const double* __restrict__ val,
+                                                const double* __restrict__ x, double* __restrict__ y) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+    double ax = 0.0;
+    for (int k = 0; k < kAgW; ++k) {
+      const int j = __ldg(col + k * N + i);
+      if (j < 0) break;
+      ax = fma(__ldg(val + k * N + i), __ldg(x + j), ax);
+    }
+    y[i] = ax;
+  }
+}
+
+// rc[I] = sum of r over the members of aggregate I (P^T r)
+__global__ void __launch_bounds__(256) k_ag_restrict(int64_t Nc, const int* __restrict__ mem, int nmem,
+                                                    const double* __restrict__ r, double* __restrict__ rc) {
+  for (int64_t I = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; I < Nc; I += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int m = 0; m < nmem; ++m) {
+      const int i = mem[m * Nc + I];
+      if (i >= 0) s += r[i];
+    }
+    rc[I] = s;
+  }
+}
+
+// x += P e (x_i += e_{agg(i)})
+__global__ void __launch_bounds__(256) k_ag_prolong(int64_t N, const int* __restrict__ agg, const double* __restrict__ e,
+                                                   double* __restrict__ x) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] += e[agg[i]];
+}
+
+// y = a x + b y ; partial sums of (y, z) if z
+__global__ void __launch_bounds__(256) k_ag_axpby(int64_t N, double a, const double* __restrict__ x, double b,
+                                                 double* __restrict__ y) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = fma(a, x[i], b * y[i]);
+}
+
+// block partials [sum x.y, sum y.y] of compact vectors (256 threads)
+__global__ void __launch_bounds__(256) k_ag_dot2(int64_t N, const double* __restrict__ x, const double* __restrict__ y,
+                                                double* partial) {
+  double red[2] = {0.0, 0.0};
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+    red[0] = fma(x[i], y[i], red[0]);
+    red[1] = fma(y[i], y[i], red[1]);
+  }
+  block_reduce_store<2, 256>(red, partial);
+}
+
+// coarsest level: dense matrix from ELL (compact rows), then x = Ainv b
+__global__ void k_ag_dense(int64_t N, const int* __restrict__ col, const double* __restrict__ val, double* __restrict__ Ad) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
+    for (int k = 0; k < kAgW; ++k) {
+      const int j = col[k * N + i];
+      if (j < 0) break;
+      Ad[i * N + j] += val[k * N + i];
+    }
+}
+__global__ void k_ag_dense_solve(int N, const double* __restrict__ Ainv, const double* __restrict__ b, double* __restrict__ x) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int j = 0; j < N; ++j) s = fma(Ainv[(int64_t)i * N + j], b[j], s);
+    x[i] = s;
+  }
+}
+
+// grid array (interior) <-> compact vector
+template <int D>
+__global__ void __launch_bounds__(kTX) k_ag_gather(LevelDev L, const double* __restrict__ g, double* __restrict__ c) {
+  FOR_INTERIOR(L) { c[(int64_t)row * L.nI + col] = g[interior_offset<D>(L, col, row)]; }
+}
+template <int D>
+__global__ void __launch_bounds__(kTX) k_ag_scatter_add(LevelDev L, const double* __restrict__ c, double* __restrict__ g) {
+  FOR_INTERIOR(L) { g[interior_offset<D>(L, col, row)] += c[(int64_t)row * L.nI + col]; }
+}
+
+}  // namespace hjb

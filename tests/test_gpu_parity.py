@@ -532,3 +532,40 @@ def test_galerkin_vcycle_and_solve_parity(name, mk):
     assert st["rres"] <= 1e-12
     assert np.abs(x.cpu().numpy()[inter] - X).max() <= 1e-8 * max(1.0, np.abs(X).max()), st
     g.close()
+
+
+@pytest.mark.parametrize("name,mk", [("cfg2_129_K8", lambda: bj_config(2, n=129, K=8)), ("probA_41", lambda: problem_A(41)),
+                                     ("cfg3_17", lambda: bj_config(3, n=17))])
+def test_agmg_solve_parity(name, mk):
+    """Aggregation AMG (NEXT-1): K-cycle-preconditioned flexible GCR
+    (hjb_solve_params.solver = 1) solves the policy system to 1e-12 and matches SuperLU."""
+    torch = require_gpu()
+    p = mk()
+    g, fields = setup(p)
+    dt = p.dt
+    U0 = p.g(p.all_idx())
+    sr = control_search(p, U0, U0, dt, dt)
+    inter = Geometry.of(p).interior_idx()
+    pol = np.zeros(p.N, dtype=np.int64)
+    pol[inter] = sr.policy
+    psi = np.zeros(p.N)
+    b = p.boundary_idx()
+    psi[b] = U0[b]
+    X, _ = solve(assemble(p, pol, dt, dt, U0, psi))
+    Fd = torch.zeros(p.N, dtype=torch.float64, device="cuda")
+    Fd[torch.from_numpy(inter).cuda()] = torch.from_numpy(sr.F).cuda()
+    x = to_dev(U0, torch)
+    st = g.solve(dt, to_dev(pol.astype(np.uint8), torch), Fd, x, solver=1)
+    assert st["rres"] <= 1e-12 and st["rres_inf"] <= 1e-9, st
+    assert np.abs(x.cpu().numpy()[inter] - X).max() <= 1e-8 * max(1.0, np.abs(X).max()), st
+    g.close()
+
+
+def test_agmg_step_parity():
+    """A march of implicit steps with the AGMG policy evaluations equals the oracle's march."""
+    p = bj_config(0)
+    Ug, polg, stats = _gpu_march(p, 2, solver=1)
+    Uo = p.g(p.all_idx())
+    for s in (1, 2):
+        Uo, _, _ = howard_step(p, Uo, s * p.dt, p.dt)
+    assert np.abs(Ug - Uo).max() <= 1e-8 * max(1.0, np.abs(Uo).max()), stats
