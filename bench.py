@@ -412,6 +412,8 @@ def run_b200(args):
         "final_R": max(st["final_R"] for st in stats),
         "max_err_vs_ustar": err, "wall_s_timed": wall,
         "gpu_launches": int(prof_timed["total_launches"]), "graph_launches": int(prof_timed["graph_launches"]),
+        "host_launch_calls_per_step": (int(prof_timed["total_launches"]) - int(prof_timed["graph_kernels"])
+                                       + int(prof_timed["graph_launches"])) / args.steps,
         "profiled_replay": None if not replay_steps else {
             "steps": replay_steps, "ms_per_step": ms_replay / replay_steps,
             "note": "roofline, hbm_frac_by_class and time_share_by_class come from this replay of the first "

@@ -368,6 +368,8 @@ typedef struct {
   int64_t graph_launches;   /* cudaGraphLaunch calls of the captured multigrid tail:
                                the cycle from the first level owning <= 70000 nodes down is captured
                                once per hierarchy and replayed; its kernels are untimed             */
+  int64_t graph_kernels;    /* kernels executed inside those graph replays (host launch calls =
+                               total_launches - graph_kernels + graph_launches)                   */
 } hjb_profile;
 
 hjb_status hjb_profile_reset(hjb_grid_t g, int32_t time_kernels);

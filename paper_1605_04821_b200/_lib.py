@@ -98,14 +98,14 @@ class Profile(C.Structure):
                 ("ms", C.c_double * HJB_KC_COUNT),
                 ("bytes", C.c_double * HJB_KC_COUNT), ("flops", C.c_double * HJB_KC_COUNT),
                 ("nodes", C.c_double * HJB_KC_COUNT), ("total_launches", C.c_int64),
-                ("timed", C.c_int32), ("graph_launches", C.c_int64)]
+                ("timed", C.c_int32), ("graph_launches", C.c_int64), ("graph_kernels", C.c_int64)]
 
     def as_dict(self):
         per = {k: dict(launches=self.launches[i], calls=self.calls[i], ms=self.ms[i], bytes=self.bytes[i],
                        flops=self.flops[i], nodes=self.nodes[i])
                for i, k in enumerate(KERNEL_CLASSES)}
         return dict(classes=per, total_launches=self.total_launches, timed=bool(self.timed),
-                    graph_launches=self.graph_launches)
+                    graph_launches=self.graph_launches, graph_kernels=self.graph_kernels)
 
 
 _lib = None

@@ -1805,6 +1805,7 @@ static hjb_status vcycle(hjb_grid* g, size_t l, const double* b, double* out) {
     g->prof.total_launches += sg->launches;
     g->prof.launches[HJB_KC_MG_COARSE] += sg->launches;
     g->prof.graph_launches += 1;
+    g->prof.graph_kernels += sg->launches;
     return HJB_OK;
   }
   Level& lv = g->levels[l];
@@ -2061,10 +2062,14 @@ static hjb_status ag_pairwise(hjb_grid* g, int64_t N, const int* col, const doub
   int *state = g->ag_i[0], *cand = g->ag_i[1], *flag = g->ag_i[2], *id = g->ag_i[3];
   CK(cudaMemsetAsync(state, 0xff, (size_t)N * sizeof(int), g->st));
   const int nb = ag_blocks(N, 128);
-  for (int round = 0; round < 4; ++round) {
-    LAUNCH(HJB_KC_COARSE, N, 0, 0, k_ag_candidates<<<nb, 128, 0, g->st>>>(N, col, val, state, cand, 0.25));
-    LAUNCH(HJB_KC_COARSE, N, 0, 0, k_ag_match<<<nb, 128, 0, g->st>>>(N, cand, state, round == 3 ? 1 : 0));
+  unsigned long long* winner = (unsigned long long*)g->ag_i[2];  // flag/id scratch: 2 ints per node
+  for (int round = 0; round < 6; ++round) {
+    CK(cudaMemsetAsync(winner, 0, (size_t)N * sizeof(unsigned long long), g->st));
+    LAUNCH(HJB_KC_COARSE, N, 0, 0, k_ag_candidates<<<nb, 128, 0, g->st>>>(N, col, val, state, cand, 0.25, round));
+    LAUNCH(HJB_KC_COARSE, N, 0, 0, k_ag_propose<<<nb, 128, 0, g->st>>>(N, col, val, state, cand, winner));
+    LAUNCH(HJB_KC_COARSE, N, 0, 0, k_ag_accept<<<nb, 128, 0, g->st>>>(N, winner, state));
   }
+  LAUNCH(HJB_KC_COARSE, N, 0, 0, k_ag_singles<<<nb, 128, 0, g->st>>>(N, state));
   CKL();
   LAUNCH(HJB_KC_COARSE, N, 0, 0, k_ag_leader_flags<<<ag_blocks(N), 256, 0, g->st>>>(N, state, flag));
   size_t need = 0;
@@ -2144,7 +2149,7 @@ static hjb_status agmg_setup(hjb_grid* g, double dt, const uint8_t* pol) {
     cudaFree(tl->col); cudaFree(tl->val); cudaFree(tl->dg); cudaFree(tl->x); cudaFree(tl->b); cudaFree(tl->r);
     cudaFree(tl->t);
     for (int k = 0; k < 2; ++k) { cudaFree(tl->z[k]); cudaFree(tl->az[k]); }
-    if (N2 * 10 >= N * 9) {  // no coarsening: stop here (the level just built is dropped)
+    if (N2 * 10 >= N * 7) {  // coarsening below 1.43x: stop here (the level just built is dropped)
       cudaFree(lf.agg); cudaFree(lf.mem);
       lf.agg = nullptr; lf.mem = nullptr;
       cudaFree(lc.col); cudaFree(lc.val); cudaFree(lc.dg); cudaFree(lc.x); cudaFree(lc.b); cudaFree(lc.r);
@@ -2155,13 +2160,12 @@ static hjb_status agmg_setup(hjb_grid* g, double dt, const uint8_t* pol) {
     g->ag.push_back(lc);
   }
   auto& lc = g->ag.back();
-  if (lc.N > 160) return fail(HJB_ERR_UNSUPPORTED, "aggregation stalled above the dense coarsest size (160)");
+  if (lc.N > kAgDenseMax)
+    return fail(HJB_ERR_UNSUPPORTED, "aggregation stalled above the dense coarsest size (" + std::to_string(lc.N) + " > 1024)");
   TRY(dalloc((void**)&lc.Ainv, (size_t)lc.N * lc.N * sizeof(double)));
   CK(cudaMemsetAsync(lc.Ainv, 0, (size_t)lc.N * lc.N * sizeof(double), g->st));
-  LAUNCH(HJB_KC_COARSE, lc.N, 0, 0, k_ag_dense<<<1, 160, 0, g->st>>>(lc.N, lc.col, lc.val, lc.Ainv));
-  const size_t smem = (size_t)lc.N * lc.N * sizeof(double);
-  if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_coarse_invert, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  LAUNCH(HJB_KC_COARSE, lc.N, 0, 0, k_coarse_invert<<<1, 1024, smem, g->st>>>(lc.Ainv, (int)lc.N));
+  LAUNCH(HJB_KC_COARSE, lc.N, 0, 0, k_ag_dense<<<ag_blocks(lc.N), 256, 0, g->st>>>(lc.N, lc.col, lc.val, lc.Ainv));
+  LAUNCH(HJB_KC_COARSE, lc.N, 0, 0, k_ag_invert<<<1, 1024, 0, g->st>>>(lc.Ainv, (int)lc.N));
   CKL();
   int flag = 0;
   CK(cudaMemcpyAsync(&flag, g->d_flag, sizeof(int), cudaMemcpyDeviceToHost, g->st));
@@ -2208,10 +2212,12 @@ static hjb_status ag_inner(hjb_grid* g, size_t c, const double* b, double* x) {
     if (!(nrm > 0.0)) break;
     LAUNCH(HJB_KC_VECTOR, N, 0, 0, k_ag_axpby<<<nb, 256, 0, g->st>>>(N, 0.0, L.az[it], 1.0 / nrm, L.az[it]));
     LAUNCH(HJB_KC_VECTOR, N, 0, 0, k_ag_axpby<<<nb, 256, 0, g->st>>>(N, 0.0, L.z[it], 1.0 / nrm, L.z[it]));
-    double gam, unused2;
-    TRY(ag_dot(g, N, L.r, L.az[it], &gam, &unused2));
+    double gam, rr;
+    TRY(ag_dot(g, N, L.az[it], L.r, &gam, &rr));
     LAUNCH(HJB_KC_VECTOR, N, 0, 0, k_ag_axpby<<<nb, 256, 0, g->st>>>(N, gam, L.z[it], 1.0, x));
     LAUNCH(HJB_KC_VECTOR, N, 0, 0, k_ag_axpby<<<nb, 256, 0, g->st>>>(N, -gam, L.az[it], 1.0, L.r));
+    // K-cycle's adaptive rule (Notay): one inner iteration suffices if it reduced the residual 4x
+    if (it == 0 && rr - gam * gam <= 0.0625 * rr) break;
   }
   CKL();
   return HJB_OK;
@@ -2223,7 +2229,7 @@ static hjb_status ag_kcycle(hjb_grid* g, size_t l, const double* b, double* x) {
   const int64_t N = L.N;
   const int nb = ag_blocks(N);
   if (l + 1 == g->ag.size()) {
-    LAUNCH(HJB_KC_COARSE, N, 0, 0, k_ag_dense_solve<<<1, 256, 0, g->st>>>((int)N, L.Ainv, b, x));
+    LAUNCH(HJB_KC_COARSE, N, 0, 0, k_ag_dense_solve<<<(int)((N + 127) / 128), 128, 0, g->st>>>((int)N, L.Ainv, b, x));
     CKL();
     return HJB_OK;
   }
