@@ -64,6 +64,12 @@ def parse():
     ap.add_argument("--nu-post", type=int, default=None, help="post-smoothing sweeps (overrides --nu)")
     ap.add_argument("--gamma", type=int, default=None, help="multigrid cycle index (default: library's 2)")
     ap.add_argument("--gamma-min", type=int, default=None, help="min coarse-level nodes for a revisit")
+    ap.add_argument("--nested-upto", type=int, default=1,
+                    help="steps 1..K of a march start from the nested coarse solve (HJB_GUESS_NESTED); "
+                         "later steps extrapolate in time; 0 = never nested")
+    ap.add_argument("--nested-min-n", type=int, default=None, help="HJB_GUESS_NESTED: smallest nested grid")
+    ap.add_argument("--stats-jsonl", default=None,
+                    help="write one JSON line of hjb_step_stats per timed step (SURVEY §5 metrics)")
     return ap.parse_args()
 
 
@@ -268,6 +274,14 @@ def run_b200(args):
     def step_of(s):          # step index within its march (1..n_steps)
         return (s - 1) % ns + 1
 
+    if args.nested_min_n is not None:
+        skw["nested_min_n"] = args.nested_min_n
+
+    def guess_of(si):        # initial iterate of step si (the fixed point does not depend on it)
+        if si <= args.nested_upto:
+            return _lib.HJB_GUESS_NESTED
+        return _lib.HJB_GUESS_EXTRAPOLATE if si >= 2 else _lib.HJB_GUESS_PREV
+
     def do_step(s, Uin, Uout, polbuf):
         # march restart: U^0 = g (a device copy, part of the step's setup a1).  Initial iterate:
         # linear extrapolation 2 U^{n-1} - U^{n-2} once two steps exist (Uout holds U^{n-2}:
@@ -277,8 +291,7 @@ def run_b200(args):
             Uin.copy_(U0)
         fb, fc = srcs[si - 1]
         g.set_source(fb, fc)
-        return g.step(p.dt, Uin, Uout, polbuf, psis[si - 1], mg=mgkw,
-                      guess=(_lib.HJB_GUESS_EXTRAPOLATE if si >= 2 else _lib.HJB_GUESS_PREV), **skw)
+        return g.step(p.dt, Uin, Uout, polbuf, psis[si - 1], mg=mgkw, guess=guess_of(si), **skw)
 
     stats = []
     for s in range(1, args.warmup + 1):
@@ -310,6 +323,9 @@ def run_b200(args):
     clocks = clk.stop()
     prof_timed = g.profile_read()
     ms_steps = [a.elapsed_time(b) for a, b in ev]
+    if args.stats_jsonl and rank == 0:
+        write_stats_jsonl(args.stats_jsonl, stats, ms_steps,
+                          [step_of(s) * p.dt for s in range(args.warmup + 1, total + 1)], nI)
     Ufinal = U.clone()
     prof = prof_timed
     replay_steps = 0
@@ -385,7 +401,8 @@ def run_b200(args):
     # --------------------------------------------------------------- e2e through host buffers
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(g, p, args, snap, stream, srcs, psis, nI, dev, lay, bar, allmax, skw, mgkw, U0, step_of)
+        e2e = run_e2e(g, p, args, snap, stream, srcs, psis, nI, dev, lay, bar, allmax, skw, mgkw, U0, step_of,
+                      guess_of)
 
     pis = [st["pi_iters"] for st in stats]
     kr = [st["krylov_iters_total"] for st in stats]
@@ -405,6 +422,11 @@ def run_b200(args):
         if args.steps >= ns else [round((step_of(s) - 1) * p.dt, 6) for s in (args.warmup + 1, total)],
         "march": f"T = {p.T:g} in {ns} implicit steps; restart from u*(0) after step {ns}",
         "pi_per_step": pis, "krylov_per_step": kr,
+        "nested_pi_per_step": [st["nested_pi_iters"] for st in stats],
+        "nested_ms_per_step": [round(st["ms_nested"], 2) for st in stats],
+        "initial_iterate": (f"steps 1..{args.nested_upto} of a march: nested coarse solve (HJB_GUESS_NESTED); "
+                            "later: 2 U^{n-1} - U^{n-2}") if args.nested_upto > 0 else
+                           "step 1: U^{n-1}; later: 2 U^{n-1} - U^{n-2}",
         "mg_cycles_per_pi": (2 * sum(kr) / max(1, sum(pis))),
         "krylov_iters_per_pi": sum(kr) / max(1, sum(pis)), "pi_iters_per_step": sum(pis) / len(pis),
         "levels": stats[-1]["n_levels"], "final_rres": max(st["final_rres"] for st in stats),
@@ -487,7 +509,22 @@ def traffic_for(cls, config, c):
     return e["dram_bytes_per_node"] * c["nodes"] / max(1, c["calls"] or c["launches"])
 
 
-def run_e2e(g, p, args, snap, stream, srcs, psis, nI, dev, lay, bar, allmax, skw, mgkw, U0, step_of):
+def write_stats_jsonl(path, stats, ms_steps, ts, nI):
+    """Per-step metrics, one JSON object per line (SURVEY §5 "Metrics / logging")."""
+    with open(path, "w") as f:
+        for st, ms, t in zip(stats, ms_steps, ts):
+            k = st["pi_iters"]
+            f.write(json.dumps({
+                "t": round(t, 12), "ms": round(ms, 3), "unknowns_steps_per_s": nI / (ms / 1e3),
+                "pi_iters": k, "krylov_iters": st["krylov_iters"], "mg_cycles": 2 * st["krylov_iters_total"],
+                "changed": st["changed"], "R": st["R"], "final_R": st["final_R"],
+                "final_rres": st["final_rres"], "final_rres_inf": st["final_rres_inf"],
+                "nested_pi_iters": st["nested_pi_iters"], "ms_nested": st["ms_nested"],
+                "ms_search": st["ms_search"], "ms_setup": st["ms_setup"], "ms_solve": st["ms_solve"],
+                "status": st.get("status")}) + "\n")
+
+
+def run_e2e(g, p, args, snap, stream, srcs, psis, nI, dev, lay, bar, allmax, skw, mgkw, U0, step_of, guess_of):
     """The SAME K steps as the timed region (replayed from its starting state) through hjb_step with
     pinned HOST buffers: each step copies U_prev, the policy and psi host->device and U + policy
     device->host inside the timed region (inside the call).  A march restart passes a pinned host
@@ -515,8 +552,7 @@ def run_e2e(g, p, args, snap, stream, srcs, psis, nI, dev, lay, bar, allmax, skw
             Uhp_np = u0h[s]
         fb, fc = srcs[si - 1]
         g.set_source(fb, fc)
-        g.step(p.dt, Uhp_np, Uh_np, pol_np, psi_np[si - 1], mg=mgkw, **skw,
-               guess=_lib.HJB_GUESS_EXTRAPOLATE if si >= 2 else _lib.HJB_GUESS_PREV)
+        g.step(p.dt, Uhp_np, Uh_np, pol_np, psi_np[si - 1], mg=mgkw, **skw, guess=guess_of(si))
         Uhp_np, Uh_np = Uh_np, Uhp_np
     ev1.record(stream)
     torch.cuda.synchronize()

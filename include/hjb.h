@@ -245,7 +245,15 @@ typedef struct {
                                 HJB_GUESS_PREV (default): U_prev, as the paper's time march;
                                 HJB_GUESS_GIVEN: U as passed by the caller;
                                 HJB_GUESS_EXTRAPOLATE: U holds U^{n-2} on entry and the iterate is
-                                2 U_prev - U^{n-2} (linear extrapolation in time, DESIGN.md xxiv).
+                                2 U_prev - U^{n-2} (linear extrapolation in time, DESIGN.md xxiv);
+                                HJB_GUESS_NESTED: nested iteration -- the same step is first solved
+                                on the grid coarsened 2^nested_coarsen times per axis (own h and
+                                k = sqrt(h); fields, U_prev and psi(t_n) injected from
+                                coincident nodes; recursively nested while the next grid keeps
+                                n >= nested_min_n) and its solution, prolonged multilinearly, is
+                                the iterate (reading xxx).  Needs (n-1) divisible by
+                                2^nested_coarsen, one rank, the interpolation boundary mode and
+                                theta = 1; otherwise it falls back to HJB_GUESS_PREV.
                                 Boundary entries are always set to psi(t_n) (if given).         */
   double krylov_rtol_inf;    /* secondary stop of an EXACT evaluation: also ||F - A X||_inf <=
                                 krylov_rtol_inf ||F||_inf (default 1e-9; 0 = off).  The 2-norm rule
@@ -267,11 +275,15 @@ typedef struct {
                                 NEXT-1): the assembled operator, double pairwise aggregation,
                                 K-cycle with 2 inner GCR iterations per coarse level.  One rank;
                                 the setup is redone per policy.  Same stopping rules.           */
+  int32_t nested_coarsen;    /* HJB_GUESS_NESTED: 2^nested_coarsen coarsening per axis (default 2) */
+  int32_t nested_min_n;      /* HJB_GUESS_NESTED: nest only onto grids with n >= nested_min_n
+                                (default 513)                                                   */
 } hjb_solve_params;
 
 #define HJB_GUESS_PREV 0
 #define HJB_GUESS_GIVEN 1
 #define HJB_GUESS_EXTRAPOLATE 2
+#define HJB_GUESS_NESTED 3
 
 typedef struct {
   int32_t iters;             /* BiCGSTAB iterations */
@@ -303,6 +315,9 @@ typedef struct {
   double ms_search, ms_setup, ms_solve;      /* device time per phase (CUDA events) */
   int32_t n_levels;
   double final_rres_inf;                     /* ||F - A X||_inf / ||F||_inf of the last solve */
+  int32_t nested_pi_iters;                   /* HJB_GUESS_NESTED: policy iterations on the coarser
+                                                grids (all nesting levels) */
+  double ms_nested;                          /* device time of the nested coarse solves */
 } hjb_step_stats;
 
 /* U may alias U_prev (in-place step): U_prev is then copied to an internal buffer first.    */

@@ -67,9 +67,10 @@ class SolveParams(C.Structure):
     _fields_ = [("krylov_rtol", C.c_double), ("krylov_maxit", C.c_int32), ("use_mg", C.c_int32),
                 ("tol_pi", C.c_double), ("max_pi", C.c_int32), ("mg", MgParams),
                 ("pi_forcing", C.c_double), ("guess", C.c_int32), ("krylov_rtol_inf", C.c_double),
-                ("theta", C.c_double), ("solver", C.c_int32)]
+                ("theta", C.c_double), ("solver", C.c_int32), ("nested_coarsen", C.c_int32),
+                ("nested_min_n", C.c_int32)]
 
-HJB_GUESS_PREV, HJB_GUESS_GIVEN, HJB_GUESS_EXTRAPOLATE = 0, 1, 2
+HJB_GUESS_PREV, HJB_GUESS_GIVEN, HJB_GUESS_EXTRAPOLATE, HJB_GUESS_NESTED = 0, 1, 2, 3
 
 
 class SolveStats(C.Structure):
@@ -81,7 +82,8 @@ class StepStats(C.Structure):
                 ("krylov_iters", C.c_int32 * HJB_MAX_PI_LOG), ("changed", C.c_int64 * HJB_MAX_PI_LOG),
                 ("R", C.c_double * HJB_MAX_PI_LOG), ("final_R", C.c_double), ("final_rres", C.c_double),
                 ("ms_search", C.c_double), ("ms_setup", C.c_double), ("ms_solve", C.c_double),
-                ("n_levels", C.c_int32), ("final_rres_inf", C.c_double)]
+                ("n_levels", C.c_int32), ("final_rres_inf", C.c_double),
+                ("nested_pi_iters", C.c_int32), ("ms_nested", C.c_double)]
 
     def as_dict(self):
         k = self.pi_iters
@@ -90,7 +92,8 @@ class StepStats(C.Structure):
                     krylov_iters=list(self.krylov_iters[:k]), changed=list(self.changed[:m]),
                     R=list(self.R[:m]), final_R=self.final_R, final_rres=self.final_rres,
                     ms_search=self.ms_search, ms_setup=self.ms_setup, ms_solve=self.ms_solve,
-                    n_levels=self.n_levels, final_rres_inf=self.final_rres_inf)
+                    n_levels=self.n_levels, final_rres_inf=self.final_rres_inf,
+                    nested_pi_iters=self.nested_pi_iters, ms_nested=self.ms_nested)
 
 
 class Profile(C.Structure):

@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = os.path.join(HERE, "csrc", "hjb.cu")
-DEPS = [os.path.join(HERE, "csrc", f) for f in ("hjb.cu", "hjb_device.cuh", "hjb_kernels.cuh", "hjb_tma.cuh", "hjb_win.cuh", "hjb_search2.cuh", "hjb_galerkin.cuh", "hjb_agmg.cuh",
+DEPS = [os.path.join(HERE, "csrc", f) for f in ("hjb.cu", "hjb_device.cuh", "hjb_kernels.cuh", "hjb_tma.cuh", "hjb_win.cuh", "hjb_search2.cuh", "hjb_galerkin.cuh", "hjb_agmg.cuh", "hjb_nested.cuh",
                                                     "hjb_comm.h")] + \
        [os.path.join(ROOT, "include", "hjb.h")]
 LIB = os.path.join(HERE, "libhjb.so")

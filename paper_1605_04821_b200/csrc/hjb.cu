@@ -23,6 +23,7 @@
 #include "hjb_search2.cuh"
 #include "hjb_galerkin.cuh"
 #include "hjb_agmg.cuh"
+#include "hjb_nested.cuh"
 #include <cub/device/device_scan.cuh>
 
 namespace hjb {
@@ -61,7 +62,9 @@ static hjb_status fail(hjb_status s, const std::string& msg) {
 #define CKL()                                                                                     \
   do {                                                                                            \
     cudaError_t e_ = cudaGetLastError();                                                          \
-    if (e_ != cudaSuccess) return fail(HJB_ERR_CUDA, std::string("launch: ") + cudaGetErrorString(e_)); \
+    if (e_ != cudaSuccess)                                                                        \
+      return fail(HJB_ERR_CUDA, std::string("launch (hjb.cu:") + std::to_string(__LINE__) + "): " +  \
+                                    cudaGetErrorString(e_));                                      \
   } while (0)
 #define TRY(x)                     \
   do {                             \
@@ -167,6 +170,17 @@ struct hjb_grid {
   double rdiff_ax[3] = {0, 0, 0}, rdrift_ax[3] = {0, 0, 0};
   double* rng_part = nullptr; // k_field_ranges block partials
   double2* upair = nullptr;   // (U_i, U_{i+1}) pair copy of the searched U (k_search_deep2)
+  double4* uquad = nullptr;   // cell-corner copy of the searched U (k_search_deep2<..., QUADS>)
+  bool search3 = false;       // k_search_deep3 on the deep rectangle (opt-in, HJB_SEARCH3=1)
+  // nested iteration (HJB_GUESS_NESTED, hjb_nested.cuh): the same problem on the grid coarsened
+  // 2^child_m times per axis, its fields injected from this grid's
+  hjb_grid* child = nullptr;
+  int child_m = 0;
+  bool child_dirty = true;    // fields / tables changed since the last injection
+  double* child_fields = nullptr;
+  double* child_U = nullptr;
+  double* child_prev = nullptr;
+  uint8_t* child_pol = nullptr;
   double* vtheta = nullptr;   // theta U + (1-theta) U_prev (theta-scheme search argument)
   bool galerkin = false;      // coarse operators by the Galerkin product (hjb_mg_params.coarse_op)
   int* gb_col = nullptr;      // B = A P scratch of the Galerkin setup (ELL [kGalWB][elems_0])
@@ -274,6 +288,22 @@ static void prof_post(hjb_grid* g, int cls, double nodes, double bytes, double f
 // 2D launch over the owned interior of level L: x covers an x1 line, y strides over lines.  All
 // CTAs are made co-resident (occupancy x SMs) so the lines in flight form one band that moves
 // through the grid and the +-reach rows it gathers from stay in L2.
+// A kernel's dynamic shared-memory limit is a process-wide attribute of the function: raise it once
+// to the device's opt-in maximum (setting it to one grid's requirement would make another grid's
+// larger launch fail -- two handles with different window plans in one process).
+static cudaError_t allow_smem(const void* fn) {
+  static std::mutex mu;
+  static std::map<const void*, bool> done;
+  std::lock_guard<std::mutex> lock(mu);
+  if (done[fn]) return cudaSuccess;
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+  if (e == cudaSuccess) done[fn] = true;
+  return e;
+}
+
 static int occupancy_of(const void* fn, size_t smem = 0, int block = kTX) {
   // shared by every handle; thread-rank grids (HJB_COMM_THREADS) call it concurrently
   static std::mutex mu;
@@ -286,7 +316,7 @@ static int occupancy_of(const void* fn, size_t smem = 0, int block = kTX) {
 #ifdef HJB_L1MAX
   cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 0);  // maximal L1
 #endif
-  if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (smem > 48 * 1024) allow_smem(fn);
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, block, smem) != cudaSuccess || occ < 1) occ = 1;
   cache[key] = occ;
   return occ;
@@ -615,6 +645,8 @@ extern "C" void hjb_solve_params_default(int32_t dim, hjb_solve_params* o) {
   o->krylov_rtol_inf = 1e-9;  // SURVEY §8c-xvii secondary stop (reading xvii)
   o->theta = 1.0;             // implicit Euler (the paper's experiments)
   o->solver = 0;              // BiCGSTAB + geometric multigrid (1: GCR + aggregation AMG, NEXT-1)
+  o->nested_coarsen = 2;      // HJB_GUESS_NESTED: 4x coarser per axis ...
+  o->nested_min_n = 513;      // ... while the coarse grid keeps n >= 513
 }
 
 // ---------------------------------------------------------------------------- API: partition
@@ -713,6 +745,11 @@ extern "C" hjb_status hjb_grid_destroy(hjb_grid_t g) {
   if (!g) return fail(HJB_ERR_INVALID_ARG, "null handle");
   cudaSetDevice(g->desc.device);
   if (g->st) cudaStreamSynchronize(g->st);
+  if (g->child) hjb_grid_destroy(g->child);
+  cudaFree(g->child_fields);
+  cudaFree(g->child_U);
+  cudaFree(g->child_prev);
+  cudaFree(g->child_pol);
   free_levels(g);
   double* bufs[] = {g->d_tab, g->r, g->rhat, g->p, g->v, g->s, g->t, g->phat, g->shat, g->F,
                     g->partial, g->red, g->red_all, g->scratch, g->stage_prev, g->stage_U, g->stage_psi};
@@ -722,6 +759,7 @@ extern "C" hjb_status hjb_grid_destroy(hjb_grid_t g) {
   cudaFree(g->d_rng);
   cudaFree(g->rng_part);
   cudaFree(g->upair);
+  cudaFree(g->uquad);
   cudaFree(g->vtheta);
   cudaFree(g->d_flag);
   agmg_free(g);
@@ -970,7 +1008,7 @@ static hjb_status setup_win(hjb_grid* g, const SkipRect& dr, bool gen, WinPlan* 
   if (!std::isfinite(best)) return HJB_OK;
   const size_t smem = ((size_t)W.tab + (size_t)W.w[0] * W.w[1] * W.w[2]) * sizeof(double) + cmb;
   const void* fn = win_fn(D, P, gen);
-  CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CK(allow_smem(fn));
   int occ = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kWinNT, smem) != cudaSuccess || occ < 1) {
     cudaGetLastError();
@@ -1074,7 +1112,7 @@ static hjb_status setup_deep(hjb_grid* g) {
     const size_t smem = (ntab + (size_t)2 * E * 2 * T.slot) * sizeof(double) + 128;
     if (T.ntx > 0 && T.nty > 0 && T.bw <= 256 && T.bh <= 256 && smem <= 200 * 1024 && tma_encoder()) {
       const void* fn = P == 1 ? (const void*)k_search_tma<1> : (const void*)k_search_tma<2>;
-      CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      CK(allow_smem(fn));
       int occ = 0;
       if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kWT, smem) == cudaSuccess && occ >= 1) {
         g->tma = T;
@@ -1119,6 +1157,7 @@ extern "C" hjb_status hjb_set_coeffs(hjb_grid_t g, const hjb_coeffs* c) {
   g->nplanes0 = (c->sigma_scale ? g->P : 0) + (c->sigma_node ? g->P * g->D : 0) + (c->b_scale ? 1 : 0) +
                 (c->b_node ? g->D : 0) + (c->c_node ? 1 : 0);
   g->have_coeffs = true;
+  g->child_dirty = true;
   g->mg_ready = false;
   for (auto& sg : g->graphs) cudaGraphExecDestroy(sg.exec);  // captured kernels hold field pointers
   g->graphs.clear();
@@ -1205,17 +1244,37 @@ static bool search2_ok(hjb_grid* g) {
   return true;
 }
 
-template <int P, int Q, bool STRIP>
+template <int P, int Q, bool STRIP, bool QUADS = false, int KU = 0>
 static void search2_launch(hjb_grid* g, const LevelDev& LL, double dt, const double* U, const double* Uprev,
                            uint8_t* pol, double* F, const SkipRect& rect, const STab& tab, const STabQuad& quad,
                            int* nblk) {
-  const void* fn = (const void*)k_search_deep2<P, Q, STRIP>;
+  const void* fn = (const void*)k_search_deep2<P, Q, STRIP, QUADS, KU>;
   const int64_t tiles = (int64_t)((LL.nI + kSBX - 1) / kSBX) * ((LL.nrows + kS2Y - 1) / kS2Y);
   const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, std::min<int64_t>((int64_t)occupancy_of(fn, 0, kS2T) * g->sms, kMaxBlocks)));
   LAUNCH(HJB_KC_SEARCH, 0, 0, 0,
-         k_search_deep2<P, Q, STRIP><<<nb, dim3(kSBX, kS2Y), 0, g->st>>>(
-             g->L0, STRIP ? coef_u(g) : g->C0, dt, U, g->upair, Uprev, pol, F, g->partial + 2 * *nblk, rect, tab, quad));
+         k_search_deep2<P, Q, STRIP, QUADS, KU><<<nb, dim3(kSBX, kS2Y), 0, g->st>>>(
+             g->L0, STRIP ? coef_u(g) : g->C0, dt, U, g->upair, g->uquad, Uprev, pol, F, g->partial + 2 * *nblk, rect,
+             tab, quad));
   *nblk += nb;
+}
+
+// the deep rectangle with k_search_deep3 (node-local bracket staged in shared memory)
+template <int P, int Q>
+static hjb_status search3_launch(hjb_grid* g, const LevelDev& LL, double dt, const double* U, const double* Uprev,
+                                 uint8_t* pol, double* F, const SkipRect& rect, const STab& tab, const STabQuad& quad,
+                                 int* nblk) {
+  const void* fn = (const void*)k_search_deep3<P, Q>;
+  const size_t smem = (size_t)g->K * kS2T * sizeof(double);
+  CK(allow_smem(fn));
+  int occ = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kS2T, smem));
+  const int64_t tiles = (int64_t)((LL.nI + kSBX - 1) / kSBX) * ((LL.nrows + kS2Y - 1) / kS2Y);
+  const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, std::min<int64_t>((int64_t)std::max(1, occ) * g->sms, kMaxBlocks)));
+  LAUNCH(HJB_KC_SEARCH, 0, 0, 0,
+         k_search_deep3<P, Q><<<nb, dim3(kSBX, kS2Y), smem, g->st>>>(g->L0, g->C0, dt, U, g->uquad, Uprev, pol, F,
+                                                                     g->partial + 2 * *nblk, rect, tab, quad));
+  *nblk += nb;
+  return HJB_OK;
 }
 
 template <int P, int Q>
@@ -1255,7 +1314,14 @@ static hjb_status launch_search2(hjb_grid* g, double dt, const double* U, const 
 #define S2(PP, QQ)                                                                                 \
   do {                                                                                             \
     search2_tables<PP, QQ>(g, tab, quad);                                                          \
-    if (!strips) search2_launch<PP, QQ, false>(g, LL, dt, U, Uprev, pol, F, rect, tab, quad, nblk); \
+    if (!strips && g->uquad && g->search3)                                                         \
+      TRY((search3_launch<PP, QQ>(g, LL, dt, U, Uprev, pol, F, rect, tab, quad, nblk)));           \
+    else if (!strips && g->uquad && g->K == 32 && PP == 2 && getenv("HJB_KUNROLL"))                \
+      search2_launch<PP, QQ, false, true, 32>(g, LL, dt, U, Uprev, pol, F, rect, tab, quad, nblk); \
+    else if (!strips && g->uquad)                                                                  \
+      search2_launch<PP, QQ, false, true>(g, LL, dt, U, Uprev, pol, F, rect, tab, quad, nblk);     \
+    else if (!strips)                                                                              \
+      search2_launch<PP, QQ, false>(g, LL, dt, U, Uprev, pol, F, rect, tab, quad, nblk);           \
     for (int k = 0; k < ns; ++k) {                                                                 \
       const LevelDev LS = shape_of(g->L0, strips[k]);                                              \
       if (LS.nI > 0 && LS.nrows > 0)                                                               \
@@ -1372,6 +1438,17 @@ static hjb_status policy_update_dev(hjb_grid* g, double dt, const double* U, con
            k_make_pairs<<<(int)std::min<int64_t>((ne + 255) / 256, (int64_t)g->sms * 8), 256, 0, g->st>>>(U, g->upair, ne));
     CKL();
 #endif
+    // opt-in variants (measured at cfg4): 256-bit corner-copy taps (HJB_QUADS=1) and the
+    // hoisted node-local bracket in shared memory (HJB_SEARCH3=1, needs the corner copy)
+    g->search3 = getenv("HJB_SEARCH3") && (size_t)g->K * kS2T * sizeof(double) <= 200 * 1024;
+    if (getenv("HJB_QUADS") || g->search3) {  // cell-corner copy of U for the 256-bit tap loads
+      if (!g->uquad) TRY(dalloc((void**)&g->uquad, (size_t)g->N * sizeof(double4)));
+      const int64_t ne = g->N;
+      LAUNCH(HJB_KC_SEARCH, 0, 0, 0,
+             k_make_quads<<<(int)std::min<int64_t>((ne + 255) / 256, (int64_t)g->sms * 8), 256, 0, g->st>>>(
+                 U, g->uquad, (int)g->L0.n, ne));
+      CKL();
+    }
     TRY(launch_search2(g, dt, U, Uprev, pol, F, rect, &nblk));
     if (ns2 > 0) TRY(launch_search2(g, dt, U, Uprev, pol, F, rect, &nblk, s2strips, ns2));
   }
@@ -1614,7 +1691,7 @@ static hjb_status inject_all(hjb_grid* g) {
          k_coarse_assemble<D><<<(int)((Nc + 127) / 128), 128, 0, g->st>>>(lc.L, lc.C, g->mg_dt, pc, lc.Ainv));
   CKL();
   const size_t smem = (size_t)Nc * Nc * sizeof(double);
-  if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_coarse_invert, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (smem > 48 * 1024) CK(allow_smem((const void*)k_coarse_invert));
   LAUNCH(HJB_KC_COARSE, Nc, 16.0 * Nc * Nc, 2.0 * Nc * Nc * Nc, k_coarse_invert<<<1, 1024, smem, g->st>>>(lc.Ainv, (int)Nc));
   CKL();
   return HJB_OK;
@@ -1667,7 +1744,7 @@ static hjb_status galerkin_setup(hjb_grid* g, double dt, const uint8_t* policy) 
     CK(cudaMemsetAsync(lc.Ainv, 0, (size_t)Nc * Nc * sizeof(double), g->st));
     LAUNCH(HJB_KC_COARSE, Nc, 0, 0, k_gal_dense<<<(int)((Nc + 127) / 128), 128, 0, g->st>>>(lc.L, lc.gcol, lc.gval, lc.Ainv));
     const size_t smem = (size_t)Nc * Nc * sizeof(double);
-    if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_coarse_invert, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (smem > 48 * 1024) CK(allow_smem((const void*)k_coarse_invert));
     LAUNCH(HJB_KC_COARSE, Nc, 16.0 * Nc * Nc, 2.0 * Nc * Nc * Nc, k_coarse_invert<<<1, 1024, smem, g->st>>>(lc.Ainv, (int)Nc));
     CKL();
   }
@@ -2491,6 +2568,11 @@ extern "C" hjb_status hjb_cfl_rate(hjb_grid_t g, const uint8_t* policy, double* 
 }
 
 // ---------------------------------------------------------------------------- step
+static hjb_status implicit_pi(hjb_grid* g, double dt, const double* dprev, double* dU, uint8_t* dpol,
+                              const hjb_solve_params* sp, hjb_step_stats& S);
+static hjb_status nested_guess(hjb_grid* g, double dt, const double* dprev, double* dU, const hjb_solve_params* sp,
+                               hjb_step_stats* S);
+
 extern "C" hjb_status hjb_step(hjb_grid_t g, double dt, const double* U_prev, double* U, uint8_t* policy,
                                const double* psi, const hjb_solve_params* p, hjb_step_stats* out) {
   if (!g || !U_prev || !U) return fail(HJB_ERR_INVALID_ARG, "null argument");
@@ -2516,13 +2598,15 @@ extern "C" hjb_status hjb_step(hjb_grid_t g, double dt, const double* U_prev, do
     CK(cudaMemcpyAsync(g->stage_prev, U_prev, vb, h_prev ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st));
     dprev = g->stage_prev;
   }
-  if (sp->guess < HJB_GUESS_PREV || sp->guess > HJB_GUESS_EXTRAPOLATE)
+  if (sp->guess < HJB_GUESS_PREV || sp->guess > HJB_GUESS_NESTED)
     return fail(HJB_ERR_INVALID_ARG, "unknown initial-guess mode");
-  const int guess = (U == U_prev) ? HJB_GUESS_PREV : sp->guess;
+  // an in-place step has no U^{n-2} or caller's guess: it starts from U_prev (nested: refined from there)
+  const int guess = (U == U_prev && sp->guess != HJB_GUESS_NESTED) ? HJB_GUESS_PREV : sp->guess;
   if (h_U) {
     if (!g->stage_U) TRY(dalloc((void**)&g->stage_U, vb));
     dU = g->stage_U;
-    if (guess != HJB_GUESS_PREV) CK(cudaMemcpyAsync(dU, U, vb, cudaMemcpyHostToDevice, st));
+    if (guess == HJB_GUESS_GIVEN || guess == HJB_GUESS_EXTRAPOLATE)
+      CK(cudaMemcpyAsync(dU, U, vb, cudaMemcpyHostToDevice, st));
   }
   if (h_pol) {
     if (!g->stage_pol) TRY(dalloc((void**)&g->stage_pol, (size_t)g->N));
@@ -2536,7 +2620,7 @@ extern "C" hjb_status hjb_step(hjb_grid_t g, double dt, const double* U_prev, do
   }
   // a1: initial iterate (U_prev, the caller's guess, or the linear extrapolation 2 U_prev - U^{n-2}),
   // then boundary entries psi(t_n)
-  if (guess == HJB_GUESS_PREV && dU != dprev) {
+  if ((guess == HJB_GUESS_PREV || guess == HJB_GUESS_NESTED) && dU != dprev) {
     CK(cudaMemcpyAsync(dU, dprev, vb, cudaMemcpyDeviceToDevice, st));
   } else if (guess == HJB_GUESS_EXTRAPOLATE) {
     const double nn = (double)g->L0.n_own;
@@ -2574,6 +2658,32 @@ extern "C" hjb_status hjb_step(hjb_grid_t g, double dt, const double* U_prev, do
     if (out) *out = S;
     return result;
   }
+  if (guess == HJB_GUESS_NESTED) {
+    cudaEventRecord(g->ev[3], st);
+    TRY(nested_guess(g, dt, dprev, dU, sp, &S));
+    cudaEventRecord(g->ev[2], st);
+    CK(cudaEventSynchronize(g->ev[2]));
+    cudaEventElapsedTime(&ms, g->ev[3], g->ev[2]);
+    S.ms_nested += ms;
+  }
+  result = implicit_pi(g, dt, dprev, dU, dpol, sp, S);
+  S.n_levels = (int32_t)g->levels.size();
+  if (h_U) CK(cudaMemcpyAsync(U, dU, vb, cudaMemcpyDeviceToHost, st));
+  if (h_pol) CK(cudaMemcpyAsync(policy, dpol, (size_t)g->N, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (out) *out = S;
+  return result;
+}
+
+// The Howard loop of an implicit step from the iterate dU (psi(t_n) on its
+// boundary): policy improvement, stop test, policy evaluation, repeat.
+static hjb_status implicit_pi(hjb_grid* g, double dt, const double* dprev, double* dU, uint8_t* dpol,
+                              const hjb_solve_params* sp, hjb_step_stats& S) {
+  cudaStream_t st = g->st;
+  Level tmpl;
+  const Level& lv0 = fine_level(g, tmpl);
+  float ms;
+  hjb_status result = HJB_OK;
   bool last_exact = true;  // the last policy evaluation reached krylov_rtol
   for (int it = 1; it <= sp->max_pi; ++it) {
     hjb_pi_stats pis{};
@@ -2619,12 +2729,125 @@ extern "C" hjb_status hjb_step(hjb_grid_t g, double dt, const double* U_prev, do
     S.final_rres_inf = ss.rres_inf;
     if (s != HJB_OK) { result = s; break; }
   }
-  S.n_levels = (int32_t)g->levels.size();
-  if (h_U) CK(cudaMemcpyAsync(U, dU, vb, cudaMemcpyDeviceToHost, st));
-  if (h_pol) CK(cudaMemcpyAsync(policy, dpol, (size_t)g->N, cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  if (out) *out = S;
   return result;
+}
+
+// ---------------------------------------------------------------------------- nested iteration
+// The coarse grid of HJB_GUESS_NESTED (created on first use; fields re-injected after set_coeffs),
+// or nullptr when nesting does not apply (reading xxx).
+static hjb_status nested_child(hjb_grid* g, const hjb_solve_params* sp, hjb_grid** out) {
+  *out = nullptr;
+  const int m = sp->nested_coarsen;
+  if (m < 1 || m > 8 || g->R > 1 || g->bsamp || !g->have_coeffs) return HJB_OK;
+  const int64_t f = 1LL << m;
+  if ((g->n - 1) % f != 0) return HJB_OK;
+  const int64_t nc = (g->n - 1) / f + 1;
+  if (nc < std::max<int64_t>(5, sp->nested_min_n)) return HJB_OK;
+  const int D = g->D;
+  int64_t Nc = nc;
+  for (int d = 1; d < D; ++d) Nc *= nc;
+  const int np_sig = g->C0.sigma_scale ? g->P : 0, np_sn = g->C0.sigma_node ? g->P * D : 0,
+            np_bs = g->C0.b_scale ? 1 : 0, np_bn = g->C0.b_node ? D : 0, np_c = g->C0.c_node ? 1 : 0,
+            np_f = (g->Q > 0 && g->C0.f_feat) ? g->Q : 0;
+  const int nplanes = np_sig + np_sn + np_bs + np_bn + np_c + np_f;
+  if (g->child && g->child_m != m) {
+    hjb_grid_destroy(g->child);
+    g->child = nullptr;
+    cudaFree(g->child_fields);
+    cudaFree(g->child_U);
+    cudaFree(g->child_prev);
+    cudaFree(g->child_pol);
+    g->child_fields = g->child_U = g->child_prev = nullptr;
+    g->child_pol = nullptr;
+  }
+  if (!g->child) {
+    hjb_grid_desc d = g->desc;
+    d.n = nc;
+    d.rank = 0;
+    d.nranks = 1;
+    d.nccl_id = nullptr;
+    d.halo = 0;
+    TRY(hjb_grid_create(&d, &g->child));
+    g->child_m = m;
+    g->child_dirty = true;
+    if (nplanes > 0) TRY(dalloc((void**)&g->child_fields, (size_t)nplanes * Nc * sizeof(double)));
+    TRY(dalloc((void**)&g->child_U, (size_t)Nc * sizeof(double)));
+    TRY(dalloc((void**)&g->child_prev, (size_t)Nc * sizeof(double)));
+    TRY(dalloc((void**)&g->child_pol, (size_t)Nc));
+    CK(cudaMemsetAsync(g->child_pol, 0, (size_t)Nc, g->st));
+  }
+  hjb_grid* c = g->child;
+  c->prof_timing = g->prof_timing;
+  c->prof.timed = g->prof.timed;
+  if (g->child_dirty) {
+    const int nb = (int)std::min<int64_t>((Nc + 255) / 256, (int64_t)g->sms * 8);
+    double* dst = g->child_fields;
+    auto inj = [&](const double* src, int np) -> const double* {
+      if (!src || np == 0) return nullptr;
+      double* o = dst;
+      if (D == 2)
+        LAUNCH(HJB_KC_TRANSFER, Nc, 16.0 * np * Nc, 0,
+               k_nest_inject<2><<<nb, 256, 0, g->st>>>(g->n, nc, (int)f, src, g->N, o, Nc, np));
+      else
+        LAUNCH(HJB_KC_TRANSFER, Nc, 16.0 * np * Nc, 0,
+               k_nest_inject<3><<<nb, 256, 0, g->st>>>(g->n, nc, (int)f, src, g->N, o, Nc, np));
+      dst += (size_t)np * Nc;
+      return o;
+    };
+    hjb_coeffs cc{};
+    cc.sigma_dir = g->h_sd.data();
+    cc.b_dir = g->h_bd.data();
+    cc.c_ctrl = g->h_cc.data();
+    cc.f_basis = g->Q > 0 ? g->h_fb.data() : nullptr;
+    cc.f_ctrl = g->h_fc.data();
+    cc.sigma_scale = inj(g->C0.sigma_scale, np_sig);
+    cc.sigma_node = inj(g->C0.sigma_node, np_sn);
+    cc.b_scale = inj(g->C0.b_scale, np_bs);
+    cc.b_node = inj(g->C0.b_node, np_bn);
+    cc.c_node = inj(g->C0.c_node, np_c);
+    cc.f_feat = inj(g->C0.f_feat, np_f);
+    CKL();
+    TRY(hjb_set_coeffs(c, &cc));
+    g->child_dirty = false;
+  }
+  TRY(hjb_set_source(c, g->Q > 0 ? g->h_fb.data() : nullptr, g->h_fc.data()));  // f at t_n
+  *out = c;
+  return HJB_OK;
+}
+
+// dU (in: the iterate with psi(t_n) on its boundary) <- the prolonged solution of the step on the
+// nested coarse grid (itself started from its own nested grid), interior entries only
+static hjb_status nested_guess(hjb_grid* g, double dt, const double* dprev, double* dU, const hjb_solve_params* sp,
+                               hjb_step_stats* S) {
+  hjb_grid* c;
+  TRY(nested_child(g, sp, &c));
+  if (!c) return HJB_OK;
+  TRY(check_dt(c, dt));
+  const int64_t f = 1LL << g->child_m, nc = c->n;
+  const int64_t Nc = c->N;
+  const int nb = (int)std::min<int64_t>((Nc + 255) / 256, (int64_t)g->sms * 8);
+  const int D = g->D;
+  if (D == 2) {
+    LAUNCH(HJB_KC_TRANSFER, Nc, 16.0 * Nc, 0, k_nest_inject<2><<<nb, 256, 0, g->st>>>(g->n, nc, (int)f, dU, g->N, g->child_U, Nc, 1));
+    LAUNCH(HJB_KC_TRANSFER, Nc, 16.0 * Nc, 0, k_nest_inject<2><<<nb, 256, 0, g->st>>>(g->n, nc, (int)f, dprev, g->N, g->child_prev, Nc, 1));
+  } else {
+    LAUNCH(HJB_KC_TRANSFER, Nc, 16.0 * Nc, 0, k_nest_inject<3><<<nb, 256, 0, g->st>>>(g->n, nc, (int)f, dU, g->N, g->child_U, Nc, 1));
+    LAUNCH(HJB_KC_TRANSFER, Nc, 16.0 * Nc, 0, k_nest_inject<3><<<nb, 256, 0, g->st>>>(g->n, nc, (int)f, dprev, g->N, g->child_prev, Nc, 1));
+  }
+  CKL();
+  hjb_step_stats Sc{};
+  TRY(nested_guess(c, dt, g->child_prev, g->child_U, sp, &Sc));
+  const hjb_status r = implicit_pi(c, dt, g->child_prev, g->child_U, g->child_pol, sp, Sc);
+  if (r != HJB_OK && r != HJB_ERR_NOT_CONVERGED) return r;  // an unconverged coarse iterate is still a guess
+  S->nested_pi_iters += Sc.pi_iters + Sc.nested_pi_iters;
+  const int64_t Nf = g->N;
+  const int nbf = (int)std::min<int64_t>((Nf + 255) / 256, (int64_t)g->sms * 8);
+  if (D == 2)
+    LAUNCH(HJB_KC_TRANSFER, Nf, 8.0 * Nf + 8.0 * Nc, 0, k_nest_prolong<2><<<nbf, 256, 0, g->st>>>(g->n, nc, (int)f, g->child_U, dU));
+  else
+    LAUNCH(HJB_KC_TRANSFER, Nf, 8.0 * Nf + 8.0 * Nc, 0, k_nest_prolong<3><<<nbf, 256, 0, g->st>>>(g->n, nc, (int)f, g->child_U, dU));
+  CKL();
+  return HJB_OK;
 }
 
 // ---------------------------------------------------------------------------- API: instrumentation
@@ -2635,6 +2858,7 @@ extern "C" hjb_status hjb_profile_reset(hjb_grid_t g, int32_t time_kernels) {
   g->prof = hjb_profile{};
   g->prof_timing = time_kernels != 0;
   g->prof.timed = g->prof_timing ? 1 : 0;
+  if (g->child) TRY(hjb_profile_reset(g->child, time_kernels));
   return HJB_OK;
 }
 
@@ -2644,5 +2868,20 @@ extern "C" hjb_status hjb_profile_read(hjb_grid_t g, hjb_profile* out) {
   prof_drain(g);
   CK(cudaStreamSynchronize(g->st));
   *out = g->prof;
+  if (g->child) {  // the nested coarse solves' launches count as this grid's
+    hjb_profile c;
+    TRY(hjb_profile_read(g->child, &c));
+    for (int k = 0; k < HJB_KC_COUNT; ++k) {
+      out->launches[k] += c.launches[k];
+      out->calls[k] += c.calls[k];
+      out->ms[k] += c.ms[k];
+      out->bytes[k] += c.bytes[k];
+      out->flops[k] += c.flops[k];
+      out->nodes[k] += c.nodes[k];
+    }
+    out->total_launches += c.total_launches;
+    out->graph_launches += c.graph_launches;
+    out->graph_kernels += c.graph_kernels;
+  }
   return HJB_OK;
 }

@@ -41,6 +41,33 @@ __global__ void __launch_bounds__(256) k_make_pairs(const double* __restrict__ U
   }
 }
 
+// Q4[i] = (U[i], U[i+1], U[i+n], U[i+n+1]): the four corners of the cell whose lower-left node is i,
+// 32 bytes, so one 256-bit load (LDG.E.ENL2.256 on sm_100a) fetches a whole bilinear tap.  Entries
+// whose corners leave the local array hold 0 (never read: deep nodes' cells are interior).
+__global__ void __launch_bounds__(256) k_make_quads(const double* __restrict__ U, double4* __restrict__ Q4, int n,
+                                                    int64_t ne) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ne; i += (int64_t)gridDim.x * blockDim.x) {
+    const double a = __ldg(U + i);
+    const double b = (i + 1 < ne) ? __ldg(U + i + 1) : 0.0;
+    const double c = (i + n < ne) ? __ldg(U + i + n) : 0.0;
+    const double d = (i + n + 1 < ne) ? __ldg(U + i + n + 1) : 0.0;
+    double4* q = Q4 + i;
+    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(q), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+  }
+}
+
+// one 256-bit read-only load of a cell's four corners
+__device__ __forceinline__ double4 ld_quad(const double4* q) {
+  double4 r;
+  asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w) : "l"(q));
+  return r;
+}
+__device__ __forceinline__ const double4* quad_at(const double4* base, int off) {
+  const double4* r;
+  asm("mad.wide.s32 %0, %1, 32, %2;" : "=l"(r) : "r"(off), "l"(base));
+  return r;
+}
+
 // bilinear value from the pairs (v00, v10) of row c1 and (v01, v11) of row c1+1 at fractions s
 __device__ __forceinline__ double interp_pairs(const double2 lo, const double2 hi, double s0, double s1) {
   const double a = fma(s0, lo.y - lo.x, lo.x);
@@ -123,10 +150,19 @@ constexpr int kSuperCols = HJB_SUPER_COLS;  // tile columns per super-column (16
 // STRIP: a boundary-layer strip of the deep rectangle's ring: per control, a warp whose endpoints are
 // all strictly inside runs the lean arithmetic above; otherwise the control takes the general
 // truncated geometry (row_geometry, exact-psi aware) for the whole warp
-template <int P, int Q, bool STRIP = false>
+// QUADS (deep rectangle only): the taps come from the corner copy Q4 (k_make_quads), one 256-bit load
+// per endpoint, and an untruncated pair is combined before interpolating: the minus endpoint's cell
+// is the plus endpoint's mirrored through the node and its fractions are 1 - s, so
+//   I(x+o) + I(x-o) = bilinear(s; P00 + M11, P10 + M01, P01 + M10, P11 + M00)
+// (P = the plus cell's corners, M = the minus cell's): 4 loads instead of 16 per (node, control) and
+// 11 instead of 14 fp64 operations per pair.
+// KU > 0: the control loop is fully unrolled for exactly KU = C.K controls, so every control-table
+// entry is a constant-bank operand of its instruction (no LDC per entry).
+template <int P, int Q, bool STRIP = false, bool QUADS = false, int KU = 0>
 __global__ void __launch_bounds__(kS2T, HJB_SEARCH2_MINB) k_search_deep2(LevelDev L, CoefDev C, double dt,
                                                                         const double* __restrict__ U,
                                                                         const double2* __restrict__ UP,
+                                                                        const double4* __restrict__ Q4,
                                                                         const double* __restrict__ Uprev,
                                                                         uint8_t* __restrict__ pol,
                                                                         double* __restrict__ F, double* partial,
@@ -178,10 +214,11 @@ __global__ void __launch_bounds__(kS2T, HJB_SEARCH2_MINB) k_search_deep2(LevelDe
                                              // wide multiply-add per load address)
       const double* u0 = U + nd.loc;
       const double* u1 = u0 + n;
+      const double4* q4 = Q4 + nd.loc;
       double best = INFINITY, fbest = 0.0;
       int arg = 0;
-#pragma unroll kS2Unroll
-      for (int a = 0; a < C.K; ++a) {
+#pragma unroll(KU > 0 ? KU : kS2Unroll)
+      for (int a = 0; a < (KU > 0 ? KU : C.K); ++a) {
 #if HJB_SEARCH2_SYNC
         __syncwarp();
         if ((a & (HJB_SEARCH2_SYNC - 1)) == 0) __syncthreads();  // keep the CTA's 4 lines in lockstep
@@ -212,6 +249,23 @@ __global__ void __launch_bounds__(kS2T, HJB_SEARCH2_MINB) k_search_deep2(LevelDe
           }
         }
         double acc = 0.0;
+        if constexpr (QUADS) {
+#pragma unroll
+          for (int p = 0; p < P; ++p) {
+            int fl0, fl1;
+            double s0, s1;
+            split_floor(ksc[p] * t[T::SD + 2 * p], fl0, s0);
+            split_floor(ksc[p] * t[T::SD + 2 * p + 1], fl1, s1);
+            const int off = fl1 * n + fl0;
+            const int offm = -off - n - 1;
+            HJB_ASSERT(nd.loc + off >= 0 && nd.loc + off + n + 1 < L.local_elems);
+            HJB_ASSERT(nd.loc + offm >= 0 && nd.loc + offm + n + 1 < L.local_elems);
+            const double4 pq = ld_quad(quad_at(q4, off)), mq = ld_quad(quad_at(q4, offm));
+            const double a00 = pq.x + mq.w, a10 = pq.y + mq.z, a01 = pq.z + mq.y, a11 = pq.w + mq.x;
+            const double lo = fma(s0, a10 - a00, a00), hi = fma(s0, a11 - a01, a01);
+            acc = fma(t[T::W + p], fma(s1, hi - lo, lo), acc);
+          }
+        } else {
 #pragma unroll
         for (int p = 0; p < P; ++p) {
           int fl0, fl1;
@@ -227,6 +281,7 @@ __global__ void __launch_bounds__(kS2T, HJB_SEARCH2_MINB) k_search_deep2(LevelDe
           const double w = t[T::W + p];
           acc = fma(w, interp_pairs(p0, p1, s0, s1), acc);
           acc = fma(w, interp_pairs_mirror(m0, m1, s0, s1), acc);
+        }
         }
         {  // drift endpoint: within one cell of the node, its quadrant is a per-control fact
           const double o0 = kbs * t[T::BD], o1 = kbs * t[T::BD + 1];
@@ -260,6 +315,134 @@ __global__ void __launch_bounds__(kS2T, HJB_SEARCH2_MINB) k_search_deep2(LevelDe
         red[0] = fmax(red[0], (R == R) ? R : INFINITY);  // NaN -> inf (reported NONFINITE)
         red[1] += (old != arg) ? 1.0 : 0.0;
       }
+    }
+  }
+  block_reduce_store<2, kS2T>(red, partial, 0x1u);
+}
+
+
+// ------------------------------------------------------------------------------------------------
+// k_search_deep3: k_search_deep2 with the node-local part of every H^a hoisted out of the gather loop.
+// What bounds k_search_deep2 at cfg4 is latency (ncu r02_o: 16 resident warps per SM at 128
+// registers, issue 41 % active; each warp's control iteration waits ~1800 cycles on its dependent
+// gathers).  Per (node, control) H^a_j splits into
+//   H^a_j = sum_p w_p [I U(x + o_p) + I U(x - o_p)]                 (the gathers: two pairs)
+//         + [ f^a_j + w_d I U(x + o_d) + (c^a_j - wsum^a) U_j ]      (node-local: no gathers)
+// The bracket needs the node's features and its 3x3 neighbourhood (drift endpoint within one cell)
+// but no memory traffic: a prologue evaluates it for all K controls into shared memory (one slot per
+// thread and control), so the gather loop holds neither the features nor the neighbourhood in
+// registers (fewer registers -> more resident warps to hide the gather latency) and issues only the
+// pair taps (256-bit corner loads) plus one shared-memory read per control.  f at the argmin (for
+// F) is re-evaluated once per node after the loop.  Same formulas, different summation order:
+// identical policies except at near-ties (test_deep_kernels_match_general).
+#ifndef HJB_SEARCH3_MINB
+#define HJB_SEARCH3_MINB 6
+#endif
+template <int P, int Q>
+__global__ void __launch_bounds__(kS2T, HJB_SEARCH3_MINB) k_search_deep3(LevelDev L, CoefDev C, double dt,
+                                                                        const double* __restrict__ U,
+                                                                        const double4* __restrict__ Q4,
+                                                                        const double* __restrict__ Uprev,
+                                                                        uint8_t* __restrict__ pol,
+                                                                        double* __restrict__ F, double* partial,
+                                                                        SkipRect it, const __grid_constant__ STab tab,
+                                                                        const __grid_constant__ STabQuad quad) {
+  using T = STabLayout<P, Q>;
+  extern __shared__ double sbase[];  // [K][kS2T]: the node-local bracket of H^a
+  const int tid = threadIdx.y * kSBX + threadIdx.x;
+  double red[2] = {0.0, 0.0};
+  const int nk = box_lines(it);
+  const int n = L.n;
+  const int K = C.K;
+  const int tx = (it.c1 - it.c0 + kSBX - 1) / kSBX, ty = (nk + kS2Y - 1) / kS2Y;
+  const int ntiles = tx * ty;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int sc = t / (kSuperCols * ty);
+    const int scw = min(kSuperCols, tx - sc * kSuperCols);
+    const int tl = t - sc * kSuperCols * ty;
+    const int trow = tl / scw, tcol = sc * kSuperCols + (tl - trow * scw);
+    const int k0 = trow * kS2Y + threadIdx.y;
+    const int col0 = it.c0 + tcol * kSBX + threadIdx.x;
+    const bool valid = k0 < nk && col0 < it.c1;
+    const int k = valid ? k0 : trow * kS2Y, col = valid ? col0 : it.c0 + tcol * kSBX;
+    const int row = box_row<2>(L, it, k);
+    Node<2> nd;
+    node_at<2>(L, col, row, nd);
+    load_fields<2>(C, nd);
+    prefetch_ahead(L, U, nd.loc, col);
+    const double Uj = __ldg(U + nd.loc);
+    const double kbs = L.k2h * nd.bs;
+    {  // prologue: the node-local bracket for every control
+      double feat[Q > 0 ? Q : 1];
+#pragma unroll
+      for (int q = 0; q < Q; ++q) feat[q] = __ldg(C.f_feat + q * C.ld + nd.loc);
+      double nb[3][3];
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) nb[r][c] = (r == 1 && c == 1) ? Uj : __ldg(U + nd.loc + (r - 1) * n + (c - 1));
+      for (int a = 0; a < K; ++a) {
+        const double* tb = tab.v + a * T::S;
+        const double o0 = kbs * tb[T::BD], o1 = kbs * tb[T::BD + 1];
+        const double s0 = o0 - floor(o0), s1 = o1 - floor(o1);
+        double dv;
+        switch (quad.v[a]) {
+          case 0: dv = interp_pairs(make_double2(nb[1][1], nb[1][2]), make_double2(nb[2][1], nb[2][2]), s0, s1); break;
+          case 1: dv = interp_pairs(make_double2(nb[1][0], nb[1][1]), make_double2(nb[2][0], nb[2][1]), s0, s1); break;
+          case 2: dv = interp_pairs(make_double2(nb[0][1], nb[0][2]), make_double2(nb[1][1], nb[1][2]), s0, s1); break;
+          default: dv = interp_pairs(make_double2(nb[0][0], nb[0][1]), make_double2(nb[1][0], nb[1][1]), s0, s1); break;
+        }
+        double f = tb[T::FC];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) f = fma(tb[T::FB + q], feat[q], f);
+        const double cw = (nd.cn + tb[T::C]) - tb[T::WSUM];
+        sbase[a * kS2T + tid] = fma(cw, Uj, fma(tb[T::WD], dv, f));
+      }
+    }
+    double ksc[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) ksc[p] = L.kh * nd.sc[p];
+    const double4* q4 = Q4 + nd.loc;
+    double best = INFINITY;
+    int arg = 0;
+    for (int a = 0; a < K; ++a) {
+#if HJB_SEARCH2_SYNC
+      if ((a & (HJB_SEARCH2_SYNC - 1)) == 0) __syncthreads();  // the CTA's 4 lines in lockstep
+#endif
+      const double* tb = tab.v + a * T::S;
+      double acc = sbase[a * kS2T + tid];
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        int fl0, fl1;
+        double s0, s1;
+        split_floor(ksc[p] * tb[T::SD + 2 * p], fl0, s0);
+        split_floor(ksc[p] * tb[T::SD + 2 * p + 1], fl1, s1);
+        const int off = fl1 * n + fl0;
+        const int offm = -off - n - 1;
+        HJB_ASSERT(nd.loc + off >= 0 && nd.loc + off + n + 1 < L.local_elems);
+        HJB_ASSERT(nd.loc + offm >= 0 && nd.loc + offm + n + 1 < L.local_elems);
+        const double4 pq = ld_quad(quad_at(q4, off)), mq = ld_quad(quad_at(q4, offm));
+        const double a00 = pq.x + mq.w, a10 = pq.y + mq.z, a01 = pq.z + mq.y, a11 = pq.w + mq.x;
+        const double lo = fma(s0, a10 - a00, a00), hi = fma(s0, a11 - a01, a01);
+        acc = fma(tb[T::W + p], fma(s1, hi - lo, lo), acc);
+      }
+      if (acc < best) {  // strict: lowest index wins exact ties (reading iv)
+        best = acc;
+        arg = a;
+      }
+    }
+    if (valid) {
+      const double* tb = tab.v + arg * T::S;
+      double fbest = tb[T::FC];
+#pragma unroll
+      for (int q = 0; q < Q; ++q) fbest = fma(tb[T::FB + q], __ldg(C.f_feat + q * C.ld + nd.loc), fbest);
+      const double Up = __ldg(Uprev + nd.loc);
+      const double R = fabs(Uj - Up - dt * best);
+      const int old = pol[nd.loc];
+      pol[nd.loc] = (uint8_t)arg;
+      F[nd.loc] = fma(dt, fbest, Up);
+      red[0] = fmax(red[0], (R == R) ? R : INFINITY);  // NaN -> inf (reported NONFINITE)
+      red[1] += (old != arg) ? 1.0 : 0.0;
     }
   }
   block_reduce_store<2, kS2T>(red, partial, 0x1u);

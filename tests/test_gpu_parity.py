@@ -176,6 +176,61 @@ def test_step_parity_extrapolated_guess(name, mk, steps):
         assert err <= 1e-8, (name, s, err, st)
 
 
+@pytest.mark.parametrize("name,mk,steps,min_n", [
+    ("cfg0_nested", lambda: bj_config(0), 2, 9),            # 33 -> 9 (one nesting level)
+    ("cfg2_129_nested", lambda: bj_config(2, n=129), 2, 9),  # 129 -> 33 -> 9 (two levels)
+    ("cfg3_17_nested", lambda: bj_config(3, n=17), 1, 5),    # 17^3 -> 5^3
+])
+def test_step_parity_nested_guess(name, mk, steps, min_n):
+    """guess = HJB_GUESS_NESTED (reading xxx): the step is first solved on the grid coarsened 4x per
+    axis (recursively), its solution prolonged as the initial iterate.  Only the iteration count may
+    change: the step's discrete solution matches the oracle's march within the NS tolerance, and the
+    nested grids did run (nested_pi_iters > 0).  Also with an in-place device step (U = U_prev)."""
+    from paper_1605_04821_b200 import _lib
+    torch = require_gpu()
+    p = mk()
+    for inplace in (False, True):
+        g, _ = setup(p)
+        U = to_dev(p.g(p.all_idx()), torch)
+        U2 = U if inplace else torch.empty_like(U)
+        pol = torch.zeros(p.N, dtype=torch.uint8, device="cuda")
+        Uo = p.g(p.all_idx())
+        for s in range(1, steps + 1):
+            t = s * p.dt
+            fb, fc = p.f_tables(t)
+            g.set_source(fb, fc)
+            st = g.step(p.dt, U, U2, pol, to_dev(p.psi(t, p.boundary_idx()), torch),
+                        guess=_lib.HJB_GUESS_NESTED, nested_min_n=min_n)
+            assert st["nested_pi_iters"] > 0, st
+            U, U2 = U2, U
+            Uo, _, _ = howard_step(p, Uo, t, p.dt)
+            err = np.abs(U.cpu().numpy() - Uo).max() / max(1.0, np.abs(Uo).max())
+            assert err <= 1e-8, (name, inplace, s, err, st)
+            assert st["final_rres"] <= 1e-12 or st["final_R"] <= 1e-10
+        g.close()
+
+
+def test_nested_guess_falls_back_without_a_coarse_grid():
+    """The nested grid would fall below nested_min_n (or n - 1 is not divisible by 2^nested_coarsen):
+    HJB_GUESS_NESTED is HJB_GUESS_PREV (no nested iterations, identical result)."""
+    from paper_1605_04821_b200 import _lib
+    torch = require_gpu()
+    p = bj_config(2, n=65, K=7)             # nested grid 17 < nested_min_n = 33
+    out = []
+    for guess in (_lib.HJB_GUESS_PREV, _lib.HJB_GUESS_NESTED):
+        g, _ = setup(p)
+        U = to_dev(p.g(p.all_idx()), torch)
+        U2 = torch.empty_like(U)
+        pol = torch.zeros(p.N, dtype=torch.uint8, device="cuda")
+        fb, fc = p.f_tables(p.dt)
+        g.set_source(fb, fc)
+        st = g.step(p.dt, U, U2, pol, to_dev(p.psi(p.dt, p.boundary_idx()), torch), guess=guess, nested_min_n=33)
+        assert st["nested_pi_iters"] == 0
+        out.append(U2.cpu().numpy())
+        g.close()
+    assert np.array_equal(out[0], out[1])
+
+
 def test_step_parity_cfg1_first_step():
     p = bj_config(1)
     Ug, polg, stats = _gpu_march(p, 1)          # library defaults (inexact early evaluations)
@@ -294,7 +349,7 @@ def test_deep_kernels_match_general(name, mk, monkeypatch):
     deep box, and over the whole interior with the general geometry) and the TMA-windowed search
     tiles give bit-identical search results and operator applications to the general kernels
     everywhere (HJB_NO_DEEP / HJB_WIN=0,1,2 / HJB_TMA=1 / HJB_NO_SEARCH2=1 select them).  The 2D
-    L1-lean deep search k_search_deep2 (hjb_search2.cuh, the default where it applies) uses
+    L1-lean deep searches k_search_deep2 (hjb_search2.cuh, the default where it applies) / k_search_deep3 use
     equivalent formulations with their own rounding: identical policies except at near-ties (both
     controls within the oracle's 1e-12 rounding window, reading iv), F and R within rounding."""
     torch = require_gpu()
@@ -304,14 +359,21 @@ def test_deep_kernels_match_general(name, mk, monkeypatch):
     U = Uprev + 0.05 * rng.uniform(-1, 1, size=p.N)
     x = random_vector(p)
     out = {}
-    for mode in ("general", "deep_legacy", "deep_win", "full_win", "deep_tma", "deep2"):
-        for k in ("HJB_NO_DEEP", "HJB_NO_TMA", "HJB_TMA", "HJB_WIN", "HJB_NO_SEARCH2"):
+    for mode in ("general", "deep_legacy", "deep_win", "full_win", "deep_tma", "deep3", "deep2_quads", "deep2"):
+        for k in ("HJB_NO_DEEP", "HJB_NO_TMA", "HJB_TMA", "HJB_WIN", "HJB_NO_SEARCH2", "HJB_QUADS",
+                  "HJB_SEARCH3"):
             monkeypatch.delenv(k, raising=False)
         if mode == "general":
             monkeypatch.setenv("HJB_NO_DEEP", "1")
         elif mode == "deep_legacy":
             monkeypatch.setenv("HJB_WIN", "0")
             monkeypatch.setenv("HJB_NO_SEARCH2", "1")
+        elif mode == "deep3":
+            monkeypatch.setenv("HJB_WIN", "0")
+            monkeypatch.setenv("HJB_SEARCH3", "1")
+        elif mode == "deep2_quads":
+            monkeypatch.setenv("HJB_WIN", "0")
+            monkeypatch.setenv("HJB_QUADS", "1")
         elif mode == "deep2":
             monkeypatch.setenv("HJB_WIN", "0")
         elif mode == "deep_win":
@@ -334,22 +396,25 @@ def test_deep_kernels_match_general(name, mk, monkeypatch):
         assert np.array_equal(out["general"][1], out[m][1]), m
         assert out["general"][2] == out[m][2], m
         assert np.array_equal(out["general"][3], out[m][3]), m
-    # k_search_deep2: near-tie aware comparison against the oracle's rounding window
-    pg, pd = out["general"][0].astype(np.int64), out["deep2"][0].astype(np.int64)
-    inter = Geometry.of(p).interior_idx()
-    diff = inter[pg[inter] != pd[inter]]
-    assert diff.size <= max(10, inter.size // 1000), diff.size
-    if diff.size:
-        f = p.fields(diff)
-        Ha, Sa, _ = hamiltonian(p, diff, pg[diff], U, p.dt, f)
-        Hb, Sb, _ = hamiltonian(p, diff, pd[diff], U, p.dt, f)
-        assert np.all(np.abs(Ha - Hb) <= 1e-12 * np.maximum(Sa, Sb)), np.abs(Ha - Hb).max()
-    same = inter[pg[inter] == pd[inter]]
-    Fg, Fd = out["general"][1][same], out["deep2"][1][same]
-    assert np.abs(Fg - Fd).max(initial=0.0) <= 1e-13 * max(1.0, np.abs(Fg).max())
-    Rg, Rd = out["general"][2]["R_max"], out["deep2"][2]["R_max"]
-    assert abs(Rg - Rd) <= 1e-12 * max(1.0, abs(Rg)), (Rg, Rd)
-    assert np.array_equal(out["general"][3], out["deep2"][3])      # the apply does not use it
+    # k_search_deep2 (default; 256-bit corner-copy taps with HJB_QUADS=1) and k_search_deep3
+    # (HJB_SEARCH3=1: node-local bracket hoisted to shared memory): near-tie aware comparison against
+    # the oracle's rounding window
+    for m in ("deep3", "deep2_quads", "deep2"):
+        pg, pd = out["general"][0].astype(np.int64), out[m][0].astype(np.int64)
+        inter = Geometry.of(p).interior_idx()
+        diff = inter[pg[inter] != pd[inter]]
+        assert diff.size <= max(10, inter.size // 1000), (m, diff.size)
+        if diff.size:
+            f = p.fields(diff)
+            Ha, Sa, _ = hamiltonian(p, diff, pg[diff], U, p.dt, f)
+            Hb, Sb, _ = hamiltonian(p, diff, pd[diff], U, p.dt, f)
+            assert np.all(np.abs(Ha - Hb) <= 1e-12 * np.maximum(Sa, Sb)), (m, np.abs(Ha - Hb).max())
+        same = inter[pg[inter] == pd[inter]]
+        Fg, Fd = out["general"][1][same], out[m][1][same]
+        assert np.abs(Fg - Fd).max(initial=0.0) <= 1e-13 * max(1.0, np.abs(Fg).max()), m
+        Rg, Rd = out["general"][2]["R_max"], out[m][2]["R_max"]
+        assert abs(Rg - Rd) <= 1e-12 * max(1.0, abs(Rg)), (m, Rg, Rd)
+        assert np.array_equal(out["general"][3], out[m][3]), m      # the apply does not use it
 
 
 @pytest.mark.parametrize("name,mk", [("cfg1", lambda: bj_config(1)), ("cfg2_513", lambda: bj_config(2, n=513)),
