@@ -68,6 +68,7 @@ def parse():
                     help="steps 1..K of a march start from the nested coarse solve (HJB_GUESS_NESTED); "
                          "later steps extrapolate in time; 0 = never nested")
     ap.add_argument("--nested-min-n", type=int, default=None, help="HJB_GUESS_NESTED: smallest nested grid")
+    ap.add_argument("--nested-coarsen", type=int, default=None, help="HJB_GUESS_NESTED: 2^m coarsening per axis")
     ap.add_argument("--stats-jsonl", default=None,
                     help="write one JSON line of hjb_step_stats per timed step (SURVEY §5 metrics)")
     return ap.parse_args()
@@ -276,6 +277,8 @@ def run_b200(args):
 
     if args.nested_min_n is not None:
         skw["nested_min_n"] = args.nested_min_n
+    if args.nested_coarsen is not None:
+        skw["nested_coarsen"] = args.nested_coarsen
 
     def guess_of(si):        # initial iterate of step si (the fixed point does not depend on it)
         if si <= args.nested_upto:

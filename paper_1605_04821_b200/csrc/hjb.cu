@@ -172,6 +172,17 @@ struct hjb_grid {
   double2* upair = nullptr;   // (U_i, U_{i+1}) pair copy of the searched U (k_search_deep2)
   double4* uquad = nullptr;   // cell-corner copy of the searched U (k_search_deep2<..., QUADS>)
   bool search3 = false;       // k_search_deep3 on the deep rectangle (opt-in, HJB_SEARCH3=1)
+  bool search2p = false;      // k_search_deep2p (software-pipelined) on the deep rectangle
+  // halo exchange overlapped with the rows that do not read halos (nranks > 1, halo_begin): the
+  // exchange runs on xst; the operator launches the inner band first, waits on xev[1], then the
+  // edge bands
+  cudaStream_t xst = nullptr;
+  cudaEvent_t xev[2] = {nullptr, nullptr};
+  struct {
+    bool pending = false;
+    int64_t H = 0;
+    bool lo = false, hi = false;  // a neighbour below / above (its halo rows are in flight)
+  } ovl;
   // nested iteration (HJB_GUESS_NESTED, hjb_nested.cuh): the same problem on the grid coarsened
   // 2^child_m times per axis, its fields injected from this grid's
   hjb_grid* child = nullptr;
@@ -299,7 +310,10 @@ static cudaError_t allow_smem(const void* fn) {
   int dev = 0, optin = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+  cudaFuncAttributes fa{};
+  cudaError_t e = cudaFuncGetAttributes(&fa, fn);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes);
   if (e == cudaSuccess) done[fn] = true;
   return e;
 }
@@ -383,8 +397,10 @@ static LevelDev full_level(int D, int64_t n, double lo, double hi, double k, dou
 
 // ---------------------------------------------------------------------------- communication
 // halo exchange of `rows` rows each side of a slab-level array x (no-op for one rank / replicated)
+static void halo_end(hjb_grid* g);
 static hjb_status halo_exchange(hjb_grid* g, const Level& lv, double* x, int64_t rows) {
   if (g->R == 1 || lv.replicated || rows <= 0) return HJB_OK;
+  if (g->st != g->xst) halo_end(g);
   const int64_t re = lv.L.row_elems, lr0 = lv.L.local_row0;
   const int64_t r0 = lv.r0s[g->rank], r1 = lv.r1s[g->rank];
   Msg m[2];
@@ -395,6 +411,35 @@ static hjb_status halo_exchange(hjb_grid* g, const Level& lv, double* x, int64_t
   std::string err;
   if (g->comm->exchange(g->st, m, nm, &err) != cudaSuccess)
     return fail(g->desc.comm == HJB_COMM_NCCL ? HJB_ERR_NCCL : HJB_ERR_CUDA, "halo exchange: " + err);
+  return HJB_OK;
+}
+
+// the stream waits for a halo exchange started by halo_begin
+static void halo_end(hjb_grid* g) {
+  if (!g->ovl.pending) return;
+  cudaStreamWaitEvent(g->st, g->xev[1], 0);
+  g->ovl.pending = false;
+}
+
+// Start the halo exchange of x on the exchange stream and return: the next launch_operator runs
+// the rows that read no halo row while the rows travel, then waits (halo_end) and runs the edge
+// rows.  Falls back to the blocking exchange without a second stream or while capturing a graph.
+static hjb_status halo_begin(hjb_grid* g, const Level& lv, double* x, int64_t rows) {
+  if (g->R == 1 || lv.replicated || rows <= 0) return HJB_OK;
+  halo_end(g);
+  if (!g->xst || g->capturing) return halo_exchange(g, lv, x, rows);
+  cudaEventRecord(g->xev[0], g->st);                // x is final on the compute stream
+  cudaStreamWaitEvent(g->xst, g->xev[0], 0);
+  cudaStream_t st = g->st;
+  g->st = g->xst;  // the exchange is enqueued on the exchange stream
+  const hjb_status r = halo_exchange(g, lv, x, rows);
+  g->st = st;
+  if (r != HJB_OK) return r;
+  cudaEventRecord(g->xev[1], g->xst);
+  g->ovl.pending = true;
+  g->ovl.H = rows;
+  g->ovl.lo = g->rank > 0;
+  g->ovl.hi = g->rank + 1 < g->R;
   return HJB_OK;
 }
 
@@ -568,6 +613,44 @@ static void launch_operator(hjb_grid* g, const LevelDev& L, const CoefDev& C, in
   const bool has_deep = rect.c1 > rect.c0 && rect.r1 > rect.r0;
   SkipRect strips[6];
   const int ns = ring_strips(full, rect, strips);
+  // pieces in launch order: with a halo exchange in flight (halo_begin), first every piece's band of
+  // slab rows that reads no halo row, then (after the exchange) the edge bands
+  SkipRect pc[2][3 * 7];
+  bool pdeep[2][3 * 7];
+  int npc[2] = {0, 0};
+  {
+    int64_t lo = 0, hi = 1 << 30;  // slab-axis rows (loop coordinates) reading no halo row
+    const bool split = g->ovl.pending;
+    if (split) {
+      const int64_t rows_own = D == 2 ? L.nrows : L.nrows / std::max(1, L.nI);
+      lo = g->ovl.lo ? g->ovl.H : 0;
+      hi = rows_own - (g->ovl.hi ? g->ovl.H : 0);
+      if (hi <= lo) {  // a thin slab: no inner band
+        halo_end(g);
+        lo = 0;
+        hi = 1 << 30;
+      }
+    }
+    auto add = [&](int ph, const SkipRect& r, int64_t a, int64_t b, bool deep) {
+      SkipRect q = r;
+      q.r0 = (int)std::max<int64_t>(r.r0, a);
+      q.r1 = (int)std::min<int64_t>(r.r1, b);
+      if (q.r1 > q.r0 && q.c1 > q.c0) {
+        pc[ph][npc[ph]] = q;
+        pdeep[ph][npc[ph]++] = deep;
+      }
+    };
+    for (int k = 0; k <= ns; ++k) {
+      const bool deep = (k == ns);
+      if (deep && !has_deep) break;
+      const SkipRect& r = deep ? rect : strips[k];
+      add(0, r, lo, hi, deep);
+      if (g->ovl.pending) {
+        add(1, r, 0, lo, deep);
+        add(1, r, hi, 1 << 30, deep);
+      }
+    }
+  }
 #define OPL1(PP, M, ND, DP, RR)                                                                             \
   do {                                                                                                      \
     const LevelDev LL = shape_of(L, RR);                                                                    \
@@ -581,8 +664,13 @@ static void launch_operator(hjb_grid* g, const LevelDev& L, const CoefDev& C, in
 #define OPLP(PP, M, ND)                                           \
   do {                                                            \
     int nb = 0;                                                   \
-    for (int k = 0; k < ns; ++k) OPL1(PP, M, ND, false, strips[k]); \
-    if (has_deep) OPL1(PP, M, ND, true, rect);                    \
+    for (int ph = 0; ph < 2; ++ph) {                              \
+      if (ph == 1) halo_end(g);                                   \
+      for (int k = 0; k < npc[ph]; ++k) {                         \
+        if (pdeep[ph][k]) OPL1(PP, M, ND, true, pc[ph][k]);       \
+        else OPL1(PP, M, ND, false, pc[ph][k]);                   \
+      }                                                           \
+    }                                                             \
     g->nblk_last = nb;                                            \
   } while (0)
 #define OPL(M, ND)                                                                                          \
@@ -764,6 +852,9 @@ extern "C" hjb_status hjb_grid_destroy(hjb_grid_t g) {
   cudaFree(g->d_flag);
   agmg_free(g);
   if (g->cap_st) cudaStreamDestroy(g->cap_st);
+  if (g->xst) cudaStreamDestroy(g->xst);
+  for (auto& e : g->xev)
+    if (e) cudaEventDestroy(e);
   cudaFree(g->S);
   cudaFree(g->pol_int);
   cudaFree(g->stage_pol);
@@ -867,6 +958,10 @@ extern "C" hjb_status hjb_grid_create(const hjb_grid_desc* d, hjb_grid_t* out) {
     return fail(HJB_ERR_OOM, "pinned alloc");
   }
   for (auto& e : g->ev) cudaEventCreate(&e);
+  if (g->R > 1 && !getenv("HJB_NO_OVERLAP")) {
+    cudaStreamCreateWithFlags(&g->xst, cudaStreamNonBlocking);
+    for (auto& e : g->xev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  }
   for (auto& e : g->pev) cudaEventCreate(&e);
   cudaError_t e = cudaStreamSynchronize(g->st);
   if (e != cudaSuccess) {
@@ -1213,14 +1308,16 @@ static const Level& fine_level(hjb_grid* g, Level& tmp) {
   return tmp;
 }
 
-// a const caller array whose halo rows must be filled: copy into scratch first (nranks > 1)
+static hjb_status halo_begin(hjb_grid* g, const Level& lv, double* x, int64_t rows);
+// a const caller array whose halo rows must be filled: copy into scratch first (nranks > 1); the
+// exchange is left in flight (halo_begin) for the launch_operator that follows
 static hjb_status halo_input(hjb_grid* g, const double* x, const double** out) {
   *out = x;
   if (g->R == 1) return HJB_OK;
   if (!g->scratch) TRY(dalloc((void**)&g->scratch, (size_t)g->N * sizeof(double)));
   CK(cudaMemcpyAsync(g->scratch, x, (size_t)g->N * sizeof(double), cudaMemcpyDeviceToDevice, g->st));
   Level tmp;
-  TRY(halo_exchange(g, fine_level(g, tmp), g->scratch, g->lay.halo));
+  TRY(halo_begin(g, fine_level(g, tmp), g->scratch, g->lay.halo));
   *out = g->scratch;
   return HJB_OK;
 }
@@ -1231,7 +1328,7 @@ static hjb_status halo_input(hjb_grid* g, const double* x, const double** out) {
 // per-control facts), drift endpoints within one cell, table entries either 0 or far from underflow
 static bool search2_ok(hjb_grid* g) {
   const int P = g->P, Q = g->Q, K = g->K;
-  const int S = 2 * P + 4 + Q + P + 2;
+  const int S = 2 * P + 4 + Q + P + 5;  // STabLayout<P, Q>::S
   if (g->D != 2 || !(Q == 1 || Q == 2 || Q == 8) || K * S > kSTabN || K > 256) return false;
   if (g->C0.sigma_node || g->C0.b_node || !g->reach_ok || !g->drift_reg) return false;
   for (int p = 0; p < P; ++p)
@@ -1256,6 +1353,21 @@ static void search2_launch(hjb_grid* g, const LevelDev& LL, double dt, const dou
              g->L0, STRIP ? coef_u(g) : g->C0, dt, U, g->upair, g->uquad, Uprev, pol, F, g->partial + 2 * *nblk, rect,
              tab, quad));
   *nblk += nb;
+}
+
+// the deep rectangle with the software-pipelined k_search_deep2p
+template <int P, int Q>
+static hjb_status search2p_launch(hjb_grid* g, const LevelDev& LL, double dt, const double* U, const double* Uprev,
+                                  uint8_t* pol, double* F, const SkipRect& rect, const STab& tab, const STabQuad& quad,
+                                  int* nblk) {
+  const void* fn = (const void*)k_search_deep2p<P, Q>;
+  const int64_t tiles = (int64_t)((LL.nI + kSBX - 1) / kSBX) * ((LL.nrows + kS2Y - 1) / kS2Y);
+  const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, std::min<int64_t>((int64_t)occupancy_of(fn, 0, kS2T) * g->sms, kMaxBlocks)));
+  LAUNCH(HJB_KC_SEARCH, 0, 0, 0,
+         k_search_deep2p<P, Q><<<nb, dim3(kSBX, kS2Y), 0, g->st>>>(g->L0, g->C0, dt, U, Uprev, pol, F,
+                                                                   g->partial + 2 * *nblk, rect, tab, quad));
+  *nblk += nb;
+  return HJB_OK;
 }
 
 // the deep rectangle with k_search_deep3 (node-local bracket staged in shared memory)
@@ -1301,6 +1413,9 @@ static void search2_tables(hjb_grid* g, STab& tab, STabQuad& quad) {
     t[T::FC] = g->h_fc[a];
     for (int q = 0; q < Q; ++q) t[T::FB + q] = g->h_fb[(size_t)a * Q + q];
     quad.v[a] = (bd[a * 2] < 0.0 ? 1 : 0) | (bd[a * 2 + 1] < 0.0 ? 2 : 0);
+    t[T::CMW] = t[T::C] - t[T::WSUM];
+    t[T::DQ] = bd[a * 2] < 0.0 ? 1.0 : 0.0;
+    t[T::DQ + 1] = bd[a * 2 + 1] < 0.0 ? 1.0 : 0.0;
   }
 }
 
@@ -1314,7 +1429,9 @@ static hjb_status launch_search2(hjb_grid* g, double dt, const double* U, const 
 #define S2(PP, QQ)                                                                                 \
   do {                                                                                             \
     search2_tables<PP, QQ>(g, tab, quad);                                                          \
-    if (!strips && g->uquad && g->search3)                                                         \
+    if (!strips && g->search2p)                                                                    \
+      TRY((search2p_launch<PP, QQ>(g, LL, dt, U, Uprev, pol, F, rect, tab, quad, nblk)));          \
+    else if (!strips && g->uquad && g->search3)                                                    \
       TRY((search3_launch<PP, QQ>(g, LL, dt, U, Uprev, pol, F, rect, tab, quad, nblk)));           \
     else if (!strips && g->uquad && g->K == 32 && PP == 2 && getenv("HJB_KUNROLL"))                \
       search2_launch<PP, QQ, false, true, 32>(g, LL, dt, U, Uprev, pol, F, rect, tab, quad, nblk); \
@@ -1342,6 +1459,7 @@ static hjb_status launch_search2(hjb_grid* g, double dt, const double* U, const 
 // U's halo rows must already be exchanged
 static hjb_status policy_update_dev(hjb_grid* g, double dt, const double* U, const double* Uprev, uint8_t* pol,
                                     double* F, hjb_pi_stats* out) {
+  halo_end(g);  // the search kernels take no row split: U's halo rows must have arrived
   const double nodes = (double)g->L0.n_own;
   const double bpn = 8.0 + 8.0 + 1.0 + 1.0 + 8.0 + 8.0 * g->Q + 8.0 * g->nplanes0;
   const double fpn = g->K * ((2.0 * g->P + 1.0) * (1 << g->D) * 2.0 + 2.0 * g->Q + 4.0);
@@ -1441,6 +1559,7 @@ static hjb_status policy_update_dev(hjb_grid* g, double dt, const double* U, con
     // opt-in variants (measured at cfg4): 256-bit corner-copy taps (HJB_QUADS=1) and the
     // hoisted node-local bracket in shared memory (HJB_SEARCH3=1, needs the corner copy)
     g->search3 = getenv("HJB_SEARCH3") && (size_t)g->K * kS2T * sizeof(double) <= 200 * 1024;
+    g->search2p = !g->search3 && !getenv("HJB_QUADS") && !getenv("HJB_NO_SEARCH2P");
     if (getenv("HJB_QUADS") || g->search3) {  // cell-corner copy of U for the 256-bit tap loads
       if (!g->uquad) TRY(dalloc((void**)&g->uquad, (size_t)g->N * sizeof(double4)));
       const int64_t ne = g->N;
@@ -1830,6 +1949,7 @@ static void level_sweep(hjb_grid* g, size_t l, int mode, const double* x, const 
   const uint8_t* pol = (l == 0) ? g->mg_pol0 : lv.pol;
   const double dt = g->mg_dt, om = level_omega(g, l);
   if (g->galerkin && l >= 1) {
+    halo_end(g);
     const int64_t nn = (int64_t)lv.L.nI * lv.L.nrows;
     const int nb = (int)std::max<int64_t>(1, std::min<int64_t>((nn + 127) / 128, (int64_t)g->sms * 16));
     const double bytes = (8.0 * 3 + 12.0 * kGalW) * nn;
@@ -1914,11 +2034,11 @@ static hjb_status vcycle(hjb_grid* g, size_t l, const double* b, double* out) {
     launch_operator<D>(g, L, lv.C, OP_JACOBI0, 0, dt, om, pol, nullptr, b, bufs[cur], nullptr, fine);
   }
   for (int k = 1; k < npre; ++k) {
-    TRY(halo_exchange(g, lv, bufs[cur], lv.H));
+    TRY(halo_begin(g, lv, bufs[cur], lv.H));
     level_sweep<D>(g, l, jmode, bufs[cur], b, bufs[1 - cur]);
     cur = 1 - cur;
   }
-  TRY(halo_exchange(g, lv, bufs[cur], lv.H));
+  TRY(halo_begin(g, lv, bufs[cur], lv.H));
   level_sweep<D>(g, l, OP_RESID, bufs[cur], b, lv.res);
   Level& lc = g->levels[l + 1];
   TRY(halo_exchange(g, lv, lv.res, 1));
@@ -1945,7 +2065,7 @@ static hjb_status vcycle(hjb_grid* g, size_t l, const double* b, double* out) {
   const int gamma = (ipow(lc.L.n - 2, D) >= g->gamma_min) ? g->mg_gamma : 1;
   for (int k = 1; k < gamma && l + 2 < g->levels.size(); ++k) {  // W-cycle: revisit the coarse level
     const uint8_t* pc = lc.pol;
-    TRY(halo_exchange(g, lc, lc.x, lc.H));
+    TRY(halo_begin(g, lc, lc.x, lc.H));
     (void)pc;
     level_sweep<D>(g, l + 1, OP_RESID, lc.x, lc.b, lc.r2);
     TRY(vcycle<D>(g, l + 1, lc.r2, lc.e2));
@@ -1958,7 +2078,7 @@ static hjb_status vcycle(hjb_grid* g, size_t l, const double* b, double* out) {
   LAUNCH(HJB_KC_TRANSFER, L.n_own, 16.0 * L.n_own + 8.0 * lc.L.n_own, 4.0 * L.n_own,
          k_prolong_add<D><<<dims(g, L, (const void*)k_prolong_add<D>), dim3(kBX, kBY), 0, st>>>(L, lc.L, lc.x, bufs[cur]));
   for (int k = 0; k < npost; ++k) {
-    TRY(halo_exchange(g, lv, bufs[cur], lv.H));
+    TRY(halo_begin(g, lv, bufs[cur], lv.H));
     level_sweep<D>(g, l, jmode, bufs[cur], b, bufs[1 - cur]);
     cur = 1 - cur;
   }
@@ -2028,7 +2148,7 @@ static hjb_status bicgstab(hjb_grid* g, double dt, const uint8_t* pol, const dou
   double tol_iter = tol;  // target of the recursive residual (tightened if the max-norm stop fails)
   for (int restart = 0; restart < 6 && !converged; ++restart) {
     // r = F - A x ; rhat = r ; p = r
-    TRY(halo_exchange(g, lv0, x, H));
+    TRY(halo_begin(g, lv0, x, H));
     launch_operator<D>(g, L, CUx, OP_RESID, 0, dt, 0.0, pol, x, F, g->r, nullptr);
     LAUNCH(HJB_KC_VECTOR, L.n_own, 24.0 * L.n_own, 2.0 * L.n_own,
            k_bicg_init<D><<<dims(g, L, (const void*)k_bicg_init<D>), dim3(kBX, kBY), 0, st>>>(L, g->r, g->rhat, g->p, g->partial));
@@ -2045,13 +2165,13 @@ static hjb_status bicgstab(hjb_grid* g, double dt, const uint8_t* pol, const dou
         LAUNCH(HJB_KC_VECTOR, L.n_own, 32.0 * L.n_own, 4.0 * L.n_own,
                k_bicg_p<D><<<dims(g, L, (const void*)k_bicg_p<D>), dim3(kBX, kBY), 0, st>>>(L, g->S, g->r, g->p, g->v));
       TRY(precond(g, mg, g->p, g->phat));
-      TRY(halo_exchange(g, lv0, g->phat, H));
+      TRY(halo_begin(g, lv0, g->phat, H));
       launch_operator<D>(g, L, C, OP_APPLY, 1, dt, 0.0, pol, g->phat, nullptr, g->v, g->rhat);
       TRY(reduce_dev(g, g->nblk_last, 0u, SC_AFTER_V));
       LAUNCH(HJB_KC_VECTOR, L.n_own, 24.0 * L.n_own, 4.0 * L.n_own,
              k_bicg_s<D><<<dims(g, L, (const void*)k_bicg_s<D>), dim3(kBX, kBY), 0, st>>>(L, g->S, g->r, g->v, g->s, g->partial));
       TRY(precond(g, mg, g->s, g->shat));
-      TRY(halo_exchange(g, lv0, g->shat, H));
+      TRY(halo_begin(g, lv0, g->shat, H));
       launch_operator<D>(g, L, C, OP_APPLY, 2, dt, 0.0, pol, g->shat, nullptr, g->t, g->s);
       TRY(reduce_dev(g, g->nblk_last, 0u, SC_AFTER_T));
       LAUNCH(HJB_KC_VECTOR, L.n_own, 64.0 * L.n_own, 10.0 * L.n_own,
@@ -2069,7 +2189,7 @@ static hjb_status bicgstab(hjb_grid* g, double dt, const uint8_t* pol, const dou
       if (!std::isfinite(rr)) return fail(HJB_ERR_NONFINITE, "non-finite residual in BiCGSTAB");
     }
     // true residual check (recursive residual drifts, SURVEY hard part 5) in both norms
-    TRY(halo_exchange(g, lv0, x, H));
+    TRY(halo_begin(g, lv0, x, H));
     launch_operator<D>(g, L, CUx, OP_RESID, 0, dt, 0.0, pol, x, F, g->r, nullptr);
     double tr2, trinf;
     TRY(norms_dev<D>(g, g->r, &tr2, &trinf));

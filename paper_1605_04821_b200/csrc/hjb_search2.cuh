@@ -103,7 +103,10 @@ __device__ __forceinline__ void split_floor(double o, int& fl, double& s) {
 template <int P, int Q>
 struct STabLayout {
   static constexpr int SD = 0, BD = 2 * P, C = 2 * P + 2, FC = 2 * P + 3, FB = 2 * P + 4, W = 2 * P + 4 + Q,
-                       WD = W + P, WSUM = W + P + 1, S = W + P + 2;
+                       WD = W + P, WSUM = W + P + 1,
+                       CMW = W + P + 2,  // c_ctrl - wsum (the diagonal part of H without c_node)
+                       DQ = W + P + 3,   // [2] drift cell offset: 1 where the drift step is negative
+                       S = W + P + 5;
 };
 struct STabQuad {
   int v[256];  // drift endpoint quadrant per control: bit 0 = cell left of the node (x), bit 1 = below (y)
@@ -114,7 +117,18 @@ struct STabQuad {
                              // 2x the gather footprint, 102 vs 38 GB DRAM); 0: 8-byte gathers from U
 #endif
 // the two values (U_c, U_{c+1}) of the cell row at offset off from the node
+#ifndef HJB_S2_PAIRSUM
+#define HJB_S2_PAIRSUM 0  // 1: pair-summed corners, drift fraction by FMA, 2-op diagonal (12 fewer fp64
+                          // operations per (node, control); measured slower at cfg4: 124 vs 107 ms)
+#endif
+#ifndef HJB_S2_EXP
+#define HJB_S2_EXP 0  // bound experiments (tools/build_variant.sh): 1 = no gathers (tap
+                      // values synthesised from the offsets); 2 = gathers kept, interpolation dropped
+#endif
 __device__ __forceinline__ double2 cell_row(const double2* up, const double* u, int off) {
+#if HJB_S2_EXP == 1
+  return make_double2(__hiloint2double(0x3ff00000, off), __hiloint2double(0x3ff00000, off + 1));
+#endif
 #if HJB_SEARCH2_PAIRS
   return __ldg(pair_at(up, off));
 #else
@@ -265,6 +279,51 @@ __global__ void __launch_bounds__(kS2T, HJB_SEARCH2_MINB) k_search_deep2(LevelDe
             const double lo = fma(s0, a10 - a00, a00), hi = fma(s0, a11 - a01, a01);
             acc = fma(t[T::W + p], fma(s1, hi - lo, lo), acc);
           }
+        } else if (HJB_S2_PAIRSUM && HJB_S2_EXP == 0 && HJB_SEARCH2_PAIRS == 0) {
+          // f first, then the taps: H = (c_node + c_a - wsum_a) U_j + f + sum of taps (two fp64
+          // operations for the diagonal part); each untruncated pair summed corner by corner before
+          // one bilinear interpolation (the minus endpoint's cell mirrored through the node, fractions
+          // 1 - s): 11 instead of 14 operations per pair
+          double f = t[T::FC];
+#pragma unroll
+          for (int q = 0; q < Q; ++q) f = fma(t[T::FB + q], feat[q], f);
+          acc = f;
+#pragma unroll
+          for (int p = 0; p < P; ++p) {
+            int fl0, fl1;
+            double s0, s1;
+            split_floor(ksc[p] * t[T::SD + 2 * p], fl0, s0);
+            split_floor(ksc[p] * t[T::SD + 2 * p + 1], fl1, s1);
+            const int off = fl1 * n + fl0;
+            const int offm = -off - n - 1;
+            HJB_ASSERT(nd.loc + off >= 0 && nd.loc + off + n + 1 < L.local_elems);
+            HJB_ASSERT(nd.loc + offm >= 0 && nd.loc + offm + n + 1 < L.local_elems);
+            const double p00 = __ldg(u0 + off), p10 = __ldg(u0 + off + 1);
+            const double p01 = __ldg(u1 + off), p11 = __ldg(u1 + off + 1);
+            const double m00 = __ldg(u0 + offm), m10 = __ldg(u0 + offm + 1);
+            const double m01 = __ldg(u1 + offm), m11 = __ldg(u1 + offm + 1);
+            const double a00 = p00 + m11, a10 = p10 + m01, a01 = p01 + m10, a11 = p11 + m00;
+            const double lo = fma(s0, a10 - a00, a00), hi = fma(s0, a11 - a01, a01);
+            acc = fma(t[T::W + p], fma(s1, hi - lo, lo), acc);
+          }
+          {  // drift endpoint within one cell: its cell offset is a per-control fact (DQ)
+            const double s0 = fma(kbs, t[T::BD], t[T::DQ]), s1 = fma(kbs, t[T::BD + 1], t[T::DQ + 1]);
+            double dv;
+            switch (quad.v[a]) {
+              case 0: dv = interp_pairs(make_double2(nb[1][1], nb[1][2]), make_double2(nb[2][1], nb[2][2]), s0, s1); break;
+              case 1: dv = interp_pairs(make_double2(nb[1][0], nb[1][1]), make_double2(nb[2][0], nb[2][1]), s0, s1); break;
+              case 2: dv = interp_pairs(make_double2(nb[0][1], nb[0][2]), make_double2(nb[1][1], nb[1][2]), s0, s1); break;
+              default: dv = interp_pairs(make_double2(nb[0][0], nb[0][1]), make_double2(nb[1][0], nb[1][1]), s0, s1); break;
+            }
+            acc = fma(t[T::WD], dv, acc);
+          }
+          const double H = fma(nd.cn + t[T::CMW], Uj, acc);
+          if (H < best) {  // strict: lowest index wins exact ties (reading iv)
+            best = H;
+            arg = a;
+            fbest = f;
+          }
+          continue;
         } else {
 #pragma unroll
         for (int p = 0; p < P; ++p) {
@@ -279,8 +338,12 @@ __global__ void __launch_bounds__(kS2T, HJB_SEARCH2_MINB) k_search_deep2(LevelDe
           const double2 p0 = cell_row(up, u0, off), p1 = cell_row(upn, u1, off);
           const double2 m0 = cell_row(up, u0, offm), m1 = cell_row(upn, u1, offm);
           const double w = t[T::W + p];
+#if HJB_S2_EXP == 2
+          acc += ((p0.x + p1.y) + (m0.x + m1.y)) + ((p0.y + p1.x) + (m0.y + m1.x)) + w * (s0 + s1);
+#else
           acc = fma(w, interp_pairs(p0, p1, s0, s1), acc);
           acc = fma(w, interp_pairs_mirror(m0, m1, s0, s1), acc);
+#endif
         }
         }
         {  // drift endpoint: within one cell of the node, its quadrant is a per-control fact
@@ -320,6 +383,162 @@ __global__ void __launch_bounds__(kS2T, HJB_SEARCH2_MINB) k_search_deep2(LevelDe
   block_reduce_store<2, kS2T>(red, partial, 0x1u);
 }
 
+
+// ------------------------------------------------------------------------------------------------
+// k_search_deep2p: k_search_deep2 (8-byte taps, same arithmetic, bit-identical results) with the
+// control loop software-pipelined: the geometry and the 16 tap loads of control a+1 are issued
+// before control a is combined, so each warp keeps two controls' gathers in flight.  What bounds
+// k_search_deep2 is latency (70 of its 107 ms at cfg4 remain with the gathers
+// removed; 16 warps per SM at 128 registers): one control's loads (~16, some of them L2 misses) are
+// waited on before its arithmetic, which no other warp fully covers.  Here the loads of the next
+// control overlap the arithmetic of the current one, at the cost of more registers (3 CTAs per SM).
+#ifndef HJB_SEARCH2P_MINB
+#define HJB_SEARCH2P_MINB 3
+#endif
+template <int P>
+struct S2Geom {
+  int off[P];
+  double s0[P], s1[P];
+};
+template <int P, int Q>
+__global__ void __launch_bounds__(kS2T, HJB_SEARCH2P_MINB) k_search_deep2p(LevelDev L, CoefDev C, double dt,
+                                                                          const double* __restrict__ U,
+                                                                          const double* __restrict__ Uprev,
+                                                                          uint8_t* __restrict__ pol,
+                                                                          double* __restrict__ F, double* partial,
+                                                                          SkipRect it, const __grid_constant__ STab tab,
+                                                                          const __grid_constant__ STabQuad quad) {
+  using T = STabLayout<P, Q>;
+  double red[2] = {0.0, 0.0};
+  const int nk = box_lines(it);
+  const int n = L.n;
+  const int K = C.K;
+  const int tx = (it.c1 - it.c0 + kSBX - 1) / kSBX, ty = (nk + kS2Y - 1) / kS2Y;
+  const int ntiles = tx * ty;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int sc = t / (kSuperCols * ty);
+    const int scw = min(kSuperCols, tx - sc * kSuperCols);
+    const int tl = t - sc * kSuperCols * ty;
+    const int trow = tl / scw, tcol = sc * kSuperCols + (tl - trow * scw);
+    const int k0 = trow * kS2Y + threadIdx.y;
+    const int col0 = it.c0 + tcol * kSBX + threadIdx.x;
+    const bool valid = k0 < nk && col0 < it.c1;
+    const int k = valid ? k0 : trow * kS2Y, col = valid ? col0 : it.c0 + tcol * kSBX;
+    const int row = box_row<2>(L, it, k);
+    Node<2> nd;
+    node_at<2>(L, col, row, nd);
+    load_fields<2>(C, nd);
+    prefetch_ahead(L, U, nd.loc, col);
+    double feat[Q > 0 ? Q : 1];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) feat[q] = __ldg(C.f_feat + q * C.ld + nd.loc);
+    const double Uj = __ldg(U + nd.loc);
+    double nb[3][3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) nb[r][c] = (r == 1 && c == 1) ? Uj : __ldg(U + nd.loc + (r - 1) * n + (c - 1));
+    double ksc[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) ksc[p] = L.kh * nd.sc[p];
+    const double kbs = L.k2h * nd.bs;
+    const double* u0 = U + nd.loc;
+    const double* u1 = u0 + n;
+    double best = INFINITY, fbest = 0.0;
+    int arg = 0;
+    auto geom = [&](int a, S2Geom<P>& g) {
+      const double* tb = tab.v + a * T::S;
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        int fl0, fl1;
+        split_floor(ksc[p] * tb[T::SD + 2 * p], fl0, g.s0[p]);
+        split_floor(ksc[p] * tb[T::SD + 2 * p + 1], fl1, g.s1[p]);
+        g.off[p] = fl1 * n + fl0;
+      }
+    };
+    auto gather = [&](const S2Geom<P>& g, double (&v)[P][8]) {
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        const int off = g.off[p], offm = -off - n - 1;
+        HJB_ASSERT(nd.loc + off >= 0 && nd.loc + off + n + 1 < L.local_elems);
+        HJB_ASSERT(nd.loc + offm >= 0 && nd.loc + offm + n + 1 < L.local_elems);
+        v[p][0] = __ldg(u0 + off);
+        v[p][1] = __ldg(u0 + off + 1);
+        v[p][2] = __ldg(u1 + off);
+        v[p][3] = __ldg(u1 + off + 1);
+        v[p][4] = __ldg(u0 + offm);
+        v[p][5] = __ldg(u0 + offm + 1);
+        v[p][6] = __ldg(u1 + offm);
+        v[p][7] = __ldg(u1 + offm + 1);
+      }
+    };
+    auto combine = [&](int a, const S2Geom<P>& g, const double (&v)[P][8]) {
+      const double* tb = tab.v + a * T::S;
+      double acc = 0.0;
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        const double w = tb[T::W + p];
+        acc = fma(w, interp_pairs(make_double2(v[p][0], v[p][1]), make_double2(v[p][2], v[p][3]), g.s0[p], g.s1[p]), acc);
+        acc = fma(w, interp_pairs_mirror(make_double2(v[p][4], v[p][5]), make_double2(v[p][6], v[p][7]), g.s0[p], g.s1[p]),
+                  acc);
+      }
+      {
+        const double o0 = kbs * tb[T::BD], o1 = kbs * tb[T::BD + 1];
+        const double s0 = o0 - floor(o0), s1 = o1 - floor(o1);
+        double dv;
+        switch (quad.v[a]) {
+          case 0: dv = interp_pairs(make_double2(nb[1][1], nb[1][2]), make_double2(nb[2][1], nb[2][2]), s0, s1); break;
+          case 1: dv = interp_pairs(make_double2(nb[1][0], nb[1][1]), make_double2(nb[2][0], nb[2][1]), s0, s1); break;
+          case 2: dv = interp_pairs(make_double2(nb[0][1], nb[0][2]), make_double2(nb[1][1], nb[1][2]), s0, s1); break;
+          default: dv = interp_pairs(make_double2(nb[0][0], nb[0][1]), make_double2(nb[1][0], nb[1][1]), s0, s1); break;
+        }
+        acc = fma(tb[T::WD], dv, acc);
+      }
+      double f = tb[T::FC];
+#pragma unroll
+      for (int q = 0; q < Q; ++q) f = fma(tb[T::FB + q], feat[q], f);
+      const double cc = nd.cn + tb[T::C];
+      const double H = (acc - tb[T::WSUM] * Uj) + cc * Uj + f;
+      if (H < best) {  // strict: lowest index wins exact ties (reading iv)
+        best = H;
+        arg = a;
+        fbest = f;
+      }
+    };
+    S2Geom<P> g0, g1;
+    double v0[P][8], v1[P][8];
+    geom(0, g0);
+    gather(g0, v0);
+    for (int a = 0; a < K; a += 2) {
+#if HJB_SEARCH2_SYNC
+      if ((a & (HJB_SEARCH2_SYNC - 1)) == 0) __syncthreads();  // the CTA's 4 lines in lockstep
+#endif
+      const bool two = a + 1 < K;
+      if (two) {
+        geom(a + 1, g1);
+        gather(g1, v1);
+      }
+      combine(a, g0, v0);
+      if (two) {
+        if (a + 2 < K) {
+          geom(a + 2, g0);
+          gather(g0, v0);
+        }
+        combine(a + 1, g1, v1);
+      }
+    }
+    if (valid) {
+      const double Up = __ldg(Uprev + nd.loc);
+      const double R = fabs(Uj - Up - dt * best);
+      const int old = pol[nd.loc];
+      pol[nd.loc] = (uint8_t)arg;
+      F[nd.loc] = fma(dt, fbest, Up);
+      red[0] = fmax(red[0], (R == R) ? R : INFINITY);  // NaN -> inf (reported NONFINITE)
+      red[1] += (old != arg) ? 1.0 : 0.0;
+    }
+  }
+  block_reduce_store<2, kS2T>(red, partial, 0x1u);
+}
 
 // ------------------------------------------------------------------------------------------------
 // k_search_deep3: k_search_deep2 with the node-local part of every H^a hoisted out of the gather loop.

@@ -1,6 +1,7 @@
 cd $GRAFT_REPO_ROOT
 O=gpurun_out
-timeout 900 python -m pytest tests -m gpu -q -x -k "nested or deep_kernels" > $O/j4_pytest.log 2>&1; echo "rc=$?" >> $O/j4_pytest.log
-timeout 900 python bench.py --config cfg4 --steps 8 --warmup 3 --no-e2e --no-cpu-baseline --nested-upto 1 --json-out $O/j4_bench_n1.json > $O/j4_bench_n1.log 2>&1
-timeout 900 python bench.py --config cfg4 --steps 8 --warmup 3 --no-e2e --no-cpu-baseline --nested-upto 3 --json-out $O/j4_bench_n3.json > $O/j4_bench_n3.log 2>&1
-timeout 900 python bench.py --config cfg4 --steps 8 --warmup 3 --no-e2e --no-cpu-baseline --nested-upto 8 --json-out $O/j4_bench_n8.json > $O/j4_bench_n8.log 2>&1
+timeout 300 python tools/opbench.py --cfg 4 --only search --reps 30 > $O/j7_opbench_2p3.log 2>&1
+HJB_LIB=build_variants/s2p4.so timeout 300 python tools/opbench.py --cfg 4 --only search --reps 30 > $O/j7_opbench_2p4.log 2>&1
+HJB_NO_SEARCH2P=1 timeout 300 python tools/opbench.py --cfg 4 --only search --reps 30 > $O/j7_opbench_deep2.log 2>&1
+timeout 300 python tools/opbench.py --cfg 2 --only search --reps 30 > $O/j7_opbench_2p3_cfg2.log 2>&1
+HJB_NO_SEARCH2P=1 timeout 300 python tools/opbench.py --cfg 2 --only search --reps 30 > $O/j7_opbench_deep2_cfg2.log 2>&1
