@@ -69,6 +69,8 @@ def parse():
                          "later steps extrapolate in time; 0 = never nested")
     ap.add_argument("--nested-min-n", type=int, default=None, help="HJB_GUESS_NESTED: smallest nested grid")
     ap.add_argument("--nested-coarsen", type=int, default=None, help="HJB_GUESS_NESTED: 2^m coarsening per axis")
+    ap.add_argument("--nested-increment", type=int, default=None,
+                    help="HJB_GUESS_NESTED: 1 = U_prev + prolonged coarse increment")
     ap.add_argument("--stats-jsonl", default=None,
                     help="write one JSON line of hjb_step_stats per timed step (SURVEY §5 metrics)")
     return ap.parse_args()
@@ -279,6 +281,8 @@ def run_b200(args):
         skw["nested_min_n"] = args.nested_min_n
     if args.nested_coarsen is not None:
         skw["nested_coarsen"] = args.nested_coarsen
+    if args.nested_increment is not None:
+        skw["nested_increment"] = args.nested_increment
 
     def guess_of(si):        # initial iterate of step si (the fixed point does not depend on it)
         if si <= args.nested_upto:

@@ -278,6 +278,10 @@ typedef struct {
   int32_t nested_coarsen;    /* HJB_GUESS_NESTED: 2^nested_coarsen coarsening per axis (default 2) */
   int32_t nested_min_n;      /* HJB_GUESS_NESTED: nest only onto grids with n >= nested_min_n
                                 (default 513)                                                   */
+  int32_t nested_increment;  /* HJB_GUESS_NESTED: 0 = the prolonged coarse solution (default);
+                                1 = U_prev + the prolonged coarse time increment U_c^n - U_c^{n-1}
+                                (keeps the fine grid's U_prev, takes only the change from the
+                                coarse step)                                                    */
 } hjb_solve_params;
 
 #define HJB_GUESS_PREV 0

@@ -68,7 +68,7 @@ class SolveParams(C.Structure):
                 ("tol_pi", C.c_double), ("max_pi", C.c_int32), ("mg", MgParams),
                 ("pi_forcing", C.c_double), ("guess", C.c_int32), ("krylov_rtol_inf", C.c_double),
                 ("theta", C.c_double), ("solver", C.c_int32), ("nested_coarsen", C.c_int32),
-                ("nested_min_n", C.c_int32)]
+                ("nested_min_n", C.c_int32), ("nested_increment", C.c_int32)]
 
 HJB_GUESS_PREV, HJB_GUESS_GIVEN, HJB_GUESS_EXTRAPOLATE, HJB_GUESS_NESTED = 0, 1, 2, 3
 

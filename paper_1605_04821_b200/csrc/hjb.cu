@@ -172,7 +172,7 @@ struct hjb_grid {
   double2* upair = nullptr;   // (U_i, U_{i+1}) pair copy of the searched U (k_search_deep2)
   double4* uquad = nullptr;   // cell-corner copy of the searched U (k_search_deep2<..., QUADS>)
   bool search3 = false;       // k_search_deep3 on the deep rectangle (opt-in, HJB_SEARCH3=1)
-  bool search2p = false;      // k_search_deep2p (software-pipelined) on the deep rectangle
+  bool search2p = false;      // k_search_deep2p (software-pipelined) on the deep rectangle (opt-in)
   // halo exchange overlapped with the rows that do not read halos (nranks > 1, halo_begin): the
   // exchange runs on xst; the operator launches the inner band first, waits on xev[1], then the
   // edge bands
@@ -735,6 +735,7 @@ extern "C" void hjb_solve_params_default(int32_t dim, hjb_solve_params* o) {
   o->solver = 0;              // BiCGSTAB + geometric multigrid (1: GCR + aggregation AMG, NEXT-1)
   o->nested_coarsen = 2;      // HJB_GUESS_NESTED: 4x coarser per axis ...
   o->nested_min_n = 513;      // ... while the coarse grid keeps n >= 513
+  o->nested_increment = 0;    // prolong the coarse solution (1: U_prev + the prolonged coarse increment)
 }
 
 // ---------------------------------------------------------------------------- API: partition
@@ -1559,7 +1560,7 @@ static hjb_status policy_update_dev(hjb_grid* g, double dt, const double* U, con
     // opt-in variants (measured at cfg4): 256-bit corner-copy taps (HJB_QUADS=1) and the
     // hoisted node-local bracket in shared memory (HJB_SEARCH3=1, needs the corner copy)
     g->search3 = getenv("HJB_SEARCH3") && (size_t)g->K * kS2T * sizeof(double) <= 200 * 1024;
-    g->search2p = !g->search3 && !getenv("HJB_QUADS") && !getenv("HJB_NO_SEARCH2P");
+    g->search2p = !g->search3 && !getenv("HJB_QUADS") && getenv("HJB_SEARCH2P");  // opt-in (slower)
     if (getenv("HJB_QUADS") || g->search3) {  // cell-corner copy of U for the 256-bit tap loads
       if (!g->uquad) TRY(dalloc((void**)&g->uquad, (size_t)g->N * sizeof(double4)));
       const int64_t ne = g->N;
@@ -2962,10 +2963,18 @@ static hjb_status nested_guess(hjb_grid* g, double dt, const double* dprev, doub
   S->nested_pi_iters += Sc.pi_iters + Sc.nested_pi_iters;
   const int64_t Nf = g->N;
   const int nbf = (int)std::min<int64_t>((Nf + 255) / 256, (int64_t)g->sms * 8);
-  if (D == 2)
+  if (sp->nested_increment) {  // U^{n-1} + P (U_c^n - U_c^{n-1})
+    if (D == 2)
+      LAUNCH(HJB_KC_TRANSFER, Nf, 16.0 * Nf + 16.0 * Nc, 0,
+             k_nest_prolong_inc<2><<<nbf, 256, 0, g->st>>>(g->n, nc, (int)f, g->child_U, g->child_prev, dprev, dU));
+    else
+      LAUNCH(HJB_KC_TRANSFER, Nf, 16.0 * Nf + 16.0 * Nc, 0,
+             k_nest_prolong_inc<3><<<nbf, 256, 0, g->st>>>(g->n, nc, (int)f, g->child_U, g->child_prev, dprev, dU));
+  } else if (D == 2) {
     LAUNCH(HJB_KC_TRANSFER, Nf, 8.0 * Nf + 8.0 * Nc, 0, k_nest_prolong<2><<<nbf, 256, 0, g->st>>>(g->n, nc, (int)f, g->child_U, dU));
-  else
+  } else {
     LAUNCH(HJB_KC_TRANSFER, Nf, 8.0 * Nf + 8.0 * Nc, 0, k_nest_prolong<3><<<nbf, 256, 0, g->st>>>(g->n, nc, (int)f, g->child_U, dU));
+  }
   CKL();
   return HJB_OK;
 }

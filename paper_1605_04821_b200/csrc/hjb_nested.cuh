@@ -74,4 +74,49 @@ __global__ void k_nest_prolong(int64_t nf, int64_t nc, int f, const double* __re
   }
 }
 
+// increment form: Uf_j = Uprev_j + (multilinear interpolation of Uc - Uc_prev)(x_j) at every fine
+// INTERIOR node (the coarse step's time increment added to the fine U^{n-1})
+template <int D>
+__global__ void k_nest_prolong_inc(int64_t nf, int64_t nc, int f, const double* __restrict__ Uc,
+                                   const double* __restrict__ Ucp, const double* __restrict__ Uprev,
+                                   double* __restrict__ Uf) {
+  int64_t total = nf;
+  for (int d = 1; d < D; ++d) total *= nf;
+  const double inv_f = 1.0 / (double)f;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = q;
+    int64_t c0[D];
+    double s[D];
+    bool interior = true;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const int64_t i = r % nf;
+      r /= nf;
+      interior &= (i > 0 && i < nf - 1);
+      c0[d] = i / f;
+      s[d] = (double)(i - c0[d] * f) * inv_f;
+      if (c0[d] > nc - 2) {
+        c0[d] = nc - 2;
+        s[d] = 1.0;
+      }
+    }
+    if (!interior) continue;
+    double acc = 0.0;
+#pragma unroll
+    for (int m = 0; m < (1 << D); ++m) {
+      double w = 1.0;
+      int64_t loc = 0, stride = 1;
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        const bool hi = (m >> d) & 1;
+        w *= hi ? s[d] : 1.0 - s[d];
+        loc += (c0[d] + (hi ? 1 : 0)) * stride;
+        stride *= nc;
+      }
+      if (w != 0.0) acc = fma(w, __ldg(Uc + loc) - __ldg(Ucp + loc), acc);
+    }
+    Uf[q] = __ldg(Uprev + q) + acc;
+  }
+}
+
 }  // namespace hjb

@@ -392,6 +392,8 @@ __global__ void __launch_bounds__(kS2T, HJB_SEARCH2_MINB) k_search_deep2(LevelDe
 // removed; 16 warps per SM at 128 registers): one control's loads (~16, some of them L2 misses) are
 // waited on before its arithmetic, which no other warp fully covers.  Here the loads of the next
 // control overlap the arithmetic of the current one, at the cost of more registers (3 CTAs per SM).
+// Measured at cfg4 (opt-in HJB_SEARCH2P=1): 148 ms against 115 ms for k_search_deep2 on the same box
+// (168 registers, 12 warps per SM); capped at 128 registers it spills (200 ms).
 #ifndef HJB_SEARCH2P_MINB
 #define HJB_SEARCH2P_MINB 3
 #endif

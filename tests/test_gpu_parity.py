@@ -185,11 +185,12 @@ def test_step_parity_nested_guess(name, mk, steps, min_n):
     """guess = HJB_GUESS_NESTED (reading xxx): the step is first solved on the grid coarsened 4x per
     axis (recursively), its solution prolonged as the initial iterate.  Only the iteration count may
     change: the step's discrete solution matches the oracle's march within the NS tolerance, and the
-    nested grids did run (nested_pi_iters > 0).  Also with an in-place device step (U = U_prev)."""
+    nested grids did run (nested_pi_iters > 0).  Also with an in-place device step (U = U_prev) and
+    in the increment form (U_prev + the prolonged coarse increment)."""
     from paper_1605_04821_b200 import _lib
     torch = require_gpu()
     p = mk()
-    for inplace in (False, True):
+    for inplace, inc in ((False, 0), (True, 0), (False, 1)):
         g, _ = setup(p)
         U = to_dev(p.g(p.all_idx()), torch)
         U2 = U if inplace else torch.empty_like(U)
@@ -200,12 +201,12 @@ def test_step_parity_nested_guess(name, mk, steps, min_n):
             fb, fc = p.f_tables(t)
             g.set_source(fb, fc)
             st = g.step(p.dt, U, U2, pol, to_dev(p.psi(t, p.boundary_idx()), torch),
-                        guess=_lib.HJB_GUESS_NESTED, nested_min_n=min_n)
+                        guess=_lib.HJB_GUESS_NESTED, nested_min_n=min_n, nested_increment=inc)
             assert st["nested_pi_iters"] > 0, st
             U, U2 = U2, U
             Uo, _, _ = howard_step(p, Uo, t, p.dt)
             err = np.abs(U.cpu().numpy() - Uo).max() / max(1.0, np.abs(Uo).max())
-            assert err <= 1e-8, (name, inplace, s, err, st)
+            assert err <= 1e-8, (name, inplace, inc, s, err, st)
             assert st["final_rres"] <= 1e-12 or st["final_R"] <= 1e-10
         g.close()
 

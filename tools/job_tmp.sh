@@ -1,7 +1,6 @@
 cd $GRAFT_REPO_ROOT
 O=gpurun_out
-timeout 300 python tools/opbench.py --cfg 4 --only search --reps 30 > $O/j7_opbench_2p3.log 2>&1
-HJB_LIB=build_variants/s2p4.so timeout 300 python tools/opbench.py --cfg 4 --only search --reps 30 > $O/j7_opbench_2p4.log 2>&1
-HJB_NO_SEARCH2P=1 timeout 300 python tools/opbench.py --cfg 4 --only search --reps 30 > $O/j7_opbench_deep2.log 2>&1
-timeout 300 python tools/opbench.py --cfg 2 --only search --reps 30 > $O/j7_opbench_2p3_cfg2.log 2>&1
-HJB_NO_SEARCH2P=1 timeout 300 python tools/opbench.py --cfg 2 --only search --reps 30 > $O/j7_opbench_deep2_cfg2.log 2>&1
+timeout 900 python -m pytest tests -m gpu -q -x -k "nested" > $O/q_pytest.log 2>&1; echo "rc=$?" >> $O/q_pytest.log
+for u in 1 3 8; do
+timeout 900 python bench.py --config cfg4 --steps 8 --warmup 3 --no-e2e --no-cpu-baseline --no-time-kernels --nested-upto $u --nested-increment 1 --json-out $O/q_bench_inc$u.json > $O/q_bench_inc$u.log 2>&1
+done
