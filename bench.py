@@ -364,7 +364,9 @@ def run_b200(args):
     # --------------------------------------------------------------- roofline (dominant class)
     peaks, peak_src = measured_peaks()
     cls = prof["classes"]
-    timed = {k: v for k, v in cls.items() if v["ms"] > 0}
+    # the nested coarse grids' work (HJB_GUESS_NESTED) is one class of other grids' kernels: not a
+    # roofline candidate (its share of the step is reported in time_share_by_class)
+    timed = {k: v for k, v in cls.items() if v["ms"] > 0 and k != "nested"}
     roof = None
     roof_search = None
     if timed:
@@ -403,7 +405,7 @@ def run_b200(args):
     if shares:   # launches over < 16384 nodes are not event-timed (library: kTimeMinNodes) + host gaps
         shares["untimed_small_launches_and_gaps"] = round(max(0.0, 1.0 - sum(shares.values())), 4)
     hbm_frac = {k: (v["bytes"] / (v["ms"] / 1e3) / 1e9) / float(peaks["hbm_gbs"])
-                for k, v in cls.items() if v["ms"] > 0 and k != "search"}
+                for k, v in cls.items() if v["ms"] > 0 and k not in ("search", "nested")}
 
     # --------------------------------------------------------------- e2e through host buffers
     e2e = None

@@ -371,7 +371,8 @@ typedef enum {
   HJB_KC_REDUCE = 7,    /* fixed-order reduction of block partials + Krylov scalar update    */
   HJB_KC_BOUNDARY = 8,  /* Dirichlet data scatter, halo check                                */
   HJB_KC_MG_COARSE = 9, /* residual / Jacobi sweeps on coarse multigrid levels               */
-  HJB_KC_COUNT = 10
+  HJB_KC_NESTED = 10,   /* everything the nested coarse grids of HJB_GUESS_NESTED launched      */
+  HJB_KC_COUNT = 11
 } hjb_kernel_class;
 
 typedef struct {

@@ -24,7 +24,7 @@ EXPORTS = ["hjb_last_error", "hjb_version", "hjb_grid_create", "hjb_grid_query",
 HJB_COMM_NCCL, HJB_COMM_THREADS = 0, 1
 
 KERNEL_CLASSES = ["search", "apply", "resid", "smooth", "transfer", "coarse", "vector", "reduce",
-                  "boundary", "mg_coarse"]
+                  "boundary", "mg_coarse", "nested"]
 HJB_KC_COUNT = len(KERNEL_CLASSES)
 
 

@@ -2997,17 +2997,18 @@ extern "C" hjb_status hjb_profile_read(hjb_grid_t g, hjb_profile* out) {
   prof_drain(g);
   CK(cudaStreamSynchronize(g->st));
   *out = g->prof;
-  if (g->child) {  // the nested coarse solves' launches count as this grid's
+  if (g->child) {  // the nested coarse solves: one class of this grid's profile (their own grid's
+                   // work, kept apart from the per-kernel roofline classes of this grid)
     hjb_profile c;
     TRY(hjb_profile_read(g->child, &c));
     for (int k = 0; k < HJB_KC_COUNT; ++k) {
-      out->launches[k] += c.launches[k];
-      out->calls[k] += c.calls[k];
-      out->ms[k] += c.ms[k];
-      out->bytes[k] += c.bytes[k];
-      out->flops[k] += c.flops[k];
-      out->nodes[k] += c.nodes[k];
+      out->launches[HJB_KC_NESTED] += c.launches[k];
+      out->ms[HJB_KC_NESTED] += c.ms[k];
+      out->bytes[HJB_KC_NESTED] += c.bytes[k];
+      out->flops[HJB_KC_NESTED] += c.flops[k];
     }
+    out->calls[HJB_KC_NESTED] += c.calls[HJB_KC_SEARCH];
+    out->nodes[HJB_KC_NESTED] += c.nodes[HJB_KC_SEARCH];
     out->total_launches += c.total_launches;
     out->graph_launches += c.graph_launches;
     out->graph_kernels += c.graph_kernels;

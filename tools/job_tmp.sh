@@ -1,6 +1,6 @@
 cd $GRAFT_REPO_ROOT
 O=gpurun_out
-timeout 900 python -m pytest tests -m gpu -q -x -k "nested" > $O/q_pytest.log 2>&1; echo "rc=$?" >> $O/q_pytest.log
-for u in 1 3 8; do
-timeout 900 python bench.py --config cfg4 --steps 8 --warmup 3 --no-e2e --no-cpu-baseline --no-time-kernels --nested-upto $u --nested-increment 1 --json-out $O/q_bench_inc$u.json > $O/q_bench_inc$u.log 2>&1
-done
+timeout 1500 python -m pytest tests -m gpu -q -rA --durations=20 > $O/r_pytest.log 2>&1; echo "rc=$?" >> $O/r_pytest.log
+timeout 1200 python tools/paper_context.py > $O/r_paper_context.log 2>&1
+timeout 600 python bench.py --config cfg2 --steps 16 --warmup 3 --no-e2e --json-out $O/r_bench_cfg2.json > $O/r_bench_cfg2.log 2>&1
+python -c "import __graft_entry__ as g; g.smoke()" > $O/r_smoke.log 2>&1
