@@ -2358,8 +2358,15 @@ static hjb_status agmg_setup(hjb_grid* g, double dt, const uint8_t* pol) {
     g->ag.push_back(lc);
   }
   auto& lc = g->ag.back();
-  if (lc.N > kAgDenseMax)
-    return fail(HJB_ERR_UNSUPPORTED, "aggregation stalled above the dense coarsest size (" + std::to_string(lc.N) + " > 1024)");
+  if (lc.N > kAgDenseMax) {
+    // aggregation stalled above the dense size (e.g. Problem A at 321^2 with dt = dx): the coarsest
+    // level is solved approximately by damped-Jacobi sweeps (the outer GCR is flexible)
+    lc.Ainv = nullptr;
+    g->ag_pol = pol;
+    g->ag_dt = dt;
+    g->ag_ready = true;
+    return HJB_OK;
+  }
   TRY(dalloc((void**)&lc.Ainv, (size_t)lc.N * lc.N * sizeof(double)));
   CK(cudaMemsetAsync(lc.Ainv, 0, (size_t)lc.N * lc.N * sizeof(double), g->st));
   LAUNCH(HJB_KC_COARSE, lc.N, 0, 0, k_ag_dense<<<ag_blocks(lc.N), 256, 0, g->st>>>(lc.N, lc.col, lc.val, lc.Ainv));
@@ -2427,7 +2434,18 @@ static hjb_status ag_kcycle(hjb_grid* g, size_t l, const double* b, double* x) {
   const int64_t N = L.N;
   const int nb = ag_blocks(N);
   if (l + 1 == g->ag.size()) {
-    LAUNCH(HJB_KC_COARSE, N, 0, 0, k_ag_dense_solve<<<(int)((N + 127) / 128), 128, 0, g->st>>>((int)N, L.Ainv, b, x));
+    if (L.Ainv) {
+      LAUNCH(HJB_KC_COARSE, N, 0, 0, k_ag_dense_solve<<<(int)((N + 127) / 128), 128, 0, g->st>>>((int)N, L.Ainv, b, x));
+    } else {  // no dense inverse (stalled aggregation): kAgCoarseSweeps damped-Jacobi sweeps from 0
+      CK(cudaMemsetAsync(L.t, 0, (size_t)N * sizeof(double), g->st));
+      double* in = L.t;
+      double* outp = x;
+      for (int k = 0; k < kAgCoarseSweeps; ++k) {
+        LAUNCH(HJB_KC_COARSE, N, 0, 0, k_ag_sweep<true><<<nb, 256, 0, g->st>>>(N, L.col, L.val, L.dg, in, b, kAgOmega, outp));
+        std::swap(in, outp);
+      }
+      if (in != x) CK(cudaMemcpyAsync(x, in, (size_t)N * sizeof(double), cudaMemcpyDeviceToDevice, g->st));
+    }
     CKL();
     return HJB_OK;
   }

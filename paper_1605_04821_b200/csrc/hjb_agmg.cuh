@@ -288,6 +288,7 @@ __global__ void k_ag_dense(int64_t N, const int* __restrict__ col, const double*
 // in-place Gauss-Jordan inverse in global memory (one block; no pivoting: the coarse matrices are
 // M-matrices with non-negative row sums and positive diagonals), N <= kAgDenseMax
 constexpr int kAgDenseMax = 1024;
+constexpr int kAgCoarseSweeps = 24;  // coarsest level without a dense inverse (stalled aggregation)
 __global__ void __launch_bounds__(1024) k_ag_invert(double* __restrict__ M, int N) {
   __shared__ double colk[kAgDenseMax];
   for (int k = 0; k < N; ++k) {

@@ -162,8 +162,10 @@ __global__ void __launch_bounds__(kTX, DEEP ? (D == 2 ? HJB_SEARCH_DEEP_MINB : 3
   const double* tfb = tfc + C.K;
   double red[2] = {0.0, 0.0};
   const int nk = box_lines(it);
-  for (int k = blockIdx.y * kSBY + threadIdx.y; k < nk; k += gridDim.y * kSBY)
-  for (int col = it.c0 + blockIdx.x * kSBX + threadIdx.x; col < it.c1; col += gridDim.x * kSBX) {
+  // a box narrower than a warp (the boundary-layer strips along x1: reach-wide, e.g. 8 of 32 lanes
+  // at cfg3) is walked as one packed index over its (line, column) pairs, so every lane has a node
+  const int width = it.c1 - it.c0;
+  auto node_work = [&](int k, int col) {
     const int row = box_row<D>(L, it, k);
     Node<D> nd;
     node_at<D>(L, col, row, nd);
@@ -217,6 +219,18 @@ __global__ void __launch_bounds__(kTX, DEEP ? (D == 2 ? HJB_SEARCH_DEEP_MINB : 3
     F[nd.loc] = fma(dt, fbest, Up);
     red[0] = fmax(red[0], (R == R) ? R : INFINITY);  // NaN -> inf (reported NONFINITE)
     red[1] += (old != arg) ? 1.0 : 0.0;
+  };
+  if (width < kSBX) {
+    const int64_t npk = (int64_t)nk * width;
+    const int64_t gstride = (int64_t)gridDim.x * gridDim.y * kSBX * kSBY;
+    for (int64_t q = (int64_t)(blockIdx.y * gridDim.x + blockIdx.x) * (kSBX * kSBY) + threadIdx.y * kSBX + threadIdx.x;
+         q < npk; q += gstride) {
+      const int k = (int)(q / width);
+      node_work(k, it.c0 + (int)(q - (int64_t)k * width));
+    }
+  } else {
+    for (int k = blockIdx.y * kSBY + threadIdx.y; k < nk; k += gridDim.y * kSBY)
+      for (int col = it.c0 + blockIdx.x * kSBX + threadIdx.x; col < it.c1; col += gridDim.x * kSBX) node_work(k, col);
   }
   block_reduce_store<2>(red, partial, 0x1u);
 }

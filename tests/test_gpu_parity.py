@@ -635,3 +635,29 @@ def test_agmg_step_parity():
     for s in (1, 2):
         Uo, _, _ = howard_step(p, Uo, s * p.dt, p.dt)
     assert np.abs(Ug - Uo).max() <= 1e-8 * max(1.0, np.abs(Uo).max()), stats
+
+
+def test_agmg_stalled_aggregation_step():
+    """Problem A at N_x = 321 with dt = dx: the pairwise aggregation stalls above the dense coarsest
+    size; the coarsest level is then solved by damped-Jacobi sweeps (flexible GCR outside) and the
+    step reaches the same discrete solution as the default solver (both to relative residual 1e-12)."""
+    import math
+    from paper_1605_04821_b200 import _lib
+    from synth.device import packed_psi
+    torch = require_gpu()
+    p = problem_A(321)
+    dt = (p.hi - p.lo) / (p.n - 1)
+    out = []
+    for solver in (1, 0):
+        g, _ = setup(p)
+        U = to_dev(p.g(p.all_idx()), torch)
+        U2 = torch.empty_like(U)
+        pol = torch.zeros(p.N, dtype=torch.uint8, device="cuda")
+        fb, fc = p.f_tables(dt)
+        g.set_source(fb, fc)
+        st = g.step(dt, U, U2, pol, packed_psi(p, dt), solver=solver, guess=_lib.HJB_GUESS_PREV)
+        assert st["final_rres"] <= 1e-12 or st["final_R"] <= 1e-10, (solver, st)
+        out.append(U2.cpu().numpy())
+        g.close()
+    assert math.isfinite(float(np.abs(out[0]).max()))
+    assert np.abs(out[0] - out[1]).max() <= 1e-8 * max(1.0, np.abs(out[1]).max())
