@@ -207,15 +207,23 @@ struct hjb_grid {
     int* mem = nullptr;   // members (<= 4) of the next level's aggregates: [4][N_next]
     double *x = nullptr, *b = nullptr, *r = nullptr, *t = nullptr, *z[2] = {nullptr, nullptr},
            *az[2] = {nullptr, nullptr};
-    double* Ainv = nullptr;
+    double* Ainv = nullptr;   // the coarsest level's dense inverse (points into ag_dense)
+    int64_t cap = 0;          // capacity of the N-sized arrays (levels are pooled across setups)
+    int64_t cap_agg = 0, cap_mem = 0;
   };
   std::vector<AgLevel> ag;
+  std::vector<AgLevel> ag_pool;   // released levels, reused by the next setup (no cudaMalloc/Free,
+                                  // which synchronise the device, on the per-policy setup path)
+  double* ag_dense = nullptr;     // kAgDenseMax^2 dense inverse of the coarsest level
+  int* ag_agg1c = nullptr;        // pass-1 copies of the pairwise matching (sized for level 0)
+  int* ag_mem1c = nullptr;
   const uint8_t* ag_pol = nullptr;
   double ag_dt = 0.0;
   bool ag_ready = false;
   int* ag_i[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};  // setup scratch
   void* ag_cub = nullptr;
   size_t ag_cub_bytes = 0;
+  double* ag_sc = nullptr;    // K-cycle inner GCR scalars on the device, 8 per level
   double* ag_Z[16] = {};      // outer FGCR directions (compact)
   double* ag_AZ[16] = {};
   const double* bsamp = nullptr;  // exact-psi mode: face samples of psi (caller-owned, retained)
@@ -2222,17 +2230,33 @@ static hjb_status bicgstab(hjb_grid* g, double dt, const uint8_t* pol, const dou
 constexpr int kAgRestart = 10;
 constexpr double kAgOmega = 0.67;   // Jacobi damping of the K-cycle smoother (the paper uses GS)
 
-static void agmg_free_levels(hjb_grid* g) {
+// the levels of the current hierarchy go back to the pool (their buffers are reused)
+static void agmg_release_levels(hjb_grid* g) {
   for (auto& l : g->ag) {
-    cudaFree(l.col); cudaFree(l.val); cudaFree(l.dg); cudaFree(l.agg); cudaFree(l.mem);
-    cudaFree(l.x); cudaFree(l.b); cudaFree(l.r); cudaFree(l.t); cudaFree(l.Ainv);
-    for (int k = 0; k < 2; ++k) { cudaFree(l.z[k]); cudaFree(l.az[k]); }
+    l.Ainv = nullptr;
+    g->ag_pool.push_back(l);
   }
   g->ag.clear();
   g->ag_ready = false;
 }
+static void agmg_free_levels(hjb_grid* g) {
+  agmg_release_levels(g);
+  for (auto& l : g->ag_pool) {
+    cudaFree(l.col); cudaFree(l.val); cudaFree(l.dg); cudaFree(l.agg); cudaFree(l.mem);
+    cudaFree(l.x); cudaFree(l.b); cudaFree(l.r); cudaFree(l.t);
+    for (int k = 0; k < 2; ++k) { cudaFree(l.z[k]); cudaFree(l.az[k]); }
+  }
+  g->ag_pool.clear();
+}
 static void agmg_free(hjb_grid* g) {
   agmg_free_levels(g);
+  cudaFree(g->ag_dense);
+  cudaFree(g->ag_sc);
+  g->ag_sc = nullptr;
+  cudaFree(g->ag_agg1c);
+  cudaFree(g->ag_mem1c);
+  g->ag_dense = nullptr;
+  g->ag_agg1c = g->ag_mem1c = nullptr;
   for (auto& p : g->ag_i) { cudaFree(p); p = nullptr; }
   cudaFree(g->ag_cub);
   g->ag_cub = nullptr;
@@ -2244,7 +2268,21 @@ static int ag_blocks(int64_t n, int bs = 256) {
 }
 
 static hjb_status ag_alloc_level(hjb_grid* g, hjb_grid::AgLevel& l, int64_t N) {
+  // the smallest pooled level that fits
+  int best = -1;
+  for (int i = 0; i < (int)g->ag_pool.size(); ++i)
+    if (g->ag_pool[i].cap >= N && (best < 0 || g->ag_pool[i].cap < g->ag_pool[best].cap)) best = i;
+  if (best >= 0) {
+    l = g->ag_pool[best];
+    g->ag_pool.erase(g->ag_pool.begin() + best);
+    l.N = N;
+    l.Ainv = nullptr;
+    CK(cudaMemsetAsync(l.col, 0xff, (size_t)kAgW * N * sizeof(int), g->st));
+    return HJB_OK;
+  }
+  l = hjb_grid::AgLevel{};
   l.N = N;
+  l.cap = N;
   TRY(dalloc((void**)&l.col, (size_t)kAgW * N * sizeof(int)));
   TRY(dalloc((void**)&l.val, (size_t)kAgW * N * sizeof(double)));
   TRY(dalloc((void**)&l.dg, (size_t)N * sizeof(double)));
@@ -2292,7 +2330,7 @@ static hjb_status ag_pairwise(hjb_grid* g, int64_t N, const int* col, const doub
 template <int D>
 static hjb_status agmg_setup(hjb_grid* g, double dt, const uint8_t* pol) {
   if (g->R != 1) return fail(HJB_ERR_UNSUPPORTED, "aggregation AMG: one rank only");
-  agmg_free_levels(g);
+  agmg_release_levels(g);
   const int64_t N0 = g->L0.n_own;
   if (!g->d_flag) TRY(dalloc((void**)&g->d_flag, sizeof(int)));
   CK(cudaMemsetAsync(g->d_flag, 0, sizeof(int), g->st));
@@ -2309,6 +2347,10 @@ static hjb_status agmg_setup(hjb_grid* g, double dt, const uint8_t* pol) {
     else AGF((D > 2 ? 3 : 2));
 #undef AGF
     CKL();
+    int flag = 0;
+    CK(cudaMemcpyAsync(&flag, g->d_flag, sizeof(int), cudaMemcpyDeviceToHost, g->st));
+    CK(cudaStreamSynchronize(g->st));
+    if (flag) return fail(HJB_ERR_UNSUPPORTED, "aggregation AMG: a fine row wider than the ELL width (96)");
   }
   const int64_t stop = std::max<int64_t>(64, (int64_t)std::cbrt((double)N0));
   while (g->ag.back().N > stop && g->ag.size() < 20) {
@@ -2323,9 +2365,11 @@ static hjb_status agmg_setup(hjb_grid* g, double dt, const uint8_t* pol) {
     LAUNCH(HJB_KC_COARSE, N1, 0, 0, k_ag_coarse<<<ag_blocks(N1, 128), 128, 0, g->st>>>(N, lf.col, lf.val, agg1, N1, mem1, 2,
                                                                                      tmp.col, tmp.val, tmp.dg, g->d_flag));
     // pass 2 on A_1 (the scratch of pass 1 moves into fresh buffers first)
-    int *agg1c = nullptr, *mem1c = nullptr;
-    TRY(dalloc((void**)&agg1c, (size_t)N * sizeof(int)));
-    TRY(dalloc((void**)&mem1c, (size_t)2 * N1 * sizeof(int)));
+    if (!g->ag_agg1c) {
+      TRY(dalloc((void**)&g->ag_agg1c, (size_t)N0 * sizeof(int)));
+      TRY(dalloc((void**)&g->ag_mem1c, (size_t)2 * N0 * sizeof(int)));
+    }
+    int *agg1c = g->ag_agg1c, *mem1c = g->ag_mem1c;
     CK(cudaMemcpyAsync(agg1c, agg1, (size_t)N * sizeof(int), cudaMemcpyDeviceToDevice, g->st));
     CK(cudaMemcpyAsync(mem1c, mem1, (size_t)2 * N1 * sizeof(int), cudaMemcpyDeviceToDevice, g->st));
     int64_t N2 = 0;
@@ -2334,25 +2378,27 @@ static hjb_status agmg_setup(hjb_grid* g, double dt, const uint8_t* pol) {
     TRY(ag_alloc_level(g, lc, N2));
     LAUNCH(HJB_KC_COARSE, N2, 0, 0, k_ag_coarse<<<ag_blocks(N2, 128), 128, 0, g->st>>>(N1, tmp.col, tmp.val, g->ag_i[4], N2,
                                                                                      g->ag_i[5], 2, lc.col, lc.val, lc.dg, g->d_flag));
-    TRY(dalloc((void**)&lf.agg, (size_t)N * sizeof(int)));
-    TRY(dalloc((void**)&lf.mem, (size_t)4 * N2 * sizeof(int)));
+    if (lf.cap_agg < N) {
+      cudaFree(lf.agg);
+      TRY(dalloc((void**)&lf.agg, (size_t)N * sizeof(int)));
+      lf.cap_agg = N;
+    }
+    if (lf.cap_mem < 4 * N2) {
+      cudaFree(lf.mem);
+      TRY(dalloc((void**)&lf.mem, (size_t)4 * N2 * sizeof(int)));
+      lf.cap_mem = 4 * N2;
+    }
     CK(cudaMemsetAsync(lf.mem, 0xff, (size_t)4 * N2 * sizeof(int), g->st));
     LAUNCH(HJB_KC_COARSE, N, 0, 0, k_ag_compose<<<ag_blocks(std::max(N, N2)), 256, 0, g->st>>>(N, agg1c, g->ag_i[4], lf.agg, N1,
                                                                                              mem1c, g->ag_i[5], N2, lf.mem));
     CKL();
+    int ovf = 0;  // a coarse row wider than the ELL width (kAgW): stop coarsening above this level
+    CK(cudaMemcpyAsync(&ovf, g->d_flag, sizeof(int), cudaMemcpyDeviceToHost, g->st));
     CK(cudaStreamSynchronize(g->st));
-    cudaFree(agg1c);
-    cudaFree(mem1c);
-    hjb_grid::AgLevel* tl = &tmp;
-    cudaFree(tl->col); cudaFree(tl->val); cudaFree(tl->dg); cudaFree(tl->x); cudaFree(tl->b); cudaFree(tl->r);
-    cudaFree(tl->t);
-    for (int k = 0; k < 2; ++k) { cudaFree(tl->z[k]); cudaFree(tl->az[k]); }
-    if (N2 * 10 >= N * 7) {  // coarsening below 1.43x: stop here (the level just built is dropped)
-      cudaFree(lf.agg); cudaFree(lf.mem);
-      lf.agg = nullptr; lf.mem = nullptr;
-      cudaFree(lc.col); cudaFree(lc.val); cudaFree(lc.dg); cudaFree(lc.x); cudaFree(lc.b); cudaFree(lc.r);
-      cudaFree(lc.t);
-      for (int k = 0; k < 2; ++k) { cudaFree(lc.z[k]); cudaFree(lc.az[k]); }
+    g->ag_pool.push_back(tmp);  // the pass-1 operator is not kept
+    if (ovf || N2 * 10 >= N * 7) {  // overflow, or coarsening below 1.43x: the level just built is dropped
+      if (ovf) CK(cudaMemsetAsync(g->d_flag, 0, sizeof(int), g->st));
+      g->ag_pool.push_back(lc);
       break;
     }
     g->ag.push_back(lc);
@@ -2367,7 +2413,8 @@ static hjb_status agmg_setup(hjb_grid* g, double dt, const uint8_t* pol) {
     g->ag_ready = true;
     return HJB_OK;
   }
-  TRY(dalloc((void**)&lc.Ainv, (size_t)lc.N * lc.N * sizeof(double)));
+  if (!g->ag_dense) TRY(dalloc((void**)&g->ag_dense, (size_t)kAgDenseMax * kAgDenseMax * sizeof(double)));
+  lc.Ainv = g->ag_dense;
   CK(cudaMemsetAsync(lc.Ainv, 0, (size_t)lc.N * lc.N * sizeof(double), g->st));
   LAUNCH(HJB_KC_COARSE, lc.N, 0, 0, k_ag_dense<<<ag_blocks(lc.N), 256, 0, g->st>>>(lc.N, lc.col, lc.val, lc.Ainv));
   LAUNCH(HJB_KC_COARSE, lc.N, 0, 0, k_ag_invert<<<1, 1024, 0, g->st>>>(lc.Ainv, (int)lc.N));
@@ -2396,12 +2443,41 @@ static hjb_status ag_kcycle(hjb_grid* g, size_t l, const double* b, double* x);
 
 // 2 flexible GCR iterations on level c (x0 = 0), preconditioned by its K-cycle: the K-cycle's
 // coarse-grid solve ("a number of Krylov subspace iterations")
+// The scalars stay on the device (k_ag_scal / k_ag_axpy_dev): no host round trip inside the cycle.
+// Notay's adaptive rule (stop after one iteration if it reduced the residual 4x) needs the residual
+// on the host, so it is applied on the first coarse level only (one read per outer iteration);
+// deeper levels always take both iterations.
 static hjb_status ag_inner(hjb_grid* g, size_t c, const double* b, double* x) {
   auto& L = g->ag[c];
   const int64_t N = L.N;
   const int nb = ag_blocks(N);
   CK(cudaMemsetAsync(x, 0, (size_t)N * sizeof(double), g->st));
   CK(cudaMemcpyAsync(L.r, b, (size_t)N * sizeof(double), cudaMemcpyDeviceToDevice, g->st));
+  if (c >= 2 || getenv("HJB_AG_DEVICE_ALL")) {
+    if (!g->ag_sc) TRY(dalloc((void**)&g->ag_sc, (size_t)8 * 32 * sizeof(double)));
+    const int base = 8 * (int)std::min<size_t>(c, 31);
+    const int nbd = std::min(ag_blocks(N), kMaxBlocks);
+    for (int it = 0; it < 2; ++it) {
+      TRY(ag_kcycle(g, c, L.r, L.z[it]));
+      LAUNCH(HJB_KC_MG_COARSE, N, 0, 0, k_ag_spmv<<<nb, 256, 0, g->st>>>(N, L.col, L.val, L.z[it], L.az[it]));
+      if (it == 1) {  // orthogonalise against the (normalised) first direction
+        LAUNCH(HJB_KC_VECTOR, N, 16.0 * N, 4.0 * N, k_ag_dot2<<<nbd, 256, 0, g->st>>>(N, L.az[0], L.az[1], g->partial));
+        LAUNCH(HJB_KC_REDUCE, nbd, 0, 0, k_ag_scal<<<1, 256, 0, g->st>>>(g->partial, nbd, g->ag_sc, base, 0));
+        LAUNCH(HJB_KC_VECTOR, N, 0, 0, k_ag_axpy_dev<<<nb, 256, 0, g->st>>>(N, g->ag_sc, base, L.az[0], L.az[1]));
+        LAUNCH(HJB_KC_VECTOR, N, 0, 0, k_ag_axpy_dev<<<nb, 256, 0, g->st>>>(N, g->ag_sc, base, L.z[0], L.z[1]));
+      }
+      LAUNCH(HJB_KC_VECTOR, N, 16.0 * N, 4.0 * N, k_ag_dot2<<<nbd, 256, 0, g->st>>>(N, L.az[it], L.az[it], g->partial));
+      LAUNCH(HJB_KC_REDUCE, nbd, 0, 0, k_ag_scal<<<1, 256, 0, g->st>>>(g->partial, nbd, g->ag_sc, base + 1, 1));
+      LAUNCH(HJB_KC_VECTOR, N, 0, 0, k_ag_scale_dev<<<nb, 256, 0, g->st>>>(N, g->ag_sc, base + 1, L.az[it]));
+      LAUNCH(HJB_KC_VECTOR, N, 0, 0, k_ag_scale_dev<<<nb, 256, 0, g->st>>>(N, g->ag_sc, base + 1, L.z[it]));
+      LAUNCH(HJB_KC_VECTOR, N, 16.0 * N, 4.0 * N, k_ag_dot2<<<nbd, 256, 0, g->st>>>(N, L.az[it], L.r, g->partial));
+      LAUNCH(HJB_KC_REDUCE, nbd, 0, 0, k_ag_scal<<<1, 256, 0, g->st>>>(g->partial, nbd, g->ag_sc, base + 2, 2));
+      LAUNCH(HJB_KC_VECTOR, N, 0, 0, k_ag_axpy_dev<<<nb, 256, 0, g->st>>>(N, g->ag_sc, base + 2, L.z[it], x));
+      LAUNCH(HJB_KC_VECTOR, N, 0, 0, k_ag_axpy_dev<<<nb, 256, 0, g->st>>>(N, g->ag_sc, base + 3, L.az[it], L.r));
+    }
+    CKL();
+    return HJB_OK;
+  }
   for (int it = 0; it < 2; ++it) {
     TRY(ag_kcycle(g, c, L.r, L.z[it]));
     LAUNCH(HJB_KC_MG_COARSE, N, 0, 0, k_ag_spmv<<<nb, 256, 0, g->st>>>(N, L.col, L.val, L.z[it], L.az[it]));

@@ -276,6 +276,57 @@ __global__ void __launch_bounds__(256) k_ag_dot2(int64_t N, const double* __rest
   block_reduce_store<2, 256>(red, partial);
 }
 
+// K-cycle inner GCR scalars on the device (no host round trip inside the cycle): one block reduces
+// the nb block partials of k_ag_dot2 in a fixed order and stores
+//   op 0: s[slot] = -x.y            (minus the projection coefficient h)
+//   op 1: s[slot] = 1 / sqrt(y.y)   (0 for a zero vector: the direction then adds nothing)
+//   op 2: s[slot] = x.y, s[slot+1] = -x.y, s[slot+2] = y.y   (gamma, -gamma, r.r)
+__global__ void __launch_bounds__(256) k_ag_scal(const double* __restrict__ partial, int nb, double* s, int slot,
+                                                int op) {
+  __shared__ double sm[2][256];
+  double a = 0.0, b = 0.0;
+  for (int i = threadIdx.x; i < nb; i += 256) {
+    a += partial[2 * i];
+    b += partial[2 * i + 1];
+  }
+  sm[0][threadIdx.x] = a;
+  sm[1][threadIdx.x] = b;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      sm[0][threadIdx.x] += sm[0][threadIdx.x + w];
+      sm[1][threadIdx.x] += sm[1][threadIdx.x + w];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double xy = sm[0][0], yy = sm[1][0];
+    if (op == 0) {
+      s[slot] = -xy;
+    } else if (op == 1) {
+      s[slot] = yy > 0.0 ? 1.0 / sqrt(yy) : 0.0;
+    } else {
+      s[slot] = xy;
+      s[slot + 1] = -xy;
+      s[slot + 2] = yy;
+    }
+  }
+}
+
+// y += s[slot] x  /  y *= s[slot]  (coefficients from k_ag_scal)
+__global__ void __launch_bounds__(256) k_ag_axpy_dev(int64_t N, const double* __restrict__ s, int slot,
+                                                    const double* __restrict__ x, double* __restrict__ y) {
+  const double a = s[slot];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = fma(a, x[i], y[i]);
+}
+__global__ void __launch_bounds__(256) k_ag_scale_dev(int64_t N, const double* __restrict__ s, int slot,
+                                                     double* __restrict__ y) {
+  const double a = s[slot];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] *= a;
+}
+
 // coarsest level: dense matrix from ELL (compact rows), then x = Ainv b
 __global__ void k_ag_dense(int64_t N, const int* __restrict__ col, const double* __restrict__ val, double* __restrict__ Ad) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)

@@ -57,14 +57,12 @@ __global__ void __launch_bounds__(kTX, (DEEP && D == 2) ? HJB_OP_DEEP_MINB : HJB
   const double* tbd = tab + C.K * P * D;
   const double* tcc = tbd + C.K * D;
   double dots[2] = {0.0, 0.0};
-  const int col = it.c0 + blockIdx.x * kBX + threadIdx.x;
   const int nk = box_lines(it);
-  const bool active = col < it.c1;
   // DEEP: ILP nodes per thread per pass (rows row, row + stride, ...): their loads and gathers are
   // in flight together (HJB_OP_ILP, default 1)
   constexpr int U = DEEP ? HJB_OP_ILP : 1;
   const int rstride = gridDim.y * kBY;
-  for (int k0 = blockIdx.y * kBY + threadIdx.y; k0 < nk; k0 += rstride * U) {
+  auto pass = [&](int k0, int col, bool active) {
     NodeIn<D, P> in[U];
     bool ok[U];
     int rows[U];
@@ -134,6 +132,23 @@ __global__ void __launch_bounds__(kTX, (DEEP && D == 2) ? HJB_OP_DEEP_MINB : HJB
       if (NDOT >= 1 && MODE != OP_JACOBI_D) dots[0] = fma(out, __ldg(u + nd[v].loc), dots[0]);
       if (NDOT >= 2) dots[1] = fma(out, out, dots[1]);
     }
+  };
+  // a general-kernel box narrower than a CTA line (the x1 boundary-layer strips: reach-wide, 4..71
+  // of 128 lanes on the coarse levels at cfg4) is walked as one packed index over its (line, column)
+  // pairs, so that every lane has a node
+  const int width = it.c1 - it.c0;
+  if (!DEEP && width < kBX) {
+    const int64_t npk = (int64_t)nk * width;
+    const int64_t step = (int64_t)gridDim.x * gridDim.y * kBX * kBY;
+    for (int64_t q = (int64_t)(blockIdx.y * gridDim.x + blockIdx.x) * (kBX * kBY) + threadIdx.y * kBX + threadIdx.x;
+         q < npk; q += step) {
+      const int k0 = (int)(q / width);
+      pass(k0, it.c0 + (int)(q - (int64_t)k0 * width), true);
+    }
+  } else {
+    const int col = it.c0 + blockIdx.x * kBX + threadIdx.x;
+    const bool active = col < it.c1;
+    for (int k0 = blockIdx.y * kBY + threadIdx.y; k0 < nk; k0 += rstride * U) pass(k0, col, active);
   }
   if (NDOT > 0) block_reduce_store<2>(dots, partial);
 }
