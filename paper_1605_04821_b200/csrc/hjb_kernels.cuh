@@ -133,17 +133,17 @@ __global__ void __launch_bounds__(kTX, (DEEP && D == 2) ? HJB_OP_DEEP_MINB : HJB
       if (NDOT >= 2) dots[1] = fma(out, out, dots[1]);
     }
   };
-  // a general-kernel box narrower than a CTA line (the x1 boundary-layer strips: reach-wide, 4..71
-  // of 128 lanes on the coarse levels at cfg4) is walked as one packed index over its (line, column)
-  // pairs, so that every lane has a node
+  // the general kernel (boundary-layer strips, small levels) walks its box as one packed index over
+  // the (line, column) pairs, so that every lane has a node: the x1 strips are only reach-wide (4..143
+  // columns on the cfg4 levels, against 128 lanes per CTA line)
   const int width = it.c1 - it.c0;
-  if (!DEEP && width < kBX) {
-    const int64_t npk = (int64_t)nk * width;
-    const int64_t step = (int64_t)gridDim.x * gridDim.y * kBX * kBY;
-    for (int64_t q = (int64_t)(blockIdx.y * gridDim.x + blockIdx.x) * (kBX * kBY) + threadIdx.y * kBX + threadIdx.x;
-         q < npk; q += step) {
-      const int k0 = (int)(q / width);
-      pass(k0, it.c0 + (int)(q - (int64_t)k0 * width), true);
+  if (!DEEP) {
+    const int npk = nk * width;  // < 2^31: local arrays hold < 2^31 nodes
+    const int step = gridDim.x * gridDim.y * kBX * kBY;
+    for (int q = (blockIdx.y * gridDim.x + blockIdx.x) * (kBX * kBY) + threadIdx.y * kBX + threadIdx.x; q < npk;
+         q += step) {
+      const int k0 = q / width;
+      pass(k0, it.c0 + (q - k0 * width), true);
     }
   } else {
     const int col = it.c0 + blockIdx.x * kBX + threadIdx.x;
@@ -177,8 +177,9 @@ __global__ void __launch_bounds__(kTX, DEEP ? (D == 2 ? HJB_SEARCH_DEEP_MINB : 3
   const double* tfb = tfc + C.K;
   double red[2] = {0.0, 0.0};
   const int nk = box_lines(it);
-  // a box narrower than a warp (the boundary-layer strips along x1: reach-wide, e.g. 8 of 32 lanes
-  // at cfg3) is walked as one packed index over its (line, column) pairs, so every lane has a node
+  // the general kernel (and any box narrower than a warp) walks its box as one packed index over
+  // the (line, column) pairs, so every lane has a node: the boundary-layer strips along x1 are only
+  // reach-wide (e.g. 8 of 32 lanes at cfg3)
   const int width = it.c1 - it.c0;
   auto node_work = [&](int k, int col) {
     const int row = box_row<D>(L, it, k);
@@ -235,13 +236,13 @@ __global__ void __launch_bounds__(kTX, DEEP ? (D == 2 ? HJB_SEARCH_DEEP_MINB : 3
     red[0] = fmax(red[0], (R == R) ? R : INFINITY);  // NaN -> inf (reported NONFINITE)
     red[1] += (old != arg) ? 1.0 : 0.0;
   };
-  if (width < kSBX) {
-    const int64_t npk = (int64_t)nk * width;
-    const int64_t gstride = (int64_t)gridDim.x * gridDim.y * kSBX * kSBY;
-    for (int64_t q = (int64_t)(blockIdx.y * gridDim.x + blockIdx.x) * (kSBX * kSBY) + threadIdx.y * kSBX + threadIdx.x;
-         q < npk; q += gstride) {
-      const int k = (int)(q / width);
-      node_work(k, it.c0 + (int)(q - (int64_t)k * width));
+  if (!DEEP || width < kSBX) {
+    const int npk = nk * width;  // < 2^31: local arrays hold < 2^31 nodes
+    const int gstride = gridDim.x * gridDim.y * kSBX * kSBY;
+    for (int q = (blockIdx.y * gridDim.x + blockIdx.x) * (kSBX * kSBY) + threadIdx.y * kSBX + threadIdx.x; q < npk;
+         q += gstride) {
+      const int k = q / width;
+      node_work(k, it.c0 + (q - k * width));
     }
   } else {
     for (int k = blockIdx.y * kSBY + threadIdx.y; k < nk; k += gridDim.y * kSBY)
