@@ -1337,7 +1337,7 @@ static hjb_status halo_input(hjb_grid* g, const double* x, const double** out) {
 // per-control facts), drift endpoints within one cell, table entries either 0 or far from underflow
 static bool search2_ok(hjb_grid* g) {
   const int P = g->P, Q = g->Q, K = g->K;
-  const int S = 2 * P + 4 + Q + P + 5;  // STabLayout<P, Q>::S
+  const int S = 2 * P + 4 + Q + P + 7;  // STabLayout<P, Q>::S
   if (g->D != 2 || !(Q == 1 || Q == 2 || Q == 8) || K * S > kSTabN || K > 256) return false;
   if (g->C0.sigma_node || g->C0.b_node || !g->reach_ok || !g->drift_reg) return false;
   for (int p = 0; p < P; ++p)
@@ -1425,6 +1425,8 @@ static void search2_tables(hjb_grid* g, STab& tab, STabQuad& quad) {
     t[T::CMW] = t[T::C] - t[T::WSUM];
     t[T::DQ] = bd[a * 2] < 0.0 ? 1.0 : 0.0;
     t[T::DQ + 1] = bd[a * 2 + 1] < 0.0 ? 1.0 : 0.0;
+    t[T::ABD] = std::fabs(bd[a * 2]);
+    t[T::ABD + 1] = std::fabs(bd[a * 2 + 1]);
   }
 }
 
@@ -2443,17 +2445,17 @@ static hjb_status ag_kcycle(hjb_grid* g, size_t l, const double* b, double* x);
 
 // 2 flexible GCR iterations on level c (x0 = 0), preconditioned by its K-cycle: the K-cycle's
 // coarse-grid solve ("a number of Krylov subspace iterations")
-// The scalars stay on the device (k_ag_scal / k_ag_axpy_dev): no host round trip inside the cycle.
-// Notay's adaptive rule (stop after one iteration if it reduced the residual 4x) needs the residual
-// on the host, so it is applied on the first coarse level only (one read per outer iteration);
-// deeper levels always take both iterations.
+// HJB_AG_DEVICE=1: the scalars stay on the device (k_ag_scal / k_ag_axpy_dev), no host round trip
+// inside the cycle, but without Notay's adaptive rule (stop after one iteration if it reduced the
+// residual 4x), which needs the residual on the host: both iterations always.
 static hjb_status ag_inner(hjb_grid* g, size_t c, const double* b, double* x) {
   auto& L = g->ag[c];
   const int64_t N = L.N;
   const int nb = ag_blocks(N);
   CK(cudaMemsetAsync(x, 0, (size_t)N * sizeof(double), g->st));
   CK(cudaMemcpyAsync(L.r, b, (size_t)N * sizeof(double), cudaMemcpyDeviceToDevice, g->st));
-  if (c >= 2 || getenv("HJB_AG_DEVICE_ALL")) {
+  if (getenv("HJB_AG_DEVICE")) {  // opt-in: measured slower (no adaptive skip below level 1 doubles
+                                  // the launch-bound coarse visits; tools/paper_context.py)
     if (!g->ag_sc) TRY(dalloc((void**)&g->ag_sc, (size_t)8 * 32 * sizeof(double)));
     const int base = 8 * (int)std::min<size_t>(c, 31);
     const int nbd = std::min(ag_blocks(N), kMaxBlocks);

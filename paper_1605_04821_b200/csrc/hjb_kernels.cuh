@@ -39,8 +39,12 @@ enum OpMode : int {
 #ifndef HJB_OP_DEEP_MINB
 #define HJB_OP_DEEP_MINB 6  // lean deep kernels fit 80 registers: 24 resident warps (cfg4 sweep -17 %)
 #endif
+// residual sweeps and the Krylov applies with fused dot products spill at 80 registers: 96 (5 CTAs)
+// for those (cfg4 fine residual 8.3 -> 7.4 ms, coarse sweeps -5 %); Jacobi and the plain apply keep 80
+template <int MODE, int NDOT>
+constexpr int op_deep_minb() { return (MODE == OP_RESID || NDOT > 0) ? HJB_OP_DEEP_MINB - 1 : HJB_OP_DEEP_MINB; }
 template <int D, int P, int MODE, int NDOT, bool DEEP>
-__global__ void __launch_bounds__(kTX, (DEEP && D == 2) ? HJB_OP_DEEP_MINB : HJB_OP_MINB) k_operator(LevelDev L, CoefDev C, double dt, double omega,
+__global__ void __launch_bounds__(kTX, (DEEP && D == 2) ? op_deep_minb<MODE, NDOT>() : HJB_OP_MINB) k_operator(LevelDev L, CoefDev C, double dt, double omega,
                                                   const uint8_t* __restrict__ pol,
                                                   const double* __restrict__ x,
                                                   const double* __restrict__ b, double* __restrict__ y,

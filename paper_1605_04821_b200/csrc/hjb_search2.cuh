@@ -106,7 +106,8 @@ struct STabLayout {
                        WD = W + P, WSUM = W + P + 1,
                        CMW = W + P + 2,  // c_ctrl - wsum (the diagonal part of H without c_node)
                        DQ = W + P + 3,   // [2] drift cell offset: 1 where the drift step is negative
-                       S = W + P + 5;
+                       ABD = W + P + 5,  // [2] |b_dir|: the drift step's magnitude per axis
+                       S = W + P + 7;
 };
 struct STabQuad {
   int v[256];  // drift endpoint quadrant per control: bit 0 = cell left of the node (x), bit 1 = below (y)
@@ -219,6 +220,17 @@ __global__ void __launch_bounds__(kS2T, HJB_SEARCH2_MINB) k_search_deep2(LevelDe
       for (int r = 0; r < 3; ++r)
 #pragma unroll
         for (int c = 0; c < 3; ++c) nb[r][c] = (r == 1 && c == 1) ? Uj : __ldg(U + nd.loc + (r - 1) * n + (c - 1));
+      // one-sided differences of the 3x3 neighbourhood (index 0: towards -1, 1: towards +1)
+      double ddx[2], ddy[2], ddxy[2][2];  // ddxy[y side][x side]
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        ddx[q] = nb[1][2 * q] - Uj;
+        ddy[q] = nb[2 * q][1] - Uj;
+      }
+#pragma unroll
+      for (int qy = 0; qy < 2; ++qy)
+#pragma unroll
+        for (int qx = 0; qx < 2; ++qx) ddxy[qy][qx] = (nb[2 * qy][2 * qx] - nb[1][2 * qx]) - (nb[2 * qy][1] - Uj);
       double ksc[P];
 #pragma unroll
       for (int p = 0; p < P; ++p) ksc[p] = L.kh * nd.sc[p];
@@ -346,16 +358,18 @@ __global__ void __launch_bounds__(kS2T, HJB_SEARCH2_MINB) k_search_deep2(LevelDe
 #endif
         }
         }
-        {  // drift endpoint: within one cell of the node, its quadrant is a per-control fact
-          const double o0 = kbs * t[T::BD], o1 = kbs * t[T::BD + 1];
-          const double s0 = o0 - floor(o0), s1 = o1 - floor(o1);
-          double dv;
+        {  // drift endpoint: within one cell of the node, its quadrant is a per-control fact; the
+           // bilinear value measured from the node, I = U_j + |o0| Dx + |o1| (Dy + |o0| Dxy), with the
+           // quadrant's one-sided differences formed once per node (7 instead of 13 fp64 operations)
+          const double o0 = kbs * t[T::ABD], o1 = kbs * t[T::ABD + 1];
+          double dx, dy, dxy;
           switch (quad.v[a]) {
-            case 0: dv = interp_pairs(make_double2(nb[1][1], nb[1][2]), make_double2(nb[2][1], nb[2][2]), s0, s1); break;
-            case 1: dv = interp_pairs(make_double2(nb[1][0], nb[1][1]), make_double2(nb[2][0], nb[2][1]), s0, s1); break;
-            case 2: dv = interp_pairs(make_double2(nb[0][1], nb[0][2]), make_double2(nb[1][1], nb[1][2]), s0, s1); break;
-            default: dv = interp_pairs(make_double2(nb[0][0], nb[0][1]), make_double2(nb[1][0], nb[1][1]), s0, s1); break;
+            case 0: dx = ddx[1]; dy = ddy[1]; dxy = ddxy[1][1]; break;
+            case 1: dx = ddx[0]; dy = ddy[1]; dxy = ddxy[1][0]; break;
+            case 2: dx = ddx[1]; dy = ddy[0]; dxy = ddxy[0][1]; break;
+            default: dx = ddx[0]; dy = ddy[0]; dxy = ddxy[0][0]; break;
           }
+          const double dv = Uj + fma(o0, dx, o1 * fma(o0, dxy, dy));
           acc = fma(t[T::WD], dv, acc);
         }
         double f = t[T::FC];
