@@ -64,6 +64,8 @@ def parse():
     ap.add_argument("--nu-post", type=int, default=None, help="post-smoothing sweeps (overrides --nu)")
     ap.add_argument("--gamma", type=int, default=None, help="multigrid cycle index (default: library's 2)")
     ap.add_argument("--gamma-min", type=int, default=None, help="min coarse-level nodes for a revisit")
+    ap.add_argument("--mg-precision", type=int, default=None, choices=[0, 1],
+                    help="multigrid cycle vectors: 0 = fp64, 1 = fp32 (default: library's)")
     ap.add_argument("--nested-upto", type=int, default=1,
                     help="steps 1..K of a march start from the nested coarse solve (HJB_GUESS_NESTED); "
                          "later steps extrapolate in time; 0 = never nested")
@@ -273,6 +275,8 @@ def run_b200(args):
         mgkw["gamma"] = args.gamma
     if args.gamma_min is not None:
         mgkw["gamma_min_nodes"] = args.gamma_min
+    if args.mg_precision is not None:
+        mgkw["precision"] = args.mg_precision
 
     def step_of(s):          # step index within its march (1..n_steps)
         return (s - 1) % ns + 1

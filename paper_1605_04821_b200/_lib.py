@@ -60,7 +60,7 @@ class MgParams(C.Structure):
     _fields_ = [("nu_pre", C.c_int32), ("nu_post", C.c_int32), ("omega", C.c_double),
                 ("coarse_max_n", C.c_int32), ("coarse_k_mode", C.c_int32), ("max_levels", C.c_int32),
                 ("gather_n", C.c_int32), ("gamma", C.c_int32), ("gamma_min_nodes", C.c_int32),
-                ("coarse_op", C.c_int32)]
+                ("coarse_op", C.c_int32), ("precision", C.c_int32)]
 
 
 class SolveParams(C.Structure):

@@ -13,6 +13,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "hjb.h"
@@ -162,6 +163,7 @@ struct hjb_grid {
   size_t tma_smem = 0;
   int tma_grid = 0;
   bool use_dg = true;          // smoother reads the stored diagonal (Level::dg)
+  bool mg_f32 = false;         // the cycle's vectors in fp32 (hjb_mg_params.precision = 1, one rank)
   int mg_gamma = 1;            // cycle index on levels owning >= gamma_min nodes (hjb_mg_params)
   int nu_coarse = 0;           // > 0: smoothing sweeps on levels >= 1 (experiment knob HJB_NU_COARSE)
   int64_t gamma_min = 0;       // revisit a coarse level only if it has >= gamma_min owned nodes
@@ -234,8 +236,8 @@ struct hjb_grid {
   // kGraphMaxNodes nodes, launch-latency bound) is captured once per hierarchy and replayed
   struct SubGraph {
     size_t level;
-    const double* b;
-    double* out;
+    const void* b;   // the captured cycle's right-hand side / output (fp64 or fp32 vectors)
+    const void* out;
     const uint8_t* pol0;
     cudaGraphExec_t exec;
     int64_t launches;
@@ -597,18 +599,24 @@ static CoefDev coef_u(const hjb_grid* g) {
 }
 
 // ---------------------------------------------------------------------------- dimension dispatch
-template <int D>
+// V: element type of x, b, y, u (float only for the multigrid modes of the fp32 cycle); given
+// explicitly (the pointer arguments do not deduce it: nullptr is a valid x / b / u)
+template <typename T>
+struct nodeduce { using type = T; };
+template <int D, typename V = double>
 static void launch_operator(hjb_grid* g, const LevelDev& L, const CoefDev& C, int mode, int ndot, double dt,
-                            double omega, const uint8_t* pol, const double* x, const double* b, double* y,
-                            const double* u, bool fine = true) {
+                            double omega, const uint8_t* pol, const typename nodeduce<V>::type* x,
+                            const typename nodeduce<V>::type* b, typename nodeduce<V>::type* y,
+                            const typename nodeduce<V>::type* u, bool fine = true) {
   cudaStream_t st = g->st;
   const int cls = mode == OP_DIAG ? HJB_KC_COARSE  // multigrid setup
                   : !fine ? HJB_KC_MG_COARSE
                           : (mode == OP_APPLY ? HJB_KC_APPLY : (mode == OP_RESID ? HJB_KC_RESID : HJB_KC_SMOOTH));
   const double nodes = (double)L.n_own;
   const bool gathers = mode != OP_JACOBI0 && mode != OP_DIAG;
-  const double bpn = 1.0 + 8.0 + (gathers ? 8.0 : 0.0) + (mode != OP_APPLY && mode != OP_DIAG ? 8.0 : 0.0) +
-                     (ndot >= 1 || mode == OP_JACOBI_D ? 8.0 : 0.0) + 8.0 * g->nplanes0;
+  const double vs = (double)sizeof(V);
+  const double bpn = 1.0 + vs + (gathers ? vs : 0.0) + (mode != OP_APPLY && mode != OP_DIAG ? vs : 0.0) +
+                     (ndot >= 1 || mode == OP_JACOBI_D ? vs : 0.0) + 8.0 * g->nplanes0;
   const double fpn = (2.0 * g->P + 1.0) * (1 << D) * 2.0 + 4.0 + 2.0 * ndot;
   const size_t tsm = (size_t)g->K * (g->P * D + D + 1) * sizeof(double);  // control tables in smem
   // the deep rectangle of this level (2D): lean fast-path kernel there, general kernel on the
@@ -664,7 +672,7 @@ static void launch_operator(hjb_grid* g, const LevelDev& L, const CoefDev& C, in
     const LevelDev LL = shape_of(L, RR);                                                                    \
     const double nn = (double)LL.nI * LL.nrows;                                                             \
     LAUNCH(cls, nn, nn * bpn, nn * fpn,                                                                     \
-           k_operator<D, PP, M, ND, DP><<<dims(g, LL, (const void*)k_operator<D, PP, M, ND, DP>, kBX, tsm), \
+           k_operator<D, PP, M, ND, DP, V><<<dims(g, LL, (const void*)k_operator<D, PP, M, ND, DP, V>, kBX, tsm), \
                                          dim3(kBX, kBY), tsm, st>>>(L, C, dt, omega, pol, x, b, y, u,       \
                                                                     g->partial + 2 * nb, RR));              \
     nb += g->nblk_last;                                                                                     \
@@ -688,7 +696,13 @@ static void launch_operator(hjb_grid* g, const LevelDev& L, const CoefDev& C, in
     else OPLP((D > 2 ? 3 : 2), M, ND);                                                                      \
   } while (0)
   if (!g->capturing && (!g->prof_timing || nodes >= kTimeMinNodes)) g->prof.calls[cls] += 1;  // timed subset
-  if (mode == OP_APPLY) {
+  if constexpr (!std::is_same<V, double>::value) {  // fp32 cycle: the multigrid modes only
+    if (mode == OP_RESID) OPL(OP_RESID, 0);
+    else if (mode == OP_JACOBI) OPL(OP_JACOBI, 0);
+    else if (mode == OP_JACOBI_D) OPL(OP_JACOBI_D, 0);
+    else if (mode == OP_DIAG) OPL(OP_DIAG, 0);
+    else OPL(OP_JACOBI0, 0);
+  } else if (mode == OP_APPLY) {
     if (ndot == 0) OPL(OP_APPLY, 0);
     else if (ndot == 1) OPL(OP_APPLY, 1);
     else OPL(OP_APPLY, 2);
@@ -726,6 +740,7 @@ extern "C" void hjb_mg_params_default(int32_t dim, hjb_mg_params* o) {
   o->gamma = (dim == 3) ? 1 : 2;  // 3D: the V-cycle already contracts by <= 0.45 (W measured slower)
   o->gamma_min_nodes = 131072;
   o->coarse_op = 0;  // rediscretised coarse operators (NS); 1 = Galerkin R A P (NEXT-4)
+  o->precision = 0;  // fp64 cycle vectors; 1 = fp32 (preconditioner only, reading xxxi)
 }
 
 extern "C" void hjb_solve_params_default(int32_t dim, hjb_solve_params* o) {
@@ -1646,6 +1661,7 @@ constexpr int64_t kGraphMaxNodes = 70000;  // 257^2 and below (measured: ~4 us o
 
 static hjb_status build_levels(hjb_grid* g, const hjb_mg_params* mp) {
   free_levels(g);
+  g->mg_f32 = mp->precision == 1 && g->R == 1 && mp->coarse_op == 0;
   const int D = g->D;
   int64_t n = g->n;
   {
@@ -1754,6 +1770,14 @@ static hjb_status build_levels(hjb_grid* g, const hjb_mg_params* mp) {
     }
   }
   Level& lc = g->levels.back();
+  if (g->mg_f32) {  // level 0's fp32 right-hand side and iterate (the caller's vectors are fp64)
+    Level& l0 = g->levels[0];
+    const size_t vb = (size_t)l0.elems * sizeof(float);
+    TRY(dalloc((void**)&l0.x, vb));
+    TRY(dalloc((void**)&l0.b, vb));
+    CK(cudaMemsetAsync(l0.x, 0, vb, g->st));
+    CK(cudaMemsetAsync(l0.b, 0, vb, g->st));
+  }
   TRY(dalloc((void**)&lc.Ainv, (size_t)lc.L.n_own * lc.L.n_own * sizeof(double)));
   g->mgp = *mp;
   // graph tail: the first level (>= 1) owning <= kGraphMaxNodes interior nodes whose whole sub-cycle
@@ -1891,7 +1915,10 @@ extern "C" hjb_status hjb_mg_setup(hjb_grid_t g, double dt, const uint8_t* polic
   CK(cudaSetDevice(g->desc.device));
   hjb_mg_params def;
   hjb_mg_params_default(g->D, &def);
-  const hjb_mg_params* p = mp ? mp : &def;
+  hjb_mg_params q = mp ? *mp : def;
+  if (const char* e = getenv("HJB_MG_PRECISION")) q.precision = atoi(e);  // A/B knob
+  const hjb_mg_params* p = &q;
+  if (p->precision < 0 || p->precision > 1) return fail(HJB_ERR_INVALID_ARG, "bad multigrid precision");
   if (p->nu_pre < 1 || p->nu_post < 0 || !(p->omega > 0.0) || p->omega > 1.0 || p->max_levels < 1 ||
       p->gamma < 1 || p->gamma > 3 || p->gamma_min_nodes < 0 || p->coarse_op < 0 || p->coarse_op > 1)
     return fail(HJB_ERR_INVALID_ARG, "bad multigrid parameters");
@@ -1936,8 +1963,15 @@ extern "C" hjb_status hjb_mg_setup(hjb_grid_t g, double dt, const uint8_t* polic
       if (g->galerkin && l >= 1) continue;  // from the Galerkin rows (galerkin_setup)
       Level& lv = g->levels[l];
       const uint8_t* pol = (l == 0) ? g->mg_pol0 : lv.pol;
-      if (g->D == 2) launch_operator<2>(g, lv.L, lv.C, OP_DIAG, 0, dt, 0.0, pol, nullptr, nullptr, lv.dg, nullptr, l == 0);
-      else launch_operator<3>(g, lv.L, lv.C, OP_DIAG, 0, dt, 0.0, pol, nullptr, nullptr, lv.dg, nullptr, l == 0);
+      if (g->mg_f32) {
+        float* dg = reinterpret_cast<float*>(lv.dg);
+        if (g->D == 2) launch_operator<2, float>(g, lv.L, lv.C, OP_DIAG, 0, dt, 0.0, pol, nullptr, nullptr, dg, nullptr, l == 0);
+        else launch_operator<3, float>(g, lv.L, lv.C, OP_DIAG, 0, dt, 0.0, pol, nullptr, nullptr, dg, nullptr, l == 0);
+      } else if (g->D == 2) {
+        launch_operator<2>(g, lv.L, lv.C, OP_DIAG, 0, dt, 0.0, pol, nullptr, nullptr, lv.dg, nullptr, l == 0);
+      } else {
+        launch_operator<3>(g, lv.L, lv.C, OP_DIAG, 0, dt, 0.0, pol, nullptr, nullptr, lv.dg, nullptr, l == 0);
+      }
     }
   CKL();
   g->mg_ready = true;
@@ -1954,12 +1988,19 @@ static double level_omega(const hjb_grid* g, size_t l) {
 
 // one residual (OP_RESID: y = b - A x) or damped-Jacobi sweep (OP_JACOBI / OP_JACOBI_D) on level l:
 // the matrix-free rediscretised operator, or on Galerkin levels (l >= 1) the stored R A P rows
-template <int D>
-static void level_sweep(hjb_grid* g, size_t l, int mode, const double* x, const double* b, double* y) {
+// halo exchanges of a cycle vector (double* plumbing): the fp32 cycle runs on one rank only, where
+// every exchange is a no-op (build_levels: mg_f32 requires R == 1)
+template <typename V>
+static double* hv(V* p) { return reinterpret_cast<double*>(p); }
+template <typename V>
+static V* lvec(double* p) { return reinterpret_cast<V*>(p); }
+
+template <int D, typename V = double>
+static void level_sweep(hjb_grid* g, size_t l, int mode, const V* x, const V* b, V* y) {
   Level& lv = g->levels[l];
   const uint8_t* pol = (l == 0) ? g->mg_pol0 : lv.pol;
   const double dt = g->mg_dt, om = level_omega(g, l);
-  if (g->galerkin && l >= 1) {
+  if constexpr (std::is_same<V, double>::value) if (g->galerkin && l >= 1) {
     halo_end(g);
     const int64_t nn = (int64_t)lv.L.nI * lv.L.nrows;
     const int nb = (int)std::max<int64_t>(1, std::min<int64_t>((nn + 127) / 128, (int64_t)g->sms * 16));
@@ -1972,13 +2013,13 @@ static void level_sweep(hjb_grid* g, size_t l, int mode, const double* x, const 
              k_gal_sweep<true><<<nb, 128, 0, g->st>>>(lv.L, lv.gcol, lv.gval, x, b, lv.dg, om, y));
     return;
   }
-  launch_operator<D>(g, lv.L, lv.C, mode, 0, dt, mode == OP_RESID ? 0.0 : om, pol, x, b, y,
-                     mode == OP_JACOBI_D ? lv.dg : nullptr, l == 0);
+  launch_operator<D, V>(g, lv.L, lv.C, mode, 0, dt, mode == OP_RESID ? 0.0 : om, pol, x, b, y,
+                        mode == OP_JACOBI_D ? lvec<V>(lv.dg) : nullptr, l == 0);
 }
 
 // V(nu_pre, nu_post) from x = 0 on level l: out = M_l^{-1} b
-template <int D>
-static hjb_status vcycle(hjb_grid* g, size_t l, const double* b, double* out) {
+template <int D, typename V = double>
+static hjb_status vcycle(hjb_grid* g, size_t l, const V* b, V* out) {
   // the whole cycle as one graph (one rank, no per-kernel timing), else its launch-bound tail
   const bool whole = l == 0 && g->R == 1 && !g->prof_timing && g->graph_level != (size_t)-1;
   if ((whole || l == g->graph_level) && !g->capturing) {
@@ -1993,7 +2034,7 @@ static hjb_status vcycle(hjb_grid* g, size_t l, const double* b, double* out) {
       g->capturing = true;
       cudaGraph_t graph = nullptr;
       cudaError_t e = cudaStreamBeginCapture(g->st, cudaStreamCaptureModeThreadLocal);
-      hjb_status st = (e == cudaSuccess) ? vcycle<D>(g, l, b, out) : HJB_ERR_CUDA;
+      hjb_status st = (e == cudaSuccess) ? vcycle<D, V>(g, l, b, out) : HJB_ERR_CUDA;
       cudaError_t e2 = cudaStreamEndCapture(g->st, &graph);
       g->capturing = false;
       g->st = keep;
@@ -2023,36 +2064,40 @@ static hjb_status vcycle(hjb_grid* g, size_t l, const double* b, double* out) {
   const bool fine = (l == 0);
   if (l + 1 == g->levels.size()) {
     const int Nc = (int)L.n_own;
-    LAUNCH(HJB_KC_COARSE, Nc, 8.0 * Nc * Nc + 16.0 * Nc, 2.0 * Nc * Nc,
-           k_coarse_solve<D><<<1, 256, Nc * sizeof(double), st>>>(L, lv.Ainv, b, out));
+    LAUNCH(HJB_KC_COARSE, Nc, 8.0 * Nc * Nc + 2.0 * sizeof(V) * Nc, 2.0 * Nc * Nc,
+           k_coarse_solve<D, V><<<1, 256, Nc * sizeof(double), st>>>(L, lv.Ainv, b, out));
     CKL();
     return HJB_OK;
   }
   const double dt = g->mg_dt, om = level_omega(g, l);
   const int npre = (l > 0 && g->nu_coarse > 0) ? g->nu_coarse : g->mgp.nu_pre;
   const int npost = (l > 0 && g->nu_coarse > 0) ? g->nu_coarse : g->mgp.nu_post;
-  double* bufs[2] = {out, lv.tmp};
+  const double vs = (double)sizeof(V);
+  V* bufs[2] = {out, lvec<V>(lv.tmp)};
+  V* res = lvec<V>(lv.res);
   int cur = ((npre - 1 + npost) % 2 == 0) ? 0 : 1;  // so the last sweep lands in `out`
   const int jmode = g->use_dg ? OP_JACOBI_D : OP_JACOBI;
   if (g->use_dg) {
     const double nn = (double)L.n_own;
     if (!g->capturing && (!g->prof_timing || nn >= kTimeMinNodes)) g->prof.calls[fine ? HJB_KC_SMOOTH : HJB_KC_MG_COARSE] += 1;
-    LAUNCH(fine ? HJB_KC_SMOOTH : HJB_KC_MG_COARSE, nn, 24.0 * nn, 2.0 * nn,
-           k_jacobi0_diag<D><<<dims(g, L, (const void*)k_jacobi0_diag<D>), dim3(kBX, kBY), 0, st>>>(L, om, b, lv.dg,
-                                                                                                  bufs[cur]));
+    LAUNCH(fine ? HJB_KC_SMOOTH : HJB_KC_MG_COARSE, nn, 3.0 * vs * nn, 2.0 * nn,
+           k_jacobi0_diag<D, V><<<dims(g, L, (const void*)k_jacobi0_diag<D, V>), dim3(kBX, kBY), 0, st>>>(
+               L, om, b, lvec<V>(lv.dg), bufs[cur]));
     CKL();
   } else {
-    launch_operator<D>(g, L, lv.C, OP_JACOBI0, 0, dt, om, pol, nullptr, b, bufs[cur], nullptr, fine);
+    launch_operator<D, V>(g, L, lv.C, OP_JACOBI0, 0, dt, om, pol, nullptr, b, bufs[cur], nullptr, fine);
   }
   for (int k = 1; k < npre; ++k) {
-    TRY(halo_begin(g, lv, bufs[cur], lv.H));
-    level_sweep<D>(g, l, jmode, bufs[cur], b, bufs[1 - cur]);
+    TRY(halo_begin(g, lv, hv(bufs[cur]), lv.H));
+    level_sweep<D, V>(g, l, jmode, bufs[cur], b, bufs[1 - cur]);
     cur = 1 - cur;
   }
-  TRY(halo_begin(g, lv, bufs[cur], lv.H));
-  level_sweep<D>(g, l, OP_RESID, bufs[cur], b, lv.res);
+  TRY(halo_begin(g, lv, hv(bufs[cur]), lv.H));
+  level_sweep<D, V>(g, l, OP_RESID, bufs[cur], b, res);
   Level& lc = g->levels[l + 1];
-  TRY(halo_exchange(g, lv, lv.res, 1));
+  V* const cb = lvec<V>(lc.b);
+  V* const cx = lvec<V>(lc.x);
+  TRY(halo_exchange(g, lv, hv(res), 1));
   if (lc.replicated && !lv.replicated) {
     // gather level: restrict my coarse rows into the full coarse array, then all-gather them
     std::vector<int64_t> J0, J1;
@@ -2062,39 +2107,57 @@ static hjb_status vcycle(hjb_grid* g, size_t l, const double* b, double* out) {
     view.nrows = (int)((J1[g->rank] - J0[g->rank]) * ipow(lc.L.n - 2, D - 2));
     view.n_own = (int64_t)view.nrows * view.nI;
     if (view.nrows > 0)
-      LAUNCH(HJB_KC_TRANSFER, L.n_own, 8.0 * (L.n_own + view.n_own), 18.0 * view.n_own,
-             k_restrict<D><<<dims(g, view, (const void*)k_restrict<D>), dim3(kBX, kBY), 0, st>>>(L, view, lv.res, lc.b));
+      LAUNCH(HJB_KC_TRANSFER, L.n_own, vs * (L.n_own + view.n_own), 18.0 * view.n_own,
+             k_restrict<D, V, V><<<dims(g, view, (const void*)k_restrict<D, V, V>), dim3(kBX, kBY), 0, st>>>(L, view, res, cb));
     CKL();
-    TRY(gather_rows(g, lc.b, 8, lc.L.row_elems, J0, J1));
+    TRY(gather_rows(g, cb, sizeof(V), lc.L.row_elems, J0, J1));
   } else {
-    LAUNCH(HJB_KC_TRANSFER, L.n_own, 8.0 * (L.n_own + lc.L.n_own), 18.0 * lc.L.n_own,
-           k_restrict<D><<<dims(g, lc.L, (const void*)k_restrict<D>), dim3(kBX, kBY), 0, st>>>(L, lc.L, lv.res, lc.b));
+    LAUNCH(HJB_KC_TRANSFER, L.n_own, vs * (L.n_own + lc.L.n_own), 18.0 * lc.L.n_own,
+           k_restrict<D, V, V><<<dims(g, lc.L, (const void*)k_restrict<D, V, V>), dim3(kBX, kBY), 0, st>>>(L, lc.L, res, cb));
     CKL();
   }
-  TRY(vcycle<D>(g, l + 1, lc.b, lc.x));
+  TRY((vcycle<D, V>(g, l + 1, cb, cx)));
   // revisit decided on the level's GLOBAL interior count, so every rank takes the same branch
   const int gamma = (ipow(lc.L.n - 2, D) >= g->gamma_min) ? g->mg_gamma : 1;
   for (int k = 1; k < gamma && l + 2 < g->levels.size(); ++k) {  // W-cycle: revisit the coarse level
     const uint8_t* pc = lc.pol;
-    TRY(halo_begin(g, lc, lc.x, lc.H));
+    TRY(halo_begin(g, lc, hv(cx), lc.H));
     (void)pc;
-    level_sweep<D>(g, l + 1, OP_RESID, lc.x, lc.b, lc.r2);
-    TRY(vcycle<D>(g, l + 1, lc.r2, lc.e2));
+    level_sweep<D, V>(g, l + 1, OP_RESID, cx, cb, lvec<V>(lc.r2));
+    TRY((vcycle<D, V>(g, l + 1, lvec<V>(lc.r2), lvec<V>(lc.e2))));
     const double nc = (double)lc.L.n_own;
-    LAUNCH(HJB_KC_VECTOR, nc, 24.0 * nc, nc,
-           k_add_interior<D><<<dims(g, lc.L, (const void*)k_add_interior<D>), dim3(kBX, kBY), 0, st>>>(lc.L, lc.e2, lc.x));
+    LAUNCH(HJB_KC_VECTOR, nc, 3.0 * vs * nc, nc,
+           k_add_interior<D, V><<<dims(g, lc.L, (const void*)k_add_interior<D, V>), dim3(kBX, kBY), 0, st>>>(lc.L, lvec<V>(lc.e2), cx));
     CKL();
   }
-  TRY(halo_exchange(g, lc, lc.x, 1));
-  LAUNCH(HJB_KC_TRANSFER, L.n_own, 16.0 * L.n_own + 8.0 * lc.L.n_own, 4.0 * L.n_own,
-         k_prolong_add<D><<<dims(g, L, (const void*)k_prolong_add<D>), dim3(kBX, kBY), 0, st>>>(L, lc.L, lc.x, bufs[cur]));
+  TRY(halo_exchange(g, lc, hv(cx), 1));
+  LAUNCH(HJB_KC_TRANSFER, L.n_own, 2.0 * vs * L.n_own + vs * lc.L.n_own, 4.0 * L.n_own,
+         k_prolong_add<D, V, V><<<dims(g, L, (const void*)k_prolong_add<D, V, V>), dim3(kBX, kBY), 0, st>>>(L, lc.L, cx, bufs[cur]));
   for (int k = 0; k < npost; ++k) {
-    TRY(halo_begin(g, lv, bufs[cur], lv.H));
-    level_sweep<D>(g, l, jmode, bufs[cur], b, bufs[1 - cur]);
+    TRY(halo_begin(g, lv, hv(bufs[cur]), lv.H));
+    level_sweep<D, V>(g, l, jmode, bufs[cur], b, bufs[1 - cur]);
     cur = 1 - cur;
   }
   CKL();
   if (bufs[cur] != out) return fail(HJB_ERR_STATE, "internal: V-cycle buffer parity");
+  return HJB_OK;
+}
+
+// x = M^{-1} b with the fp32 cycle: b rounded to fp32 on entry, the result widened on exit
+template <int D>
+static hjb_status precond_f32(hjb_grid* g, const double* b, double* x) {
+  Level& l0 = g->levels[0];
+  float* b32 = reinterpret_cast<float*>(l0.b);
+  float* x32 = reinterpret_cast<float*>(l0.x);
+  const double nn = (double)g->L0.n_own;
+  LAUNCH(HJB_KC_VECTOR, nn, 12.0 * nn, 0,
+         k_copy_interior<D, double, float><<<dims(g, g->L0, (const void*)k_copy_interior<D, double, float>),
+                                             dim3(kBX, kBY), 0, g->st>>>(g->L0, b, b32));
+  TRY((vcycle<D, float>(g, 0, b32, x32)));
+  LAUNCH(HJB_KC_VECTOR, nn, 12.0 * nn, 0,
+         k_copy_interior<D, float, double><<<dims(g, g->L0, (const void*)k_copy_interior<D, float, double>),
+                                             dim3(kBX, kBY), 0, g->st>>>(g->L0, x32, x));
+  CKL();
   return HJB_OK;
 }
 
@@ -2110,6 +2173,7 @@ static hjb_status precond(hjb_grid* g, bool use_mg, const double* b, double* x) 
     CKL();
     return HJB_OK;
   }
+  if (g->mg_f32) return g->D == 2 ? precond_f32<2>(g, b, x) : precond_f32<3>(g, b, x);
   return g->D == 2 ? vcycle<2>(g, 0, b, x) : vcycle<3>(g, 0, b, x);
 }
 

@@ -181,9 +181,9 @@ struct NodeIn {
   int a;
 };
 
-template <int D, int P, bool XJ, bool BJ>
+template <int D, int P, bool XJ, bool BJ, typename V = double>
 __device__ __forceinline__ void fetch_node(const LevelDev& L, const CoefDev& C, const uint8_t* __restrict__ pol,
-                                           const double* __restrict__ x, const double* __restrict__ b, int col,
+                                           const V* __restrict__ x, const V* __restrict__ b, int col,
                                            int row, NodeIn<D, P>& in) {
   const int j = interior_offset<D>(L, col, row);
 #pragma unroll
@@ -197,8 +197,8 @@ __device__ __forceinline__ void fetch_node(const LevelDev& L, const CoefDev& C, 
   for (int d = 0; d < D; ++d) in.bn[d] = C.b_node ? __ldg(C.b_node + d * C.ld + j) : 0.0;
   in.cn = C.c_node ? __ldg(C.c_node + j) : 0.0;
   in.a = __ldg(pol + j);
-  in.xj = XJ ? __ldg(x + j) : 0.0;
-  in.bj = BJ ? __ldg(b + j) : 0.0;
+  in.xj = XJ ? (double)__ldg(x + j) : 0.0;
+  in.bj = BJ ? (double)__ldg(b + j) : 0.0;
 }
 
 template <int D, int P>
@@ -500,6 +500,41 @@ __device__ __forceinline__ double tap_value(const LevelDev& L, const double* __r
   return interp_at<D, false>(v + tap_base<D>(L, t), L.n, L.n * L.n, t.s);
 }
 
+// fp32 multigrid vectors (hjb_mg_params.precision = 1): the cell corners are fp32, the fractions
+// (fp64 geometry) rounded once to fp32, the multilinear combination in fp32 -- a preconditioner
+// approximation, never part of a residual the solver stops on (reading xxxi)
+template <int D>
+__device__ __forceinline__ double interp_at_f32(const float* __restrict__ p, int sy, int sz, const double* sd) {
+  const float s0 = (float)sd[0], s1 = (float)sd[1];
+  if (D == 2) {
+    const float v00 = __ldg(p), v10 = __ldg(p + 1);
+    const float v01 = __ldg(p + sy), v11 = __ldg(p + sy + 1);
+    const float a = fmaf(s0, v10 - v00, v00);
+    const float b = fmaf(s0, v11 - v01, v01);
+    return (double)fmaf(s1, b - a, a);
+  } else {
+    const float s2 = (float)sd[D > 2 ? 2 : 0];
+    const float v000 = __ldg(p), v100 = __ldg(p + 1);
+    const float v010 = __ldg(p + sy), v110 = __ldg(p + sy + 1);
+    const float v001 = __ldg(p + sz), v101 = __ldg(p + sz + 1);
+    const float v011 = __ldg(p + sz + sy), v111 = __ldg(p + sz + sy + 1);
+    const float a0 = fmaf(s0, v100 - v000, v000);
+    const float b0 = fmaf(s0, v110 - v010, v010);
+    const float a1 = fmaf(s0, v101 - v001, v001);
+    const float b1 = fmaf(s0, v111 - v011, v011);
+    const float p0 = fmaf(s1, b0 - a0, a0);
+    const float p1 = fmaf(s1, b1 - a1, a1);
+    return (double)fmaf(s2, p1 - p0, p0);
+  }
+}
+
+template <int D>
+__device__ __forceinline__ double tap_value(const LevelDev& L, const float* __restrict__ v, const Tap<D>& t) {
+  HJB_ASSERT(tap_base<D>(L, t) >= 0 &&
+             tap_base<D>(L, t) + (D == 2 ? L.n + 1 : L.n * L.n + L.n + 1) < L.local_elems);
+  return interp_at_f32<D>(v + tap_base<D>(L, t), L.n, L.n * L.n, t.s);
+}
+
 // cubic Lagrange weights at x for nodes 0, 1, 2, 3
 __device__ __forceinline__ void cubic_weights(double x, double* w) {
   const double a = x - 1.0, b = x - 2.0, c = x - 3.0;
@@ -553,6 +588,13 @@ template <int D>
 __device__ __forceinline__ double tap_value_u(const LevelDev& L, const CoefDev& C, const double* __restrict__ v,
                                               const Tap<D>& t) {
   if (C.bsamp != nullptr && t.face >= 0) return face_value<D>(C, t);
+  return tap_value<D>(L, v, t);
+}
+
+// fp32 multigrid vectors are corrections with homogeneous boundary data: no face samples
+template <int D>
+__device__ __forceinline__ double tap_value_u(const LevelDev& L, const CoefDev&, const float* __restrict__ v,
+                                              const Tap<D>& t) {
   return tap_value<D>(L, v, t);
 }
 

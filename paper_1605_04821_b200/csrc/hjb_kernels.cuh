@@ -43,12 +43,14 @@ enum OpMode : int {
 // for those (cfg4 fine residual 8.3 -> 7.4 ms, coarse sweeps -5 %); Jacobi and the plain apply keep 80
 template <int MODE, int NDOT>
 constexpr int op_deep_minb() { return (MODE == OP_RESID || NDOT > 0) ? HJB_OP_DEEP_MINB - 1 : HJB_OP_DEEP_MINB; }
-template <int D, int P, int MODE, int NDOT, bool DEEP>
+// V: element type of x, b, y and the stored diagonal u (double; float for the fp32 multigrid
+// vectors of hjb_mg_params.precision = 1 -- geometry and accumulation stay fp64)
+template <int D, int P, int MODE, int NDOT, bool DEEP, typename V = double>
 __global__ void __launch_bounds__(kTX, (DEEP && D == 2) ? op_deep_minb<MODE, NDOT>() : HJB_OP_MINB) k_operator(LevelDev L, CoefDev C, double dt, double omega,
                                                   const uint8_t* __restrict__ pol,
-                                                  const double* __restrict__ x,
-                                                  const double* __restrict__ b, double* __restrict__ y,
-                                                  const double* __restrict__ u, double* partial,
+                                                  const V* __restrict__ x,
+                                                  const V* __restrict__ b, V* __restrict__ y,
+                                                  const V* __restrict__ u, double* partial,
                                                   SkipRect it) {
   constexpr bool GATHER = (MODE != OP_JACOBI0 && MODE != OP_DIAG);
   constexpr bool SELF = (MODE == OP_JACOBI || MODE == OP_JACOBI0 || MODE == OP_DIAG);
@@ -74,7 +76,7 @@ __global__ void __launch_bounds__(kTX, (DEEP && D == 2) ? op_deep_minb<MODE, NDO
     for (int v = 0; v < U; ++v) {
       ok[v] = active && k0 + v * rstride < nk;
       rows[v] = ok[v] ? box_row<D>(L, it, k0 + v * rstride) : 0;
-      if (ok[v]) fetch_node<D, P, XJ, BJ>(L, C, pol, x, b, col, rows[v], in[v]);
+      if (ok[v]) fetch_node<D, P, XJ, BJ, V>(L, C, pol, x, b, col, rows[v], in[v]);
     }
     Node<D> nd[U];
     Tap<D> taps[U][E];
@@ -128,12 +130,12 @@ __global__ void __launch_bounds__(kTX, (DEEP && D == 2) ? op_deep_minb<MODE, NDO
         } else if (MODE == OP_RESID) {
           out = in[v].bj - Ax;
         } else {
-          const double diag = (MODE == OP_JACOBI_D) ? __ldg(u + nd[v].loc) : 1.0 + dt * (wsum[v] - self - c);
+          const double diag = (MODE == OP_JACOBI_D) ? (double)__ldg(u + nd[v].loc) : 1.0 + dt * (wsum[v] - self - c);
           out = xj + omega * (in[v].bj - Ax) / diag;
         }
       }
-      y[nd[v].loc] = out;
-      if (NDOT >= 1 && MODE != OP_JACOBI_D) dots[0] = fma(out, __ldg(u + nd[v].loc), dots[0]);
+      y[nd[v].loc] = (V)out;
+      if (NDOT >= 1 && MODE != OP_JACOBI_D) dots[0] = fma(out, (double)__ldg(u + nd[v].loc), dots[0]);
       if (NDOT >= 2) dots[1] = fma(out, out, dots[1]);
     }
   };
@@ -528,30 +530,31 @@ __global__ void __launch_bounds__(kTX, HJB_SEARCH_MINB) k_cfl(LevelDev L, CoefDe
 
 // first smoothing sweep from x = 0 with the stored diagonal: y = omega b / D (the arithmetic of
 // k_operator<..., OP_JACOBI0>, without its per-node geometry)
-template <int D>
-__global__ void __launch_bounds__(kTX) k_jacobi0_diag(LevelDev L, double omega, const double* __restrict__ b,
-                                                      const double* __restrict__ dg, double* __restrict__ y) {
+template <int D, typename V = double>
+__global__ void __launch_bounds__(kTX) k_jacobi0_diag(LevelDev L, double omega, const V* __restrict__ b,
+                                                      const V* __restrict__ dg, V* __restrict__ y) {
   FOR_INTERIOR(L) {
     const int j = interior_offset<D>(L, col, row);
-    y[j] = omega * __ldg(b + j) / __ldg(dg + j);
+    y[j] = (V)(omega * (double)__ldg(b + j) / (double)__ldg(dg + j));
   }
 }
 
-template <int D>
-__global__ void __launch_bounds__(kTX) k_add_interior(LevelDev L, const double* __restrict__ a,
-                                                      double* __restrict__ y) {
+template <int D, typename V = double>
+__global__ void __launch_bounds__(kTX) k_add_interior(LevelDev L, const V* __restrict__ a,
+                                                          V* __restrict__ y) {
   FOR_INTERIOR(L) {
     const int j = interior_offset<D>(L, col, row);
     y[j] += a[j];
   }
 }
 
-template <int D>
-__global__ void __launch_bounds__(kTX) k_copy_interior(LevelDev L, const double* __restrict__ a,
-                                                           double* __restrict__ b) {
+// b = a at the interior nodes (with a type conversion: the fp32 multigrid's entry and exit)
+template <int D, typename VA = double, typename VB = double>
+__global__ void __launch_bounds__(kTX) k_copy_interior(LevelDev L, const VA* __restrict__ a,
+                                                           VB* __restrict__ b) {
   FOR_INTERIOR(L) {
     const int j = interior_offset<D>(L, col, row);
-    b[j] = a[j];
+    b[j] = (VB)a[j];
   }
 }
 
@@ -591,9 +594,9 @@ __global__ void k_scatter_psi(LevelDev L, int64_t nb, const double* __restrict__
 
 // ================================================================== multigrid transfers
 // full weighting r_f -> b_c at coarse interior nodes (weights 1/4,1/2,1/4 per dim)
-template <int D>
-__global__ void __launch_bounds__(kTX) k_restrict(LevelDev Lf, LevelDev Lc, const double* __restrict__ rf,
-                                                      double* __restrict__ bc) {
+template <int D, typename VF = double, typename VC = double>
+__global__ void __launch_bounds__(kTX) k_restrict(LevelDev Lf, LevelDev Lc, const VF* __restrict__ rf,
+                                                      VC* __restrict__ bc) {
   FOR_INTERIOR(Lc) {
     Node<D> nd;
     node_at<D>(Lc, col, row, nd);
@@ -606,7 +609,7 @@ __global__ void __launch_bounds__(kTX) k_restrict(LevelDev Lf, LevelDev Lc, cons
 #pragma unroll
         for (int o1 = -1; o1 <= 1; ++o1) {
           const double w1 = o1 == 0 ? 0.5 : 0.25;
-          acc = fma(w1 * w2, __ldg(rf + base + o2 * Lf.n + o1), acc);
+          acc = fma(w1 * w2, (double)__ldg(rf + base + o2 * Lf.n + o1), acc);
         }
       }
     } else {
@@ -621,19 +624,19 @@ __global__ void __launch_bounds__(kTX) k_restrict(LevelDev Lf, LevelDev Lc, cons
 #pragma unroll
           for (int o1 = -1; o1 <= 1; ++o1) {
             const double w1 = o1 == 0 ? 0.5 : 0.25;
-            acc = fma(w1 * w2 * w3, __ldg(rf + base + (o3 * nf + o2) * nf + o1), acc);
+            acc = fma(w1 * w2 * w3, (double)__ldg(rf + base + (o3 * nf + o2) * nf + o1), acc);
           }
         }
       }
     }
-    bc[nd.loc] = acc;
+    bc[nd.loc] = (VC)acc;
   }
 }
 
 // x_f += P e_c (multilinear prolongation) at fine interior nodes
-template <int D>
-__global__ void __launch_bounds__(kTX) k_prolong_add(LevelDev Lf, LevelDev Lc, const double* __restrict__ ec,
-                                                         double* __restrict__ xf) {
+template <int D, typename VC = double, typename VF = double>
+__global__ void __launch_bounds__(kTX) k_prolong_add(LevelDev Lf, LevelDev Lc, const VC* __restrict__ ec,
+                                                         VF* __restrict__ xf) {
   FOR_INTERIOR(Lf) {
     Node<D> nd;
     node_at<D>(Lf, col, row, nd);
@@ -662,9 +665,9 @@ __global__ void __launch_bounds__(kTX) k_prolong_add(LevelDev Lf, LevelDev Lc, c
       int64_t loc = (int64_t)(cc[D - 1] - Lc.local_row0);
 #pragma unroll
       for (int d = D - 2; d >= 0; --d) loc = loc * nc + cc[d];
-      acc = fma(w, __ldg(ec + loc), acc);
+      acc = fma(w, (double)__ldg(ec + loc), acc);
     }
-    xf[nd.loc] += acc;
+    xf[nd.loc] = (VF)((double)xf[nd.loc] + acc);
   }
 }
 
@@ -829,14 +832,14 @@ __global__ void k_coarse_invert(double* __restrict__ A, int Nc) {
 }
 
 // x_c = Ainv b_c on the coarsest interior
-template <int D>
-__global__ void k_coarse_solve(LevelDev L, const double* __restrict__ Ainv, const double* __restrict__ b,
-                               double* __restrict__ x) {
+template <int D, typename V = double>
+__global__ void k_coarse_solve(LevelDev L, const double* __restrict__ Ainv, const V* __restrict__ b,
+                               V* __restrict__ x) {
   extern __shared__ double bs[];
   const int Nc = (int)L.n_own;
   for (int t = threadIdx.x; t < Nc; t += blockDim.x) {
     const int row = t / L.nI;
-    bs[t] = b[interior_offset<D>(L, t - row * L.nI, row)];
+    bs[t] = (double)b[interior_offset<D>(L, t - row * L.nI, row)];
   }
   __syncthreads();
   for (int t = threadIdx.x; t < Nc; t += blockDim.x) {
@@ -844,7 +847,7 @@ __global__ void k_coarse_solve(LevelDev L, const double* __restrict__ Ainv, cons
     const double* rowp = Ainv + (int64_t)t * Nc;
     for (int i = 0; i < Nc; ++i) acc = fma(rowp[i], bs[i], acc);
     const int row = t / L.nI;
-    x[interior_offset<D>(L, t - row * L.nI, row)] = acc;
+    x[interior_offset<D>(L, t - row * L.nI, row)] = (V)acc;
   }
 }
 

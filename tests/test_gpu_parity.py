@@ -661,3 +661,51 @@ def test_agmg_stalled_aggregation_step():
         g.close()
     assert math.isfinite(float(np.abs(out[0]).max()))
     assert np.abs(out[0] - out[1]).max() <= 1e-8 * max(1.0, np.abs(out[1]).max())
+
+
+@pytest.mark.parametrize("name,mk", [("cfg1", lambda: bj_config(1)), ("cfg2_513", lambda: bj_config(2, n=513)),
+                                     ("cfg3_33", lambda: bj_config(3, n=33))])
+def test_fp32_cycle_approximates_fp64_cycle(name, mk):
+    """hjb_mg_params.precision = 1 (reading xxxi): the same cycle with fp32 vectors.  Its result is
+    the fp64 cycle's up to fp32 rounding amplified by the cycle (bound 1e-4 relative in the max
+    norm; measured ~1e-6), with the graph replay and the stored fp32 diagonal in the loop."""
+    torch = require_gpu()
+    p = mk()
+    x = to_dev(random_vector(p), torch)
+    g, _ = setup(p)
+    U0 = to_dev(p.g(p.all_idx()), torch)
+    pol = torch.zeros(p.N, dtype=torch.uint8, device="cuda")
+    F = torch.zeros(p.N, dtype=torch.float64, device="cuda")
+    g.policy_update(p.dt, U0 + 0.05 * x, U0, pol, F)
+    ys = {}
+    for prec in (0, 1, 0, 1):
+        g.mg_setup(p.dt, pol, precision=prec)
+        y = torch.zeros(p.N, dtype=torch.float64, device="cuda")
+        g.mg_apply(x, y)
+        g.mg_apply(x, y)   # second application: graph replay
+        ys.setdefault(prec, []).append(y.cpu().numpy())
+    torch.cuda.synchronize()
+    g.close()
+    assert np.array_equal(ys[0][0], ys[0][1]) and np.array_equal(ys[1][0], ys[1][1])
+    a, b = ys[0][0], ys[1][0]
+    rel = np.abs(a - b).max() / np.abs(a).max()
+    assert 0 < rel <= 1e-4, rel
+
+
+@pytest.mark.parametrize("name,mk,steps", [
+    ("cfg0_fp32", lambda: bj_config(0), 3),
+    ("cfg2_129_fp32", lambda: bj_config(2, n=129), 2),
+    ("cfg3_17_fp32", lambda: bj_config(3, n=17), 1),
+])
+def test_step_parity_fp32_cycle(name, mk, steps):
+    """The fp32 preconditioner changes iteration counts only: BiCGSTAB's residuals and stopping tests
+    stay fp64, so the step reaches the oracle's solution to the same bar (reading xxxi)."""
+    p = mk()
+    Ug, _, stats = _gpu_march(p, steps, mg={"precision": 1})
+    Uo = p.g(p.all_idx())
+    for s in range(1, steps + 1):
+        Uo, _, _ = howard_step(p, Uo, s * p.dt, p.dt)
+    err = np.abs(Ug - Uo).max() / max(1.0, np.abs(Uo).max())
+    assert err <= 1e-8, (name, err, stats[-1])
+    for st in stats:
+        assert st["final_rres"] <= 1e-12 or st["final_R"] <= 1e-10

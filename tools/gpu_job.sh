@@ -33,12 +33,6 @@ case $job in
       timeout 1500 ncu --set full --clock-control none --import-source on -k "regex:$re" -s $skip -c ${COUNT:-2} \
         -o $O/prof_$tag "$@" > $O/ncu_$tag.log 2>&1
     echo "ncu rc=$?" >> $O/ncu_$tag.log ;;
-  sanitize)
-    # compute-sanitizer TOOL over CMD (one tool per call of this job); summary in sanitize_<tag>_<tool>.log
-    tag=$1; tool=$2; shift 2
-    timeout ${TIMEOUT:-900} compute-sanitizer --tool $tool --error-exitcode 17 --print-limit 50 \
-      --target-processes all "$@" > $O/sanitize_${tag}_$tool.log 2>&1
-    echo "sanitizer rc=$?" >> $O/sanitize_${tag}_$tool.log ;;
   opbench)
     tag=$1; cfg=$2; shift 2
     timeout 600 python tools/opbench.py --cfg $cfg "$@" > $O/opbench_${tag}_$cfg.log 2>&1 ;;

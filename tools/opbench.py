@@ -68,6 +68,21 @@ if "vcycle" in only:
     for _ in range(max(1, args.reps // 4)):
         g.mg_apply(x, y)
     report("vcycle", args.reps // 4)
+    # whole cycles without per-kernel events (graph replay on one rank), CUDA events on the stream
+    g.profile_reset(False)
+    for prec in (0, 1):
+        g.mg_setup(p.dt, pol, precision=prec)
+        g.mg_apply(x, y)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = max(1, args.reps // 2)
+        e0.record()
+        for _ in range(reps):
+            g.mg_apply(x, y)
+        e1.record()
+        torch.cuda.synchronize()
+        print(f"  [vcycle] precision={prec} (0 fp64, 1 fp32): {e0.elapsed_time(e1) / reps:.3f} ms per cycle "
+              f"(untimed kernels, {reps} cycles)", flush=True)
 if "search" in only:
     g.profile_reset(True)
     for _ in range(max(1, args.reps // 10)):
