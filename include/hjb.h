@@ -214,13 +214,14 @@ typedef struct {
                                 "constructed using the Galerkin principle"),
                                 stored ELL (<= 96 entries per row), 2D on one rank only
                                 (HJB_ERR_UNSUPPORTED otherwise)                               */
-  int32_t precision;         /* element type of the cycle's vectors: 0 = fp64 (default), 1 = fp32
+  int32_t precision;         /* element type of the cycle's vectors: 0 = fp64, 1 = fp32 (default)
                                 (iterates, right-hand sides, residuals and the stored diagonal of
                                 every level in fp32; geometry, weights and row sums in fp64;
                                 b converted on entry, M^{-1} b returned in fp64).  The cycle is
                                 only the preconditioner: BiCGSTAB's residuals, stopping tests and
-                                iterate stay fp64 (reading xxxi).  One rank and
-                                coarse_op = 0 only; otherwise the cycle runs in fp64.          */
+                                iterate stay fp64 (reading xxxi).  coarse_op = 0
+                                only (the Galerkin cycle runs in fp64).  Measured at cfg4: one
+                                cycle 66.6 -> 57.2 ms, the same Krylov iteration counts.       */
 } hjb_mg_params;
 
 void hjb_mg_params_default(int32_t dim, hjb_mg_params* out);

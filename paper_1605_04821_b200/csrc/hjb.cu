@@ -163,7 +163,7 @@ struct hjb_grid {
   size_t tma_smem = 0;
   int tma_grid = 0;
   bool use_dg = true;          // smoother reads the stored diagonal (Level::dg)
-  bool mg_f32 = false;         // the cycle's vectors in fp32 (hjb_mg_params.precision = 1, one rank)
+  bool mg_f32 = false;         // the cycle's vectors in fp32 (hjb_mg_params.precision = 1, not Galerkin)
   int mg_gamma = 1;            // cycle index on levels owning >= gamma_min nodes (hjb_mg_params)
   int nu_coarse = 0;           // > 0: smoothing sweeps on levels >= 1 (experiment knob HJB_NU_COARSE)
   int64_t gamma_min = 0;       // revisit a coarse level only if it has >= gamma_min owned nodes
@@ -408,16 +408,19 @@ static LevelDev full_level(int D, int64_t n, double lo, double hi, double k, dou
 // ---------------------------------------------------------------------------- communication
 // halo exchange of `rows` rows each side of a slab-level array x (no-op for one rank / replicated)
 static void halo_end(hjb_grid* g);
-static hjb_status halo_exchange(hjb_grid* g, const Level& lv, double* x, int64_t rows) {
+// (esz: element size -- 8 for fp64 arrays, 4 for the fp32 cycle vectors)
+static hjb_status halo_exchange(hjb_grid* g, const Level& lv, void* xv, int64_t rows, size_t esz = sizeof(double)) {
   if (g->R == 1 || lv.replicated || rows <= 0) return HJB_OK;
+  char* x = static_cast<char*>(xv);
   if (g->st != g->xst) halo_end(g);
   const int64_t re = lv.L.row_elems, lr0 = lv.L.local_row0;
   const int64_t r0 = lv.r0s[g->rank], r1 = lv.r1s[g->rank];
   Msg m[2];
   int nm = 0;
-  const size_t bytes = (size_t)(rows * re) * sizeof(double);
-  if (g->rank > 0) m[nm++] = Msg{g->rank - 1, x + (r0 - lr0) * re, x + (r0 - rows - lr0) * re, bytes};
-  if (g->rank + 1 < g->R) m[nm++] = Msg{g->rank + 1, x + (r1 - rows - lr0) * re, x + (r1 - lr0) * re, bytes};
+  const size_t bytes = (size_t)(rows * re) * esz;
+  const int64_t e = (int64_t)esz;
+  if (g->rank > 0) m[nm++] = Msg{g->rank - 1, x + (r0 - lr0) * re * e, x + (r0 - rows - lr0) * re * e, bytes};
+  if (g->rank + 1 < g->R) m[nm++] = Msg{g->rank + 1, x + (r1 - rows - lr0) * re * e, x + (r1 - lr0) * re * e, bytes};
   std::string err;
   if (g->comm->exchange(g->st, m, nm, &err) != cudaSuccess)
     return fail(g->desc.comm == HJB_COMM_NCCL ? HJB_ERR_NCCL : HJB_ERR_CUDA, "halo exchange: " + err);
@@ -434,15 +437,15 @@ static void halo_end(hjb_grid* g) {
 // Start the halo exchange of x on the exchange stream and return: the next launch_operator runs
 // the rows that read no halo row while the rows travel, then waits (halo_end) and runs the edge
 // rows.  Falls back to the blocking exchange without a second stream or while capturing a graph.
-static hjb_status halo_begin(hjb_grid* g, const Level& lv, double* x, int64_t rows) {
+static hjb_status halo_begin(hjb_grid* g, const Level& lv, void* x, int64_t rows, size_t esz = sizeof(double)) {
   if (g->R == 1 || lv.replicated || rows <= 0) return HJB_OK;
   halo_end(g);
-  if (!g->xst || g->capturing) return halo_exchange(g, lv, x, rows);
+  if (!g->xst || g->capturing) return halo_exchange(g, lv, x, rows, esz);
   cudaEventRecord(g->xev[0], g->st);                // x is final on the compute stream
   cudaStreamWaitEvent(g->xst, g->xev[0], 0);
   cudaStream_t st = g->st;
   g->st = g->xst;  // the exchange is enqueued on the exchange stream
-  const hjb_status r = halo_exchange(g, lv, x, rows);
+  const hjb_status r = halo_exchange(g, lv, x, rows, esz);
   g->st = st;
   if (r != HJB_OK) return r;
   cudaEventRecord(g->xev[1], g->xst);
@@ -740,7 +743,7 @@ extern "C" void hjb_mg_params_default(int32_t dim, hjb_mg_params* o) {
   o->gamma = (dim == 3) ? 1 : 2;  // 3D: the V-cycle already contracts by <= 0.45 (W measured slower)
   o->gamma_min_nodes = 131072;
   o->coarse_op = 0;  // rediscretised coarse operators (NS); 1 = Galerkin R A P (NEXT-4)
-  o->precision = 0;  // fp64 cycle vectors; 1 = fp32 (preconditioner only, reading xxxi)
+  o->precision = 1;  // fp32 cycle vectors (preconditioner only, reading xxxi); 0 = fp64
 }
 
 extern "C" void hjb_solve_params_default(int32_t dim, hjb_solve_params* o) {
@@ -1332,7 +1335,7 @@ static const Level& fine_level(hjb_grid* g, Level& tmp) {
   return tmp;
 }
 
-static hjb_status halo_begin(hjb_grid* g, const Level& lv, double* x, int64_t rows);
+static hjb_status halo_begin(hjb_grid* g, const Level& lv, void* x, int64_t rows, size_t esz);
 // a const caller array whose halo rows must be filled: copy into scratch first (nranks > 1); the
 // exchange is left in flight (halo_begin) for the launch_operator that follows
 static hjb_status halo_input(hjb_grid* g, const double* x, const double** out) {
@@ -1661,7 +1664,7 @@ constexpr int64_t kGraphMaxNodes = 70000;  // 257^2 and below (measured: ~4 us o
 
 static hjb_status build_levels(hjb_grid* g, const hjb_mg_params* mp) {
   free_levels(g);
-  g->mg_f32 = mp->precision == 1 && g->R == 1 && mp->coarse_op == 0;
+  g->mg_f32 = mp->precision == 1 && mp->coarse_op == 0;
   const int D = g->D;
   int64_t n = g->n;
   {
@@ -1988,10 +1991,6 @@ static double level_omega(const hjb_grid* g, size_t l) {
 
 // one residual (OP_RESID: y = b - A x) or damped-Jacobi sweep (OP_JACOBI / OP_JACOBI_D) on level l:
 // the matrix-free rediscretised operator, or on Galerkin levels (l >= 1) the stored R A P rows
-// halo exchanges of a cycle vector (double* plumbing): the fp32 cycle runs on one rank only, where
-// every exchange is a no-op (build_levels: mg_f32 requires R == 1)
-template <typename V>
-static double* hv(V* p) { return reinterpret_cast<double*>(p); }
 template <typename V>
 static V* lvec(double* p) { return reinterpret_cast<V*>(p); }
 
@@ -2088,16 +2087,16 @@ static hjb_status vcycle(hjb_grid* g, size_t l, const V* b, V* out) {
     launch_operator<D, V>(g, L, lv.C, OP_JACOBI0, 0, dt, om, pol, nullptr, b, bufs[cur], nullptr, fine);
   }
   for (int k = 1; k < npre; ++k) {
-    TRY(halo_begin(g, lv, hv(bufs[cur]), lv.H));
+    TRY(halo_begin(g, lv, bufs[cur], lv.H, sizeof(V)));
     level_sweep<D, V>(g, l, jmode, bufs[cur], b, bufs[1 - cur]);
     cur = 1 - cur;
   }
-  TRY(halo_begin(g, lv, hv(bufs[cur]), lv.H));
+  TRY(halo_begin(g, lv, bufs[cur], lv.H, sizeof(V)));
   level_sweep<D, V>(g, l, OP_RESID, bufs[cur], b, res);
   Level& lc = g->levels[l + 1];
   V* const cb = lvec<V>(lc.b);
   V* const cx = lvec<V>(lc.x);
-  TRY(halo_exchange(g, lv, hv(res), 1));
+  TRY(halo_exchange(g, lv, res, 1, sizeof(V)));
   if (lc.replicated && !lv.replicated) {
     // gather level: restrict my coarse rows into the full coarse array, then all-gather them
     std::vector<int64_t> J0, J1;
@@ -2121,7 +2120,7 @@ static hjb_status vcycle(hjb_grid* g, size_t l, const V* b, V* out) {
   const int gamma = (ipow(lc.L.n - 2, D) >= g->gamma_min) ? g->mg_gamma : 1;
   for (int k = 1; k < gamma && l + 2 < g->levels.size(); ++k) {  // W-cycle: revisit the coarse level
     const uint8_t* pc = lc.pol;
-    TRY(halo_begin(g, lc, hv(cx), lc.H));
+    TRY(halo_begin(g, lc, cx, lc.H, sizeof(V)));
     (void)pc;
     level_sweep<D, V>(g, l + 1, OP_RESID, cx, cb, lvec<V>(lc.r2));
     TRY((vcycle<D, V>(g, l + 1, lvec<V>(lc.r2), lvec<V>(lc.e2))));
@@ -2130,11 +2129,11 @@ static hjb_status vcycle(hjb_grid* g, size_t l, const V* b, V* out) {
            k_add_interior<D, V><<<dims(g, lc.L, (const void*)k_add_interior<D, V>), dim3(kBX, kBY), 0, st>>>(lc.L, lvec<V>(lc.e2), cx));
     CKL();
   }
-  TRY(halo_exchange(g, lc, hv(cx), 1));
+  TRY(halo_exchange(g, lc, cx, 1, sizeof(V)));
   LAUNCH(HJB_KC_TRANSFER, L.n_own, 2.0 * vs * L.n_own + vs * lc.L.n_own, 4.0 * L.n_own,
          k_prolong_add<D, V, V><<<dims(g, L, (const void*)k_prolong_add<D, V, V>), dim3(kBX, kBY), 0, st>>>(L, lc.L, cx, bufs[cur]));
   for (int k = 0; k < npost; ++k) {
-    TRY(halo_begin(g, lv, hv(bufs[cur]), lv.H));
+    TRY(halo_begin(g, lv, bufs[cur], lv.H, sizeof(V)));
     level_sweep<D, V>(g, l, jmode, bufs[cur], b, bufs[1 - cur]);
     cur = 1 - cur;
   }
