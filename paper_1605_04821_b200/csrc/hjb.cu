@@ -173,6 +173,16 @@ struct hjb_grid {
   double* rng_part = nullptr; // k_field_ranges block partials
   double2* upair = nullptr;   // (U_i, U_{i+1}) pair copy of the searched U (k_search_deep2)
   double4* uquad = nullptr;   // cell-corner copy of the searched U (k_search_deep2<..., QUADS>)
+  // certified search skipping inside hjb_step (k_search_deep2<..., GAP>)
+  float* gap = nullptr;             // [N] per-node lower bound of H_second - H_best
+  double* uold[2] = {nullptr, nullptr};  // U at the previous search of the step (ping-pong)
+  int uold_cur = 0;
+  unsigned long long* d_gapred = nullptr;  // k_gap_delta maxima (+ the skipped-CTA counter)
+  bool gap_on = false;      // the next policy_update_dev scans with gap bookkeeping
+  bool gap_valid = false;   // gap / uold describe the previous search of this step
+  double gap_G = 0.0, gap_D = 0.0, gap_umax = 0.0;  // cell-difference / max |dU| / max |U| bounds
+  bool gap_first = true;    // the next GAP scan is a full one (bskip < 0)
+  int64_t gap_skipped = 0, gap_ctas = 0;  // diagnostics (HJB_SKIP_DEBUG)
   bool search3 = false;       // k_search_deep3 on the deep rectangle (opt-in, HJB_SEARCH3=1)
   bool search2p = false;      // k_search_deep2p (software-pipelined) on the deep rectangle (opt-in)
   // halo exchange overlapped with the rows that do not read halos (nranks > 1, halo_begin): the
@@ -875,6 +885,10 @@ extern "C" hjb_status hjb_grid_destroy(hjb_grid_t g) {
   cudaFree(g->rng_part);
   cudaFree(g->upair);
   cudaFree(g->uquad);
+  cudaFree(g->gap);
+  cudaFree(g->uold[0]);
+  cudaFree(g->uold[1]);
+  cudaFree(g->d_gapred);
   cudaFree(g->vtheta);
   cudaFree(g->d_flag);
   agmg_free(g);
@@ -1368,17 +1382,18 @@ static bool search2_ok(hjb_grid* g) {
   return true;
 }
 
-template <int P, int Q, bool STRIP, bool QUADS = false, int KU = 0>
+template <int P, int Q, bool STRIP, bool QUADS = false, int KU = 0, bool GAP = false>
 static void search2_launch(hjb_grid* g, const LevelDev& LL, double dt, const double* U, const double* Uprev,
                            uint8_t* pol, double* F, const SkipRect& rect, const STab& tab, const STabQuad& quad,
-                           int* nblk) {
-  const void* fn = (const void*)k_search_deep2<P, Q, STRIP, QUADS, KU>;
+                           int* nblk, const GapArgs& ga = GapArgs{}) {
+  const void* fn = (const void*)k_search_deep2<P, Q, STRIP, QUADS, KU, GAP>;
   const int64_t tiles = (int64_t)((LL.nI + kSBX - 1) / kSBX) * ((LL.nrows + kS2Y - 1) / kS2Y);
   const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, std::min<int64_t>((int64_t)occupancy_of(fn, 0, kS2T) * g->sms, kMaxBlocks)));
   LAUNCH(HJB_KC_SEARCH, 0, 0, 0,
-         k_search_deep2<P, Q, STRIP, QUADS, KU><<<nb, dim3(kSBX, kS2Y), 0, g->st>>>(
+         k_search_deep2<P, Q, STRIP, QUADS, KU, GAP><<<nb, dim3(kSBX, kS2Y), 0, g->st>>>(
              g->L0, STRIP ? coef_u(g) : g->C0, dt, U, g->upair, g->uquad, Uprev, pol, F, g->partial + 2 * *nblk, rect,
-             tab, quad));
+             tab, quad, ga));
+  if (GAP) g->gap_ctas += nb > 0 ? (int64_t)((LL.nI + kSBX - 1) / kSBX) * ((LL.nrows + kS2Y - 1) / kS2Y) : 0;
   *nblk += nb;
 }
 
@@ -1449,6 +1464,40 @@ static void search2_tables(hjb_grid* g, STab& tab, STabQuad& quad) {
 }
 
 // the deep rectangle (strips = nullptr) or the boundary-layer strips around it (ns boxes)
+// this search's skip bound and rounding margins (k_search_deep2<..., GAP>) from the control tables:
+//   |H^a_j(U) - H^a_j(U_old)| <= sum_e w_e |I dU(z_e) - dU_j| + |c^a| |dU_j|
+// and a multilinear interpolant moves by at most G per cell along either axis (G = max |dU_i' - dU_i|
+// over grid edges), so |I dU(z_e) - dU_j| <= G (|o_e,1| + |o_e,2|) with o_e the endpoint offsets in
+// cells, bounded by the scale-field maxima (DESIGN.md §6 "Certified search skipping")
+template <int P, int Q>
+static GapArgs gap_args(hjb_grid* g, const STab& tab) {
+  using T = STabLayout<P, Q>;
+  GapArgs ga{};
+  ga.gap = g->gap;
+  ga.nskip = reinterpret_cast<int*>(g->d_gapred + 3);
+  const double eps = 2.220446049250313e-16;
+  const double G = g->gap_G + 4.0 * eps * g->gap_umax, Dm = g->gap_D + 2.0 * eps * g->gap_umax;
+  const double bsmax = g->h_rng[2 * P + 1];
+  double B = 0.0, wc = 0.0, fc = 0.0;
+  for (int q = 0; q < 8; ++q) ga.fbmax[q] = 0.0;
+  for (int a = 0; a < g->K; ++a) {
+    const double* t = tab.v + a * T::S;
+    double b = std::fabs(t[T::C]) * Dm;
+    for (int p = 0; p < P; ++p)
+      b += 2.0 * t[T::W + p] * G * g->L0.kh * g->h_rng[2 * p + 1] *
+           (std::fabs(t[T::SD + 2 * p]) + std::fabs(t[T::SD + 2 * p + 1]));
+    b += t[T::WD] * G * g->L0.k2h * bsmax * (std::fabs(t[T::BD]) + std::fabs(t[T::BD + 1]));
+    B = std::max(B, b);
+    wc = std::max(wc, 2.0 * t[T::WSUM] + std::fabs(t[T::C]));
+    fc = std::max(fc, std::fabs(t[T::FC]));
+    for (int q = 0; q < Q && q < 8; ++q) ga.fbmax[q] = std::max(ga.fbmax[q], std::fabs(t[T::FB + q]));
+  }
+  ga.bskip = g->gap_first ? -1.0 : B * (1.0 + 1e-9);
+  ga.gmargin = 128.0 * eps * wc * g->gap_umax;
+  ga.fcmax = fc;
+  return ga;
+}
+
 static hjb_status launch_search2(hjb_grid* g, double dt, const double* U, const double* Uprev, uint8_t* pol,
                                  double* F, const SkipRect& rect, int* nblk, const SkipRect* strips = nullptr,
                                  int ns = 0) {
@@ -1466,6 +1515,9 @@ static hjb_status launch_search2(hjb_grid* g, double dt, const double* U, const 
       search2_launch<PP, QQ, false, true, 32>(g, LL, dt, U, Uprev, pol, F, rect, tab, quad, nblk); \
     else if (!strips && g->uquad)                                                                  \
       search2_launch<PP, QQ, false, true>(g, LL, dt, U, Uprev, pol, F, rect, tab, quad, nblk);     \
+    else if (!strips && g->gap_on)                                                                 \
+      search2_launch<PP, QQ, false, false, 0, true>(g, LL, dt, U, Uprev, pol, F, rect, tab, quad,  \
+                                                    nblk, gap_args<PP, QQ>(g, tab));               \
     else if (!strips)                                                                              \
       search2_launch<PP, QQ, false>(g, LL, dt, U, Uprev, pol, F, rect, tab, quad, nblk);           \
     for (int k = 0; k < ns; ++k) {                                                                 \
@@ -1486,6 +1538,45 @@ static hjb_status launch_search2(hjb_grid* g, double dt, const double* U, const 
 }
 
 // U's halo rows must already be exchanged
+// Certified search skipping, called before each search of hjb_step's policy iteration (first: the
+// step's first search, a full scan that records the gaps).  One pass of k_gap_delta gives max |U|,
+// max |dU| and the largest cell difference of dU = U - U_old, and snapshots U as the next U_old.
+static hjb_status gap_prepare(hjb_grid* g, const double* U, bool first) {
+  g->gap_on = false;
+  if (g->R != 1 || g->D != 2 || g->C0.c_node || getenv("HJB_NO_SKIP") || getenv("HJB_QUADS") ||
+      getenv("HJB_SEARCH3") || getenv("HJB_SEARCH2P") || getenv("HJB_KUNROLL") || !search2_ok(g)) {
+    g->gap_valid = false;
+    return HJB_OK;
+  }
+  const size_t N = (size_t)g->N;
+  if (!g->gap) {
+    TRY(dalloc((void**)&g->gap, N * sizeof(float)));
+    TRY(dalloc((void**)&g->uold[0], N * sizeof(double)));
+    TRY(dalloc((void**)&g->uold[1], N * sizeof(double)));
+    TRY(dalloc((void**)&g->d_gapred, 4 * sizeof(unsigned long long)));
+  }
+  first = first || !g->gap_valid;
+  CK(cudaMemsetAsync(g->d_gapred, 0, 4 * sizeof(unsigned long long), g->st));
+  const double* uo = first ? nullptr : g->uold[g->uold_cur];
+  double* un = g->uold[first ? g->uold_cur : 1 - g->uold_cur];
+  const double nn = (double)N;
+  LAUNCH(HJB_KC_SEARCH, nn, (first ? 16.0 : 24.0) * nn, 6.0 * nn,
+         k_gap_delta<<<(int)std::min<int64_t>(((int64_t)N + 255) / 256, (int64_t)g->sms * 8), 256, 0, g->st>>>(
+             U, uo, un, g->L0.n, (int64_t)N, g->d_gapred));
+  CKL();
+  double m[3];
+  CK(cudaMemcpyAsync(m, g->d_gapred, 3 * sizeof(double), cudaMemcpyDeviceToHost, g->st));
+  CK(cudaStreamSynchronize(g->st));
+  if (!first) g->uold_cur = 1 - g->uold_cur;
+  g->gap_umax = m[0];
+  g->gap_D = m[1];
+  g->gap_G = m[2];
+  g->gap_first = first;
+  g->gap_on = std::isfinite(m[0]) && std::isfinite(m[1]) && std::isfinite(m[2]);
+  if (!g->gap_on) g->gap_valid = false;
+  return HJB_OK;
+}
+
 static hjb_status policy_update_dev(hjb_grid* g, double dt, const double* U, const double* Uprev, uint8_t* pol,
                                     double* F, hjb_pi_stats* out) {
   halo_end(g);  // the search kernels take no row split: U's halo rows must have arrived
@@ -1516,6 +1607,7 @@ static hjb_status policy_update_dev(hjb_grid* g, double dt, const double* U, con
   const int nds = (has_deep && !wp && !deep2) ? ring_strips(rect, tiles, dstrips) : 0;
   // with k_search_deep2 the boundary strips take its STRIP variant (HJB_NO_STRIP2: the general kernel)
   const bool strip2 = deep2 && !getenv("HJB_NO_STRIP2");
+  if (!deep2 || g->uquad) g->gap_on = false;  // gap bookkeeping lives in the plain deep2 kernel only
   SkipRect s2strips[6];
   int ns2 = 0;
   if (strip2) {
@@ -1614,6 +1706,19 @@ static hjb_status policy_update_dev(hjb_grid* g, double dt, const double* U, con
   double changed = 0.0;
   const double R = host_finalize(g, nblk, 0x1u, SC_NONE, &err, &changed);
   if (err != HJB_OK) return err;
+  if (g->gap_on) {  // the scan kept the gaps: the next search of the step may skip
+    unsigned long long ns = 0;
+    CK(cudaMemcpy(&ns, g->d_gapred + 3, sizeof(ns), cudaMemcpyDeviceToHost));
+    g->gap_skipped += (int64_t)(ns & 0xffffffffu);
+    if (getenv("HJB_SKIP_DEBUG"))
+      fprintf(stderr, "[hjb] search: %s, max|U| %.3e max|dU| %.3e G %.3e, skipped CTAs %lld (total so far %lld / %lld)\n",
+              g->gap_first ? "full scan" : "gap-certified", g->gap_umax, g->gap_D, g->gap_G,
+              (long long)(ns & 0xffffffffu), (long long)g->gap_skipped, (long long)g->gap_ctas);
+    g->gap_valid = true;
+    g->gap_on = false;
+  } else {
+    g->gap_valid = false;
+  }
   if (out) {
     out->R_max = R;
     out->changed = (int64_t)changed;
@@ -2969,6 +3074,7 @@ static hjb_status implicit_pi(hjb_grid* g, double dt, const double* dprev, doubl
     hjb_pi_stats pis{};
     cudaEventRecord(g->ev[0], st);
     TRY(halo_exchange(g, lv0, dU, g->lay.halo));
+    TRY(gap_prepare(g, dU, it == 1));
     TRY(policy_update_dev(g, dt, dU, dprev, dpol, g->F, &pis));
     cudaEventRecord(g->ev[1], st);
     cudaEventSynchronize(g->ev[1]);

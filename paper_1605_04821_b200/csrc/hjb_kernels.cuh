@@ -1,5 +1,7 @@
 // hjb_kernels.cuh -- __global__ kernels of the hot path (sm_100a, fp64).
 #pragma once
+#include <type_traits>
+
 #include "hjb_device.cuh"
 
 namespace hjb {
@@ -43,10 +45,20 @@ enum OpMode : int {
 // for those (cfg4 fine residual 8.3 -> 7.4 ms, coarse sweeps -5 %); Jacobi and the plain apply keep 80
 template <int MODE, int NDOT>
 constexpr int op_deep_minb() { return (MODE == OP_RESID || NDOT > 0) ? HJB_OP_DEEP_MINB - 1 : HJB_OP_DEEP_MINB; }
+// fp32 cycle vectors (hjb_mg_params.precision = 1): half the registers per gathered corner
+#ifndef HJB_OP_DEEP_MINB_F32
+#define HJB_OP_DEEP_MINB_F32 HJB_OP_DEEP_MINB
+#endif
+template <int MODE, int NDOT, typename V>
+constexpr int op_deep_minb_v() {
+  return std::is_same<V, double>::value ? op_deep_minb<MODE, NDOT>()
+                                        : ((MODE == OP_JACOBI_D || MODE == OP_JACOBI || MODE == OP_JACOBI0)
+                                               ? HJB_OP_DEEP_MINB_F32 : op_deep_minb<MODE, NDOT>());
+}
 // V: element type of x, b, y and the stored diagonal u (double; float for the fp32 multigrid
 // vectors of hjb_mg_params.precision = 1 -- geometry and accumulation stay fp64)
 template <int D, int P, int MODE, int NDOT, bool DEEP, typename V = double>
-__global__ void __launch_bounds__(kTX, (DEEP && D == 2) ? op_deep_minb<MODE, NDOT>() : HJB_OP_MINB) k_operator(LevelDev L, CoefDev C, double dt, double omega,
+__global__ void __launch_bounds__(kTX, (DEEP && D == 2) ? op_deep_minb_v<MODE, NDOT, V>() : HJB_OP_MINB) k_operator(LevelDev L, CoefDev C, double dt, double omega,
                                                   const uint8_t* __restrict__ pol,
                                                   const V* __restrict__ x,
                                                   const V* __restrict__ b, V* __restrict__ y,
@@ -589,6 +601,34 @@ __global__ void k_scatter_psi(LevelDev L, int64_t nb, const double* __restrict__
     int64_t loc = (slow - L.local_row0);
     for (int d = D - 2; d >= 0; --d) loc = loc * n + i[d];
     U[loc] = psi[q];
+  }
+}
+
+// ================================================================== certified search skipping
+// One pass over the whole local grid (interior and boundary): out[0] = max |U|, out[1] = max |dU|,
+// out[2] = max over grid edges of |dU_i' - dU_i| (i' the neighbour along x1 or x2), dU = U - uo;
+// un = U (the next search's U_old; uo == nullptr: only max |U| and the copy).  Non-negative doubles
+// order like their bit patterns, so the maxima are atomicMax on the 64-bit words.
+__global__ void __launch_bounds__(256) k_gap_delta(const double* __restrict__ U, const double* __restrict__ uo,
+                                                   double* __restrict__ un, int64_t n, int64_t N,
+                                                   unsigned long long* __restrict__ out) {
+  double m[3] = {0.0, 0.0, 0.0};
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < N; j += (int64_t)gridDim.x * blockDim.x) {
+    const double u = U[j];
+    un[j] = u;
+    m[0] = fmax(m[0], fabs(u));
+    if (uo) {
+      const double d = u - uo[j];
+      m[1] = fmax(m[1], fabs(d));
+      if ((j % n) != n - 1) m[2] = fmax(m[2], fabs((U[j + 1] - uo[j + 1]) - d));
+      if (j + n < N) m[2] = fmax(m[2], fabs((U[j + n] - uo[j + n]) - d));
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    double v = m[k];
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out + k, (unsigned long long)__double_as_longlong(v));
   }
 }
 

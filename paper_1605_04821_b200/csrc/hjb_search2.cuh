@@ -109,6 +109,15 @@ struct STabLayout {
                        ABD = W + P + 5,  // [2] |b_dir|: the drift step's magnitude per axis
                        S = W + P + 7;
 };
+// certified search skipping (k_search_deep2<..., GAP>): per-node gap bounds and this search's bound
+struct GapArgs {
+  float* gap;          // [N] lower bound of H_second - H_best per node (fp32, rounded down)
+  double bskip;        // bound of |H^a_j(U) - H^a_j(U_old)| over all a, j; < 0: full scan everywhere
+  double gmargin;      // rounding margin, U part: 4 * 32 eps (2 wsum + |c|)_max max|U|
+  double fcmax;        // max_a |f_ctrl^a|
+  double fbmax[8];     // max_a |f_basis^a_q|
+  int* nskip;          // device counter of skipped CTAs
+};
 struct STabQuad {
   int v[256];  // drift endpoint quadrant per control: bit 0 = cell left of the node (x), bit 1 = below (y)
 };
@@ -173,7 +182,16 @@ constexpr int kSuperCols = HJB_SUPER_COLS;  // tile columns per super-column (16
 // 11 instead of 14 fp64 operations per pair.
 // KU > 0: the control loop is fully unrolled for exactly KU = C.K controls, so every control-table
 // entry is a constant-bank operand of its instruction (no LDC per entry).
-template <int P, int Q, bool STRIP = false, bool QUADS = false, int KU = 0>
+// GAP (policy iteration inside hjb_step, deep rectangle, one rank): certified search skipping.
+// gap[j] holds a lower bound of H_second - H_best at node j (fp32, rounded down) from the previous
+// search of the step.  Between two searches H^a_j(U) changes by at most bskip for every a (the host
+// bound from the per-axis cell differences of dU = U - U_old, DESIGN.md §6 "Certified search
+// skipping"), so when gap[j] > 2 bskip + gmargin (gmargin: the rounding of both evaluations) the
+// argmin at j cannot change.  A CTA whose nodes all pass that test evaluates only the current
+// control of each node (F, R from it: bit-identical to the full scan, whose minimum it is) and
+// lowers the stored gaps by 2 bskip; otherwise the CTA scans all K controls and stores fresh gaps.
+// bskip < 0: full scan everywhere (the step's first search).
+template <int P, int Q, bool STRIP = false, bool QUADS = false, int KU = 0, bool GAP = false>
 __global__ void __launch_bounds__(kS2T, HJB_SEARCH2_MINB) k_search_deep2(LevelDev L, CoefDev C, double dt,
                                                                         const double* __restrict__ U,
                                                                         const double2* __restrict__ UP,
@@ -182,7 +200,8 @@ __global__ void __launch_bounds__(kS2T, HJB_SEARCH2_MINB) k_search_deep2(LevelDe
                                                                         uint8_t* __restrict__ pol,
                                                                         double* __restrict__ F, double* partial,
                                                                         SkipRect it, const __grid_constant__ STab tab,
-                                                                        const __grid_constant__ STabQuad quad) {
+                                                                        const __grid_constant__ STabQuad quad,
+                                                                        const GapArgs ga) {
   using T = STabLayout<P, Q>;
   double red[2] = {0.0, 0.0};
   const int nk = box_lines(it);
@@ -241,13 +260,36 @@ __global__ void __launch_bounds__(kS2T, HJB_SEARCH2_MINB) k_search_deep2(LevelDe
       const double* u0 = U + nd.loc;
       const double* u1 = u0 + n;
       const double4* q4 = Q4 + nd.loc;
-      double best = INFINITY, fbest = 0.0;
+      double best = INFINITY, fbest = 0.0, best2 = INFINITY;
       int arg = 0;
+      // GAP: the CTA-uniform skip decision (lanes past the box edge vote yes)
+      int a_lo = 0, a_hi = KU > 0 ? KU : C.K;
+      bool skip = false;
+      float gj = 0.0f;
+      double gmarg = 0.0;
+      if constexpr (GAP) {
+        // rounding margin of this node: 4 E_j, E_j <= 32 eps S_j, S_j = sum of |terms| of any H^a_j:
+        // ga.gmargin covers the U terms (2 wsum + |c|) max|U|, the f terms are bounded per node
+        double fs = ga.fcmax;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) fs = fma(ga.fbmax[q], fabs(feat[q]), fs);
+        gmarg = ga.gmargin + 128.0 * 2.220446049250313e-16 * fs;
+        gj = valid ? ga.gap[nd.loc] : 0.0f;
+        const bool ok = ga.bskip >= 0.0 && (double)gj > 2.0 * ga.bskip + gmarg;
+        skip = __syncthreads_and(ok || !valid) != 0;
+        if (skip) {
+          a_lo = pol[nd.loc];
+          a_hi = a_lo + 1;
+          if (threadIdx.x == 0 && threadIdx.y == 0) atomicAdd(ga.nskip, 1);
+        }
+      }
 #pragma unroll(KU > 0 ? KU : kS2Unroll)
-      for (int a = 0; a < (KU > 0 ? KU : C.K); ++a) {
+      for (int a = a_lo; a < a_hi; ++a) {
 #if HJB_SEARCH2_SYNC
-        __syncwarp();
-        if ((a & (HJB_SEARCH2_SYNC - 1)) == 0) __syncthreads();  // keep the CTA's 4 lines in lockstep
+        if (!GAP || !skip) {
+          __syncwarp();
+          if ((a & (HJB_SEARCH2_SYNC - 1)) == 0) __syncthreads();  // keep the CTA's 4 lines in lockstep
+        }
 #endif
         const double* t = tab.v + a * T::S;
         if (STRIP) {
@@ -378,9 +420,19 @@ __global__ void __launch_bounds__(kS2T, HJB_SEARCH2_MINB) k_search_deep2(LevelDe
         const double cc = nd.cn + t[T::C];
         const double H = (acc - t[T::WSUM] * Uj) + cc * Uj + f;
         if (H < best) {  // strict: lowest index wins exact ties (reading iv)
+          if constexpr (GAP) best2 = best;
           best = H;
           arg = a;
           fbest = f;
+        } else if constexpr (GAP) {
+          best2 = fmin(best2, H);
+        }
+      }
+      if constexpr (GAP) {
+        if (valid) {
+          // skipped: the bound carried forward; scanned: the fresh gap less the rounding margin
+          const double gn = skip ? (double)gj - 2.0 * ga.bskip : (best2 - best) - gmarg;
+          ga.gap[nd.loc] = __double2float_rd(fmax(gn, 0.0));
         }
       }
       if (valid) {

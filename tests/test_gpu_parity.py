@@ -711,3 +711,29 @@ def test_step_parity_fp32_cycle(name, mk, steps):
     assert err <= 1e-8, (name, err, stats[-1])
     for st in stats:
         assert st["final_rres"] <= 1e-12 or st["final_R"] <= 1e-10
+
+
+@pytest.mark.parametrize("name,mk,steps", [("cfg2_513", lambda: bj_config(2, n=513), 3),
+                                           ("cfg1", lambda: bj_config(1), 3)])
+def test_certified_search_skipping_is_bit_identical(name, mk, steps, monkeypatch, capfd):
+    """Certified search skipping: a CTA whose nodes all keep a stored gap larger than
+    twice the bound on the change of every H^a evaluates only the current control.  The skipped
+    nodes' argmin provably cannot change, and F and R come from the same control evaluation, so the
+    march is bit-identical to full scans (HJB_NO_SKIP=1): U, policy, PI and Krylov counts."""
+    from paper_1605_04821_b200 import _lib
+    out = {}
+    for mode in ("skip", "full"):
+        monkeypatch.delenv("HJB_NO_SKIP", raising=False)
+        monkeypatch.setenv("HJB_SKIP_DEBUG", "1")
+        if mode == "full":
+            monkeypatch.setenv("HJB_NO_SKIP", "1")
+        p = mk()
+        U, pol, stats = _gpu_march(p, steps, guess=_lib.HJB_GUESS_PREV, pi_forcing=1e-2)
+        out[mode] = (U, pol, [(s["pi_iters"], s["krylov_iters_total"], s["final_R"]) for s in stats])
+    err = capfd.readouterr().err
+    assert np.array_equal(out["skip"][0], out["full"][0])
+    assert np.array_equal(out["skip"][1], out["full"][1])
+    assert out["skip"][2] == out["full"][2]
+    certified = [ln for ln in err.splitlines() if "gap-certified" in ln]
+    assert certified, err[-2000:]
+    assert max(int(ln.split("skipped CTAs ")[1].split()[0]) for ln in certified) > 0, certified
