@@ -1543,7 +1543,10 @@ static hjb_status launch_search2(hjb_grid* g, double dt, const double* U, const 
 // max |dU| and the largest cell difference of dU = U - U_old, and snapshots U as the next U_old.
 static hjb_status gap_prepare(hjb_grid* g, const double* U, bool first) {
   g->gap_on = false;
-  if (g->R != 1 || g->D != 2 || g->C0.c_node || getenv("HJB_NO_SKIP") || getenv("HJB_QUADS") ||
+  // opt-in (HJB_SKIP=1): measured slower at cfg4 (1708 vs 1600 ms per step, profiles/r02_s_*): the GAP
+  // scan costs +25 % per full search and the grid-wide bound certifies too few CTAs
+  const char* skip_env = getenv("HJB_SKIP");
+  if (!skip_env || atoi(skip_env) == 0 || g->R != 1 || g->D != 2 || g->C0.c_node || getenv("HJB_NO_SKIP") || getenv("HJB_QUADS") ||
       getenv("HJB_SEARCH3") || getenv("HJB_SEARCH2P") || getenv("HJB_KUNROLL") || !search2_ok(g)) {
     g->gap_valid = false;
     return HJB_OK;
@@ -1560,7 +1563,8 @@ static hjb_status gap_prepare(hjb_grid* g, const double* U, bool first) {
   const double* uo = first ? nullptr : g->uold[g->uold_cur];
   double* un = g->uold[first ? g->uold_cur : 1 - g->uold_cur];
   const double nn = (double)N;
-  LAUNCH(HJB_KC_SEARCH, nn, (first ? 16.0 : 24.0) * nn, 6.0 * nn,
+  // a streaming pass: counted with the vector kernels (not in the search's flop roofline)
+  LAUNCH(HJB_KC_VECTOR, nn, (first ? 16.0 : 24.0) * nn, 6.0 * nn,
          k_gap_delta<<<(int)std::min<int64_t>(((int64_t)N + 255) / 256, (int64_t)g->sms * 8), 256, 0, g->st>>>(
              U, uo, un, g->L0.n, (int64_t)N, g->d_gapred));
   CKL();

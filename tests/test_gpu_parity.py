@@ -724,6 +724,8 @@ def test_certified_search_skipping_is_bit_identical(name, mk, steps, monkeypatch
     out = {}
     for mode in ("skip", "full"):
         monkeypatch.delenv("HJB_NO_SKIP", raising=False)
+        monkeypatch.setenv("HJB_SKIP", "1")      # opt-in (measured slower at cfg4)
+        monkeypatch.setenv("HJB_WIN", "0")       # the gap bookkeeping lives in k_search_deep2
         monkeypatch.setenv("HJB_SKIP_DEBUG", "1")
         if mode == "full":
             monkeypatch.setenv("HJB_NO_SKIP", "1")
