@@ -47,7 +47,7 @@ template <int MODE, int NDOT>
 constexpr int op_deep_minb() { return (MODE == OP_RESID || NDOT > 0) ? HJB_OP_DEEP_MINB - 1 : HJB_OP_DEEP_MINB; }
 // fp32 cycle vectors (hjb_mg_params.precision = 1): half the registers per gathered corner
 #ifndef HJB_OP_DEEP_MINB_F32
-#define HJB_OP_DEEP_MINB_F32 HJB_OP_DEEP_MINB
+#define HJB_OP_DEEP_MINB_F32 7  // 72 registers, 28 resident warps: cfg4 step 1605 -> 1563 ms (8: 1575; r02_t)
 #endif
 template <int MODE, int NDOT, typename V>
 constexpr int op_deep_minb_v() {
