@@ -1487,7 +1487,10 @@ static GapArgs gap_args(hjb_grid* g, const STab& tab) {
       b += 2.0 * t[T::W + p] * G * g->L0.kh * g->h_rng[2 * p + 1] *
            (std::fabs(t[T::SD + 2 * p]) + std::fabs(t[T::SD + 2 * p + 1]));
     b += t[T::WD] * G * g->L0.k2h * bsmax * (std::fabs(t[T::BD]) + std::fabs(t[T::BD + 1]));
-    B = std::max(B, b);
+    // second bound: every tap is a convex combination of dU values, so |I dU(z_e) - dU_j| <= 2 max|dU|;
+    // it wins when dU is rough at the cell scale (G ~ max|dU|: the late searches of a step)
+    const double b2 = (2.0 * t[T::WSUM] + std::fabs(t[T::C])) * Dm;
+    B = std::max(B, std::min(b, b2));
     wc = std::max(wc, 2.0 * t[T::WSUM] + std::fabs(t[T::C]));
     fc = std::max(fc, std::fabs(t[T::FC]));
     for (int q = 0; q < Q && q < 8; ++q) ga.fbmax[q] = std::max(ga.fbmax[q], std::fabs(t[T::FB + q]));
@@ -3078,7 +3081,14 @@ static hjb_status implicit_pi(hjb_grid* g, double dt, const double* dprev, doubl
     hjb_pi_stats pis{};
     cudaEventRecord(g->ev[0], st);
     TRY(halo_exchange(g, lv0, dU, g->lay.halo));
-    TRY(gap_prepare(g, dU, it == 1));
+    // the step's first search is the plain scan (the GAP scan is ~25 % slower); the second one records
+    // the gaps, from the third on CTAs may skip
+    if (it == 1) {
+      g->gap_on = false;
+      g->gap_valid = false;
+    } else {
+      TRY(gap_prepare(g, dU, false));
+    }
     TRY(policy_update_dev(g, dt, dU, dprev, dpol, g->F, &pis));
     cudaEventRecord(g->ev[1], st);
     cudaEventSynchronize(g->ev[1]);
